@@ -1,0 +1,157 @@
+/*
+ * mpsim_gpu.h — C ABI of the B200-native MPS gate-application engine.
+ *
+ * Drop-in boundary for the reference mpsim simulator API (arXiv 2601.04422
+ * TN-Sim; /root/reference/proj). Every entry point cites the reference
+ * interface it replaces. Plain pointers and sizes only; complex numbers are
+ * interleaved (re, im) doubles; matrices and site tensors are row-major with
+ * the last index fastest (tensor.hpp:17-18, :116-125); a site is (Dl, 2, Dr)
+ * with flat index (l*2 + p)*Dr + r (mps.hpp:36-40).
+ *
+ * Status codes (the reference's C++ exceptions, mapped like
+ * exit_code_for_error, runner.cpp:330-341):
+ *   MPSIM_OK 0, MPSIM_EINVAL 1 (std::invalid_argument), MPSIM_ENUMERIC 3
+ *   (mpsim::NumericError), MPSIM_ELOGIC 4 (std::logic_error), MPSIM_ECUDA 5
+ *   (device/runtime failure). mpsim_gpu_last_error() returns the message of
+ *   the calling thread's last failure.
+ *
+ * Threading: a state handle is not thread-safe (the reference MpsState is
+ * shared only through execute_parallel's disjoint-span contract,
+ * gate_apply.hpp:20-24); batching disjoint gates is done inside
+ * mpsim_gpu_apply_layer / mpsim_gpu_execute.
+ */
+#ifndef MPSIM_GPU_H_
+#define MPSIM_GPU_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MPSIM_OK 0
+#define MPSIM_EINVAL 1
+#define MPSIM_ENUMERIC 3
+#define MPSIM_ELOGIC 4
+#define MPSIM_ECUDA 5
+
+#define MPSIM_UNBOUNDED INT64_MAX /* kUnbounded, tensor.hpp:44 */
+
+#define MPSIM_NONLOCAL_SWAP 0     /* NonlocalMethod::Swap, gate_apply.hpp:71 */
+#define MPSIM_NONLOCAL_BONDPROP 1 /* NonlocalMethod::BondProp */
+
+typedef struct mpsim_gpu_state mpsim_gpu_state;
+
+/* TruncationPolicy, gate_apply.hpp:35-38 (max_bond >= 1, cutoff in [0,1)). */
+typedef struct {
+  int64_t max_bond;
+  double cutoff;
+} mpsim_policy;
+
+/* ApplyReport, gate_apply.hpp:40-44. */
+typedef struct {
+  double discarded_weight;
+  int64_t new_bond;
+  int32_t svd_count;
+  int32_t reserved;
+} mpsim_report;
+
+/* FusedGate, circuit.hpp:71-81: q1 = -1 for a one-qubit gate. Two-qubit
+ * gates take (q0, q1) in any order with the 4x4 matrix in the (q0, q1)
+ * basis (row = 2*bit(q0) + bit(q1)); (high, low) orders are folded by SWAP
+ * conjugation (gates.cpp:206, gate_apply.cpp:156-159). u holds 4 (2x2) or
+ * 16 (4x4) interleaved complex entries. */
+typedef struct {
+  int32_t q0;
+  int32_t q1;
+  double u[32];
+} mpsim_gate;
+
+/* ExecStats, executor.hpp:44-57. */
+typedef struct {
+  int64_t peak_bond;
+  double total_discarded_weight;
+  int32_t layers;
+  int32_t gates;          /* local gates executed after SWAP lowering */
+  int64_t kernel_launches; /* device kernels launched by the call */
+  double device_ms;        /* CUDA-event time of the call on the state's stream */
+} mpsim_exec_stats;
+
+const char* mpsim_gpu_last_error(void);
+
+/* ---- state (MpsState, mps.hpp:33-75) ---------------------------------- */
+/* |0...0> on n qubits (mps.cpp:99-110). chi_hint sizes the padded site
+ * store; it grows on demand. device = CUDA ordinal. */
+int mpsim_gpu_state_create(int32_t n_qubits, int64_t chi_hint, int32_t device, mpsim_gpu_state** out);
+int mpsim_gpu_state_destroy(mpsim_gpu_state* s);
+int mpsim_gpu_state_copy(const mpsim_gpu_state* s, mpsim_gpu_state** out); /* mps.cpp:112-130 */
+int mpsim_gpu_num_qubits(const mpsim_gpu_state* s, int32_t* out);
+int mpsim_gpu_bond_dims(const mpsim_gpu_state* s, int64_t* out /* n+1 */); /* mps.hpp:49-52 */
+int mpsim_gpu_chi_capacity(const mpsim_gpu_state* s, int64_t* out);
+int mpsim_gpu_ortho_center(const mpsim_gpu_state* s, int32_t* out /* -1 unknown */); /* mps.hpp:57-60 */
+int mpsim_gpu_set_ortho_center(mpsim_gpu_state* s, int32_t c);
+int mpsim_gpu_set_bond_dim(mpsim_gpu_state* s, int32_t i, int64_t d); /* mps.hpp:50 */
+int mpsim_gpu_validate(const mpsim_gpu_state* s); /* mps.cpp:150-169 */
+/* Host export/import of one site (MpsState::site(i), mps.hpp:45-46):
+ * get with out == NULL only reports dims; set replaces site i and records
+ * bonds i and i+1 (test_util.cpp:104-106). */
+int mpsim_gpu_get_site(const mpsim_gpu_state* s, int32_t i, int64_t* dl, int64_t* dr, double* out);
+int mpsim_gpu_set_site(mpsim_gpu_state* s, int32_t i, int64_t dl, int64_t dr, const double* data);
+
+/* ---- gate application (gate_apply.hpp:48-78) --------------------------- */
+int mpsim_gpu_apply_1q(mpsim_gpu_state* s, const double* u2x2, int32_t q, mpsim_report* rep);
+/* apply_2q_local (q1 == q0+1), apply_2q_swap / apply_2q_bondprop otherwise. */
+int mpsim_gpu_apply_2q(mpsim_gpu_state* s, const double* u4x4, int32_t q0, int32_t q1, int32_t method,
+                       const mpsim_policy* policy, mpsim_report* rep);
+/* One batched launch sequence for a set of gates on pairwise disjoint spans
+ * (one layer of LayerPlan, circuit.hpp:85-95): local 2q and 1q gates only.
+ * reports (nullable) receives one ApplyReport per gate, in input order. */
+int mpsim_gpu_apply_layer(mpsim_gpu_state* s, const mpsim_gate* gates, int32_t count,
+                          const mpsim_policy* policy, mpsim_report* reports);
+/* execute_serial semantics (executor.cpp:73-97) over a fused gate list:
+ * method SWAP lowers non-local gates (fusion.cpp:137-161), layerizes
+ * (fusion.cpp:163-190) and runs every layer as one batched launch sequence
+ * — bit-identical to gate-by-gate order because layer gates touch disjoint
+ * sites. method BONDPROP runs gate by gate. reports (nullable): one per
+ * input gate (aggregated over a SWAP chain as apply_2q_swap does). */
+int mpsim_gpu_execute(mpsim_gpu_state* s, const mpsim_gate* gates, int32_t count, const mpsim_policy* policy,
+                      int32_t method, mpsim_exec_stats* stats, mpsim_report* reports);
+
+/* ---- queries (mps.hpp:79-100) ------------------------------------------ */
+int mpsim_gpu_norm(const mpsim_gpu_state* s, double* out);                       /* mps.cpp:189-202 */
+/* count bit strings of n chars '0'/'1' packed back to back (mps.cpp:204-221) */
+int mpsim_gpu_amplitudes(const mpsim_gpu_state* s, const char* bits, int32_t count, double* out);
+int mpsim_gpu_overlap(const mpsim_gpu_state* a, const mpsim_gpu_state* b, double* out); /* mps.cpp:223-239 */
+int mpsim_gpu_to_statevector(const mpsim_gpu_state* s, int32_t max_qubits, double* out); /* mps.cpp:241-256 */
+int mpsim_gpu_move_center(mpsim_gpu_state* s, int32_t center);                    /* mps.cpp:177-187 */
+/* <psi| O_q |psi> for a 2x2 operator (the P9 definition: overlap(psi,
+ * apply_1q(copy psi, O, q))); out = complex. */
+int mpsim_gpu_expect_1q(const mpsim_gpu_state* s, const double* op2x2, int32_t q, double* out);
+/* <psi| O_a (x) O_b |psi> for one-site operators on two distinct qubits. */
+int mpsim_gpu_expect_2q(const mpsim_gpu_state* s, const double* op_a, int32_t qa, const double* op_b,
+                        int32_t qb, double* out);
+
+/* ---- sampling (Sampler, sampler.hpp:50-86) ------------------------------- */
+typedef struct mpsim_gpu_sampler mpsim_gpu_sampler;
+int mpsim_gpu_sampler_create(const mpsim_gpu_state* s, int32_t memoize, uint64_t max_cache_entries,
+                             mpsim_gpu_sampler** out); /* sampler.cpp:35-66 */
+int mpsim_gpu_sampler_destroy(mpsim_gpu_sampler* sp);
+/* Draws shots (sampler.cpp:80-143); afterwards *unique distinct strings are
+ * available, in lexicographic order, through mpsim_gpu_sampler_result. */
+int mpsim_gpu_sample(mpsim_gpu_sampler* sp, uint64_t shots, uint64_t seed, int32_t* unique);
+int mpsim_gpu_sampler_result(const mpsim_gpu_sampler* sp, int32_t i, char* bits /* n chars */, uint64_t* count);
+int mpsim_gpu_sampler_stats(const mpsim_gpu_sampler* sp, uint64_t* cache_hits, uint64_t* cache_size);
+int mpsim_gpu_sampler_clear_cache(mpsim_gpu_sampler* sp);
+
+/* ---- instrumentation ----------------------------------------------------- */
+/* Kernel launches and device time accumulated on the state's stream since
+ * the last reset (bench.py's gpu_launches / roofline legs). */
+int mpsim_gpu_counters(const mpsim_gpu_state* s, int64_t* launches, double* device_ms, int64_t* svd_sweeps);
+int mpsim_gpu_reset_counters(mpsim_gpu_state* s);
+int mpsim_gpu_synchronize(mpsim_gpu_state* s);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MPSIM_GPU_H_ */

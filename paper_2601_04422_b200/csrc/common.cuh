@@ -1,0 +1,93 @@
+// Shared device-side definitions for the B200 MPS gate-application engine.
+//
+// Data layout in HBM:
+//   * Site store: n_sites slots of (chi_cap x 2 x chi_cap) complex128, row-major
+//     (l, p, r) with r fastest — the reference's site layout (tensor.hpp:139-148,
+//     "(l*2+p)*Dr + r") with the leading dimension padded to chi_cap. Real bond
+//     dimensions live in the host-side bond array (mps.hpp:72-74).
+//   * Jacobi workspace, per two-qubit gate: X (n_pad vectors x m_pad elements,
+//     vector-major, complex128) and a pristine copy X0 of the same matrix.
+//     X = theta (vectors = columns (p1',r)) when 2Dl >= 2Dr, else X = theta^H
+//     (vectors = conjugated rows (l,p0')), so the vector count is
+//     n = min(2Dl, 2Dr) — the number of singular values the reference's thin
+//     SVD returns (svd.hpp:95).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mpsim_gpu {
+
+typedef double2 cplx;
+
+// Block-Jacobi geometry: W vectors per block, a pair of blocks = 2W vectors,
+// E elements per streamed chunk.
+constexpr int kW = 16;
+constexpr int kP = 2 * kW;  // vectors per block pair
+constexpr int kE = 64;      // element chunk
+constexpr int kPad = 33;    // padded smem row (complex) for [e][vector] tiles
+
+// One two-qubit gate of a batched layer launch.
+struct GateDesc {
+  int q;            // left site; the gate acts on (q, q+1)
+  int dl, dm, dr;   // bond dims left of q, between q and q+1, right of q+1
+  int m, n;         // vector length / vector count of X (n = min(2dl, 2dr))
+  int trans;        // 0: X = theta ; 1: X = theta^H
+  int n_pad, m_pad; // n_pad multiple of kP, m_pad multiple of kE
+  int nb;           // blocks of kW vectors (n_pad / kW), even
+  long long ws_off; // offset (complex elements) of X in the workspace; X0 follows
+  long long max_bond;
+  double cutoff;
+  cplx u[16];       // 4x4 gate, (low, high) basis, row = 2*p_low + p_high (circuit.hpp:20-22)
+};
+
+// Per-gate outputs of the split epilogue.
+struct GateOut {
+  int k;            // kept rank (new bond)
+  int status;       // 0 ok, 3 numeric (non-convergence / non-finite)
+  double w;         // discarded weight (pre-rescale, gate_apply.cpp:143)
+  double scale;     // 1/sqrt(1-w) if w > 0 else 1 (gate_apply.cpp:44-51)
+};
+
+// One single-qubit gate.
+struct Gate1Desc {
+  int q, dl, dr, pad;
+  cplx u[4];
+};
+
+struct GemmArgs {
+  int M, N, K;
+  const cplx* A;
+  long long lda;
+  int opA;  // 0: A[i][k] = A[i*lda+k]; 1: A[i][k] = conj(A[k*lda+i])
+  const cplx* B;
+  long long ldb;
+  int opB;  // 0: B[k][j] = B[k*ldb+j]; 1: B[k][j] = conj(B[j*ldb+k])
+  cplx* C;
+  long long ldc;
+  cplx alpha;
+  int accumulate;  // C = alpha*op(A)op(B) (+ C if accumulate)
+};
+
+__device__ __forceinline__ cplx cadd(cplx a, cplx b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// acc += a * b
+__device__ __forceinline__ void cfma(cplx& acc, cplx a, cplx b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(-a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(a.y, b.x, acc.y);
+}
+// acc += conj(a) * b
+__device__ __forceinline__ void cfmac(cplx& acc, cplx a, cplx b) {
+  acc.x = fma(a.x, b.x, acc.x);
+  acc.x = fma(a.y, b.y, acc.x);
+  acc.y = fma(a.x, b.y, acc.y);
+  acc.y = fma(-a.y, b.x, acc.y);
+}
+__device__ __forceinline__ cplx conjc(cplx a) { return make_double2(a.x, -a.y); }
+__device__ __forceinline__ double cabs2(cplx a) { return a.x * a.x + a.y * a.y; }
+
+}  // namespace mpsim_gpu

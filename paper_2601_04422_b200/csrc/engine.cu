@@ -1,0 +1,1089 @@
+// Host-side engine: the HBM site store, the layer scheduler that turns a
+// brick layer of disjoint gates into one batched launch sequence, the
+// transfer-matrix queries, and the extern "C" boundary (include/mpsim_gpu.h).
+//
+// Reference correspondence (paths relative to /root/reference/proj):
+//   MpsState                     include/mpsim/mps.hpp:33-75, src/mps.cpp
+//   apply_1q / apply_2q_local    src/gate_apply.cpp:99-147
+//   apply_2q_swap                src/gate_apply.cpp:149-179
+//   execute_serial / _parallel   src/executor.cpp:73-232
+//   decompose_nonlocal/layerize  src/fusion.cpp:137-190
+//   norm/amplitude/overlap/...   src/mps.cpp:189-256
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "engine.h"
+#include "mpsim_gpu.h"
+
+namespace mpsim_gpu {
+
+// ---- launchers implemented in the kernel translation units
+void launch_theta(const GateDesc*, int, int, const cplx*, long long, int, cplx*, double*, cudaStream_t);
+int theta_tiles(int dl, int dr);
+void jacobi_init();
+size_t jacobi_smem_bytes();
+void launch_jacobi_round(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, int, const double*, double,
+                         cudaStream_t);
+void launch_norms(const GateDesc*, int, int, const cplx*, double*, long long, cudaStream_t);
+void launch_truncate(const GateDesc*, int, double*, int*, long long, GateOut*, cudaStream_t);
+void launch_write_factors(const GateDesc*, int, int, int, const cplx*, const double*, const int*, long long,
+                          const GateOut*, cplx*, long long, int, cudaStream_t);
+void launch_apply1q(const Gate1Desc*, int, long long, cplx*, long long, int, cudaStream_t);
+void launch_regrow(const cplx*, long long, int, cplx*, long long, int, const int*, int, cudaStream_t);
+void launch_cgemm(const GemmArgs&, cudaStream_t);
+void launch_amp_step(const cplx*, long long, cplx*, long long, const char*, int, int, int, const cplx*, int, int,
+                     int, cudaStream_t);
+void launch_fill(cplx*, long long, cplx, cudaStream_t);
+
+Error::Error(int c, std::string m) : std::runtime_error(std::move(m)), code(c) {}
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+#define CK(x)                                                                              \
+  do {                                                                                     \
+    cudaError_t e_ = (x);                                                                  \
+    if (e_ != cudaSuccess) fail(MPSIM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+static void check_launch() {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fail(MPSIM_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+}
+
+void DeviceBuf::ensure(size_t b) {
+  if (b <= bytes) return;
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+  size_t nb = std::max(b, bytes + bytes / 2);
+  if (cudaMalloc(&p, nb) != cudaSuccess) {
+    cudaGetLastError();
+    if (cudaMalloc(&p, b) != cudaSuccess) {
+      cudaGetLastError();
+      fail(MPSIM_ECUDA, "device allocation of " + std::to_string(b) + " bytes failed");
+    }
+    nb = b;
+  }
+  bytes = nb;
+}
+void DeviceBuf::release() {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = 0;
+}
+void PinnedBuf::ensure(size_t b) {
+  if (b <= bytes) return;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  size_t nb = std::max(b, bytes + bytes / 2);
+  CK(cudaMallocHost(&p, nb));
+  bytes = nb;
+}
+void PinnedBuf::release() {
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  bytes = 0;
+}
+
+DeviceGuard::DeviceGuard(int dev) {
+  cudaGetDevice(&prev);
+  if (prev != dev) CK(cudaSetDevice(dev));
+}
+DeviceGuard::~DeviceGuard() {
+  int cur = -1;
+  cudaGetDevice(&cur);
+  if (cur != prev) cudaSetDevice(prev);
+}
+
+static int next_pow2(long long x) {
+  int c = 1;
+  while (c < x) c <<= 1;
+  return c;
+}
+
+}  // namespace mpsim_gpu
+
+using namespace mpsim_gpu;
+using cd = std::complex<double>;
+
+// ============================================================== state
+
+State::State(int n_, long long chi_hint, int dev) : n(n_), device(dev) {
+  if (n_ < 1) fail(MPSIM_EINVAL, "state needs at least one qubit");
+  DeviceGuard g(dev);
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  CK(cudaEventCreate(&ev0));
+  CK(cudaEventCreate(&ev1));
+  static bool inited = false;
+  if (!inited) {
+    jacobi_init();
+    inited = true;
+  }
+  chi = next_pow2(std::max<long long>(2, std::min<long long>(chi_hint, 1 << 14)));
+  stride = (long long)chi * 2 * chi;
+  sites_buf.ensure((size_t)n * stride * sizeof(cplx));
+  sites = (cplx*)sites_buf.p;
+  // |0...0>: every site (1,2,1) = [1, 0] (mps.cpp:99-110)
+  CK(cudaMemsetAsync(sites, 0, (size_t)n * stride * sizeof(cplx), st));
+  launch_fill_sites_zero_state();
+  bonds.assign((size_t)n + 1, 1);
+  sdl.assign((size_t)n, 1);
+  sdr.assign((size_t)n, 1);
+  CK(cudaStreamSynchronize(st));
+}
+
+void State::launch_fill_sites_zero_state() {
+  // element (0,0,0) of every site = 1: a strided 2D copy from a pinned pattern.
+  const cplx one = make_double2(1.0, 0.0);
+  h_small.ensure(sizeof(cplx) * (size_t)n);
+  cplx* h = (cplx*)h_small.p;
+  for (int i = 0; i < n; ++i) h[i] = one;
+  CK(cudaMemcpy2DAsync(sites, stride * sizeof(cplx), h, sizeof(cplx), sizeof(cplx), n, cudaMemcpyHostToDevice, st));
+}
+
+State::~State() {
+  DeviceGuard g(device);
+  cudaStreamSynchronize(st);
+  sites_buf.release();
+  for (DeviceBuf* b : {&ws, &d_gates, &d_out, &d_sigma, &d_order, &d_active, &d_rot, &d_frob, &d_g1, &q1, &q2, &q3, &q4, &qbits})
+    b->release();
+  for (PinnedBuf* b : {&h_gates, &h_out, &h_rot, &h_g1, &h_small}) b->release();
+  cudaEventDestroy(ev0);
+  cudaEventDestroy(ev1);
+  cudaStreamDestroy(st);
+}
+
+void State::grow(int new_chi) {
+  if (new_chi <= chi) return;
+  DeviceGuard g(device);
+  const long long nstride = (long long)new_chi * 2 * new_chi;
+  DeviceBuf nb;
+  nb.ensure((size_t)n * nstride * sizeof(cplx));
+  CK(cudaMemsetAsync(nb.p, 0, (size_t)n * nstride * sizeof(cplx), st));
+  std::vector<int> dims(2 * (size_t)n);
+  for (int i = 0; i < n; ++i) {
+    dims[2 * i] = (int)sdl[i];
+    dims[2 * i + 1] = (int)sdr[i];
+  }
+  DeviceBuf dd;
+  dd.ensure(dims.size() * sizeof(int));
+  CK(cudaMemcpyAsync(dd.p, dims.data(), dims.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+  launch_regrow(sites, stride, chi, (cplx*)nb.p, nstride, new_chi, (const int*)dd.p, n, st);
+  check_launch();
+  ++launches;
+  CK(cudaStreamSynchronize(st));
+  dd.release();
+  sites_buf.release();
+  sites_buf = nb;
+  nb.p = nullptr;
+  nb.bytes = 0;
+  sites = (cplx*)sites_buf.p;
+  chi = new_chi;
+  stride = nstride;
+}
+
+static void check_policy(const mpsim_policy& p) {  // gate_apply.cpp:26-33
+  if (p.max_bond < 1) fail(MPSIM_EINVAL, "truncation policy needs max_bond >= 1");
+  if (!(p.cutoff >= 0.0 && p.cutoff < 1.0)) fail(MPSIM_EINVAL, "truncation cutoff must lie in [0, 1)");
+}
+
+static void update_center(State& s, int lo, int hi) {  // gate_apply.cpp:70-77
+  if (s.center < 0) return;
+  s.center = (s.center >= lo && s.center <= hi) ? hi : -1;
+}
+
+// ============================================================== layer execution
+
+namespace {
+
+struct G2 {
+  int q;
+  cplx u[16];
+  int idx;
+};
+struct G1 {
+  int q;
+  cplx u[4];
+  int idx;
+};
+struct Rep {
+  double w = 0.0;
+  long long k = 1;
+  int svd = 0;
+};
+
+constexpr int kMaxSweeps = 60;
+constexpr double kEps = 2.220446049250313e-16;
+
+void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs) {
+  const int ng = (int)descs.size();
+  long long ws_elems = 0;
+  int max_tiles = 1, max_nb = 2, max_m = 1, max_n = 1;
+  for (const GateDesc& d : descs) {
+    ws_elems = std::max(ws_elems, d.ws_off + 2LL * d.n_pad * d.m_pad);
+    max_tiles = std::max(max_tiles, theta_tiles(d.dl, d.dr));
+    max_nb = std::max(max_nb, d.nb);
+    max_m = std::max(max_m, d.m);
+    max_n = std::max(max_n, d.n);
+  }
+  const long long sig_stride = ((max_n + 31) / 32) * 32;
+  s.ws.ensure((size_t)ws_elems * sizeof(cplx));
+  s.d_gates.ensure(sizeof(GateDesc) * ng);
+  s.d_out.ensure(sizeof(GateOut) * ng);
+  s.d_sigma.ensure(sizeof(double) * sig_stride * ng);
+  s.d_order.ensure(sizeof(int) * sig_stride * ng);
+  s.d_active.ensure(sizeof(int) * ng);
+  s.d_rot.ensure(sizeof(int) * ng);
+  s.d_frob.ensure(sizeof(double) * ng);
+  s.h_gates.ensure(sizeof(GateDesc) * ng);
+  s.h_out.ensure(sizeof(GateOut) * ng);
+  s.h_rot.ensure(sizeof(int) * ng);
+  std::memcpy(s.h_gates.p, descs.data(), sizeof(GateDesc) * ng);
+  cudaStream_t st = s.st;
+  CK(cudaMemcpyAsync(s.d_gates.p, s.h_gates.p, sizeof(GateDesc) * ng, cudaMemcpyHostToDevice, st));
+  CK(cudaMemsetAsync(s.ws.p, 0, (size_t)ws_elems * sizeof(cplx), st));
+  const GateDesc* dg = (const GateDesc*)s.d_gates.p;
+  cplx* ws = (cplx*)s.ws.p;
+  CK(cudaMemsetAsync(s.d_frob.p, 0, sizeof(double) * ng, st));
+  launch_theta(dg, ng, max_tiles, s.sites, s.stride, s.chi, ws, (double*)s.d_frob.p, st);
+  check_launch();
+  ++s.launches;
+
+  int* h_rot = (int*)s.h_rot.p;
+  for (int i = 0; i < ng; ++i) h_rot[i] = 1;
+  CK(cudaMemcpyAsync(s.d_active.p, h_rot, sizeof(int) * ng, cudaMemcpyHostToDevice, st));
+  bool converged = false;
+  std::vector<int> still(ng, 1);
+  for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+    CK(cudaMemsetAsync(s.d_rot.p, 0, sizeof(int) * ng, st));
+    for (int round = 0; round < max_nb - 1; ++round) {
+      launch_jacobi_round(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps,
+                          2.0 * kEps, 12, (const double*)s.d_frob.p, (64.0 * kEps) * (64.0 * kEps), st);
+      ++s.launches;
+    }
+    check_launch();
+    ++s.sweeps;
+    CK(cudaMemcpyAsync(h_rot, s.d_rot.p, sizeof(int) * ng, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    bool any = false;
+    for (int i = 0; i < ng; ++i) {
+      still[i] = h_rot[i];
+      any = any || h_rot[i];
+    }
+    if (!any) {
+      converged = true;
+      break;
+    }
+    CK(cudaMemcpyAsync(s.d_active.p, s.d_rot.p, sizeof(int) * ng, cudaMemcpyDeviceToDevice, st));
+  }
+  launch_norms(dg, ng, max_n, ws, (double*)s.d_sigma.p, sig_stride, st);
+  launch_truncate(dg, ng, (double*)s.d_sigma.p, (int*)s.d_order.p, sig_stride, (GateOut*)s.d_out.p, st);
+  launch_write_factors(dg, ng, max_m, max_n, ws, (const double*)s.d_sigma.p, (const int*)s.d_order.p, sig_stride,
+                       (const GateOut*)s.d_out.p, s.sites, s.stride, s.chi, st);
+  check_launch();
+  s.launches += 4;
+  CK(cudaMemcpyAsync(s.h_out.p, s.d_out.p, sizeof(GateOut) * ng, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  outs.assign((GateOut*)s.h_out.p, (GateOut*)s.h_out.p + ng);
+  if (!converged)
+    for (int i = 0; i < ng; ++i)
+      if (still[i]) outs[i].status = 3;
+}
+
+// Applies disjoint local gates. reports[idx] is filled for every gate.
+void run_layer(State& s, const std::vector<G2>& two, const std::vector<G1>& one, const mpsim_policy& pol,
+               std::vector<Rep>& reports) {
+  cudaStream_t st = s.st;
+  if (!one.empty()) {
+    const int ng = (int)one.size();
+    s.h_g1.ensure(sizeof(Gate1Desc) * ng);
+    s.d_g1.ensure(sizeof(Gate1Desc) * ng);
+    Gate1Desc* h = (Gate1Desc*)s.h_g1.p;
+    long long max_elems = 1;
+    for (int i = 0; i < ng; ++i) {
+      const G1& g = one[i];
+      h[i].q = g.q;
+      h[i].dl = (int)s.sdl[g.q];
+      h[i].dr = (int)s.sdr[g.q];
+      std::memcpy(h[i].u, g.u, sizeof(g.u));
+      max_elems = std::max(max_elems, (long long)h[i].dl * h[i].dr);
+      Rep r;
+      r.k = std::max(s.bonds[g.q], s.bonds[g.q + 1]);  // gate_apply.cpp:107
+      reports[g.idx] = r;
+    }
+    CK(cudaMemcpyAsync(s.d_g1.p, h, sizeof(Gate1Desc) * ng, cudaMemcpyHostToDevice, st));
+    launch_apply1q((const Gate1Desc*)s.d_g1.p, ng, max_elems, s.sites, s.stride, s.chi, st);
+    check_launch();
+    ++s.launches;
+    // The pinned descriptor buffer is reused by the next call: fence here.
+    CK(cudaStreamSynchronize(st));
+  }
+  if (two.empty()) return;
+  check_policy(pol);
+  // Capacity: the kept rank is at most min(2Dl, 2Dr, max_bond).
+  long long need = 1;
+  for (const G2& g : two) {
+    if (s.sdr[g.q] != s.sdl[g.q + 1])
+      fail(MPSIM_EINVAL, "contract: extent mismatch between sites " + std::to_string(g.q) + " and " +
+                             std::to_string(g.q + 1));
+    long long k = std::min(2 * s.sdl[g.q], 2 * s.sdr[g.q + 1]);
+    k = std::min<long long>(k, pol.max_bond);
+    need = std::max(need, k);
+  }
+  if (need > s.chi) s.grow(next_pow2(need));
+
+  // Build descriptors, chunked so the Jacobi workspace fits the budget.
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const long long budget_elems =
+      (long long)(std::min<double>((double)free_b * 0.6 + (double)s.ws.bytes, 64e9) / sizeof(cplx));
+  std::vector<GateDesc> chunk;
+  std::vector<const G2*> chunk_src;
+  long long off = 0;
+  auto flush = [&]() {
+    if (chunk.empty()) return;
+    std::vector<GateOut> outs;
+    run_two_chunk(s, chunk, outs);
+    for (size_t i = 0; i < chunk.size(); ++i) {
+      const GateDesc& d = chunk[i];
+      const GateOut& o = outs[i];
+      if (o.status != 0)
+        fail(MPSIM_ENUMERIC, "singular value decomposition did not converge for (" + std::to_string(2 * d.dl) + "," +
+                                 std::to_string(2 * d.dr) + ") matrix");
+      s.sdr[d.q] = o.k;
+      s.sdl[d.q + 1] = o.k;
+      s.bonds[d.q + 1] = o.k;
+      update_center(s, d.q, d.q + 1);
+      Rep r;
+      r.w = o.w;
+      r.k = o.k;
+      r.svd = 1;
+      reports[chunk_src[i]->idx] = r;
+    }
+    chunk.clear();
+    chunk_src.clear();
+    off = 0;
+  };
+  for (const G2& g : two) {
+    GateDesc d{};
+    d.q = g.q;
+    d.dl = (int)s.sdl[g.q];
+    d.dm = (int)s.sdr[g.q];
+    d.dr = (int)s.sdr[g.q + 1];
+    const int M = 2 * d.dl, N = 2 * d.dr;
+    d.trans = M >= N ? 0 : 1;
+    d.m = std::max(M, N);
+    d.n = std::min(M, N);
+    d.n_pad = ((d.n + kP - 1) / kP) * kP;
+    d.m_pad = ((d.m + kE - 1) / kE) * kE;
+    d.nb = d.n_pad / kW;
+    d.max_bond = pol.max_bond;
+    d.cutoff = pol.cutoff;
+    std::memcpy(d.u, g.u, sizeof(d.u));
+    const long long sz = 2LL * d.n_pad * d.m_pad;
+    if (!chunk.empty() && off + sz > budget_elems) flush();
+    d.ws_off = off;
+    off += sz;
+    chunk.push_back(d);
+    chunk_src.push_back(&g);
+  }
+  flush();
+}
+
+void to_cplx(const double* u, int count, cplx* out) {
+  for (int i = 0; i < count; ++i) out[i] = make_double2(u[2 * i], u[2 * i + 1]);
+}
+
+// SWAP conjugation (gate_apply.cpp:86-95): (high, low) -> (low, high) basis.
+void swap_conjugate4(cplx* m) {
+  cplx o[16];
+  auto rev = [](int x) { return ((x & 1) << 1) | (x >> 1); };
+  for (int r = 0; r < 4; ++r)
+    for (int c = 0; c < 4; ++c) o[r * 4 + c] = m[rev(r) * 4 + rev(c)];
+  std::memcpy(m, o, sizeof(o));
+}
+
+void swap_matrix(cplx* m) {  // gate_apply.cpp:79-84
+  for (int i = 0; i < 16; ++i) m[i] = make_double2(0.0, 0.0);
+  m[0] = m[6] = m[9] = m[15] = make_double2(1.0, 0.0);
+}
+
+// A lowered, local gate with the index of the input gate it belongs to.
+struct Lowered {
+  int q0, q1;  // q1 = -1 or q0+1
+  cplx u[16];
+  int src;
+};
+
+void lower(const mpsim_gate* gates, int count, int n, std::vector<Lowered>& out) {
+  for (int i = 0; i < count; ++i) {
+    const mpsim_gate& g = gates[i];
+    Lowered L{};
+    L.src = i;
+    if (g.q1 < 0) {
+      if (g.q0 < 0 || g.q0 >= n) fail(MPSIM_EINVAL, "qubit " + std::to_string(g.q0) + " out of range");
+      L.q0 = g.q0;
+      L.q1 = -1;
+      to_cplx(g.u, 4, L.u);
+      out.push_back(L);
+      continue;
+    }
+    int a = g.q0, b = g.q1;
+    cplx m[16];
+    to_cplx(g.u, 16, m);
+    if (a == b) fail(MPSIM_EINVAL, "two-qubit gate needs two distinct qubits");
+    if (a > b) {
+      std::swap(a, b);
+      swap_conjugate4(m);
+    }
+    if (a < 0 || b >= n) fail(MPSIM_EINVAL, "gate qubits out of range");
+    // fusion.cpp:137-161: SWAPs i = a..b-2, the gate on (b-1, b), SWAPs back.
+    cplx sw[16];
+    swap_matrix(sw);
+    for (int q = a; q < b - 1; ++q) {
+      Lowered s{};
+      s.q0 = q;
+      s.q1 = q + 1;
+      std::memcpy(s.u, sw, sizeof(sw));
+      s.src = i;
+      out.push_back(s);
+    }
+    L.q0 = b - 1;
+    L.q1 = b;
+    std::memcpy(L.u, m, sizeof(m));
+    out.push_back(L);
+    for (int q = b - 2; q >= a; --q) {
+      Lowered s{};
+      s.q0 = q;
+      s.q1 = q + 1;
+      std::memcpy(s.u, sw, sizeof(sw));
+      s.src = i;
+      out.push_back(s);
+    }
+  }
+}
+
+// fusion.cpp:163-190 — greedy ASAP layering; in-layer order = input order.
+std::vector<std::vector<int>> layerize(const std::vector<Lowered>& g, int n) {
+  std::vector<int> last((size_t)n, -1);
+  std::vector<std::vector<int>> plan;
+  for (int i = 0; i < (int)g.size(); ++i) {
+    const int lo = g[i].q0, hi = g[i].q1 < 0 ? g[i].q0 : g[i].q1;
+    int layer = 0;
+    for (int q = lo; q <= hi; ++q) layer = std::max(layer, last[q] + 1);
+    if ((size_t)layer >= plan.size()) plan.resize((size_t)layer + 1);
+    plan[(size_t)layer].push_back(i);
+    for (int q = lo; q <= hi; ++q) last[q] = layer;
+  }
+  return plan;
+}
+
+// Runs a list of local lowered gates layer by layer; returns per-lowered reports.
+void run_plan(State& s, const std::vector<Lowered>& low, const mpsim_policy& pol, std::vector<Rep>& rep,
+              int* n_layers, long long* peak) {
+  const auto plan = layerize(low, s.n);
+  rep.assign(low.size(), Rep{});
+  long long pk = *std::max_element(s.bonds.begin(), s.bonds.end());
+  for (const auto& layer : plan) {
+    std::vector<G2> two;
+    std::vector<G1> one;
+    for (int i : layer) {
+      const Lowered& L = low[(size_t)i];
+      if (L.q1 < 0) {
+        G1 g;
+        g.q = L.q0;
+        std::memcpy(g.u, L.u, sizeof(g.u));
+        g.idx = i;
+        one.push_back(g);
+      } else {
+        G2 g;
+        g.q = L.q0;
+        std::memcpy(g.u, L.u, sizeof(g.u));
+        g.idx = i;
+        two.push_back(g);
+      }
+    }
+    run_layer(s, two, one, pol, rep);
+    pk = std::max(pk, *std::max_element(s.bonds.begin(), s.bonds.end()));
+  }
+  if (n_layers) *n_layers = (int)plan.size();
+  if (peak) *peak = pk;
+}
+
+}  // namespace
+
+// ============================================================== bond propagation
+// (apply_2q_bondprop, gate_apply.cpp:181-255) lives in bondprop.cu.
+namespace mpsim_gpu {
+void apply_bondprop(State& s, const cplx* u_lowhigh, int q0, int q1, const mpsim_policy& pol, double* w,
+                    long long* k, int* svd);
+}
+
+// ============================================================== queries
+
+namespace {
+
+// E' = sum_p A_p^H op_p(E B_p) over one site; op = optional 2x2 operator on the
+// ket side (B'_p = sum_p' O[p][p'] B_p').
+void transfer_step(State& a, int i, const State& b, const cplx* E, long long ldE, cplx* E2, long long ldE2, cplx* T0,
+                   cplx* T1, long long ldT, const cd* op, cudaStream_t st) {
+  const int dla = (int)a.sdl[i], dra = (int)a.sdr[i];
+  const int dlb = (int)b.sdl[i], drb = (int)b.sdr[i];
+  const cplx* As = a.sites + (long long)i * a.stride;
+  const cplx* Bs = b.sites + (long long)i * b.stride;
+  auto gemm = [&](int M, int N, int K, const cplx* A, long long lda, int opA, const cplx* B, long long ldb,
+                  int opB, cplx* C, long long ldc, cplx alpha, int acc) {
+    GemmArgs g{M, N, K, A, lda, opA, B, ldb, opB, C, ldc, alpha, acc};
+    launch_cgemm(g, st);
+    ++a.launches;
+  };
+  const cplx one = make_double2(1.0, 0.0);
+  // T_p' = E (dla x dlb) * B_p' (dlb x drb)
+  gemm(dla, drb, dlb, E, ldE, 0, Bs, 2LL * b.chi, 0, T0, ldT, one, 0);
+  gemm(dla, drb, dlb, E, ldE, 0, Bs + b.chi, 2LL * b.chi, 0, T1, ldT, one, 0);
+  bool first = true;
+  for (int p = 0; p < 2; ++p) {
+    const cplx* Ap = As + (long long)p * a.chi;
+    if (!op) {
+      gemm(dra, drb, dla, Ap, 2LL * a.chi, 1, p == 0 ? T0 : T1, ldT, 0, E2, ldE2, one, first ? 0 : 1);
+      first = false;
+    } else {
+      for (int pp = 0; pp < 2; ++pp) {
+        const cd o = op[p * 2 + pp];
+        if (o == cd(0.0, 0.0)) continue;
+        gemm(dra, drb, dla, Ap, 2LL * a.chi, 1, pp == 0 ? T0 : T1, ldT, 0, E2, ldE2, make_double2(o.real(), o.imag()),
+             first ? 0 : 1);
+        first = false;
+      }
+    }
+  }
+  if (first) launch_fill(E2, (long long)dra * ldE2, make_double2(0.0, 0.0), st);
+}
+
+cd chain_contract(State& a, const State& b, const std::map<int, const cd*>& ops) {
+  if (a.n != b.n) fail(MPSIM_EINVAL, "overlap requires equal qubit counts");
+  if (a.device != b.device) fail(MPSIM_EINVAL, "overlap requires both states on one device");
+  DeviceGuard g(a.device);
+  cudaStream_t st = a.st;
+  if (&a != &b) CK(cudaStreamSynchronize(b.st));
+  const long long c = std::max(a.chi, b.chi);
+  a.q1.ensure(sizeof(cplx) * c * c);
+  a.q2.ensure(sizeof(cplx) * c * c);
+  a.q3.ensure(sizeof(cplx) * c * c);
+  a.q4.ensure(sizeof(cplx) * c * c);
+  cplx* E = (cplx*)a.q1.p;
+  cplx* E2 = (cplx*)a.q2.p;
+  const cplx one = make_double2(1.0, 0.0);
+  CK(cudaMemcpyAsync(E, &one, sizeof(cplx), cudaMemcpyHostToDevice, st));
+  for (int i = 0; i < a.n; ++i) {
+    auto it = ops.find(i);
+    transfer_step(a, i, b, E, c, E2, c, (cplx*)a.q3.p, (cplx*)a.q4.p, c, it == ops.end() ? nullptr : it->second, st);
+    std::swap(E, E2);
+  }
+  check_launch();
+  cplx r;
+  CK(cudaMemcpyAsync(&r, E, sizeof(cplx), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return cd(r.x, r.y);
+}
+
+}  // namespace
+
+// ============================================================== C ABI
+
+namespace {
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MPSIM_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return MPSIM_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MPSIM_ELOGIC;
+  }
+}
+
+State& S(mpsim_gpu_state* s) {
+  if (!s) fail(MPSIM_EINVAL, "null state");
+  return *reinterpret_cast<State*>(s);
+}
+const State& S(const mpsim_gpu_state* s) {
+  if (!s) fail(MPSIM_EINVAL, "null state");
+  return *reinterpret_cast<const State*>(s);
+}
+
+void put_rep(mpsim_report* r, const Rep& x) {
+  if (!r) return;
+  r->discarded_weight = x.w;
+  r->new_bond = x.k;
+  r->svd_count = x.svd;
+  r->reserved = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mpsim_gpu_last_error(void) { return g_err.c_str(); }
+
+int mpsim_gpu_state_create(int32_t n, int64_t chi_hint, int32_t device, mpsim_gpu_state** out) {
+  return guarded([&] {
+    if (!out) fail(MPSIM_EINVAL, "null output");
+    *out = reinterpret_cast<mpsim_gpu_state*>(new State(n, chi_hint, device));
+  });
+}
+
+int mpsim_gpu_state_destroy(mpsim_gpu_state* s) {
+  return guarded([&] { delete reinterpret_cast<State*>(s); });
+}
+
+int mpsim_gpu_state_copy(const mpsim_gpu_state* src, mpsim_gpu_state** out) {
+  return guarded([&] {
+    const State& a = S(src);
+    DeviceGuard g(a.device);
+    State* b = new State(a.n, a.chi, a.device);
+    CK(cudaStreamSynchronize(a.st));
+    CK(cudaMemcpyAsync(b->sites, a.sites, (size_t)a.n * a.stride * sizeof(cplx), cudaMemcpyDeviceToDevice, b->st));
+    CK(cudaStreamSynchronize(b->st));
+    b->bonds = a.bonds;
+    b->sdl = a.sdl;
+    b->sdr = a.sdr;
+    b->center = a.center;
+    *out = reinterpret_cast<mpsim_gpu_state*>(b);
+  });
+}
+
+int mpsim_gpu_num_qubits(const mpsim_gpu_state* s, int32_t* out) {
+  return guarded([&] { *out = S(s).n; });
+}
+
+int mpsim_gpu_bond_dims(const mpsim_gpu_state* s, int64_t* out) {
+  return guarded([&] {
+    const State& a = S(s);
+    std::memcpy(out, a.bonds.data(), a.bonds.size() * sizeof(int64_t));
+  });
+}
+
+int mpsim_gpu_chi_capacity(const mpsim_gpu_state* s, int64_t* out) {
+  return guarded([&] { *out = S(s).chi; });
+}
+
+int mpsim_gpu_ortho_center(const mpsim_gpu_state* s, int32_t* out) {
+  return guarded([&] { *out = S(s).center; });
+}
+
+int mpsim_gpu_set_ortho_center(mpsim_gpu_state* s, int32_t c) {
+  return guarded([&] { S(s).center = c < 0 ? -1 : c; });
+}
+
+int mpsim_gpu_set_bond_dim(mpsim_gpu_state* s, int32_t i, int64_t d) {
+  return guarded([&] {
+    State& a = S(s);
+    if (i < 0 || i > a.n) fail(MPSIM_EINVAL, "bond index out of range");
+    a.bonds[(size_t)i] = d;
+  });
+}
+
+int mpsim_gpu_validate(const mpsim_gpu_state* s) {  // mps.cpp:150-169
+  return guarded([&] {
+    const State& a = S(s);
+    if (a.bonds.size() != (size_t)a.n + 1) fail(MPSIM_ELOGIC, "bond bookkeeping has wrong length");
+    if (a.bonds.front() != 1 || a.bonds.back() != 1) fail(MPSIM_ELOGIC, "boundary bonds must have dimension 1");
+    for (int i = 0; i < a.n; ++i)
+      if (a.sdl[i] != a.bonds[i] || a.sdr[i] != a.bonds[i + 1])
+        fail(MPSIM_ELOGIC, "site " + std::to_string(i) + " disagrees with recorded bond dimensions");
+  });
+}
+
+int mpsim_gpu_get_site(const mpsim_gpu_state* s, int32_t i, int64_t* dl, int64_t* dr, double* out) {
+  return guarded([&] {
+    const State& a = S(s);
+    if (i < 0 || i >= a.n) fail(MPSIM_EINVAL, "site index out of range");
+    *dl = a.sdl[i];
+    *dr = a.sdr[i];
+    if (!out) return;
+    DeviceGuard g(a.device);
+    CK(cudaMemcpy2DAsync(out, (size_t)a.sdr[i] * sizeof(cplx), a.sites + (long long)i * a.stride,
+                         (size_t)a.chi * sizeof(cplx), (size_t)a.sdr[i] * sizeof(cplx), (size_t)a.sdl[i] * 2,
+                         cudaMemcpyDeviceToHost, a.st));
+    CK(cudaStreamSynchronize(a.st));
+  });
+}
+
+int mpsim_gpu_set_site(mpsim_gpu_state* s, int32_t i, int64_t dl, int64_t dr, const double* data) {
+  return guarded([&] {
+    State& a = S(s);
+    if (i < 0 || i >= a.n) fail(MPSIM_EINVAL, "site index out of range");
+    if (dl < 1 || dr < 1) fail(MPSIM_EINVAL, "tensor extents must be positive");
+    DeviceGuard g(a.device);
+    if (std::max(dl, dr) > a.chi) a.grow(next_pow2(std::max(dl, dr)));
+    CK(cudaMemcpy2DAsync(a.sites + (long long)i * a.stride, (size_t)a.chi * sizeof(cplx), data,
+                         (size_t)dr * sizeof(cplx), (size_t)dr * sizeof(cplx), (size_t)dl * 2,
+                         cudaMemcpyHostToDevice, a.st));
+    CK(cudaStreamSynchronize(a.st));
+    a.sdl[i] = dl;
+    a.sdr[i] = dr;
+    a.bonds[(size_t)i] = dl;
+    a.bonds[(size_t)i + 1] = dr;
+  });
+}
+
+int mpsim_gpu_apply_1q(mpsim_gpu_state* s, const double* u, int32_t q, mpsim_report* rep) {
+  return guarded([&] {
+    State& a = S(s);
+    if (q < 0 || q >= a.n) fail(MPSIM_EINVAL, "qubit " + std::to_string(q) + " out of range");
+    DeviceGuard g(a.device);
+    G1 g1;
+    g1.q = q;
+    g1.idx = 0;
+    to_cplx(u, 4, g1.u);
+    std::vector<Rep> r(1);
+    run_layer(a, {}, {g1}, mpsim_policy{MPSIM_UNBOUNDED, 0.0}, r);
+    put_rep(rep, r[0]);
+  });
+}
+
+int mpsim_gpu_apply_2q(mpsim_gpu_state* s, const double* u, int32_t q0, int32_t q1, int32_t method,
+                       const mpsim_policy* policy, mpsim_report* rep) {
+  return guarded([&] {
+    State& a = S(s);
+    if (!policy) fail(MPSIM_EINVAL, "null policy");
+    DeviceGuard g(a.device);
+    if (q0 == q1) fail(MPSIM_EINVAL, "two-qubit gate needs two distinct qubits");
+    if (method == MPSIM_NONLOCAL_BONDPROP) {
+      check_policy(*policy);
+      cplx m[16];
+      to_cplx(u, 16, m);
+      int a0 = q0, b0 = q1;
+      if (a0 > b0) {
+        std::swap(a0, b0);
+        swap_conjugate4(m);
+      }
+      if (a0 < 0 || b0 >= a.n)
+        fail(MPSIM_EINVAL, "qubit pair (" + std::to_string(a0) + "," + std::to_string(b0) + ") out of range");
+      Rep r;
+      apply_bondprop(a, m, a0, b0, *policy, &r.w, &r.k, &r.svd);
+      put_rep(rep, r);
+      return;
+    }
+    if (std::min(q0, q1) < 0 || std::max(q0, q1) >= a.n)
+      fail(MPSIM_EINVAL, "adjacent pair (" + std::to_string(std::min(q0, q1)) + "," +
+                             std::to_string(std::max(q0, q1)) + ") out of range");
+    check_policy(*policy);
+    mpsim_gate gate;
+    gate.q0 = q0;
+    gate.q1 = q1;
+    std::memcpy(gate.u, u, sizeof(double) * 32);
+    std::vector<Lowered> low;
+    lower(&gate, 1, a.n, low);
+    Rep tot;
+    tot.k = 1;
+    // Sequential single-gate layers, in SWAP-chain order (gate_apply.cpp:171-177).
+    for (size_t i = 0; i < low.size(); ++i) {
+      G2 g2;
+      g2.q = low[i].q0;
+      std::memcpy(g2.u, low[i].u, sizeof(g2.u));
+      g2.idx = 0;
+      std::vector<Rep> r(1);
+      run_layer(a, {g2}, {}, *policy, r);
+      tot.w += r[0].w;
+      tot.k = std::max(tot.k, r[0].k);
+      tot.svd += r[0].svd;
+    }
+    put_rep(rep, tot);
+  });
+}
+
+int mpsim_gpu_apply_layer(mpsim_gpu_state* s, const mpsim_gate* gates, int32_t count, const mpsim_policy* policy,
+                          mpsim_report* reports) {
+  return guarded([&] {
+    State& a = S(s);
+    DeviceGuard g(a.device);
+    std::vector<char> busy((size_t)a.n, 0);
+    std::vector<G2> two;
+    std::vector<G1> one;
+    for (int i = 0; i < count; ++i) {
+      const mpsim_gate& gt = gates[i];
+      int lo = gt.q0, hi = gt.q1 < 0 ? gt.q0 : gt.q1;
+      if (gt.q1 >= 0 && lo > hi) std::swap(lo, hi);
+      if (lo < 0 || hi >= a.n) fail(MPSIM_EINVAL, "gate qubits out of range");
+      if (gt.q1 >= 0 && hi != lo + 1) fail(MPSIM_EINVAL, "parallel execution requires a local-gate plan");
+      // SpanGuard (executor.cpp:41-69): disjoint spans inside one layer.
+      for (int q = lo; q <= hi; ++q) {
+        if (busy[(size_t)q])
+          fail(MPSIM_ELOGIC, "layer contract violated: two in-flight gates touch site " + std::to_string(q));
+        busy[(size_t)q] = 1;
+      }
+      if (gt.q1 < 0) {
+        G1 g1;
+        g1.q = gt.q0;
+        to_cplx(gt.u, 4, g1.u);
+        g1.idx = i;
+        one.push_back(g1);
+      } else {
+        G2 g2;
+        g2.q = lo;
+        to_cplx(gt.u, 16, g2.u);
+        if (gt.q0 > gt.q1) swap_conjugate4(g2.u);
+        g2.idx = i;
+        two.push_back(g2);
+      }
+    }
+    if (!two.empty() && !policy) fail(MPSIM_EINVAL, "null policy");
+    std::vector<Rep> r((size_t)count);
+    run_layer(a, two, one, policy ? *policy : mpsim_policy{MPSIM_UNBOUNDED, 0.0}, r);
+    if (reports)
+      for (int i = 0; i < count; ++i) put_rep(&reports[i], r[(size_t)i]);
+  });
+}
+
+int mpsim_gpu_execute(mpsim_gpu_state* s, const mpsim_gate* gates, int32_t count, const mpsim_policy* policy,
+                      int32_t method, mpsim_exec_stats* stats, mpsim_report* reports) {
+  return guarded([&] {
+    State& a = S(s);
+    if (!policy) fail(MPSIM_EINVAL, "null policy");
+    DeviceGuard g(a.device);
+    const long long l0 = a.launches;
+    CK(cudaEventRecord(a.ev0, a.st));
+    std::vector<Rep> per_input((size_t)count);
+    long long peak = *std::max_element(a.bonds.begin(), a.bonds.end());
+    int n_layers = 0, n_local = 0;
+    if (method == MPSIM_NONLOCAL_BONDPROP) {
+      // execute_serial with BondProp: gate by gate (executor.cpp:84-92).
+      for (int i = 0; i < count; ++i) {
+        const mpsim_gate& gt = gates[i];
+        const bool nonlocal = gt.q1 >= 0 && std::abs(gt.q1 - gt.q0) != 1;
+        if (nonlocal) {
+          mpsim_report r;
+          const int rc = mpsim_gpu_apply_2q(s, gt.u, gt.q0, gt.q1, MPSIM_NONLOCAL_BONDPROP, policy, &r);
+          if (rc != MPSIM_OK) fail(rc, g_err);
+          per_input[(size_t)i] = Rep{r.discarded_weight, r.new_bond, r.svd_count};
+          ++n_layers;
+          ++n_local;
+        } else {
+          std::vector<Lowered> low;
+          lower(&gt, 1, a.n, low);
+          std::vector<Rep> rep;
+          int nl = 0;
+          run_plan(a, low, *policy, rep, &nl, nullptr);
+          per_input[(size_t)i] = rep[0];
+          n_layers += nl;
+          n_local += (int)low.size();
+        }
+        peak = std::max(peak, *std::max_element(a.bonds.begin(), a.bonds.end()));
+      }
+    } else {
+      std::vector<Lowered> low;
+      lower(gates, count, a.n, low);
+      bool any2 = false;
+      for (const Lowered& L : low) any2 = any2 || L.q1 >= 0;
+      if (any2) check_policy(*policy);
+      std::vector<Rep> rep;
+      long long pk = 0;
+      run_plan(a, low, *policy, rep, &n_layers, &pk);
+      peak = std::max(peak, pk);
+      n_local = (int)low.size();
+      // Aggregate SWAP chains per input gate (gate_apply.cpp:163-167).
+      std::vector<char> seen((size_t)count, 0);
+      for (size_t i = 0; i < low.size(); ++i) {
+        Rep& t = per_input[(size_t)low[i].src];
+        const Rep& x = rep[i];
+        if (!seen[(size_t)low[i].src]) {
+          t = x;
+          seen[(size_t)low[i].src] = 1;
+        } else {
+          t.w += x.w;
+          t.k = std::max(t.k, x.k);
+          t.svd += x.svd;
+        }
+      }
+    }
+    CK(cudaEventRecord(a.ev1, a.st));
+    CK(cudaEventSynchronize(a.ev1));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a.ev0, a.ev1));
+    a.device_ms += ms;
+    double total_w = 0.0;
+    for (const Rep& r : per_input) total_w += r.w;  // executor.cpp:90, input order
+    if (stats) {
+      stats->peak_bond = peak;
+      stats->total_discarded_weight = total_w;
+      stats->layers = n_layers;
+      stats->gates = n_local;
+      stats->kernel_launches = a.launches - l0;
+      stats->device_ms = ms;
+    }
+    if (reports)
+      for (int i = 0; i < count; ++i) put_rep(&reports[i], per_input[(size_t)i]);
+    // executor.cpp:93 validates the final state.
+    if (mpsim_gpu_validate(s) != MPSIM_OK) fail(MPSIM_ELOGIC, g_err);
+  });
+}
+
+int mpsim_gpu_norm(const mpsim_gpu_state* s, double* out) {
+  return guarded([&] {
+    State& a = const_cast<State&>(S(s));
+    const cd v = chain_contract(a, a, {});
+    *out = std::sqrt(std::max(0.0, v.real()));
+  });
+}
+
+int mpsim_gpu_overlap(const mpsim_gpu_state* x, const mpsim_gpu_state* y, double* out) {
+  return guarded([&] {
+    State& a = const_cast<State&>(S(x));
+    const cd v = chain_contract(a, S(y), {});
+    out[0] = v.real();
+    out[1] = v.imag();
+  });
+}
+
+int mpsim_gpu_expect_1q(const mpsim_gpu_state* s, const double* op, int32_t q, double* out) {
+  return guarded([&] {
+    State& a = const_cast<State&>(S(s));
+    if (q < 0 || q >= a.n) fail(MPSIM_EINVAL, "qubit out of range");
+    cd o[4];
+    for (int i = 0; i < 4; ++i) o[i] = cd(op[2 * i], op[2 * i + 1]);
+    const cd v = chain_contract(a, a, {{q, o}});
+    out[0] = v.real();
+    out[1] = v.imag();
+  });
+}
+
+int mpsim_gpu_expect_2q(const mpsim_gpu_state* s, const double* op_a, int32_t qa, const double* op_b, int32_t qb,
+                        double* out) {
+  return guarded([&] {
+    State& a = const_cast<State&>(S(s));
+    if (qa < 0 || qa >= a.n || qb < 0 || qb >= a.n || qa == qb) fail(MPSIM_EINVAL, "invalid qubit pair");
+    cd oa[4], ob[4];
+    for (int i = 0; i < 4; ++i) {
+      oa[i] = cd(op_a[2 * i], op_a[2 * i + 1]);
+      ob[i] = cd(op_b[2 * i], op_b[2 * i + 1]);
+    }
+    const cd v = chain_contract(a, a, {{qa, oa}, {qb, ob}});
+    out[0] = v.real();
+    out[1] = v.imag();
+  });
+}
+
+int mpsim_gpu_amplitudes(const mpsim_gpu_state* s, const char* bits, int32_t count, double* out) {
+  return guarded([&] {
+    State& a = const_cast<State&>(S(s));
+    if (count < 0) fail(MPSIM_EINVAL, "negative count");
+    for (long long i = 0; i < (long long)count * a.n; ++i)
+      if (bits[i] != '0' && bits[i] != '1') fail(MPSIM_EINVAL, "bit string must contain only 0 and 1");
+    if (count == 0) return;
+    DeviceGuard g(a.device);
+    cudaStream_t st = a.st;
+    const int chunk = 4096;
+    a.qbits.ensure((size_t)std::min(count, chunk) * a.n);
+    a.q1.ensure(sizeof(cplx) * (size_t)std::min(count, chunk) * a.chi);
+    a.q2.ensure(sizeof(cplx) * (size_t)std::min(count, chunk) * a.chi);
+    for (int c0 = 0; c0 < count; c0 += chunk) {
+      const int c = std::min(chunk, count - c0);
+      CK(cudaMemcpyAsync(a.qbits.p, bits + (long long)c0 * a.n, (size_t)c * a.n, cudaMemcpyHostToDevice, st));
+      cplx* E = (cplx*)a.q1.p;
+      cplx* E2 = (cplx*)a.q2.p;
+      launch_fill(E, c, make_double2(1.0, 0.0), st);  // env = ones(1) per string, ld = 1 at site 0
+      long long ld = 1;
+      for (int i = 0; i < a.n; ++i) {
+        launch_amp_step(E, ld, E2, a.sdr[i], (const char*)a.qbits.p, a.n, i, c, a.sites + (long long)i * a.stride,
+                        a.chi, (int)a.sdl[i], (int)a.sdr[i], st);
+        ++a.launches;
+        ld = a.sdr[i];
+        std::swap(E, E2);
+      }
+      check_launch();
+      std::vector<cplx> h((size_t)c);
+      CK(cudaMemcpyAsync(h.data(), E, sizeof(cplx) * c, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (int i = 0; i < c; ++i) {
+        out[2 * (c0 + i)] = h[(size_t)i].x;
+        out[2 * (c0 + i) + 1] = h[(size_t)i].y;
+      }
+    }
+  });
+}
+
+int mpsim_gpu_to_statevector(const mpsim_gpu_state* s, int32_t max_qubits, double* out) {
+  return guarded([&] {
+    State& a = const_cast<State&>(S(s));
+    if (a.n > max_qubits)
+      fail(MPSIM_EINVAL, "statevector export capped at " + std::to_string(max_qubits) + " qubits, got " +
+                             std::to_string(a.n));
+    DeviceGuard g(a.device);
+    cudaStream_t st = a.st;
+    const size_t cap = (size_t)1 << a.n;
+    size_t need = cap;
+    // acc is (rows x dl); grown is (rows x 2dr) = (2 rows x dr).
+    long long rows = 1;
+    for (int i = 0; i < a.n; ++i) {
+      need = std::max(need, (size_t)(rows * 2 * a.sdr[i]));
+      rows *= 2;
+    }
+    a.q1.ensure(sizeof(cplx) * need);
+    a.q2.ensure(sizeof(cplx) * need);
+    cplx* acc = (cplx*)a.q1.p;
+    cplx* nx = (cplx*)a.q2.p;
+    const cplx one = make_double2(1.0, 0.0);
+    CK(cudaMemcpyAsync(acc, &one, sizeof(cplx), cudaMemcpyHostToDevice, st));
+    rows = 1;
+    for (int i = 0; i < a.n; ++i) {
+      const int dl = (int)a.sdl[i], dr = (int)a.sdr[i];
+      const cplx* site = a.sites + (long long)i * a.stride;
+      for (int p = 0; p < 2; ++p) {
+        GemmArgs ga{(int)rows, dr, dl, acc, dl, 0, site + (long long)p * a.chi, 2LL * a.chi, 0, nx + (long long)p * dr,
+                    2LL * dr, one, 0};
+        launch_cgemm(ga, st);
+        ++a.launches;
+      }
+      rows *= 2;
+      std::swap(acc, nx);
+    }
+    check_launch();
+    CK(cudaMemcpyAsync(out, acc, sizeof(cplx) * cap, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int mpsim_gpu_counters(const mpsim_gpu_state* s, int64_t* launches, double* device_ms, int64_t* sweeps) {
+  return guarded([&] {
+    const State& a = S(s);
+    if (launches) *launches = a.launches;
+    if (device_ms) *device_ms = a.device_ms;
+    if (sweeps) *sweeps = a.sweeps;
+  });
+}
+
+int mpsim_gpu_reset_counters(mpsim_gpu_state* s) {
+  return guarded([&] {
+    State& a = S(s);
+    a.launches = 0;
+    a.device_ms = 0.0;
+    a.sweeps = 0;
+  });
+}
+
+int mpsim_gpu_synchronize(mpsim_gpu_state* s) {
+  return guarded([&] {
+    State& a = S(s);
+    DeviceGuard g(a.device);
+    CK(cudaStreamSynchronize(a.st));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// Host-side engine types shared by the engine translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace mpsim_gpu {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, std::string m);
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+
+struct DeviceBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t b);
+  void release();
+};
+
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t b);
+  void release();
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev);
+  ~DeviceGuard();
+};
+
+// The HBM-resident MPS (MpsState, mps.hpp:33-75): n sites of (chi x 2 x chi)
+// complex128 slots; real dims per site in sdl/sdr; bonds as the reference
+// records them (bond_dims_, mps.hpp:73).
+struct State {
+  int n = 0;
+  int device = 0;
+  int chi = 0;          // padded capacity (power of two)
+  long long stride = 0; // complex elements per site slot
+  cplx* sites = nullptr;
+  DeviceBuf sites_buf;
+  std::vector<long long> bonds;   // n+1
+  std::vector<long long> sdl, sdr;  // site extents
+  int center = -1;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  // workspaces
+  DeviceBuf ws, d_gates, d_out, d_sigma, d_order, d_active, d_rot, d_frob, d_g1, q1, q2, q3, q4, qbits;
+  PinnedBuf h_gates, h_out, h_rot, h_g1, h_small;
+  // instrumentation
+  long long launches = 0;
+  double device_ms = 0.0;
+  long long sweeps = 0;
+
+  State(int n, long long chi_hint, int device);
+  ~State();
+  State(const State&) = delete;
+  State& operator=(const State&) = delete;
+  void grow(int new_chi);
+  void launch_fill_sites_zero_state();
+};
+
+}  // namespace mpsim_gpu

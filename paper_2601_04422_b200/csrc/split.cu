@@ -1,0 +1,275 @@
+// Split epilogue of a batched two-qubit layer: singular values, the
+// reference truncation rule, renormalisation and the write-back of
+//   site q   <- U        (Dl, 2, k)   (gate_apply.cpp:136)
+//   site q+1 <- S V^dag  (k, 2, Dr)   (gate_apply.cpp:137-138, scale_rows :54-64)
+// After the Jacobi sweeps the vectors of X are orthogonal: X = U_X Sigma.
+//   trans = 0 (X = theta):   U = X/sigma,           S V^dag = U^H theta = (X/sigma)^H X0
+//   trans = 1 (X = theta^H): S V^dag = X^H,         U = theta X Sigma^-2 = X0^H X / sigma^2
+// so one "cross-Gram" kernel (C = P^H Q over vector-major operands) produces
+// whichever factor is not a plain copy.
+#include <float.h>
+
+#include "common.cuh"
+
+namespace mpsim_gpu {
+
+// ---- vector norms: one warp per vector, coalesced along the element axis.
+__global__ void __launch_bounds__(256) norms_kernel(const GateDesc* __restrict__ gates,
+                                                    const cplx* __restrict__ ws,
+                                                    double* __restrict__ sigma, long long sig_stride) {
+  const GateDesc& g = gates[blockIdx.y];
+  const int v = blockIdx.x * 8 + threadIdx.x / 32;
+  const int lane = threadIdx.x % 32;
+  if (v >= g.n) return;
+  const cplx* x = ws + g.ws_off + (long long)v * g.m_pad;
+  double s = 0.0;
+  for (int e = lane; e < g.m; e += 32) s += cabs2(x[e]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) sigma[blockIdx.y * sig_stride + v] = sqrt(s);
+}
+
+// ---- sort descending + truncation rule (svd.hpp:48-74) + renorm factor.
+// One CTA (1024 threads) per gate; n <= 2048.
+__global__ void __launch_bounds__(1024) truncate_kernel(const GateDesc* __restrict__ gates,
+                                                        double* __restrict__ sigma,
+                                                        int* __restrict__ order, long long sig_stride,
+                                                        GateOut* __restrict__ out) {
+  const GateDesc& g = gates[blockIdx.y];
+  __shared__ double key[2048];
+  __shared__ int idx[2048];
+  __shared__ int bad;
+  const int n = g.n;
+  int n2 = 1;
+  while (n2 < n) n2 <<= 1;
+  double* sg = sigma + blockIdx.y * sig_stride;
+  int* od = order + blockIdx.y * sig_stride;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+    const double v = i < n ? sg[i] : -1.0;
+    if (i < n && !(v <= DBL_MAX)) bad = 1;  // NaN or inf
+    key[i] = v;
+    idx[i] = i;
+  }
+  __syncthreads();
+  // Bitonic sort: descending key, ascending index on ties.
+  for (int size = 2; size <= n2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool desc = ((i & size) == 0);
+          const double ki = key[i], kj = key[j];
+          const int ii = idx[i], ij = idx[j];
+          // "i before j" in the final order
+          const bool i_first = (ki > kj) || (ki == kj && ii < ij);
+          if (desc != i_first) {
+            key[i] = kj;
+            key[j] = ki;
+            idx[i] = ij;
+            idx[j] = ii;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    sg[i] = key[i];
+    od[i] = idx[i];
+  }
+  if (threadIdx.x == 0) {
+    // Same accumulation order as the reference loop.
+    double total = 0.0;
+    for (int i = 0; i < n; ++i) total += key[i] * key[i];
+    long long keep = n;
+    if (total > 0.0) {
+      double tail = 0.0;
+      while (keep > 1 && tail + key[keep - 1] * key[keep - 1] <= g.cutoff * total) {
+        tail += key[keep - 1] * key[keep - 1];
+        --keep;
+      }
+    } else {
+      keep = 1;
+    }
+    const long long cap = g.max_bond < 1 ? 1 : g.max_bond;
+    if (keep > cap) keep = cap;
+    double dropped = 0.0;
+    for (long long i = keep; i < n; ++i) dropped += key[i] * key[i];
+    const double w = total > 0.0 ? dropped / total : 0.0;
+    GateOut o;
+    o.k = (int)keep;
+    o.w = w;
+    o.scale = w > 0.0 ? 1.0 / sqrt(1.0 - w) : 1.0;  // gate_apply.cpp:44-51
+    o.status = bad ? 3 : 0;
+    out[blockIdx.y] = o;
+  }
+}
+
+// ---- plain-copy factor.
+//  trans 0: site q   [e*chi + j]                 = X[o_j][e] / sigma_j   (e < m = 2dl, j < k)
+//  trans 1: site q+1 [j*2chi + p1*chi + r]       = scale * conj(X[o_j][e]), e = p1*dr + r
+__global__ void __launch_bounds__(256) copy_factor_kernel(const GateDesc* __restrict__ gates,
+                                                          const cplx* __restrict__ ws,
+                                                          const double* __restrict__ sigma,
+                                                          const int* __restrict__ order, long long sig_stride,
+                                                          const GateOut* __restrict__ out,
+                                                          cplx* __restrict__ sites, long long site_stride,
+                                                          int chi) {
+  const GateDesc& g = gates[blockIdx.z];
+  const GateOut o = out[blockIdx.z];
+  const int k = o.k;
+  const int j0 = blockIdx.y * 32, e0 = blockIdx.x * 32;
+  if (j0 >= k || e0 >= g.m) return;
+  const double* sg = sigma + blockIdx.z * sig_stride;
+  const int* od = order + blockIdx.z * sig_stride;
+  const cplx* X = ws + g.ws_off;
+  __shared__ cplx tile[32][33];
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  if (g.trans == 0) {
+    // Read along e (coalesced), write along j (coalesced) through a transpose.
+    for (int jj = ty; jj < 32; jj += 8) {
+      const int j = j0 + jj, e = e0 + tx;
+      cplx v = make_double2(0.0, 0.0);
+      if (j < k && e < g.m) {
+        const double s = sg[j];
+        if (s > 0.0) {
+          const cplx x = X[(long long)od[j] * g.m_pad + e];
+          v = make_double2(x.x / s, x.y / s);
+        } else {
+          v = make_double2(e == j ? 1.0 : 0.0, 0.0);  // zero matrix: any unit column
+        }
+      }
+      tile[jj][tx] = v;
+    }
+    __syncthreads();
+    cplx* site = sites + (long long)g.q * site_stride;
+    for (int ee = ty; ee < 32; ee += 8) {
+      const int e = e0 + ee, j = j0 + tx;
+      if (e < g.m && j < k) site[(long long)e * chi + j] = tile[tx][ee];
+    }
+  } else {
+    cplx* site = sites + (long long)(g.q + 1) * site_stride;
+    for (int jj = ty; jj < 32; jj += 8) {
+      const int j = j0 + jj, e = e0 + tx;
+      if (j < k && e < g.m) {
+        const cplx x = X[(long long)od[j] * g.m_pad + e];
+        const int p1 = e / g.dr, r = e % g.dr;
+        site[(long long)j * 2 * chi + (long long)p1 * chi + r] = make_double2(o.scale * x.x, -o.scale * x.y);
+      }
+    }
+  }
+}
+
+// ---- cross-Gram factor, C[a][b] = sum_e conj(P_a[e]) Q_b[e].
+//  trans 0: a = j (X, ordered), b = v (X0):  site q+1[(j*2+p1)*chi + r] = scale/sigma_j * C, v = p1*dr + r
+//  trans 1: a = v (X0), b = j (X, ordered):  site q  [v*chi + j]        = C / sigma_j^2
+__global__ void __launch_bounds__(256) cross_gram_kernel(const GateDesc* __restrict__ gates,
+                                                         const cplx* __restrict__ ws,
+                                                         const double* __restrict__ sigma,
+                                                         const int* __restrict__ order, long long sig_stride,
+                                                         const GateOut* __restrict__ out,
+                                                         cplx* __restrict__ sites, long long site_stride,
+                                                         int chi) {
+  const GateDesc& g = gates[blockIdx.z];
+  const GateOut o = out[blockIdx.z];
+  const int k = o.k;
+  const int n_a = g.trans == 0 ? k : g.n;
+  const int n_b = g.trans == 0 ? g.n : k;
+  const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32;
+  if (a0 >= n_a || b0 >= n_b) return;
+  const double* sg = sigma + blockIdx.z * sig_stride;
+  const int* od = order + blockIdx.z * sig_stride;
+  const cplx* X = ws + g.ws_off;
+  const cplx* X0 = X + (long long)g.n_pad * g.m_pad;
+  constexpr int kCE = 32;
+  __shared__ cplx Ta[kCE][kPad];
+  __shared__ cplx Tb[kCE][kPad];
+  const int t = threadIdx.x;
+  auto pa = [&](int i) -> const cplx* {
+    const int a = a0 + i;
+    if (a >= n_a) return nullptr;
+    return g.trans == 0 ? X + (long long)od[a] * g.m_pad : X0 + (long long)a * g.m_pad;
+  };
+  auto pb = [&](int i) -> const cplx* {
+    const int b = b0 + i;
+    if (b >= n_b) return nullptr;
+    return g.trans == 0 ? X0 + (long long)b * g.m_pad : X + (long long)od[b] * g.m_pad;
+  };
+  const int ip = t / 16, jp = t % 16;
+  cplx acc[2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) acc[a][b] = make_double2(0.0, 0.0);
+  for (int e0 = 0; e0 < g.m_pad; e0 += kCE) {
+#pragma unroll
+    for (int s = 0; s < (32 * kCE) / 256; ++s) {
+      const int idx = t + 256 * s;
+      const int vi = idx / kCE, ee = idx % kCE;
+      const cplx* xa = pa(vi);
+      const cplx* xb = pb(vi);
+      Ta[ee][vi] = xa ? xa[e0 + ee] : make_double2(0.0, 0.0);
+      Tb[ee][vi] = xb ? xb[e0 + ee] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int ee = 0; ee < kCE; ++ee) {
+      const cplx x0 = Ta[ee][2 * ip], x1 = Ta[ee][2 * ip + 1];
+      const cplx y0 = Tb[ee][2 * jp], y1 = Tb[ee][2 * jp + 1];
+      cfmac(acc[0][0], x0, y0);
+      cfmac(acc[0][1], x0, y1);
+      cfmac(acc[1][0], x1, y0);
+      cfmac(acc[1][1], x1, y1);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int ai = 0; ai < 2; ++ai)
+#pragma unroll
+    for (int bi = 0; bi < 2; ++bi) {
+      const int a = a0 + 2 * ip + ai, b = b0 + 2 * jp + bi;
+      if (a >= n_a || b >= n_b) continue;
+      const cplx c = acc[ai][bi];
+      if (g.trans == 0) {
+        const double s = sg[a];
+        const double f = s > 0.0 ? o.scale / s : 0.0;
+        const int p1 = b / g.dr, r = b % g.dr;
+        sites[(long long)(g.q + 1) * site_stride + (long long)(a * 2 + p1) * chi + r] =
+            make_double2(f * c.x, f * c.y);
+      } else {
+        const double s = sg[b];
+        cplx v;
+        if (s > 0.0) {
+          const double f = 1.0 / (s * s);
+          v = make_double2(f * c.x, f * c.y);
+        } else {
+          v = make_double2(a == b ? 1.0 : 0.0, 0.0);
+        }
+        sites[(long long)g.q * site_stride + (long long)a * chi + b] = v;
+      }
+    }
+}
+
+void launch_norms(const GateDesc* d_gates, int n_gates, int max_n, const cplx* ws, double* sigma,
+                  long long sig_stride, cudaStream_t st) {
+  norms_kernel<<<dim3((max_n + 7) / 8, n_gates), 256, 0, st>>>(d_gates, ws, sigma, sig_stride);
+}
+
+void launch_truncate(const GateDesc* d_gates, int n_gates, double* sigma, int* order, long long sig_stride,
+                     GateOut* d_out, cudaStream_t st) {
+  truncate_kernel<<<dim3(1, n_gates), 1024, 0, st>>>(d_gates, sigma, order, sig_stride, d_out);
+}
+
+void launch_write_factors(const GateDesc* d_gates, int n_gates, int max_m, int max_n, const cplx* ws,
+                          const double* sigma, const int* order, long long sig_stride, const GateOut* d_out,
+                          cplx* sites, long long site_stride, int chi, cudaStream_t st) {
+  // k <= n, so n bounds every tile count.
+  copy_factor_kernel<<<dim3((max_m + 31) / 32, (max_n + 31) / 32, n_gates), 256, 0, st>>>(
+      d_gates, ws, sigma, order, sig_stride, d_out, sites, site_stride, chi);
+  cross_gram_kernel<<<dim3((max_n + 31) / 32, (max_n + 31) / 32, n_gates), 256, 0, st>>>(
+      d_gates, ws, sigma, order, sig_stride, d_out, sites, site_stride, chi);
+}
+
+}  // namespace mpsim_gpu

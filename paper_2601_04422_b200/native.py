@@ -1,0 +1,129 @@
+"""ctypes binding of ``libmpsim_gpu.so`` (the C ABI in ``include/mpsim_gpu.h``).
+
+There is no CPU fallback: importing this module on a machine without the
+built library raises immediately, and every call that fails on the device
+raises with the library's message.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libmpsim_gpu.so")
+
+MPSIM_OK, MPSIM_EINVAL, MPSIM_ENUMERIC, MPSIM_ELOGIC, MPSIM_ECUDA = 0, 1, 3, 4, 5
+UNBOUNDED = (1 << 63) - 1
+NONLOCAL_SWAP, NONLOCAL_BONDPROP = 0, 1
+
+I32, I64, U64, DBL = C.c_int32, C.c_int64, C.c_uint64, C.c_double
+DP = C.POINTER(C.c_double)
+VP = C.c_void_p
+
+
+class Policy(C.Structure):
+    _fields_ = [("max_bond", I64), ("cutoff", DBL)]
+
+
+class Report(C.Structure):
+    _fields_ = [("discarded_weight", DBL), ("new_bond", I64), ("svd_count", I32), ("reserved", I32)]
+
+    def __repr__(self):
+        return f"Report(w={self.discarded_weight}, k={self.new_bond}, svd={self.svd_count})"
+
+
+class Gate(C.Structure):
+    _fields_ = [("q0", I32), ("q1", I32), ("u", DBL * 32)]
+
+
+class ExecStats(C.Structure):
+    _fields_ = [("peak_bond", I64), ("total_discarded_weight", DBL), ("layers", I32), ("gates", I32),
+                ("kernel_launches", I64), ("device_ms", DBL)]
+
+
+class NumericError(RuntimeError):
+    """mpsim::NumericError (errors.hpp:45-48)."""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error (validate / span guard)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA runtime failure."""
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    L = C.CDLL(LIB_PATH)
+    sig = {
+        "mpsim_gpu_last_error": (C.c_char_p, []),
+        "mpsim_gpu_state_create": (C.c_int, [I32, I64, I32, C.POINTER(VP)]),
+        "mpsim_gpu_state_destroy": (C.c_int, [VP]),
+        "mpsim_gpu_state_copy": (C.c_int, [VP, C.POINTER(VP)]),
+        "mpsim_gpu_num_qubits": (C.c_int, [VP, C.POINTER(I32)]),
+        "mpsim_gpu_bond_dims": (C.c_int, [VP, C.POINTER(I64)]),
+        "mpsim_gpu_chi_capacity": (C.c_int, [VP, C.POINTER(I64)]),
+        "mpsim_gpu_ortho_center": (C.c_int, [VP, C.POINTER(I32)]),
+        "mpsim_gpu_set_ortho_center": (C.c_int, [VP, I32]),
+        "mpsim_gpu_set_bond_dim": (C.c_int, [VP, I32, I64]),
+        "mpsim_gpu_validate": (C.c_int, [VP]),
+        "mpsim_gpu_get_site": (C.c_int, [VP, I32, C.POINTER(I64), C.POINTER(I64), DP]),
+        "mpsim_gpu_set_site": (C.c_int, [VP, I32, I64, I64, DP]),
+        "mpsim_gpu_apply_1q": (C.c_int, [VP, DP, I32, C.POINTER(Report)]),
+        "mpsim_gpu_apply_2q": (C.c_int, [VP, DP, I32, I32, I32, C.POINTER(Policy), C.POINTER(Report)]),
+        "mpsim_gpu_apply_layer": (C.c_int, [VP, C.POINTER(Gate), I32, C.POINTER(Policy), C.POINTER(Report)]),
+        "mpsim_gpu_execute": (C.c_int, [VP, C.POINTER(Gate), I32, C.POINTER(Policy), I32, C.POINTER(ExecStats),
+                                        C.POINTER(Report)]),
+        "mpsim_gpu_norm": (C.c_int, [VP, DP]),
+        "mpsim_gpu_amplitudes": (C.c_int, [VP, C.c_char_p, I32, DP]),
+        "mpsim_gpu_overlap": (C.c_int, [VP, VP, DP]),
+        "mpsim_gpu_to_statevector": (C.c_int, [VP, I32, DP]),
+        "mpsim_gpu_move_center": (C.c_int, [VP, I32]),
+        "mpsim_gpu_expect_1q": (C.c_int, [VP, DP, I32, DP]),
+        "mpsim_gpu_expect_2q": (C.c_int, [VP, DP, I32, DP, I32, DP]),
+        "mpsim_gpu_sampler_create": (C.c_int, [VP, I32, U64, C.POINTER(VP)]),
+        "mpsim_gpu_sampler_destroy": (C.c_int, [VP]),
+        "mpsim_gpu_sample": (C.c_int, [VP, U64, U64, C.POINTER(I32)]),
+        "mpsim_gpu_sampler_result": (C.c_int, [VP, I32, C.c_char_p, C.POINTER(U64)]),
+        "mpsim_gpu_sampler_stats": (C.c_int, [VP, C.POINTER(U64), C.POINTER(U64)]),
+        "mpsim_gpu_sampler_clear_cache": (C.c_int, [VP]),
+        "mpsim_gpu_counters": (C.c_int, [VP, C.POINTER(I64), DP, C.POINTER(I64)]),
+        "mpsim_gpu_reset_counters": (C.c_int, [VP]),
+        "mpsim_gpu_synchronize": (C.c_int, [VP]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def exported_symbols():
+    """Names declared in include/mpsim_gpu.h (for the ABI-surface test)."""
+    import re
+    hdr = os.path.join(os.path.dirname(_HERE), "include", "mpsim_gpu.h")
+    with open(hdr) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(mpsim_gpu_[a-z0-9_]+)\s*\(", text)))
+
+
+def check(rc: int):
+    if rc == MPSIM_OK:
+        return
+    msg = lib().mpsim_gpu_last_error().decode()
+    if rc == MPSIM_EINVAL:
+        raise ValueError(msg)
+    if rc == MPSIM_ENUMERIC:
+        raise NumericError(msg)
+    if rc == MPSIM_ELOGIC:
+        raise LogicError(msg)
+    raise DeviceError(msg)
