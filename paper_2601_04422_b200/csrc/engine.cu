@@ -52,9 +52,20 @@ Error::Error(int c, std::string m) : std::runtime_error(std::move(m)), code(c) {
     if (e_ != cudaSuccess) fail(MPSIM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
   } while (0)
 
-static void check_launch() {
+// MPSIM_SYNC_DEBUG=1 synchronises after every checked launch so a device
+// fault is attributed to the kernel that raised it.
+static bool sync_debug() {
+  static const bool on = [] {
+    const char* v = std::getenv("MPSIM_SYNC_DEBUG");
+    return v != nullptr && v[0] == '1';
+  }();
+  return on;
+}
+
+static void check_launch(const char* what = "kernel") {
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) fail(MPSIM_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  if (e == cudaSuccess && sync_debug()) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) fail(MPSIM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
 void DeviceBuf::ensure(size_t b) {
@@ -253,7 +264,7 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
   cplx* ws = (cplx*)s.ws.p;
   CK(cudaMemsetAsync(s.d_frob.p, 0, sizeof(double) * ng, st));
   launch_theta(dg, ng, max_tiles, s.sites, s.stride, s.chi, ws, (double*)s.d_frob.p, st);
-  check_launch();
+  check_launch("theta_kernel");
   ++s.launches;
 
   int* h_rot = (int*)s.h_rot.p;
@@ -267,8 +278,9 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
       launch_jacobi_round(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps,
                           2.0 * kEps, 12, (const double*)s.d_frob.p, (64.0 * kEps) * (64.0 * kEps), st);
       ++s.launches;
+      if (sync_debug()) check_launch("jacobi_round_kernel");
     }
-    check_launch();
+    check_launch("jacobi_round_kernel");
     ++s.sweeps;
     CK(cudaMemcpyAsync(h_rot, s.d_rot.p, sizeof(int) * ng, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -284,10 +296,12 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
     CK(cudaMemcpyAsync(s.d_active.p, s.d_rot.p, sizeof(int) * ng, cudaMemcpyDeviceToDevice, st));
   }
   launch_norms(dg, ng, max_n, ws, (double*)s.d_sigma.p, sig_stride, st);
+  check_launch("norms_kernel");
   launch_truncate(dg, ng, (double*)s.d_sigma.p, (int*)s.d_order.p, sig_stride, (GateOut*)s.d_out.p, st);
+  check_launch("truncate_kernel");
   launch_write_factors(dg, ng, max_m, max_n, ws, (const double*)s.d_sigma.p, (const int*)s.d_order.p, sig_stride,
                        (const GateOut*)s.d_out.p, s.sites, s.stride, s.chi, st);
-  check_launch();
+  check_launch("write_factors");
   s.launches += 4;
   CK(cudaMemcpyAsync(s.h_out.p, s.d_out.p, sizeof(GateOut) * ng, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));

@@ -68,6 +68,12 @@ __global__ void __launch_bounds__(256) jacobi_round_kernel(const GateDesc* __res
     const int v = i < kW ? ba * kW + i : bb * kW + (i - kW);
     return X + (long long)v * mp;
   };
+#ifdef MPSIM_BOUNDS_CHECK
+  if (threadIdx.x == 0 && ((long long)(bb > ba ? bb : ba) * kW + kW > g.n_pad || g.ws_off < 0)) {
+    printf("jacobi OOB: gate %d ba %d bb %d nb %d n_pad %d ws_off %lld\n", gi, ba, bb, nb, g.n_pad, g.ws_off);
+    asm volatile("trap;");
+  }
+#endif
 
   // ---- 1. Gram block
   const int ip = t / 16, jp = t % 16;
@@ -226,18 +232,18 @@ __global__ void __launch_bounds__(256) jacobi_round_kernel(const GateDesc* __res
       }
       __syncthreads();
     }
-    if (!S.any) break;
+    // Every thread must read the flag before thread 0 clears it for the next
+    // sweep, or the CTA would diverge at the barriers.
+    const int any = S.any;
+    __syncthreads();
+    if (!any) break;
   }
-  // Sort eigenvectors by descending eigenvalue (larger vectors to block a).
-  if (t < kP) {
-    const double li = S.G[t * kPad + t].x;
-    int rank = 0;
-    for (int j = 0; j < kP; ++j) {
-      const double lj = S.G[j * kPad + j].x;
-      rank += (lj > li) || (lj == li && j < t);
-    }
-    S.perm[rank] = t;
-  }
+  // The eigenvector order is NOT sorted: R stays a product of small-angle
+  // (|t| <= 1) rotations, close to the identity near convergence. Sorting
+  // would permute R and break the uniformly-bounded-cosine property that
+  // block Jacobi needs to converge (observed: linear convergence and
+  // restarts when sorted). Singular values are sorted once in the epilogue.
+  if (t < kP) S.perm[t] = t;
   __syncthreads();
 
   // ---- 4. apply X_P <- X_P R
