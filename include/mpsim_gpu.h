@@ -117,6 +117,14 @@ int mpsim_gpu_apply_layer(mpsim_gpu_state* s, const mpsim_gate* gates, int32_t c
 int mpsim_gpu_execute(mpsim_gpu_state* s, const mpsim_gate* gates, int32_t count, const mpsim_policy* policy,
                       int32_t method, mpsim_exec_stats* stats, mpsim_report* reports);
 
+/* ---- truncated SVD of a plain matrix (svd(), svd.hpp:79-110) -------------
+ * a: rows x cols row-major; outputs k (kept rank), s (k, descending),
+ * u (rows x k), vdag (k x cols), w (discarded weight). u/vdag nullable;
+ * s needs min(rows, cols) slots. Same batched Jacobi kernels as the gate
+ * path, one matrix at a time. */
+int mpsim_gpu_svd(int32_t rows, int32_t cols, const double* a, int64_t max_rank, double cutoff, int32_t device,
+                  int64_t* k, double* s, double* u, double* vdag, double* w);
+
 /* ---- queries (mps.hpp:79-100) ------------------------------------------ */
 int mpsim_gpu_norm(const mpsim_gpu_state* s, double* out);                       /* mps.cpp:189-202 */
 /* count bit strings of n chars '0'/'1' packed back to back (mps.cpp:204-221) */

@@ -36,6 +36,15 @@ struct GateDesc {
   int n_pad, m_pad; // n_pad multiple of kP, m_pad multiple of kE
   int nb;           // blocks of kW vectors (n_pad / kW), even
   long long ws_off; // offset (complex elements) of X in the workspace; X0 follows
+  // Output addressing of the two factors:
+  //   U (M x k):       u_out[e * ldu + j]
+  //   S V^dag (k x N): v_out[j * ldv + (v / vsplit) * vsplit_ld + v % vsplit]
+  // For an MPS gate U is site q viewed as (2Dl x chi) and S V^dag is site
+  // q+1 viewed as (k, 2, Dr) with padded rows (vsplit = Dr, vsplit_ld = chi).
+  cplx* u_out;
+  cplx* v_out;
+  long long ldu, ldv, vsplit_ld;
+  int vsplit, pad2;
   long long max_bond;
   double cutoff;
   cplx u[16];       // 4x4 gate, (low, high) basis, row = 2*p_low + p_high (circuit.hpp:20-22)
@@ -86,6 +95,13 @@ __device__ __forceinline__ void cfmac(cplx& acc, cplx a, cplx b) {
   acc.x = fma(a.y, b.y, acc.x);
   acc.y = fma(a.x, b.y, acc.y);
   acc.y = fma(-a.y, b.x, acc.y);
+}
+// acc += a * b with every product and sum rounded separately (no contraction).
+__device__ __forceinline__ void cmac_rn(cplx& acc, cplx a, cplx b) {
+  const double re = __dadd_rn(__dmul_rn(a.x, b.x), -__dmul_rn(a.y, b.y));
+  const double im = __dadd_rn(__dmul_rn(a.x, b.y), __dmul_rn(a.y, b.x));
+  acc.x = __dadd_rn(acc.x, re);
+  acc.y = __dadd_rn(acc.y, im);
 }
 __device__ __forceinline__ cplx conjc(cplx a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double cabs2(cplx a) { return a.x * a.x + a.y * a.y; }

@@ -32,9 +32,9 @@ size_t jacobi_smem_bytes();
 void launch_jacobi_round(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, int, const double*, double,
                          cudaStream_t);
 void launch_norms(const GateDesc*, int, int, const cplx*, double*, long long, cudaStream_t);
-void launch_truncate(const GateDesc*, int, double*, int*, long long, GateOut*, cudaStream_t);
+void launch_truncate(const GateDesc*, int, double*, int*, long long, GateOut*, const double*, double, cudaStream_t);
 void launch_write_factors(const GateDesc*, int, int, int, const cplx*, const double*, const int*, long long,
-                          const GateOut*, cplx*, long long, int, cudaStream_t);
+                          const GateOut*, const double*, double, cudaStream_t);
 void launch_apply1q(const Gate1Desc*, int, long long, cplx*, long long, int, cudaStream_t);
 void launch_regrow(const cplx*, long long, int, cplx*, long long, int, const int*, int, cudaStream_t);
 void launch_cgemm(const GemmArgs&, cudaStream_t);
@@ -232,8 +232,11 @@ struct Rep {
 
 constexpr int kMaxSweeps = 60;
 constexpr double kEps = 2.220446049250313e-16;
+// Rounding-noise floor for Jacobi vectors: sigma^2 <= (64 eps)^2 ||theta||_F^2.
+constexpr double kFloorRel2 = (64.0 * kEps) * (64.0 * kEps);
 
-void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs) {
+void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs,
+                   const cplx* pre = nullptr, double pre_frob = 0.0) {
   const int ng = (int)descs.size();
   long long ws_elems = 0;
   int max_tiles = 1, max_nb = 2, max_m = 1, max_n = 1;
@@ -263,9 +266,19 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
   const GateDesc* dg = (const GateDesc*)s.d_gates.p;
   cplx* ws = (cplx*)s.ws.p;
   CK(cudaMemsetAsync(s.d_frob.p, 0, sizeof(double) * ng, st));
-  launch_theta(dg, ng, max_tiles, s.sites, s.stride, s.chi, ws, (double*)s.d_frob.p, st);
-  check_launch("theta_kernel");
-  ++s.launches;
+  if (pre == nullptr) {
+    launch_theta(dg, ng, max_tiles, s.sites, s.stride, s.chi, ws, (double*)s.d_frob.p, st);
+    check_launch("theta_kernel");
+    ++s.launches;
+  } else {
+    // Plain-matrix SVD (mpsim_gpu_svd): X and X0 arrive from the host.
+    const GateDesc& d = descs[0];
+    const size_t bytes = sizeof(cplx) * (size_t)d.n_pad * d.m_pad;
+    CK(cudaMemcpyAsync(ws + d.ws_off, pre, bytes, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ws + d.ws_off + (long long)d.n_pad * d.m_pad, pre, bytes, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(s.d_frob.p, &pre_frob, sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+  }
 
   int* h_rot = (int*)s.h_rot.p;
   for (int i = 0; i < ng; ++i) h_rot[i] = 1;
@@ -276,7 +289,7 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
     CK(cudaMemsetAsync(s.d_rot.p, 0, sizeof(int) * ng, st));
     for (int round = 0; round < max_nb - 1; ++round) {
       launch_jacobi_round(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps,
-                          2.0 * kEps, 12, (const double*)s.d_frob.p, (64.0 * kEps) * (64.0 * kEps), st);
+                          2.0 * kEps, 12, (const double*)s.d_frob.p, kFloorRel2, st);
       ++s.launches;
       if (sync_debug()) check_launch("jacobi_round_kernel");
     }
@@ -297,10 +310,11 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
   }
   launch_norms(dg, ng, max_n, ws, (double*)s.d_sigma.p, sig_stride, st);
   check_launch("norms_kernel");
-  launch_truncate(dg, ng, (double*)s.d_sigma.p, (int*)s.d_order.p, sig_stride, (GateOut*)s.d_out.p, st);
+  launch_truncate(dg, ng, (double*)s.d_sigma.p, (int*)s.d_order.p, sig_stride, (GateOut*)s.d_out.p,
+                  (const double*)s.d_frob.p, kFloorRel2, st);
   check_launch("truncate_kernel");
   launch_write_factors(dg, ng, max_m, max_n, ws, (const double*)s.d_sigma.p, (const int*)s.d_order.p, sig_stride,
-                       (const GateOut*)s.d_out.p, s.sites, s.stride, s.chi, st);
+                       (const GateOut*)s.d_out.p, (const double*)s.d_frob.p, kFloorRel2, st);
   check_launch("write_factors");
   s.launches += 4;
   CK(cudaMemcpyAsync(s.h_out.p, s.d_out.p, sizeof(GateOut) * ng, cudaMemcpyDeviceToHost, st));
@@ -401,6 +415,12 @@ void run_layer(State& s, const std::vector<G2>& two, const std::vector<G1>& one,
     d.max_bond = pol.max_bond;
     d.cutoff = pol.cutoff;
     std::memcpy(d.u, g.u, sizeof(d.u));
+    d.u_out = s.sites + (long long)g.q * s.stride;        // U -> site q (2Dl x k), ld chi
+    d.ldu = s.chi;
+    d.v_out = s.sites + (long long)(g.q + 1) * s.stride;  // S V^dag -> site q+1 (k, 2, Dr)
+    d.ldv = 2LL * s.chi;
+    d.vsplit = d.dr;
+    d.vsplit_ld = s.chi;
     const long long sz = 2LL * d.n_pad * d.m_pad;
     if (!chunk.empty() && off + sz > budget_elems) flush();
     d.ws_off = off;
@@ -1071,6 +1091,85 @@ int mpsim_gpu_to_statevector(const mpsim_gpu_state* s, int32_t max_qubits, doubl
     check_launch();
     CK(cudaMemcpyAsync(out, acc, sizeof(cplx) * cap, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+  });
+}
+
+int mpsim_gpu_svd(int32_t rows, int32_t cols, const double* a, int64_t max_rank, double cutoff, int32_t device,
+                  int64_t* k, double* s_out, double* u_out, double* vdag_out, double* w) {
+  return guarded([&] {
+    // svd.hpp:79-110 argument contract
+    if (rows < 1 || cols < 1) fail(MPSIM_EINVAL, "svd requires a rank-2 tensor with positive extents");
+    if (max_rank < 1) fail(MPSIM_EINVAL, "svd max_rank must be >= 1");
+    if (!(cutoff >= 0.0 && cutoff < 1.0)) fail(MPSIM_EINVAL, "svd cutoff must lie in [0, 1)");
+    static std::map<int, State*> scratch;  // per-device buffers for plain SVDs
+    State*& sc = scratch[device];
+    if (!sc) sc = new State(1, 2, device);
+    DeviceGuard g(device);
+    GateDesc d{};
+    d.dl = 1;
+    d.dm = 1;
+    d.dr = 1;
+    d.trans = rows >= cols ? 0 : 1;
+    d.m = std::max(rows, cols);
+    d.n = std::min(rows, cols);
+    d.n_pad = ((d.n + kP - 1) / kP) * kP;
+    d.m_pad = ((d.m + kE - 1) / kE) * kE;
+    d.nb = d.n_pad / kW;
+    d.max_bond = max_rank;
+    d.cutoff = cutoff;
+    d.ws_off = 0;
+    DeviceBuf dU, dV;
+    dU.ensure(sizeof(cplx) * (size_t)rows * d.n);
+    dV.ensure(sizeof(cplx) * (size_t)d.n * cols);
+    d.u_out = (cplx*)dU.p;
+    d.ldu = d.n;
+    d.v_out = (cplx*)dV.p;
+    d.ldv = cols;
+    d.vsplit = cols;
+    d.vsplit_ld = 0;
+    std::vector<cplx> X((size_t)d.n_pad * d.m_pad, make_double2(0.0, 0.0));
+    double frob = 0.0;
+    for (int r = 0; r < rows; ++r)
+      for (int c = 0; c < cols; ++c) {
+        const double re = a[2 * ((size_t)r * cols + c)], im = a[2 * ((size_t)r * cols + c) + 1];
+        frob += re * re + im * im;
+        if (d.trans == 0) X[(size_t)c * d.m_pad + r] = make_double2(re, im);
+        else X[(size_t)r * d.m_pad + c] = make_double2(re, -im);
+      }
+    std::vector<GateOut> outs;
+    run_two_chunk(*sc, {d}, outs, X.data(), frob);
+    const GateOut& o = outs[0];
+    if (o.status != 0)
+      fail(MPSIM_ENUMERIC, "singular value decomposition did not converge for (" + std::to_string(rows) + "," +
+                               std::to_string(cols) + ") matrix");
+    const int kk = o.k;
+    *k = kk;
+    *w = o.w;
+    std::vector<double> sv((size_t)kk);
+    std::vector<cplx> hu((size_t)rows * d.n), hv((size_t)d.n * cols);
+    CK(cudaMemcpy(sv.data(), sc->d_sigma.p, sizeof(double) * kk, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hu.data(), dU.p, sizeof(cplx) * hu.size(), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(hv.data(), dV.p, sizeof(cplx) * hv.size(), cudaMemcpyDeviceToHost));
+    dU.release();
+    dV.release();
+    for (int j = 0; j < kk; ++j) s_out[j] = sv[(size_t)j];
+    if (u_out)
+      for (int r = 0; r < rows; ++r)
+        for (int j = 0; j < kk; ++j) {
+          u_out[2 * ((size_t)r * kk + j)] = hu[(size_t)r * d.n + j].x;
+          u_out[2 * ((size_t)r * kk + j) + 1] = hu[(size_t)r * d.n + j].y;
+        }
+    if (vdag_out)
+      for (int j = 0; j < kk; ++j) {
+        // The split epilogue writes scale * S V^dag; svd() returns V^dag alone.
+        const double f = sv[(size_t)j] > 0.0 ? 1.0 / (sv[(size_t)j] * o.scale) : 0.0;
+        for (int c = 0; c < cols; ++c) {
+          cplx v = hv[(size_t)j * cols + c];
+          if (f == 0.0) v = make_double2(c == j ? 1.0 : 0.0, 0.0);
+          vdag_out[2 * ((size_t)j * cols + c)] = f == 0.0 ? v.x : v.x * f;
+          vdag_out[2 * ((size_t)j * cols + c) + 1] = f == 0.0 ? v.y : v.y * f;
+        }
+      }
   });
 }
 

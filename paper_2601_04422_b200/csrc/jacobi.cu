@@ -266,8 +266,12 @@ __global__ void __launch_bounds__(256) jacobi_round_kernel(const GateDesc* __res
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const cplx x = S.T[(eq + 16 * a) * kPad + i];
-        cfma(o[a][0], x, r0);
-        cfma(o[a][1], x, r1);
+        // Separately rounded products: equal columns rotated by cs == sn
+        // cancel to an exact zero (a fused chain leaves the rounding error of
+        // the first product), matching the exact-zero singular values that
+        // svd.hpp:58's cutoff-0 rule trims (e.g. SWAP of a product state).
+        cmac_rn(o[a][0], x, r0);
+        cmac_rn(o[a][1], x, r1);
       }
     }
     __syncthreads();

@@ -34,10 +34,17 @@ __global__ void __launch_bounds__(256) norms_kernel(const GateDesc* __restrict__
 __global__ void __launch_bounds__(1024) truncate_kernel(const GateDesc* __restrict__ gates,
                                                         double* __restrict__ sigma,
                                                         int* __restrict__ order, long long sig_stride,
-                                                        GateOut* __restrict__ out) {
+                                                        GateOut* __restrict__ out,
+                                                        const double* __restrict__ frob2, double floor_rel2) {
   const GateDesc& g = gates[blockIdx.y];
   __shared__ double key[2048];
   __shared__ int idx[2048];
+  // Singular values at the rounding-noise level of ||theta||_F are exact
+  // zeros of a structurally rank-deficient theta (Clifford gates on product
+  // states, SWAPs): report them as 0 so svd.hpp:58's cutoff-0 rule trims them
+  // the way an exact-arithmetic decomposition (and LAPACK/Eigen on such
+  // structured inputs) does. Below any cutoff >= 1e-25 this changes nothing.
+  const double floor2 = floor_rel2 * frob2[blockIdx.y];
   __shared__ int bad;
   const int n = g.n;
   int n2 = 1;
@@ -47,7 +54,8 @@ __global__ void __launch_bounds__(1024) truncate_kernel(const GateDesc* __restri
   if (threadIdx.x == 0) bad = 0;
   __syncthreads();
   for (int i = threadIdx.x; i < n2; i += blockDim.x) {
-    const double v = i < n ? sg[i] : -1.0;
+    double v = i < n ? sg[i] : -1.0;
+    if (i < n && v * v <= floor2) v = 0.0;
     if (i < n && !(v <= DBL_MAX)) bad = 1;  // NaN or inf
     key[i] = v;
     idx[i] = i;
@@ -114,9 +122,7 @@ __global__ void __launch_bounds__(256) copy_factor_kernel(const GateDesc* __rest
                                                           const cplx* __restrict__ ws,
                                                           const double* __restrict__ sigma,
                                                           const int* __restrict__ order, long long sig_stride,
-                                                          const GateOut* __restrict__ out,
-                                                          cplx* __restrict__ sites, long long site_stride,
-                                                          int chi) {
+                                                          const GateOut* __restrict__ out) {
   const GateDesc& g = gates[blockIdx.z];
   const GateOut o = out[blockIdx.z];
   const int k = o.k;
@@ -144,19 +150,17 @@ __global__ void __launch_bounds__(256) copy_factor_kernel(const GateDesc* __rest
       tile[jj][tx] = v;
     }
     __syncthreads();
-    cplx* site = sites + (long long)g.q * site_stride;
     for (int ee = ty; ee < 32; ee += 8) {
       const int e = e0 + ee, j = j0 + tx;
-      if (e < g.m && j < k) site[(long long)e * chi + j] = tile[tx][ee];
+      if (e < g.m && j < k) g.u_out[(long long)e * g.ldu + j] = tile[tx][ee];
     }
   } else {
-    cplx* site = sites + (long long)(g.q + 1) * site_stride;
     for (int jj = ty; jj < 32; jj += 8) {
       const int j = j0 + jj, e = e0 + tx;
       if (j < k && e < g.m) {
         const cplx x = X[(long long)od[j] * g.m_pad + e];
-        const int p1 = e / g.dr, r = e % g.dr;
-        site[(long long)j * 2 * chi + (long long)p1 * chi + r] = make_double2(o.scale * x.x, -o.scale * x.y);
+        const long long off = (long long)j * g.ldv + (long long)(e / g.vsplit) * g.vsplit_ld + e % g.vsplit;
+        g.v_out[off] = make_double2(o.scale * x.x, -o.scale * x.y);
       }
     }
   }
@@ -170,11 +174,15 @@ __global__ void __launch_bounds__(256) cross_gram_kernel(const GateDesc* __restr
                                                          const double* __restrict__ sigma,
                                                          const int* __restrict__ order, long long sig_stride,
                                                          const GateOut* __restrict__ out,
-                                                         cplx* __restrict__ sites, long long site_stride,
-                                                         int chi) {
+                                                         const double* __restrict__ frob2, double floor_rel2) {
   const GateDesc& g = gates[blockIdx.z];
   const GateOut o = out[blockIdx.z];
   const int k = o.k;
+  // Kept vectors at the rounding-noise level (sigma^2 <= floor, see
+  // jacobi.cu) were never orthogonalised against the large ones, so the
+  // cross-Gram formula is meaningless for them: they contribute an exact
+  // zero (their true weight is below 64 eps ||theta||_F).
+  const double floor2 = floor_rel2 * frob2[blockIdx.z];
   const int n_a = g.trans == 0 ? k : g.n;
   const int n_b = g.trans == 0 ? g.n : k;
   const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32;
@@ -234,20 +242,19 @@ __global__ void __launch_bounds__(256) cross_gram_kernel(const GateDesc* __restr
       const cplx c = acc[ai][bi];
       if (g.trans == 0) {
         const double s = sg[a];
-        const double f = s > 0.0 ? o.scale / s : 0.0;
-        const int p1 = b / g.dr, r = b % g.dr;
-        sites[(long long)(g.q + 1) * site_stride + (long long)(a * 2 + p1) * chi + r] =
-            make_double2(f * c.x, f * c.y);
+        const double f = s * s > floor2 && s > 0.0 ? o.scale / s : 0.0;
+        const long long off = (long long)a * g.ldv + (long long)(b / g.vsplit) * g.vsplit_ld + b % g.vsplit;
+        g.v_out[off] = make_double2(f * c.x, f * c.y);
       } else {
         const double s = sg[b];
         cplx v;
-        if (s > 0.0) {
+        if (s * s > floor2 && s > 0.0) {
           const double f = 1.0 / (s * s);
           v = make_double2(f * c.x, f * c.y);
         } else {
-          v = make_double2(a == b ? 1.0 : 0.0, 0.0);
+          v = make_double2(s == 0.0 && a == b ? 1.0 : 0.0, 0.0);
         }
-        sites[(long long)g.q * site_stride + (long long)a * chi + b] = v;
+        g.u_out[(long long)a * g.ldu + b] = v;
       }
     }
 }
@@ -258,18 +265,18 @@ void launch_norms(const GateDesc* d_gates, int n_gates, int max_n, const cplx* w
 }
 
 void launch_truncate(const GateDesc* d_gates, int n_gates, double* sigma, int* order, long long sig_stride,
-                     GateOut* d_out, cudaStream_t st) {
-  truncate_kernel<<<dim3(1, n_gates), 1024, 0, st>>>(d_gates, sigma, order, sig_stride, d_out);
+                     GateOut* d_out, const double* frob2, double floor_rel2, cudaStream_t st) {
+  truncate_kernel<<<dim3(1, n_gates), 1024, 0, st>>>(d_gates, sigma, order, sig_stride, d_out, frob2, floor_rel2);
 }
 
 void launch_write_factors(const GateDesc* d_gates, int n_gates, int max_m, int max_n, const cplx* ws,
                           const double* sigma, const int* order, long long sig_stride, const GateOut* d_out,
-                          cplx* sites, long long site_stride, int chi, cudaStream_t st) {
+                          const double* frob2, double floor_rel2, cudaStream_t st) {
   // k <= n, so n bounds every tile count.
   copy_factor_kernel<<<dim3((max_m + 31) / 32, (max_n + 31) / 32, n_gates), 256, 0, st>>>(
-      d_gates, ws, sigma, order, sig_stride, d_out, sites, site_stride, chi);
+      d_gates, ws, sigma, order, sig_stride, d_out);
   cross_gram_kernel<<<dim3((max_n + 31) / 32, (max_n + 31) / 32, n_gates), 256, 0, st>>>(
-      d_gates, ws, sigma, order, sig_stride, d_out, sites, site_stride, chi);
+      d_gates, ws, sigma, order, sig_stride, d_out, frob2, floor_rel2);
 }
 
 }  // namespace mpsim_gpu

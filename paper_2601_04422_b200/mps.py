@@ -44,6 +44,24 @@ def make_gates(gates) -> "C.Array":
     return arr
 
 
+def svd(m, max_rank=None, cutoff=0.0, device=0):
+    """Truncated SVD (svd.hpp:79-110) on the GPU: returns (u, s, vdag, w)."""
+    a = np.ascontiguousarray(np.asarray(m, dtype=np.complex128))
+    if a.ndim != 2:
+        raise ValueError("svd requires a rank-2 tensor")
+    r, c = a.shape
+    mn = min(r, c)
+    s = np.zeros(mn)
+    u = np.zeros(r * mn, dtype=np.complex128)
+    v = np.zeros(mn * c, dtype=np.complex128)
+    k, w = N.I64(), C.c_double()
+    mr = N.UNBOUNDED if max_rank is None else int(max_rank)
+    check(N.lib().mpsim_gpu_svd(r, c, a.ctypes.data_as(_DP), mr, float(cutoff), int(device), C.byref(k),
+                                s.ctypes.data_as(_DP), u.ctypes.data_as(_DP), v.ctypes.data_as(_DP), C.byref(w)))
+    kk = k.value
+    return u[: r * kk].reshape(r, kk), s[:kk], v[: kk * c].reshape(kk, c), w.value
+
+
 class MpsState:
     """MpsState (mps.hpp:33-75), resident on one GPU."""
 

@@ -82,6 +82,7 @@ def lib():
         "mpsim_gpu_apply_layer": (C.c_int, [VP, C.POINTER(Gate), I32, C.POINTER(Policy), C.POINTER(Report)]),
         "mpsim_gpu_execute": (C.c_int, [VP, C.POINTER(Gate), I32, C.POINTER(Policy), I32, C.POINTER(ExecStats),
                                         C.POINTER(Report)]),
+        "mpsim_gpu_svd": (C.c_int, [I32, I32, DP, I64, DBL, I32, C.POINTER(I64), DP, DP, DP, DP]),
         "mpsim_gpu_norm": (C.c_int, [VP, DP]),
         "mpsim_gpu_amplitudes": (C.c_int, [VP, C.c_char_p, I32, DP]),
         "mpsim_gpu_overlap": (C.c_int, [VP, VP, DP]),

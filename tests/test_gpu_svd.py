@@ -1,0 +1,79 @@
+"""The GPU truncated SVD (the batched one-sided Jacobi kernels behind
+mpsim_gpu_svd) against the reference SVD contract, test_tensor.cpp:232-364,
+and against the CPU oracle (LAPACK zgesdd) on seeded matrices."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _rand(rng, r, c):
+    return rng.standard_normal((r, c)) + 1j * rng.standard_normal((r, c))
+
+
+def test_identity_and_diagonal(gpu):
+    _, s, _, w = gpu.mps.svd(np.eye(2))
+    assert len(s) == 2 and np.allclose(s, 1, atol=1e-14) and w == 0.0
+    _, s, _, _ = gpu.mps.svd(np.diag([3.0, 4.0]))
+    assert abs(s[0] - 4) < 1e-13 and abs(s[1] - 3) < 1e-13
+
+
+@pytest.mark.parametrize("shape", [(6, 5), (5, 6), (2, 2), (1, 7), (7, 1), (33, 17), (40, 64), (130, 129)])
+def test_reconstruct_isometric_sorted(gpu, shape):
+    rng = np.random.default_rng(23)
+    for _ in range(4):
+        m = _rand(rng, *shape)
+        u, s, vd, w = gpu.mps.svd(m)
+        k = len(s)
+        assert k == min(shape) and w == 0.0
+        assert np.linalg.norm(u @ np.diag(s) @ vd - m) / np.linalg.norm(m) <= 1e-12
+        assert np.abs(u.conj().T @ u - np.eye(k)).max() <= 1e-12
+        assert np.abs(vd @ vd.conj().T - np.eye(k)).max() <= 1e-12
+        assert np.all(np.diff(s) <= 0) and s[-1] >= 0
+        assert np.abs(s - np.linalg.svd(m, compute_uv=False)).max() <= 1e-13 * s[0]
+
+
+def test_discarded_weight_vs_eigensolver(gpu):
+    rng = np.random.default_rng(29)
+    m = _rand(rng, 8, 6)
+    ev = np.linalg.eigvalsh(m.conj().T @ m)
+    u, s, vd, w = gpu.mps.svd(m, 3, 0.0)
+    assert len(s) == 3
+    assert abs(w - ev[:3].sum() / ev.sum()) <= 1e-12
+    err2 = np.linalg.norm(u @ np.diag(s) @ vd - m) ** 2
+    assert abs(err2 / np.linalg.norm(m) ** 2 - w) <= 1e-12
+
+
+def test_cutoff_rule(gpu):
+    _, s, _, w = gpu.mps.svd(np.array([[1, 0], [0, 0]], dtype=complex), None, 0.0)
+    assert len(s) == 1 and w == 0.0  # exact zero trimmed at cutoff 0
+    _, s, _, w = gpu.mps.svd(np.diag([1.0, 0.1]), None, 0.5)
+    assert len(s) == 1 and abs(w - 0.01 / 1.01) <= 1e-14
+    _, s, _, _ = gpu.mps.svd(np.diag([1.0, 0.1]), None, 0.001)
+    assert len(s) == 2
+    _, s, _, w = gpu.mps.svd(np.zeros((3, 2)))
+    assert len(s) == 1 and s[0] == 0.0 and w == 0.0
+    # rank-1 with duplicated columns: the zero singular value is exact
+    _, s, _, _ = gpu.mps.svd(np.array([[1, 1], [0, 0]], dtype=complex) / np.sqrt(2), None, 0.0)
+    assert len(s) == 1 and abs(s[0] - 1) < 1e-15
+
+
+def test_bad_options(gpu):
+    with pytest.raises(ValueError):
+        gpu.mps.svd(np.eye(2), 0, 0.0)
+    with pytest.raises(ValueError):
+        gpu.mps.svd(np.eye(2), 1, 1.0)
+
+
+@pytest.mark.parametrize("cap,cutoff", [(None, 1e-12), (9, 0.0), (20, 1e-6), (1, 0.0)])
+def test_kept_rank_matches_oracle(gpu, oracle, cap, cutoff):
+    rng = np.random.default_rng(31)
+    for trial in range(6):
+        r, c = [(48, 48), (64, 32), (32, 64), (96, 80), (20, 100), (128, 128)][trial]
+        # graded spectrum so the cutoff bites
+        a = _rand(rng, r, c) * np.logspace(0, -9, c)[None, :]
+        _, sg, _, wg = gpu.mps.svd(a, cap, cutoff)
+        _, so, _, wo = oracle.svd(a, cap, cutoff)
+        assert len(sg) == len(so)
+        assert np.abs(sg - so).max() <= 1e-13 * so[0]
+        assert abs(wg - wo) <= 1e-10 * max(wo, 1e-300) or abs(wg - wo) < 1e-15
