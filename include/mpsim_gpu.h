@@ -98,6 +98,16 @@ int mpsim_gpu_validate(const mpsim_gpu_state* s); /* mps.cpp:150-169 */
 int mpsim_gpu_get_site(const mpsim_gpu_state* s, int32_t i, int64_t* dl, int64_t* dr, double* out);
 int mpsim_gpu_set_site(mpsim_gpu_state* s, int32_t i, int64_t dl, int64_t dr, const double* data);
 
+/* ---- site-sharded chains (multi-GPU) -----------------------
+ * A shard holds a contiguous site range of a longer chain, so its boundary
+ * bonds may exceed 1 (validate then skips the "boundary bonds are 1" check).
+ * Boundary sites move between shards as whole padded slots (chi x 2 x chi
+ * complex128, contiguous) over NCCL; site_slot exposes the device address of
+ * a slot and set_site_dims records the extents of a slot written that way. */
+int mpsim_gpu_set_open_boundaries(mpsim_gpu_state* s, int32_t open);
+int mpsim_gpu_site_slot(const mpsim_gpu_state* s, int32_t i, void** device_ptr, int64_t* chi);
+int mpsim_gpu_set_site_dims(mpsim_gpu_state* s, int32_t i, int64_t dl, int64_t dr);
+
 /* ---- gate application (gate_apply.hpp:48-78) --------------------------- */
 int mpsim_gpu_apply_1q(mpsim_gpu_state* s, const double* u2x2, int32_t q, mpsim_report* rep);
 /* apply_2q_local (q1 == q0+1), apply_2q_swap / apply_2q_bondprop otherwise. */
@@ -155,6 +165,14 @@ int mpsim_gpu_sampler_clear_cache(mpsim_gpu_sampler* sp);
 /* Kernel launches and device time accumulated on the state's stream since
  * the last reset (bench.py's gpu_launches / roofline legs). */
 int mpsim_gpu_counters(const mpsim_gpu_state* s, int64_t* launches, double* device_ms, int64_t* svd_sweeps);
+/* The dominant kernel's share: jacobi_round_kernel launches and their
+ * CUDA-event time, and the algorithmic flops of the work done (SURVEY 8(d):
+ * svd = 32 M N^2 per decomposed theta, gate = full F_2q per applied gate). */
+int mpsim_gpu_kernel_counters(const mpsim_gpu_state* s, int64_t* jacobi_launches, double* jacobi_ms,
+                              double* svd_flops, double* gate_flops);
+/* Host<->device bytes moved by the gate path (descriptors in, reports and
+ * convergence flags out) since the last reset. */
+int mpsim_gpu_transfer_counters(const mpsim_gpu_state* s, int64_t* h2d_bytes, int64_t* d2h_bytes);
 int mpsim_gpu_reset_counters(mpsim_gpu_state* s);
 int mpsim_gpu_synchronize(mpsim_gpu_state* s);
 

@@ -132,6 +132,8 @@ State::State(int n_, long long chi_hint, int dev) : n(n_), device(dev) {
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   CK(cudaEventCreate(&ev0));
   CK(cudaEventCreate(&ev1));
+  CK(cudaEventCreate(&evj0));
+  CK(cudaEventCreate(&evj1));
   static bool inited = false;
   if (!inited) {
     jacobi_init();
@@ -168,6 +170,8 @@ State::~State() {
   for (PinnedBuf* b : {&h_gates, &h_out, &h_rot, &h_g1, &h_small}) b->release();
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
+  cudaEventDestroy(evj0);
+  cudaEventDestroy(evj1);
   cudaStreamDestroy(st);
 }
 
@@ -262,6 +266,7 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
   std::memcpy(s.h_gates.p, descs.data(), sizeof(GateDesc) * ng);
   cudaStream_t st = s.st;
   CK(cudaMemcpyAsync(s.d_gates.p, s.h_gates.p, sizeof(GateDesc) * ng, cudaMemcpyHostToDevice, st));
+  s.h2d_bytes += (long long)sizeof(GateDesc) * ng + (long long)sizeof(int) * ng;
   CK(cudaMemsetAsync(s.ws.p, 0, (size_t)ws_elems * sizeof(cplx), st));
   const GateDesc* dg = (const GateDesc*)s.d_gates.p;
   cplx* ws = (cplx*)s.ws.p;
@@ -287,16 +292,25 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
   std::vector<int> still(ng, 1);
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
     CK(cudaMemsetAsync(s.d_rot.p, 0, sizeof(int) * ng, st));
+    CK(cudaEventRecord(s.evj0, st));
     for (int round = 0; round < max_nb - 1; ++round) {
       launch_jacobi_round(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps,
                           2.0 * kEps, 12, (const double*)s.d_frob.p, kFloorRel2, st);
       ++s.launches;
+      ++s.jacobi_launches;
       if (sync_debug()) check_launch("jacobi_round_kernel");
     }
+    CK(cudaEventRecord(s.evj1, st));
     check_launch("jacobi_round_kernel");
     ++s.sweeps;
     CK(cudaMemcpyAsync(h_rot, s.d_rot.p, sizeof(int) * ng, cudaMemcpyDeviceToHost, st));
+    s.d2h_bytes += (long long)sizeof(int) * ng;
     CK(cudaStreamSynchronize(st));
+    {
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, s.evj0, s.evj1));
+      s.jacobi_ms += ms;
+    }
     bool any = false;
     for (int i = 0; i < ng; ++i) {
       still[i] = h_rot[i];
@@ -318,8 +332,15 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
   check_launch("write_factors");
   s.launches += 4;
   CK(cudaMemcpyAsync(s.h_out.p, s.d_out.p, sizeof(GateOut) * ng, cudaMemcpyDeviceToHost, st));
+  s.d2h_bytes += (long long)sizeof(GateOut) * ng;
   CK(cudaStreamSynchronize(st));
   outs.assign((GateOut*)s.h_out.p, (GateOut*)s.h_out.p + ng);
+  for (const GateDesc& d : descs) {
+    // F_2q = 32 Dl Dm Dr + 128 Dl Dr + 32 M N^2 (M = max, N = min of 2Dl, 2Dr)
+    const double M = d.m, N = d.n;
+    s.svd_flops += 32.0 * M * N * N;
+    if (pre == nullptr) s.gate_flops += 32.0 * d.dl * (double)d.dm * d.dr + 128.0 * d.dl * (double)d.dr + 32.0 * M * N * N;
+  }
   if (!converged)
     for (int i = 0; i < ng; ++i)
       if (still[i]) outs[i].status = 3;
@@ -347,6 +368,7 @@ void run_layer(State& s, const std::vector<G2>& two, const std::vector<G1>& one,
       reports[g.idx] = r;
     }
     CK(cudaMemcpyAsync(s.d_g1.p, h, sizeof(Gate1Desc) * ng, cudaMemcpyHostToDevice, st));
+    s.h2d_bytes += (long long)sizeof(Gate1Desc) * ng;
     launch_apply1q((const Gate1Desc*)s.d_g1.p, ng, max_elems, s.sites, s.stride, s.chi, st);
     check_launch();
     ++s.launches;
@@ -733,11 +755,37 @@ int mpsim_gpu_set_bond_dim(mpsim_gpu_state* s, int32_t i, int64_t d) {
   });
 }
 
+int mpsim_gpu_set_open_boundaries(mpsim_gpu_state* s, int32_t open) {
+  return guarded([&] { S(s).open_boundaries = open != 0; });
+}
+
+int mpsim_gpu_site_slot(const mpsim_gpu_state* s, int32_t i, void** device_ptr, int64_t* chi) {
+  return guarded([&] {
+    const State& a = S(s);
+    if (i < 0 || i >= a.n) fail(MPSIM_EINVAL, "site index out of range");
+    *device_ptr = (void*)(a.sites + (long long)i * a.stride);
+    *chi = a.chi;
+  });
+}
+
+int mpsim_gpu_set_site_dims(mpsim_gpu_state* s, int32_t i, int64_t dl, int64_t dr) {
+  return guarded([&] {
+    State& a = S(s);
+    if (i < 0 || i >= a.n) fail(MPSIM_EINVAL, "site index out of range");
+    if (dl < 1 || dr < 1 || dl > a.chi || dr > a.chi) fail(MPSIM_EINVAL, "site extents outside the slot");
+    a.sdl[i] = dl;
+    a.sdr[i] = dr;
+    a.bonds[(size_t)i] = dl;
+    a.bonds[(size_t)i + 1] = dr;
+  });
+}
+
 int mpsim_gpu_validate(const mpsim_gpu_state* s) {  // mps.cpp:150-169
   return guarded([&] {
     const State& a = S(s);
     if (a.bonds.size() != (size_t)a.n + 1) fail(MPSIM_ELOGIC, "bond bookkeeping has wrong length");
-    if (a.bonds.front() != 1 || a.bonds.back() != 1) fail(MPSIM_ELOGIC, "boundary bonds must have dimension 1");
+    if (!a.open_boundaries && (a.bonds.front() != 1 || a.bonds.back() != 1))
+      fail(MPSIM_ELOGIC, "boundary bonds must have dimension 1");
     for (int i = 0; i < a.n; ++i)
       if (a.sdl[i] != a.bonds[i] || a.sdr[i] != a.bonds[i + 1])
         fail(MPSIM_ELOGIC, "site " + std::to_string(i) + " disagrees with recorded bond dimensions");
@@ -1182,12 +1230,37 @@ int mpsim_gpu_counters(const mpsim_gpu_state* s, int64_t* launches, double* devi
   });
 }
 
+int mpsim_gpu_kernel_counters(const mpsim_gpu_state* s, int64_t* jacobi_launches, double* jacobi_ms,
+                              double* svd_flops, double* gate_flops) {
+  return guarded([&] {
+    const State& a = S(s);
+    if (jacobi_launches) *jacobi_launches = a.jacobi_launches;
+    if (jacobi_ms) *jacobi_ms = a.jacobi_ms;
+    if (svd_flops) *svd_flops = a.svd_flops;
+    if (gate_flops) *gate_flops = a.gate_flops;
+  });
+}
+
 int mpsim_gpu_reset_counters(mpsim_gpu_state* s) {
   return guarded([&] {
     State& a = S(s);
     a.launches = 0;
     a.device_ms = 0.0;
     a.sweeps = 0;
+    a.jacobi_launches = 0;
+    a.jacobi_ms = 0.0;
+    a.svd_flops = 0.0;
+    a.gate_flops = 0.0;
+    a.h2d_bytes = 0;
+    a.d2h_bytes = 0;
+  });
+}
+
+int mpsim_gpu_transfer_counters(const mpsim_gpu_state* s, int64_t* h2d_bytes, int64_t* d2h_bytes) {
+  return guarded([&] {
+    const State& a = S(s);
+    if (h2d_bytes) *h2d_bytes = a.h2d_bytes;
+    if (d2h_bytes) *d2h_bytes = a.d2h_bytes;
   });
 }
 

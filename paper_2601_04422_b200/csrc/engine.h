@@ -50,6 +50,7 @@ struct State {
   std::vector<long long> bonds;   // n+1
   std::vector<long long> sdl, sdr;  // site extents
   int center = -1;
+  bool open_boundaries = false;  // shard of a longer chain (multi-GPU)
   cudaStream_t st = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // workspaces
@@ -59,6 +60,12 @@ struct State {
   long long launches = 0;
   double device_ms = 0.0;
   long long sweeps = 0;
+  long long jacobi_launches = 0;  // jacobi_round_kernel launches
+  double jacobi_ms = 0.0;         // CUDA-event time of those launches
+  double svd_flops = 0.0;         // algorithmic SVD flops of the decomposed matrices (32 M N^2)
+  double gate_flops = 0.0;        // algorithmic F_2q of applied gates
+  cudaEvent_t evj0 = nullptr, evj1 = nullptr;
+  long long h2d_bytes = 0, d2h_bytes = 0;  // gate-path host<->device traffic
 
   State(int n, long long chi_hint, int device);
   ~State();

@@ -138,6 +138,19 @@ class MpsState:
             raise ValueError("site must be a (left, 2, right) tensor")
         check(N.lib().mpsim_gpu_set_site(self._h, int(i), t.shape[0], t.shape[2], t.ctypes.data_as(_DP)))
 
+    # ---- shard plumbing (multi-GPU chains)
+    def set_open_boundaries(self, open_=True):
+        check(N.lib().mpsim_gpu_set_open_boundaries(self._h, 1 if open_ else 0))
+
+    def site_slot(self, i):
+        """(device pointer, chi) of site i's padded (chi, 2, chi) slot."""
+        p, chi = C.c_void_p(), N.I64()
+        check(N.lib().mpsim_gpu_site_slot(self._h, int(i), C.byref(p), C.byref(chi)))
+        return p.value, chi.value
+
+    def set_site_dims(self, i, dl, dr):
+        check(N.lib().mpsim_gpu_set_site_dims(self._h, int(i), int(dl), int(dr)))
+
     def total_elements(self) -> int:
         b = self.bond_dims()
         return int(sum(b[i] * 2 * b[i + 1] for i in range(self.n)))
@@ -234,7 +247,13 @@ class MpsState:
     def counters(self):
         l, ms, sw = N.I64(), C.c_double(), N.I64()
         check(N.lib().mpsim_gpu_counters(self._h, C.byref(l), C.byref(ms), C.byref(sw)))
-        return dict(launches=l.value, device_ms=ms.value, sweeps=sw.value)
+        jl, jms, sf, gf = N.I64(), C.c_double(), C.c_double(), C.c_double()
+        check(N.lib().mpsim_gpu_kernel_counters(self._h, C.byref(jl), C.byref(jms), C.byref(sf), C.byref(gf)))
+        h2d, d2h = N.I64(), N.I64()
+        check(N.lib().mpsim_gpu_transfer_counters(self._h, C.byref(h2d), C.byref(d2h)))
+        return dict(launches=l.value, device_ms=ms.value, sweeps=sw.value, jacobi_launches=jl.value,
+                    jacobi_ms=jms.value, svd_flops=sf.value, gate_flops=gf.value, h2d_bytes=h2d.value,
+                    d2h_bytes=d2h.value)
 
     def reset_counters(self):
         check(N.lib().mpsim_gpu_reset_counters(self._h))

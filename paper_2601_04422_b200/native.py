@@ -77,6 +77,9 @@ def lib():
         "mpsim_gpu_validate": (C.c_int, [VP]),
         "mpsim_gpu_get_site": (C.c_int, [VP, I32, C.POINTER(I64), C.POINTER(I64), DP]),
         "mpsim_gpu_set_site": (C.c_int, [VP, I32, I64, I64, DP]),
+        "mpsim_gpu_set_open_boundaries": (C.c_int, [VP, I32]),
+        "mpsim_gpu_site_slot": (C.c_int, [VP, I32, C.POINTER(VP), C.POINTER(I64)]),
+        "mpsim_gpu_set_site_dims": (C.c_int, [VP, I32, I64, I64]),
         "mpsim_gpu_apply_1q": (C.c_int, [VP, DP, I32, C.POINTER(Report)]),
         "mpsim_gpu_apply_2q": (C.c_int, [VP, DP, I32, I32, I32, C.POINTER(Policy), C.POINTER(Report)]),
         "mpsim_gpu_apply_layer": (C.c_int, [VP, C.POINTER(Gate), I32, C.POINTER(Policy), C.POINTER(Report)]),
@@ -97,6 +100,8 @@ def lib():
         "mpsim_gpu_sampler_stats": (C.c_int, [VP, C.POINTER(U64), C.POINTER(U64)]),
         "mpsim_gpu_sampler_clear_cache": (C.c_int, [VP]),
         "mpsim_gpu_counters": (C.c_int, [VP, C.POINTER(I64), DP, C.POINTER(I64)]),
+        "mpsim_gpu_kernel_counters": (C.c_int, [VP, C.POINTER(I64), DP, DP, DP]),
+        "mpsim_gpu_transfer_counters": (C.c_int, [VP, C.POINTER(I64), C.POINTER(I64)]),
         "mpsim_gpu_reset_counters": (C.c_int, [VP]),
         "mpsim_gpu_synchronize": (C.c_int, [VP]),
     }

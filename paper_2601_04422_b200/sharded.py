@@ -1,0 +1,162 @@
+"""Contiguous site sharding of one MPS chain across GPUs.
+
+Rank r owns sites [lo, hi) with even boundaries, so even brick layers never
+straddle a shard and odd layers straddle at exactly world-1 gates. A shard
+that is not the last keeps one extra "ghost" slot after its last site. For a
+layer with a gate on (hi-1, hi):
+  1. rank r+1 sends its first site (a whole padded slot, NCCL send/recv over
+     NVLink) and its extents to rank r, which records it in the ghost slot;
+  2. every rank applies its own gates (the straddling one included on rank r)
+     as one batched launch sequence;
+  3. rank r sends the updated ghost site (k, 2, Dr) back; rank r+1 stores it
+     as its first site, whose left bond is now k.
+Gates are disjoint within a layer, so this reproduces the single-GPU result
+gate for gate: the per-gate inputs never change with the shard count.
+torch.distributed is only plumbing here: it carries the slot bytes; all the
+arithmetic runs in libmpsim_gpu.so.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import native as N
+from .mps import MpsState, execute
+
+
+def shard_bounds(n: int, world: int):
+    """Even-aligned contiguous ranges [b_r, b_{r+1})."""
+    b = [0]
+    for r in range(1, world):
+        x = int(round(r * n / world))
+        x -= x % 2
+        b.append(max(b[-1] + 2, x))
+    b.append(n)
+    return b
+
+
+class _CudaArray:
+    """__cuda_array_interface__ view of a device slot, for torch.as_tensor."""
+
+    def __init__(self, ptr, nelem):
+        self.__cuda_array_interface__ = {"shape": (nelem,), "typestr": "<c16", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+class ShardedChain:
+    def __init__(self, n, chi, rank=0, world=1, device=0, dist=None):
+        self.n, self.chi, self.rank, self.world, self.dist = n, chi, rank, world, dist
+        b = shard_bounds(n, world)
+        self.lo, self.hi = b[rank], b[rank + 1]
+        self.has_right = rank < world - 1
+        self.n_local = self.hi - self.lo + (1 if self.has_right else 0)
+        self.state = MpsState(self.n_local, chi_hint=chi, device=device)
+        if world > 1:
+            self.state.set_open_boundaries(True)
+        self.device = device
+        self._torch = None
+        if world > 1:
+            import torch
+            self._torch = torch
+
+    # ---- setup
+    def set_site(self, i, t):
+        assert self.lo <= i < self.hi
+        self.state.set_site(i - self.lo, t)
+
+    def finalize_setup(self):
+        """Give the ghost slot extents consistent with the last owned bond."""
+        if self.has_right:
+            b = self.state.bond_dims()
+            self.state.set_site_dims(self.n_local - 1, int(b[self.hi - self.lo]), 1)
+
+    # ---- plumbing
+    def _slot_tensor(self, local_i):
+        ptr, chi = self.state.site_slot(local_i)
+        return self._torch.as_tensor(_CudaArray(ptr, chi * 2 * chi), device=f"cuda:{self.device}")
+
+    def barrier(self):
+        if self.world > 1:
+            self._torch.cuda.synchronize()
+            self.dist.barrier()
+        self.state.synchronize()
+
+    def max_over_ranks(self, x: float) -> float:
+        if self.world == 1:
+            return x
+        t = self._torch.tensor([x], dtype=self._torch.float64, device=f"cuda:{self.device}")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def _exchange_in(self, straddle_left, straddle_right):
+        """Step 1: ghost <- first site of the right neighbour."""
+        torch, dist = self._torch, self.dist
+        ops = []
+        if straddle_left:  # my first site goes to rank-1
+            b = self.state.bond_dims()
+            dims = torch.tensor([b[0], b[1]], dtype=torch.int64, device=f"cuda:{self.device}")
+            ops += [dist.P2POp(dist.isend, dims, self.rank - 1), dist.P2POp(dist.isend, self._slot_tensor(0),
+                                                                          self.rank - 1)]
+        if straddle_right:
+            self._dims_in = torch.zeros(2, dtype=torch.int64, device=f"cuda:{self.device}")
+            ops += [dist.P2POp(dist.irecv, self._dims_in, self.rank + 1),
+                    dist.P2POp(dist.irecv, self._slot_tensor(self.n_local - 1), self.rank + 1)]
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+            torch.cuda.synchronize()
+        if straddle_right:
+            dl, dr = (int(x) for x in self._dims_in.tolist())
+            self.state.set_site_dims(self.n_local - 1, dl, dr)
+
+    def _exchange_out(self, straddle_left, straddle_right):
+        """Step 3: updated ghost -> first site of the right neighbour."""
+        torch, dist = self._torch, self.dist
+        ops = []
+        if straddle_right:
+            b = self.state.bond_dims()
+            dims = torch.tensor([b[-2], b[-1]], dtype=torch.int64, device=f"cuda:{self.device}")
+            ops += [dist.P2POp(dist.isend, dims, self.rank + 1),
+                    dist.P2POp(dist.isend, self._slot_tensor(self.n_local - 1), self.rank + 1)]
+        if straddle_left:
+            dims_in = torch.zeros(2, dtype=torch.int64, device=f"cuda:{self.device}")
+            ops += [dist.P2POp(dist.irecv, dims_in, self.rank - 1),
+                    dist.P2POp(dist.irecv, self._slot_tensor(0), self.rank - 1)]
+        if ops:
+            for r in dist.batch_isend_irecv(ops):
+                r.wait()
+            torch.cuda.synchronize()
+        if straddle_left:
+            dl, dr = (int(x) for x in dims_in.tolist())
+            self.state.set_site_dims(0, dl, dr)
+
+    # ---- one layer of disjoint gates in global site indices
+    def apply_layer(self, gates, max_bond=None, cutoff=0.0):
+        local = []
+        straddle_left = straddle_right = False
+        for (q0, q1, u) in gates:
+            a, b = min(q0, q1), max(q0, q1)
+            if self.lo <= a and b < self.hi:
+                local.append((q0 - self.lo, q1 - self.lo, u))
+            elif self.has_right and a == self.hi - 1 and b == self.hi:
+                local.append((q0 - self.lo, q1 - self.lo, u))
+                straddle_right = True
+            elif self.rank > 0 and a == self.lo - 1 and b == self.lo:
+                straddle_left = True
+        if self.world > 1:
+            self._exchange_in(straddle_left, straddle_right)
+        st = execute(self.state, local, max_bond, cutoff) if local else dict(device_ms=0.0)
+        if self.world > 1:
+            self._exchange_out(straddle_left, straddle_right)
+        return st
+
+    def bond_dims(self):
+        """Bonds of the owned range [lo, hi]."""
+        return self.state.bond_dims()[: self.hi - self.lo + 1]
+
+    def counters(self):
+        return self.state.counters()
+
+    def reset_counters(self):
+        self.state.reset_counters()
