@@ -44,13 +44,15 @@ __device__ __forceinline__ void pair_of(int step, int k, int M, int& a, int& b) 
   }
 }
 
-__global__ void __launch_bounds__(256) jacobi_round_kernel(const GateDesc* __restrict__ gates,
+__global__ void __launch_bounds__(256, 2) jacobi_round_kernel(const GateDesc* __restrict__ gates,
                                                            cplx* __restrict__ ws,
                                                            const int* __restrict__ active,
                                                            int* __restrict__ rotated, int round,
                                                            double tol, double tol_in, int max_in,
                                                            const double* __restrict__ frob2,
-                                                           double floor_rel2) {
+                                                           double floor_rel2,
+                                                           const int* __restrict__ perm,
+                                                           long long perm_stride) {
   const int gi = blockIdx.y;
   if (!active[gi]) return;
   const GateDesc& g = gates[gi];
@@ -64,9 +66,12 @@ __global__ void __launch_bounds__(256) jacobi_round_kernel(const GateDesc* __res
   const int t = threadIdx.x;
   const long long mp = g.m_pad;
   cplx* X = ws + g.ws_off;
+  // Slot -> vector map of this sweep (de Rijk ordering: vectors sorted by
+  // decreasing norm at the start of every sweep).
+  const int* pm = perm + gi * perm_stride;
   auto vec = [&](int i) -> cplx* {
-    const int v = i < kW ? ba * kW + i : bb * kW + (i - kW);
-    return X + (long long)v * mp;
+    const int slot = i < kW ? ba * kW + i : bb * kW + (i - kW);
+    return X + (long long)pm[slot] * mp;
   };
 #ifdef MPSIM_BOUNDS_CHECK
   if (threadIdx.x == 0 && ((long long)(bb > ba ? bb : ba) * kW + kW > g.n_pad || g.ws_off < 0)) {
@@ -76,12 +81,14 @@ __global__ void __launch_bounds__(256) jacobi_round_kernel(const GateDesc* __res
 #endif
 
   // ---- 1. Gram block
-  const int ip = t / 16, jp = t % 16;
-  cplx acc[2][2];
+  // Split-K over 4 thread groups; each group of 64 threads holds the whole
+  // 32x32 block as 4x4 register tiles (8 shared loads per 16 complex MACs).
+  const int kg = t / 64, tg = t % 64, ti = tg / 8, tj = tg % 8;
+  cplx acc[4][4];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 2; ++b) acc[a][b] = make_double2(0.0, 0.0);
+    for (int b = 0; b < 4; ++b) acc[a][b] = make_double2(0.0, 0.0);
   for (int e0 = 0; e0 < g.m_pad; e0 += kE) {
 #pragma unroll
     for (int s = 0; s < (kP * kE) / 256; ++s) {
@@ -90,23 +97,35 @@ __global__ void __launch_bounds__(256) jacobi_round_kernel(const GateDesc* __res
       S.T[ee * kPad + vi] = vec(vi)[e0 + ee];
     }
     __syncthreads();
-#pragma unroll 8
-    for (int ee = 0; ee < kE; ++ee) {
+#pragma unroll 4
+    for (int ee = kg; ee < kE; ee += 4) {
       const cplx* row = S.T + ee * kPad;
-      const cplx a0 = row[2 * ip], a1 = row[2 * ip + 1];
-      const cplx b0 = row[2 * jp], b1 = row[2 * jp + 1];
-      cfmac(acc[0][0], a0, b0);
-      cfmac(acc[0][1], a0, b1);
-      cfmac(acc[1][0], a1, b0);
-      cfmac(acc[1][1], a1, b1);
+      cplx av[4], bv[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) av[x] = row[ti + 8 * x];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bv[y] = row[tj + 8 * y];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) cfmac(acc[x][y], av[x], bv[y]);
     }
     __syncthreads();
   }
+  // Reduce the four partial Gram blocks group by group.
+  for (int grp = 0; grp < 4; ++grp) {
+    if (kg == grp) {
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+      for (int x = 0; x < 4; ++x)
 #pragma unroll
-    for (int b = 0; b < 2; ++b) S.G[(2 * ip + a) * kPad + 2 * jp + b] = acc[a][b];
-  __syncthreads();
+        for (int y = 0; y < 4; ++y) {
+          cplx* gp = S.G + (ti + 8 * x) * kPad + tj + 8 * y;
+          *gp = grp == 0 ? acc[x][y] : cadd(*gp, acc[x][y]);
+        }
+    }
+    __syncthreads();
+  }
+  const int ip = t / 16, jp = t % 16;
 
   // ---- 2. convergence test on the true columns (tol scales with sqrt(m),
   // the dot-product rounding level, like LAPACK zgesvj's ctol = sqrt(m)).
@@ -266,12 +285,8 @@ __global__ void __launch_bounds__(256) jacobi_round_kernel(const GateDesc* __res
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const cplx x = S.T[(eq + 16 * a) * kPad + i];
-        // Separately rounded products: equal columns rotated by cs == sn
-        // cancel to an exact zero (a fused chain leaves the rounding error of
-        // the first product), matching the exact-zero singular values that
-        // svd.hpp:58's cutoff-0 rule trims (e.g. SWAP of a product state).
-        cmac_rn(o[a][0], x, r0);
-        cmac_rn(o[a][1], x, r1);
+        cfma(o[a][0], x, r0);
+        cfma(o[a][1], x, r1);
       }
     }
     __syncthreads();
@@ -301,9 +316,71 @@ void jacobi_init() {
 
 void launch_jacobi_round(const GateDesc* d_gates, int n_gates, int max_pairs, cplx* ws,
                          const int* d_active, int* d_rotated, int round, double tol, double tol_in,
-                         int max_in, const double* frob2, double floor_rel2, cudaStream_t st) {
+                         int max_in, const double* frob2, double floor_rel2, const int* perm,
+                         long long perm_stride, cudaStream_t st) {
   jacobi_round_kernel<<<dim3(max_pairs, n_gates), 256, sizeof(JacobiSmem), st>>>(
-      d_gates, ws, d_active, d_rotated, round, tol, tol_in, max_in, frob2, floor_rel2);
+      d_gates, ws, d_active, d_rotated, round, tol, tol_in, max_in, frob2, floor_rel2, perm, perm_stride);
+}
+
+// ---- de Rijk ordering: per gate, sort the n_pad vector slots by decreasing
+// norm (zero padding last). One CTA per gate; n_pad <= 2048.
+__global__ void __launch_bounds__(1024) derijk_kernel(const GateDesc* __restrict__ gates,
+                                                      const cplx* __restrict__ ws, const int* __restrict__ active,
+                                                      int* __restrict__ perm, long long perm_stride) {
+  const int gi = blockIdx.x;
+  const GateDesc& g = gates[gi];
+  if (!active[gi]) return;
+  __shared__ double key[2048];
+  __shared__ int idx[2048];
+  const int n2 = g.n_pad;  // multiple of 32; pad to a power of two below
+  int p2 = 1;
+  while (p2 < n2) p2 <<= 1;
+  const cplx* X = ws + g.ws_off;
+  // norms: one warp per vector
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  for (int v = warp; v < p2; v += blockDim.x / 32) {
+    double s = -1.0;
+    if (v < g.n) {
+      s = 0.0;
+      const cplx* x = X + (long long)v * g.m_pad;
+      for (int e = lane; e < g.m; e += 32) s += cabs2(x[e]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    } else if (v < n2) {
+      s = -0.5;  // zero padding vectors: after every real vector
+    }
+    if (lane == 0) {
+      key[v] = s;
+      idx[v] = v;
+    }
+  }
+  __syncthreads();
+  for (int size = 2; size <= p2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+        const int j = i ^ stride;
+        if (j > i) {
+          const bool desc = ((i & size) == 0);
+          const double ki = key[i], kj = key[j];
+          const int ii = idx[i], ij = idx[j];
+          const bool i_first = (ki > kj) || (ki == kj && ii < ij);
+          if (desc != i_first) {
+            key[i] = kj;
+            key[j] = ki;
+            idx[i] = ij;
+            idx[j] = ii;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int i = threadIdx.x; i < n2; i += blockDim.x) perm[gi * perm_stride + i] = idx[i];
+}
+
+void launch_derijk(const GateDesc* d_gates, int n_gates, const cplx* ws, const int* d_active, int* perm,
+                   long long perm_stride, cudaStream_t st) {
+  derijk_kernel<<<n_gates, 1024, 0, st>>>(d_gates, ws, d_active, perm, perm_stride);
 }
 
 }  // namespace mpsim_gpu
