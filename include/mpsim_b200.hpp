@@ -1,0 +1,340 @@
+// mpsim_b200.hpp — header-only C++ facade of the B200 engine with the
+// reference simulator's API (namespace mpsim; /root/reference/proj/include/
+// mpsim/{tensor,mps,gate_apply,executor,sampler,errors}.hpp). A caller of the
+// reference switches the include path and links libmpsim_gpu.so; names,
+// argument meaning and exception types are kept:
+//   std::invalid_argument  <- MPSIM_EINVAL
+//   mpsim::NumericError    <- MPSIM_ENUMERIC
+//   std::logic_error       <- MPSIM_ELOGIC
+//   std::runtime_error     <- MPSIM_ECUDA
+// Differences, by design: the state lives in HBM, so MpsState::site(i)
+// returns a host copy (write back with set_site) instead of a mutable
+// reference (mps.hpp:45-46); execute_parallel's `workers` only selects the
+// batched launch path (every layer is one launch sequence).
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <limits>
+#include <map>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <string_view>
+#include <vector>
+
+#include "mpsim_gpu.h"
+
+namespace mpsim {
+
+using Index = std::int64_t;
+using Complex = std::complex<double>;
+inline constexpr Index kUnbounded = std::numeric_limits<Index>::max();  // tensor.hpp:44
+
+class NumericError : public std::runtime_error {  // errors.hpp:45-48
+ public:
+  using std::runtime_error::runtime_error;
+};
+
+namespace detail {
+inline void check(int rc) {
+  if (rc == MPSIM_OK) return;
+  const std::string msg = mpsim_gpu_last_error();
+  switch (rc) {
+    case MPSIM_EINVAL: throw std::invalid_argument(msg);
+    case MPSIM_ENUMERIC: throw NumericError(msg);
+    case MPSIM_ELOGIC: throw std::logic_error(msg);
+    default: throw std::runtime_error(msg);
+  }
+}
+}  // namespace detail
+
+// Minimal dense row-major tensor (tensor.hpp:66-152) for gates and site copies.
+class CTensor {
+ public:
+  CTensor() : data_(1) {}
+  explicit CTensor(std::vector<Index> shape) : shape_(std::move(shape)) { data_.assign(count(), Complex{}); }
+  CTensor(std::vector<Index> shape, std::vector<Complex> data) : shape_(std::move(shape)), data_(std::move(data)) {
+    if (static_cast<Index>(data_.size()) != count()) throw std::invalid_argument("tensor data length mismatch");
+  }
+  int rank() const { return static_cast<int>(shape_.size()); }
+  const std::vector<Index>& shape() const { return shape_; }
+  Index extent(int a) const { return shape_.at(static_cast<size_t>(a)); }
+  Index size() const { return static_cast<Index>(data_.size()); }
+  Complex* data() { return data_.data(); }
+  const Complex* data() const { return data_.data(); }
+  Complex& operator[](Index i) { return data_[static_cast<size_t>(i)]; }
+  const Complex& operator[](Index i) const { return data_[static_cast<size_t>(i)]; }
+
+ private:
+  Index count() const {
+    Index n = 1;
+    for (Index e : shape_) {
+      if (e <= 0) throw std::invalid_argument("tensor extents must be positive");
+      n *= e;
+    }
+    return n;
+  }
+  std::vector<Index> shape_;
+  std::vector<Complex> data_;
+};
+
+struct TruncationPolicy {  // gate_apply.hpp:35-38
+  Index max_bond = kUnbounded;
+  double cutoff = 0.0;
+};
+
+struct ApplyReport {  // gate_apply.hpp:40-44
+  double discarded_weight = 0.0;
+  Index new_bond = 1;
+  int svd_count = 0;
+};
+
+enum class NonlocalMethod { Swap, BondProp };  // gate_apply.hpp:71
+
+struct FusedGate {  // circuit.hpp:71-81
+  int q0 = 0;
+  int q1 = -1;
+  bool flipped = false;
+  CTensor matrix;
+  bool two_qubit() const { return q1 >= 0; }
+  bool local() const { return !two_qubit() || q1 == q0 + 1; }
+};
+
+struct LayerPlan {  // circuit.hpp:85-95
+  std::vector<std::vector<FusedGate>> layers;
+};
+
+struct ExecStats {  // executor.hpp:44-57 (per-layer timing replaced by device time)
+  Index peak_bond = 1;
+  double total_discarded_weight = 0.0;
+  int layers = 0;
+  double device_ms = 0.0;
+};
+
+class MpsState {  // mps.hpp:33-75
+ public:
+  explicit MpsState(int n_qubits, Index chi_hint = 16, int device = 0) {
+    detail::check(mpsim_gpu_state_create(n_qubits, chi_hint, device, &h_));
+  }
+  MpsState(const MpsState& o) { detail::check(mpsim_gpu_state_copy(o.h_, &h_)); }
+  MpsState& operator=(const MpsState& o) {
+    if (this != &o) {
+      mpsim_gpu_state* n = nullptr;
+      detail::check(mpsim_gpu_state_copy(o.h_, &n));
+      mpsim_gpu_state_destroy(h_);
+      h_ = n;
+    }
+    return *this;
+  }
+  MpsState(MpsState&& o) noexcept : h_(o.h_) { o.h_ = nullptr; }
+  MpsState& operator=(MpsState&& o) noexcept {
+    std::swap(h_, o.h_);
+    return *this;
+  }
+  ~MpsState() {
+    if (h_) mpsim_gpu_state_destroy(h_);
+  }
+
+  int num_qubits() const {
+    int32_t n = 0;
+    detail::check(mpsim_gpu_num_qubits(h_, &n));
+    return n;
+  }
+  std::vector<Index> bond_dims() const {
+    std::vector<Index> b(static_cast<size_t>(num_qubits()) + 1);
+    detail::check(mpsim_gpu_bond_dims(h_, b.data()));
+    return b;
+  }
+  Index bond_dim(int i) const { return bond_dims().at(static_cast<size_t>(i)); }
+  void set_bond_dim(int i, Index d) { detail::check(mpsim_gpu_set_bond_dim(h_, i, d)); }
+  Index max_bond_dim() const {
+    Index m = 0;
+    for (Index b : bond_dims()) m = b > m ? b : m;
+    return m;
+  }
+  std::optional<int> ortho_center() const {
+    int32_t c = -1;
+    detail::check(mpsim_gpu_ortho_center(h_, &c));
+    return c < 0 ? std::nullopt : std::optional<int>(c);
+  }
+  void set_ortho_center(std::optional<int> c) { detail::check(mpsim_gpu_set_ortho_center(h_, c.value_or(-1))); }
+  void validate() const { detail::check(mpsim_gpu_validate(h_)); }
+  Index total_elements() const {
+    const auto b = bond_dims();
+    Index t = 0;
+    for (size_t i = 0; i + 1 < b.size(); ++i) t += b[i] * 2 * b[i + 1];
+    return t;
+  }
+  // Host copy of site i, shape (Dl, 2, Dr).
+  CTensor site(int i) const {
+    int64_t dl = 0, dr = 0;
+    detail::check(mpsim_gpu_get_site(h_, i, &dl, &dr, nullptr));
+    CTensor t({dl, 2, dr});
+    detail::check(mpsim_gpu_get_site(h_, i, &dl, &dr, reinterpret_cast<double*>(t.data())));
+    return t;
+  }
+  void set_site(int i, const CTensor& t) {
+    if (t.rank() != 3 || t.extent(1) != 2) throw std::invalid_argument("site must be (left, 2, right)");
+    detail::check(mpsim_gpu_set_site(h_, i, t.extent(0), t.extent(2), reinterpret_cast<const double*>(t.data())));
+  }
+  mpsim_gpu_state* handle() const { return h_; }
+
+ private:
+  mpsim_gpu_state* h_ = nullptr;
+};
+
+inline ApplyReport to_report(const mpsim_report& r) { return ApplyReport{r.discarded_weight, r.new_bond, r.svd_count}; }
+
+inline ApplyReport apply_1q(MpsState& s, const CTensor& u, int q) {  // gate_apply.cpp:99-110
+  if (u.rank() != 2 || u.extent(0) != 2 || u.extent(1) != 2) throw std::invalid_argument("gate matrix must be 2x2");
+  mpsim_report r{};
+  detail::check(mpsim_gpu_apply_1q(s.handle(), reinterpret_cast<const double*>(u.data()), q, &r));
+  return to_report(r);
+}
+
+inline ApplyReport apply_2q(MpsState& s, const CTensor& u, int q0, int q1, const TruncationPolicy& p, int method) {
+  if (u.rank() != 2 || u.extent(0) != 4 || u.extent(1) != 4) throw std::invalid_argument("gate matrix must be 4x4");
+  mpsim_policy pol{p.max_bond, p.cutoff};
+  mpsim_report r{};
+  detail::check(mpsim_gpu_apply_2q(s.handle(), reinterpret_cast<const double*>(u.data()), q0, q1, method, &pol, &r));
+  return to_report(r);
+}
+
+inline ApplyReport apply_2q_local(MpsState& s, const CTensor& u, int q, const TruncationPolicy& p) {
+  if (q < 0 || q + 1 >= s.num_qubits()) throw std::invalid_argument("adjacent pair out of range");
+  return apply_2q(s, u, q, q + 1, p, MPSIM_NONLOCAL_SWAP);  // gate_apply.cpp:112-147
+}
+inline ApplyReport apply_2q_swap(MpsState& s, const CTensor& u, int q0, int q1, const TruncationPolicy& p) {
+  return apply_2q(s, u, q0, q1, p, MPSIM_NONLOCAL_SWAP);  // gate_apply.cpp:149-179
+}
+inline ApplyReport apply_2q_bondprop(MpsState& s, const CTensor& u, int q0, int q1, const TruncationPolicy& p) {
+  return apply_2q(s, u, q0, q1, p, MPSIM_NONLOCAL_BONDPROP);  // gate_apply.cpp:181-255
+}
+inline ApplyReport apply_gate(MpsState& s, const FusedGate& g, const TruncationPolicy& p,
+                              NonlocalMethod m = NonlocalMethod::Swap) {  // gate_apply.cpp:257-268
+  if (!g.two_qubit()) return apply_1q(s, g.matrix, g.q0);
+  return apply_2q(s, g.matrix, g.q0, g.q1, p, m == NonlocalMethod::Swap ? MPSIM_NONLOCAL_SWAP : MPSIM_NONLOCAL_BONDPROP);
+}
+
+inline std::vector<mpsim_gate> to_abi(const std::vector<FusedGate>& gates) {
+  std::vector<mpsim_gate> out(gates.size());
+  for (size_t i = 0; i < gates.size(); ++i) {
+    const FusedGate& g = gates[i];
+    out[i].q0 = g.q0;
+    out[i].q1 = g.two_qubit() ? g.q1 : -1;
+    const double* d = reinterpret_cast<const double*>(g.matrix.data());
+    for (Index k = 0; k < 2 * g.matrix.size() && k < 32; ++k) out[i].u[k] = d[k];
+  }
+  return out;
+}
+
+// execute_serial (executor.cpp:73-97): layered batched launches, same result.
+inline ExecStats execute_serial(MpsState& s, const std::vector<FusedGate>& gates, const TruncationPolicy& p,
+                                NonlocalMethod m = NonlocalMethod::Swap) {
+  const auto abi = to_abi(gates);
+  mpsim_policy pol{p.max_bond, p.cutoff};
+  mpsim_exec_stats st{};
+  detail::check(mpsim_gpu_execute(s.handle(), abi.data(), static_cast<int32_t>(abi.size()), &pol,
+                                  m == NonlocalMethod::Swap ? MPSIM_NONLOCAL_SWAP : MPSIM_NONLOCAL_BONDPROP, &st,
+                                  nullptr));
+  return ExecStats{st.peak_bond, st.total_discarded_weight, st.layers, st.device_ms};
+}
+
+// execute_parallel (executor.cpp:99-232): each layer is one batched launch sequence.
+inline ExecStats execute_parallel(MpsState& s, const LayerPlan& plan, const TruncationPolicy& p, int workers) {
+  if (workers < 1) throw std::invalid_argument("worker count must be >= 1");
+  std::vector<FusedGate> flat;
+  for (const auto& layer : plan.layers)
+    for (const FusedGate& g : layer) {
+      if (!g.local()) throw std::invalid_argument("parallel execution requires a local-gate plan");
+      flat.push_back(g);
+    }
+  return execute_serial(s, flat, p, NonlocalMethod::Swap);
+}
+
+inline void move_center(MpsState& s, int c) { detail::check(mpsim_gpu_move_center(s.handle(), c)); }
+inline void left_canonicalize(MpsState& s) { move_center(s, s.num_qubits() - 1); }
+inline void right_canonicalize(MpsState& s) { move_center(s, 0); }
+
+inline double norm(const MpsState& s) {
+  double v = 0.0;
+  detail::check(mpsim_gpu_norm(s.handle(), &v));
+  return v;
+}
+inline Complex amplitude(const MpsState& s, std::string_view bits) {
+  if (static_cast<int>(bits.size()) != s.num_qubits()) throw std::invalid_argument("bit string length mismatch");
+  double out[2];
+  detail::check(mpsim_gpu_amplitudes(s.handle(), bits.data(), 1, out));
+  return {out[0], out[1]};
+}
+inline Complex overlap(const MpsState& a, const MpsState& b) {
+  double out[2];
+  detail::check(mpsim_gpu_overlap(a.handle(), b.handle(), out));
+  return {out[0], out[1]};
+}
+inline std::vector<Complex> to_statevector(const MpsState& s, int max_qubits = 20) {
+  const int n = s.num_qubits();
+  if (n > max_qubits) throw std::invalid_argument("statevector export capped");
+  std::vector<Complex> v(size_t{1} << n);
+  detail::check(mpsim_gpu_to_statevector(s.handle(), max_qubits, reinterpret_cast<double*>(v.data())));
+  return v;
+}
+
+struct ShotResult {  // sampler.hpp:39-43
+  std::map<std::string, std::uint64_t> counts;
+  std::uint64_t shots = 0;
+  std::uint64_t seed = 0;
+};
+struct SamplerOptions {
+  bool memoize = true;
+  std::size_t max_cache_entries = 0;
+};
+
+class Sampler {  // sampler.hpp:50-86
+ public:
+  explicit Sampler(const MpsState& s, SamplerOptions o = {}) : n_(s.num_qubits()) {
+    detail::check(mpsim_gpu_sampler_create(s.handle(), o.memoize ? 1 : 0, o.max_cache_entries, &h_));
+  }
+  Sampler(const Sampler&) = delete;
+  Sampler& operator=(const Sampler&) = delete;
+  ~Sampler() {
+    if (h_) mpsim_gpu_sampler_destroy(h_);
+  }
+  ShotResult sample(std::uint64_t shots, std::uint64_t seed) {
+    int32_t unique = 0;
+    detail::check(mpsim_gpu_sample(h_, shots, seed, &unique));
+    ShotResult r;
+    r.shots = shots;
+    r.seed = seed;
+    std::string bits(static_cast<size_t>(n_), '0');
+    for (int i = 0; i < unique; ++i) {
+      std::uint64_t c = 0;
+      detail::check(mpsim_gpu_sampler_result(h_, i, bits.data(), &c));
+      r.counts[bits] = c;
+    }
+    return r;
+  }
+  void clear_cache() { detail::check(mpsim_gpu_sampler_clear_cache(h_)); }
+  std::size_t cache_size() const {
+    uint64_t hits = 0, size = 0;
+    detail::check(mpsim_gpu_sampler_stats(h_, &hits, &size));
+    return size;
+  }
+  std::uint64_t cache_hits() const {
+    uint64_t hits = 0, size = 0;
+    detail::check(mpsim_gpu_sampler_stats(h_, &hits, &size));
+    return hits;
+  }
+
+ private:
+  int n_;
+  mpsim_gpu_sampler* h_ = nullptr;
+};
+
+inline ShotResult sample(const MpsState& s, std::uint64_t shots, std::uint64_t seed, SamplerOptions o = {}) {
+  Sampler sp(s, o);
+  return sp.sample(shots, seed);
+}
+
+}  // namespace mpsim

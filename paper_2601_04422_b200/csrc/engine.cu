@@ -47,6 +47,11 @@ Error::Error(int c, std::string m) : std::runtime_error(std::move(m)), code(c) {
 
 [[noreturn]] void fail(int code, const std::string& msg) { throw Error(code, msg); }
 
+std::string& last_error_slot() {
+  thread_local std::string s;
+  return s;
+}
+
 #define CK(x)                                                                              \
   do {                                                                                     \
     cudaError_t e_ = (x);                                                                  \
@@ -667,7 +672,8 @@ cd chain_contract(State& a, const State& b, const std::map<int, const cd*>& ops)
 // ============================================================== C ABI
 
 namespace {
-thread_local std::string g_err;
+// The calling thread's message slot (shared with the sampler translation unit).
+#define g_err (last_error_slot())
 
 template <class F>
 int guarded(F&& f) {
@@ -1027,6 +1033,10 @@ int mpsim_gpu_execute(mpsim_gpu_state* s, const mpsim_gate* gates, int32_t count
     // executor.cpp:93 validates the final state.
     if (mpsim_gpu_validate(s) != MPSIM_OK) fail(MPSIM_ELOGIC, g_err);
   });
+}
+
+int mpsim_gpu_move_center(mpsim_gpu_state* s, int32_t center) {  // mps.cpp:177-187
+  return guarded([&] { move_center_impl(S(s), center); });
 }
 
 int mpsim_gpu_norm(const mpsim_gpu_state* s, double* out) {

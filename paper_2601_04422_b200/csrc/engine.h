@@ -16,6 +16,7 @@ struct Error : std::runtime_error {
   Error(int c, std::string m);
 };
 [[noreturn]] void fail(int code, const std::string& msg);
+std::string& last_error_slot();  // mpsim_gpu_last_error() of the calling thread
 
 struct DeviceBuf {
   void* p = nullptr;
@@ -74,5 +75,8 @@ struct State {
   void grow(int new_chi);
   void launch_fill_sites_zero_state();
 };
+
+// QR sweeps of move_center (canon.cu).
+void move_center_impl(State& s, int center);
 
 }  // namespace mpsim_gpu

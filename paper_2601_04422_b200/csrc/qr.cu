@@ -1,0 +1,231 @@
+// Blocked Householder QR for orthogonality-centre moves (thin_qr, mps.cpp:57-65;
+// sweep_left_of / sweep_right_of, mps.cpp:69-95).
+//
+// A (m x n, row-major, ld) is factored in place LAPACK-style (zgeqrf): panels
+// of 32 columns are factored by one CTA (Householder vectors below the
+// diagonal, R on and above it, tau, and the compact-WY T factor of the panel,
+// Q_panel = I - V T V^H); the trailing matrix is updated with three complex
+// GEMMs, A2 <- (I - V T^H V^H) A2. The thin Q (m x k, k = min(m, n)) is then
+// formed by applying the block reflectors to [I; 0] in reverse order.
+#include "common.cuh"
+
+namespace mpsim_gpu {
+
+constexpr int kQB = 32;  // panel width
+
+// Factor panel columns [c0, c0 + jb) of A (row-major, ld), rows [c0, m).
+// Writes: A (R part + Householder vectors below the diagonal), V (explicit,
+// row-major (m - c0) x kQB, unit diagonal, zeros above), T (kQB x kQB,
+// row-major, upper triangular), tau[c0 + j].
+__global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, long long lda, int m, int c0, int jb,
+                                                        cplx* __restrict__ P, cplx* __restrict__ V,
+                                                        cplx* __restrict__ T, cplx* __restrict__ tau) {
+  const int L = m - c0;  // rows in the panel
+  const int t = threadIdx.x, warp = t / 32, lane = t % 32, nw = blockDim.x / 32;
+  // P: column-major panel copy, column j at P + j * L.
+  for (int idx = t; idx < L * jb; idx += blockDim.x) {
+    const int r = idx / jb, j = idx % jb;
+    P[(long long)j * L + r] = A[(long long)(c0 + r) * lda + c0 + j];
+  }
+  __shared__ double red[32];
+  __shared__ cplx s_tau, s_beta;
+  __shared__ cplx z[kQB];
+  __shared__ cplx Ts[kQB][kQB + 1];
+  for (int i = t; i < kQB * (kQB + 1); i += blockDim.x) Ts[i / (kQB + 1)][i % (kQB + 1)] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int j = 0; j < jb; ++j) {
+    cplx* x = P + (long long)j * L;
+    // ||x[j+1:]||^2
+    double s = 0.0;
+    for (int r = j + 1 + t; r < L; r += blockDim.x) s += cabs2(x[r]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    if (t == 0) {
+      double xn2 = 0.0;
+      for (int w = 0; w < nw; ++w) xn2 += red[w];
+      const cplx alpha = x[j];
+      cplx tv = make_double2(0.0, 0.0), beta = alpha;
+      if (!(xn2 == 0.0 && alpha.y == 0.0)) {  // zlarfg
+        const double b = -copysign(sqrt(cabs2(alpha) + xn2), alpha.x);
+        tv = make_double2((b - alpha.x) / b, -alpha.y / b);
+        beta = make_double2(b, 0.0);
+      }
+      s_tau = tv;
+      s_beta = beta;
+    }
+    __syncthreads();
+    const cplx tv = s_tau, beta = s_beta, alpha = x[j];
+    if (tv.x != 0.0 || tv.y != 0.0) {
+      // v = x / (alpha - beta) below the diagonal
+      const cplx d = make_double2(alpha.x - beta.x, alpha.y - beta.y);
+      const double dd = cabs2(d);
+      const cplx inv = make_double2(d.x / dd, -d.y / dd);
+      for (int r = j + 1 + t; r < L; r += blockDim.x) x[r] = cmul(x[r], inv);
+    }
+    __syncthreads();
+    if (t == 0) {
+      x[j] = beta;
+      tau[c0 + j] = tv;
+    }
+    __syncthreads();
+    // apply H^H = I - conj(tau) v v^H to panel columns j+1..jb-1 (one warp per column)
+    if (tv.x != 0.0 || tv.y != 0.0) {
+      for (int c = j + 1 + warp; c < jb; c += nw) {
+        cplx* y = P + (long long)c * L;
+        cplx w = lane == 0 ? y[j] : make_double2(0.0, 0.0);
+        for (int r = j + 1 + lane; r < L; r += 32) cfmac(w, x[r], y[r]);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          w.x += __shfl_xor_sync(0xffffffffu, w.x, o);
+          w.y += __shfl_xor_sync(0xffffffffu, w.y, o);
+        }
+        const cplx f = cmul(conjc(tv), w);  // conj(tau) * (v^H y)
+        if (lane == 0) y[j] = make_double2(y[j].x - f.x, y[j].y - f.y);
+        for (int r = j + 1 + lane; r < L; r += 32) {
+          const cplx u = cmul(x[r], f);
+          y[r] = make_double2(y[r].x - u.x, y[r].y - u.y);
+        }
+      }
+    }
+    // T column j: T[0:j, j] = -tau_j T[0:j, 0:j] (V[:, 0:j]^H v_j)  (zlarft, forward)
+    for (int l = warp; l < j; l += nw) {
+      const cplx* vl = P + (long long)l * L;
+      cplx acc = make_double2(0.0, 0.0);
+      // v_j has an implicit 1 at row j and zeros above; v_l has its stored entries below l.
+      if (lane == 0) acc = conjc(vl[j]);
+      for (int r = j + 1 + lane; r < L; r += 32) cfmac(acc, vl[r], x[r]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      if (lane == 0) z[l] = acc;
+    }
+    __syncthreads();
+    if (t < j) {
+      cplx acc = make_double2(0.0, 0.0);
+      for (int l = t; l < j; ++l) cfma(acc, Ts[t][l], z[l]);
+      const cplx v = cmul(acc, tv);
+      Ts[t][j] = make_double2(-v.x, -v.y);
+    }
+    if (t == 0) Ts[j][j] = tv;
+    __syncthreads();
+  }
+  // write back the panel, the explicit V and T
+  for (int idx = t; idx < L * jb; idx += blockDim.x) {
+    const int r = idx / jb, j = idx % jb;
+    const cplx p = P[(long long)j * L + r];
+    A[(long long)(c0 + r) * lda + c0 + j] = p;
+    V[(long long)r * kQB + j] = r > j ? p : make_double2(r == j ? 1.0 : 0.0, 0.0);
+  }
+  for (int idx = t; idx < L * (kQB - jb); idx += blockDim.x) {
+    const int r = idx / (kQB - jb), j = jb + idx % (kQB - jb);
+    V[(long long)r * kQB + j] = make_double2(0.0, 0.0);
+  }
+  for (int idx = t; idx < kQB * kQB; idx += blockDim.x) T[idx] = Ts[idx / kQB][idx % kQB];
+}
+
+// Y (m x k, row-major ld) = [I_k; 0]
+__global__ void set_identity_kernel(cplx* Y, long long ld, int m, int k) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)m * k;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / k), c = (int)(i % k);
+    Y[(long long)r * ld + c] = make_double2(r == c ? 1.0 : 0.0, 0.0);
+  }
+}
+
+// dst (rows x cols, ld_d) = op(src): op 0 copy, 1 conjugate transpose
+// (src is cols x rows then), 2 upper-triangular copy (zeros below diagonal).
+__global__ void copy_matrix_kernel(const cplx* __restrict__ src, long long ld_s, cplx* __restrict__ dst,
+                                   long long ld_d, int rows, int cols, int op) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)rows * cols;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / cols), c = (int)(i % cols);
+    cplx v;
+    if (op == 1) {
+      v = src[(long long)c * ld_s + r];
+      v.y = -v.y;
+    } else {
+      v = src[(long long)r * ld_s + c];
+      if (op == 2 && c < r) v = make_double2(0.0, 0.0);
+    }
+    dst[(long long)r * ld_d + c] = v;
+  }
+}
+
+// Right-sweep operand: A[e][l] = conj(site[(l*2+p)*chi + r]), e = p*dr + r
+// (the (Dl x 2Dr)^H matricisation, mps.cpp:84-95).
+__global__ void site_adjoint_kernel(const cplx* __restrict__ site, int chi, int dl, int dr, cplx* __restrict__ A,
+                                    long long lda) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)dl * 2 * dr;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int l = (int)(i / (2 * dr)), e = (int)(i % (2 * dr));
+    const int p = e / dr, r = e % dr;
+    cplx v = site[(long long)(l * 2 + p) * chi + r];
+    v.y = -v.y;
+    A[(long long)e * lda + l] = v;
+  }
+}
+
+// site[(j*2+p)*chi + r] = conj(Q[e][j]), e = p*dr + r, j < k  (site i <- Q^H)
+__global__ void site_from_adjoint_kernel(const cplx* __restrict__ Q, long long ldq, int k, int dr,
+                                         cplx* __restrict__ site, int chi) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)k * 2 * dr;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i / (2 * dr)), e = (int)(i % (2 * dr));
+    const int p = e / dr, r = e % dr;
+    cplx v = Q[(long long)e * ldq + j];
+    v.y = -v.y;
+    site[(long long)(j * 2 + p) * chi + r] = v;
+  }
+}
+
+__global__ void sum_abs2_kernel(const cplx* __restrict__ A, long long lda, int rows, int cols, double* out) {
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < (long long)rows * cols; i += blockDim.x) {
+    const int r = (int)(i / cols), c = (int)(i % cols);
+    s += cabs2(A[(long long)r * lda + c]);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ double red[32];
+  if (threadIdx.x % 32 == 0) red[threadIdx.x / 32] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) t += red[w];
+    *out = t;
+  }
+}
+
+static unsigned blocks_for(long long n) {
+  long long b = (n + 255) / 256;
+  if (b < 1) b = 1;
+  if (b > 4096) b = 4096;
+  return (unsigned)b;
+}
+
+void launch_qr_panel(cplx* A, long long lda, int m, int c0, int jb, cplx* P, cplx* V, cplx* T, cplx* tau,
+                     cudaStream_t st) {
+  qr_panel_kernel<<<1, 1024, 0, st>>>(A, lda, m, c0, jb, P, V, T, tau);
+}
+void launch_set_identity(cplx* Y, long long ld, int m, int k, cudaStream_t st) {
+  set_identity_kernel<<<blocks_for((long long)m * k), 256, 0, st>>>(Y, ld, m, k);
+}
+void launch_copy_matrix(const cplx* src, long long ld_s, cplx* dst, long long ld_d, int rows, int cols, int op,
+                        cudaStream_t st) {
+  copy_matrix_kernel<<<blocks_for((long long)rows * cols), 256, 0, st>>>(src, ld_s, dst, ld_d, rows, cols, op);
+}
+void launch_site_adjoint(const cplx* site, int chi, int dl, int dr, cplx* A, long long lda, cudaStream_t st) {
+  site_adjoint_kernel<<<blocks_for((long long)dl * 2 * dr), 256, 0, st>>>(site, chi, dl, dr, A, lda);
+}
+void launch_site_from_adjoint(const cplx* Q, long long ldq, int k, int dr, cplx* site, int chi, cudaStream_t st) {
+  site_from_adjoint_kernel<<<blocks_for((long long)k * 2 * dr), 256, 0, st>>>(Q, ldq, k, dr, site, chi);
+}
+void launch_sum_abs2(const cplx* A, long long lda, int rows, int cols, double* out, cudaStream_t st) {
+  sum_abs2_kernel<<<1, 1024, 0, st>>>(A, lda, rows, cols, out);
+}
+
+}  // namespace mpsim_gpu

@@ -1,0 +1,31 @@
+"""The header-only C++ facade (include/mpsim_b200.hpp) compiles against the C
+ABI here, and runs its reference-style known answers on the GPU."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SRC = os.path.join(ROOT, "tests", "cpp", "facade_test.cpp")
+LIBDIR = os.path.join(ROOT, "paper_2601_04422_b200")
+OUT = os.path.join(ROOT, "tests", "cpp", "facade_test")
+
+
+def _compile():
+    subprocess.run(["g++", "-std=c++17", "-O1", "-I", os.path.join(ROOT, "include"), "-I", "/usr/local/cuda/include",
+                    SRC, "-o", OUT, "-L", LIBDIR, "-lmpsim_gpu", f"-Wl,-rpath,{LIBDIR}"], check=True)
+
+
+def test_facade_compiles():
+    if not os.path.exists(os.path.join(LIBDIR, "libmpsim_gpu.so")):
+        subprocess.run(["make", "-s", "-C", os.path.join(LIBDIR, "csrc"), "-j8"], check=True)
+    _compile()
+    assert os.path.exists(OUT)
+
+
+@pytest.mark.gpu
+def test_facade_runs_on_gpu():
+    _compile()
+    out = subprocess.run([OUT], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    assert "facade ok" in out.stdout

@@ -1,0 +1,126 @@
+"""GPU orthogonality-centre moves (blocked Householder QR sweeps) and the
+batched-shot perfect sampler against the reference's known answers
+(test_mps.cpp:138-198, test_sampler.cpp) and the CPU oracle."""
+import numpy as np
+import pytest
+
+from tests.helpers import CX, HAD, copy_state_to_gpu, max_dev
+
+pytestmark = pytest.mark.gpu
+
+
+def _left_defect(t):
+    a = t.reshape(-1, t.shape[2])
+    return np.abs(a.conj().T @ a - np.eye(a.shape[1])).max()
+
+
+def _right_defect(t):
+    b = t.reshape(t.shape[0], -1)
+    return np.abs(b @ b.conj().T - np.eye(b.shape[0])).max()
+
+
+def test_canonicalization_isometries_and_state(gpu, oracle):
+    zero = gpu.MpsState(4)
+    before = zero.to_statevector()
+    zero.left_canonicalize()
+    assert max_dev(before, zero.to_statevector()) <= 1e-12 and zero.ortho_center == 3
+    for seed in range(40, 46):
+        o = oracle.MpsState.random(6, 8, seed)
+        g = copy_state_to_gpu(gpu, o)
+        ref = o.to_statevector()
+        g.left_canonicalize()
+        o.move_center(5)
+        g.validate()
+        assert g.ortho_center == 5
+        assert (g.bond_dims() == o.bond_dims()).all()  # k = min(2Dl, Dr) may shrink bonds
+        for i in range(5):
+            assert _left_defect(g.site(i)) <= 1e-11
+        assert max_dev(ref, g.to_statevector()) <= 1e-11
+        assert abs(g.norm() - 1) <= 1e-12
+        g.right_canonicalize()
+        o.move_center(0)
+        assert g.ortho_center == 0 and (g.bond_dims() == o.bond_dims()).all()
+        for i in range(1, 6):
+            assert _right_defect(g.site(i)) <= 1e-11
+        assert max_dev(ref, g.to_statevector()) <= 1e-11
+
+
+def test_move_center_mixed_form_large_bonds(gpu, oracle):
+    o = oracle.MpsState.random(12, 64, 60)  # bonds up to 64: multi-panel QR (k > 32)
+    g = copy_state_to_gpu(gpu, o, chi_hint=64)
+    bits = ["".join(np.random.default_rng(3).choice(["0", "1"], 12)) for _ in range(32)]
+    ref = np.array([o.amplitude(b) for b in bits])
+    g.move_center(6)
+    o.move_center(6)
+    assert g.ortho_center == 6 and (g.bond_dims() == o.bond_dims()).all()
+    for i in range(6):
+        assert _left_defect(g.site(i)) <= 1e-11
+    for i in range(7, 12):
+        assert _right_defect(g.site(i)) <= 1e-11
+    assert np.max(np.abs(g.amplitudes(bits) - ref) / np.abs(ref)) <= 1e-10
+
+
+def test_idempotent_and_zero_norm(gpu, oracle):
+    g = copy_state_to_gpu(gpu, oracle.MpsState.random(5, 6, 55))
+    g.left_canonicalize()
+    once = g.to_statevector()
+    g.left_canonicalize()
+    assert max_dev(once, g.to_statevector()) <= 1e-11
+    z = gpu.MpsState(3)
+    z.set_site(0, np.zeros((1, 2, 1)))
+    with pytest.raises(gpu.NumericError):
+        z.left_canonicalize()
+
+
+def test_sampler_deterministic_and_ghz(gpu):
+    assert gpu.sample(gpu.MpsState(5), 1000, 7) == {"00000": 1000}
+    s = gpu.MpsState(4)
+    s.apply_1q(HAD, 0)
+    for i in range(3):
+        s.apply_2q_local(CX, i)
+    counts = gpu.sample(s, 100000, 42)
+    assert set(counts) <= {"0000", "1111"}
+    assert abs(counts["0000"] - 50000) <= 5 * np.sqrt(25000)
+
+
+def test_sampler_counts_match_oracle_exactly(gpu, oracle):
+    for seed, (n, chi, shots) in zip([90, 92, 94], [(5, 4, 20000), (8, 8, 5000), (10, 16, 3000)]):
+        o = oracle.MpsState.random(n, chi, seed)
+        g = copy_state_to_gpu(gpu, o, chi_hint=chi)
+        a = gpu.Sampler(g).sample(shots, 1234)
+        b = oracle.Sampler(o).sample(shots, 1234)
+        assert a == b
+
+
+def test_sampler_memo_semantics(gpu, oracle):
+    # test_sampler.cpp:112-164
+    o = oracle.MpsState.random(5, 4, 92)
+    g = copy_state_to_gpu(gpu, o)
+    a = gpu.sample(g, 5000, 99, memoize=True)
+    b = gpu.sample(g, 5000, 99, memoize=False)
+    assert a == b
+    assert a != gpu.sample(g, 5000, 100)
+    sp = gpu.Sampler(copy_state_to_gpu(gpu, oracle.MpsState.random(5, 4, 93)))
+    warm = sp.sample(2000, 5)
+    sp.clear_cache()
+    assert sp.cache_size == 0
+    assert sp.sample(2000, 5) == warm
+    z = gpu.Sampler(gpu.MpsState(5))
+    z.sample(1000, 3)
+    assert z.cache_hits == 999 * 5 and z.cache_size == 5
+    # hits/size replay matches the reference statistics exactly
+    for cap in (0, 8):
+        og = oracle.MpsState.random(6, 4, 94)
+        gs = gpu.Sampler(copy_state_to_gpu(gpu, og), cache_cap=cap)
+        os_ = oracle.Sampler(og, cache_cap=cap)
+        assert gs.sample(500, 17) == os_.sample(500, 17)
+        assert (gs.cache_hits, gs.cache_size) == (os_.cache_hits, os_.cache_size)
+
+
+def test_sampler_rejects_bad_inputs(gpu):
+    s = gpu.MpsState(3)
+    s.set_site(0, s.site(0) * 3.0)
+    with pytest.raises(gpu.NumericError):
+        gpu.Sampler(s)
+    with pytest.raises(ValueError):
+        gpu.sample(gpu.MpsState(2), 0, 1)
