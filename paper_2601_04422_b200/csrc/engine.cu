@@ -245,8 +245,14 @@ constexpr double kEps = 2.220446049250313e-16;
 // Rounding-noise floor for Jacobi vectors: sigma^2 <= (64 eps)^2 ||theta||_F^2.
 constexpr double kFloorRel2 = (64.0 * kEps) * (64.0 * kEps);
 
-void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs,
-                   const cplx* pre = nullptr, double pre_frob = 0.0) {
+}  // namespace
+
+// Runs the batched Jacobi SVD + truncation + split for the descriptors. The
+// operand comes from the theta kernel (pre == pre_dev == nullptr), from host
+// memory already in X layout (pre, mpsim_gpu_svd) or from a row-major device
+// matrix (pre_dev, bond propagation).
+void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs,
+                              const cplx* pre, double pre_frob, const cplx* pre_dev, long long pre_ld) {
   const int ng = (int)descs.size();
   long long ws_elems = 0;
   int max_tiles = 1, max_nb = 2, max_m = 1, max_n = 1;
@@ -280,11 +286,11 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
   const GateDesc* dg = (const GateDesc*)s.d_gates.p;
   cplx* ws = (cplx*)s.ws.p;
   CK(cudaMemsetAsync(s.d_frob.p, 0, sizeof(double) * ng, st));
-  if (pre == nullptr) {
+  if (pre == nullptr && pre_dev == nullptr) {
     launch_theta(dg, ng, max_tiles, s.sites, s.stride, s.chi, ws, (double*)s.d_frob.p, st);
     check_launch("theta_kernel");
     ++s.launches;
-  } else {
+  } else if (pre_dev == nullptr) {
     // Plain-matrix SVD (mpsim_gpu_svd): X and X0 arrive from the host.
     const GateDesc& d = descs[0];
     const size_t bytes = sizeof(cplx) * (size_t)d.n_pad * d.m_pad;
@@ -292,6 +298,13 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
     CK(cudaMemcpyAsync(ws + d.ws_off + (long long)d.n_pad * d.m_pad, pre, bytes, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(s.d_frob.p, &pre_frob, sizeof(double), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
+  } else {
+    // A device-resident matrix (bond-propagation carriers): load X, X0, ||.||^2.
+    const GateDesc& d = descs[0];
+    launch_load_matrix(pre_dev, pre_ld, d.trans == 0 ? d.m : d.n, d.trans == 0 ? d.n : d.m, d.trans, ws + d.ws_off,
+                       ws + d.ws_off + (long long)d.n_pad * d.m_pad, d.m_pad, (double*)s.d_frob.p, st);
+    check_launch("load_matrix_kernel");
+    ++s.launches;
   }
 
   int* h_rot = (int*)s.h_rot.p;
@@ -356,12 +369,14 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
     // F_2q = 32 Dl Dm Dr + 128 Dl Dr + 32 M N^2 (M = max, N = min of 2Dl, 2Dr)
     const double M = d.m, N = d.n;
     s.svd_flops += 32.0 * M * N * N;
-    if (pre == nullptr) s.gate_flops += 32.0 * d.dl * (double)d.dm * d.dr + 128.0 * d.dl * (double)d.dr + 32.0 * M * N * N;
+    if (pre == nullptr && pre_dev == nullptr) s.gate_flops +=32.0 * d.dl * (double)d.dm * d.dr + 128.0 * d.dl * (double)d.dr + 32.0 * M * N * N;
   }
   if (!converged)
     for (int i = 0; i < ng; ++i)
       if (still[i]) outs[i].status = 3;
 }
+
+namespace {
 
 // Applies disjoint local gates. reports[idx] is filled for every gate.
 void run_layer(State& s, const std::vector<G2>& two, const std::vector<G1>& one, const mpsim_policy& pol,

@@ -79,4 +79,12 @@ struct State {
 // QR sweeps of move_center (canon.cu).
 void move_center_impl(State& s, int center);
 
+// Batched Jacobi SVD + truncation + split of the descriptors (engine.cu).
+void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs,
+                   const cplx* pre = nullptr, double pre_frob = 0.0, const cplx* pre_dev = nullptr,
+                   long long pre_ld = 0);
+void launch_load_matrix(const cplx* A, long long lda, int rows, int cols, int trans, cplx* X, cplx* X0, int m_pad,
+                        double* frob2, cudaStream_t st);
+void launch_cgemm(const GemmArgs&, cudaStream_t);
+
 }  // namespace mpsim_gpu
