@@ -36,6 +36,30 @@ def shard_bounds(n: int, world: int):
     return b
 
 
+def partition_layer(gates, lo, hi, rank, world):
+    """Split one layer (global indices) for the shard [lo, hi): the gates this
+    rank applies (local indices; a gate on (hi-1, hi) uses the ghost slot) and
+    whether it lends its first site left / borrows the right neighbour's."""
+    local = []
+    straddle_left = straddle_right = False
+    for (q0, q1, u) in gates:
+        if q1 is None or q1 < 0:
+            if lo <= q0 < hi:
+                local.append((q0 - lo, -1, u))
+            continue
+        a, b = min(q0, q1), max(q0, q1)
+        if b != a + 1:
+            raise ValueError("sharded layers take local gates (lower non-local gates to SWAP chains first)")
+        if lo <= a and b < hi:
+            local.append((q0 - lo, q1 - lo, u))
+        elif rank < world - 1 and a == hi - 1:
+            local.append((q0 - lo, q1 - lo, u))
+            straddle_right = True
+        elif rank > 0 and b == lo:
+            straddle_left = True
+    return local, straddle_left, straddle_right
+
+
 class _CudaArray:
     """__cuda_array_interface__ view of a device slot, for torch.as_tensor."""
 
@@ -133,17 +157,7 @@ class ShardedChain:
 
     # ---- one layer of disjoint gates in global site indices
     def apply_layer(self, gates, max_bond=None, cutoff=0.0):
-        local = []
-        straddle_left = straddle_right = False
-        for (q0, q1, u) in gates:
-            a, b = min(q0, q1), max(q0, q1)
-            if self.lo <= a and b < self.hi:
-                local.append((q0 - self.lo, q1 - self.lo, u))
-            elif self.has_right and a == self.hi - 1 and b == self.hi:
-                local.append((q0 - self.lo, q1 - self.lo, u))
-                straddle_right = True
-            elif self.rank > 0 and a == self.lo - 1 and b == self.lo:
-                straddle_left = True
+        local, straddle_left, straddle_right = partition_layer(gates, self.lo, self.hi, self.rank, self.world)
         if self.world > 1:
             self._exchange_in(straddle_left, straddle_right)
         st = execute(self.state, local, max_bond, cutoff) if local else dict(device_ms=0.0)
