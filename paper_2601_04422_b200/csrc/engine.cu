@@ -28,6 +28,18 @@ namespace mpsim_gpu {
 void launch_theta(const GateDesc*, int, int, const cplx*, long long, int, cplx*, double*, cudaStream_t);
 int theta_tiles(int dl, int dr);
 void jacobi_init();
+void jacobi_dmma_init();
+void launch_jacobi_round_dmma(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, int,
+                              const double*, double, const int*, long long, cudaStream_t);
+// Jacobi round kernel: DMMA (FP64 tensor path) by default, MPSIM_JACOBI=simt
+// selects the DFMA kernel.
+static bool use_dmma() {
+  static const bool on = [] {
+    const char* v = std::getenv("MPSIM_JACOBI");
+    return !(v != nullptr && std::string(v) == "simt");
+  }();
+  return on;
+}
 size_t jacobi_smem_bytes();
 void launch_jacobi_round(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, int, const double*, double,
                          const int*, long long, cudaStream_t);
@@ -143,6 +155,7 @@ State::State(int n_, long long chi_hint, int dev) : n(n_), device(dev) {
   static bool inited = false;
   if (!inited) {
     jacobi_init();
+    jacobi_dmma_init();
     inited = true;
   }
   chi = next_pow2(std::max<long long>(2, std::min<long long>(chi_hint, 1 << 14)));
@@ -322,10 +335,9 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // outer iteration needs the same number of sweeps as with a fully
       // converged inner EVD (measured in emulation and on the B200), at a
       // fraction of the cost. Final orthogonality is at the tol level.
-      launch_jacobi_round(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps,
-                          2.0 * kEps, 1, (const double*)s.d_frob.p, kFloorRel2,
-                          (const int*)s.d_perm.p,
-                          perm_stride, st);
+      (use_dmma() ? launch_jacobi_round_dmma : launch_jacobi_round)(
+          dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps, 2.0 * kEps, 1,
+          (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p, perm_stride, st);
       ++s.launches;
       ++s.jacobi_launches;
       if (sync_debug()) check_launch("jacobi_round_kernel");

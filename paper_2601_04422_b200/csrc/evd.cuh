@@ -1,0 +1,155 @@
+// Shared pieces of the block-Jacobi pair step: the relative convergence test
+// on a 2W x 2W complex Gram block and one cyclic complex Jacobi EVD of it
+// (see jacobi.cu for the algorithm notes). 256-thread CTAs, kP = 32.
+//
+// Per step of the parallel (round-robin) ordering the 16 disjoint rotations
+// J_k = [[cs, sn], [-ph sn, ph cs]] are applied in ONE pass: thread (a, b)
+// owns the 2x2 block of G at (pair a rows, pair b cols) and computes
+// J_a^H G_ab J_b, plus rows (p_a, q_a) x cols (p_b, q_b) of R <- R J. Blocks
+// are disjoint, so a step costs two barriers.
+//
+// The rotation angle t is computed in FP32 (fast SFU ops); cs = 1/sqrt(1+t^2),
+// sn = cs t and the phase ph = conj(g)/|g| are formed in FP64, so every J is
+// unitary to FP64 rounding whatever the angle's accuracy. An angle accurate to
+// ~1e-7 only means a rotated off-diagonal is reduced by ~1e-7 instead of to
+// zero; the outer sweeps keep rotating a pair until the FP64 test passes.
+#pragma once
+
+#include "common.cuh"
+
+namespace mpsim_gpu {
+
+struct EvdScratch {
+  double cs[kP / 2], sn[kP / 2];
+  cplx ph[kP / 2];
+  int pp[kP / 2], pq[kP / 2];
+  int any;
+};
+
+__device__ __forceinline__ void rr_pair(int step, int k, int M, int& a, int& b) {
+  // Round-robin tournament over M+1 players (M odd); player M is fixed.
+  if (k == 0) {
+    a = step;
+    b = M;
+  } else {
+    a = (step + k) % M;
+    b = (step - k + M) % M;
+  }
+}
+
+// True if any off-diagonal |G_ij| > tolg sqrt(G_ii G_jj) among columns above
+// the noise floor. All 256 threads must call it.
+__device__ __forceinline__ bool pair_needs_rotation(const cplx* G, int t, double tolg, double floor2) {
+  const int ip = t / 16, jp = t % 16;
+  bool need = false;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int i = 2 * ip + a, j = 2 * jp + b;
+      if (i < j) {
+        const double gij = sqrt(cabs2(G[i * kPad + j]));
+        const double gii = G[i * kPad + i].x, gjj = G[j * kPad + j].x;
+        if (gij > 0.0 && gij > tolg * sqrt(gii * gjj) && fmin(gii, gjj) > floor2) need = true;
+      }
+    }
+  return __syncthreads_or(need);
+}
+
+// R <- eigenvectors of the Hermitian G (in place, G is destroyed), max_in
+// cyclic sweeps.
+__device__ __forceinline__ void pair_evd(cplx* G, cplx* R, EvdScratch& S, int t, double tol_in, double floor2,
+                                         int max_in) {
+  for (int idx = t; idx < kP * kP; idx += 256) {
+    const int i = idx / kP, j = idx % kP;
+    R[i * kPad + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+  }
+  if (t < kP) G[t * kPad + t].y = 0.0;
+  const double tol2 = tol_in * tol_in;
+  const int ba = t / (kP / 2), bb = t % (kP / 2);  // this thread's (row pair, column pair)
+  __syncthreads();
+  for (int sweep = 0; sweep < max_in; ++sweep) {
+    if (t == 0) S.any = 0;
+    __syncthreads();
+    for (int step = 0; step < kP - 1; ++step) {
+      if (t < kP / 2) {
+        int p, q;
+        rr_pair(step, t, kP - 1, p, q);
+        const double a = G[p * kPad + p].x, b = G[q * kPad + q].x;
+        const cplx g = G[p * kPad + q];
+        const double c2 = cabs2(g);
+        double cs = 1.0, sn = 0.0;
+        cplx ph = make_double2(1.0, 0.0);
+        if (c2 > 0.0 && c2 > tol2 * fabs(a * b) && fmin(a, b) > floor2) {
+          const double inv_c = rsqrt(c2);
+          ph = make_double2(g.x * inv_c, -g.y * inv_c);  // e^{-i phi}, |ph| = 1 to rounding
+          const float zf = (float)((b - a) * 0.5 * inv_c);
+          const float az = fabsf(zf);
+          const float tf = copysignf(1.0f, zf) / (az > 1e18f ? 2.0f * az : az + sqrtf(1.0f + zf * zf));
+          const double tt = (double)tf;
+          cs = rsqrt(1.0 + tt * tt);
+          sn = cs * tt;
+          S.any = 1;
+        }
+        S.cs[t] = cs;
+        S.sn[t] = sn;
+        S.ph[t] = ph;
+        S.pp[t] = p;
+        S.pq[t] = q;
+      }
+      __syncthreads();
+      const double csa = S.cs[ba], sna = S.sn[ba], csb = S.cs[bb], snb = S.sn[bb];
+      if (sna != 0.0 || snb != 0.0) {
+        const int pa = S.pp[ba], qa = S.pq[ba], pb = S.pp[bb], qb = S.pq[bb];
+        const cplx pha = S.ph[ba], phb = S.ph[bb];
+        // J entries: Jpp = cs, Jpq = sn, Jqp = -ph sn, Jqq = ph cs
+        const cplx jb_qp = make_double2(-phb.x * snb, -phb.y * snb), jb_qq = make_double2(phb.x * csb, phb.y * csb);
+        // conj(J_a) entries used on the left: conj(Jpp)=cs, conj(Jqp)=-conj(ph) sn, conj(Jpq)=sn, conj(Jqq)=conj(ph) cs
+        const cplx ca_qp = make_double2(-pha.x * sna, pha.y * sna), ca_qq = make_double2(pha.x * csa, -pha.y * csa);
+        const cplx b00 = G[pa * kPad + pb], b01 = G[pa * kPad + qb], b10 = G[qa * kPad + pb], b11 = G[qa * kPad + qb];
+        // M = J_a^H B
+        cplx m00 = make_double2(csa * b00.x, csa * b00.y), m01 = make_double2(csa * b01.x, csa * b01.y);
+        cplx m10 = make_double2(sna * b00.x, sna * b00.y), m11 = make_double2(sna * b01.x, sna * b01.y);
+        cfma(m00, ca_qp, b10);
+        cfma(m01, ca_qp, b11);
+        cfma(m10, ca_qq, b10);
+        cfma(m11, ca_qq, b11);
+        // N = M J_b
+        cplx n00 = make_double2(csb * m00.x, csb * m00.y), n01 = make_double2(snb * m00.x, snb * m00.y);
+        cplx n10 = make_double2(csb * m10.x, csb * m10.y), n11 = make_double2(snb * m10.x, snb * m10.y);
+        cfma(n00, m01, jb_qp);
+        cfma(n01, m01, jb_qq);
+        cfma(n10, m11, jb_qp);
+        cfma(n11, m11, jb_qq);
+        if (ba == bb) {  // the rotated pair itself: exact zeros off the diagonal, real diagonal
+          n00.y = 0.0;
+          n11.y = 0.0;
+          n01 = make_double2(0.0, 0.0);
+          n10 = make_double2(0.0, 0.0);
+        }
+        G[pa * kPad + pb] = n00;
+        G[pa * kPad + qb] = n01;
+        G[qa * kPad + pb] = n10;
+        G[qa * kPad + qb] = n11;
+        if (snb != 0.0) {  // R <- R J_b on rows (pa, qa), columns (pb, qb)
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int row = r == 0 ? pa : qa;
+            const cplx x0 = R[row * kPad + pb], x1 = R[row * kPad + qb];
+            cplx y0 = make_double2(csb * x0.x, csb * x0.y), y1 = make_double2(snb * x0.x, snb * x0.y);
+            cfma(y0, x1, jb_qp);
+            cfma(y1, x1, jb_qq);
+            R[row * kPad + pb] = y0;
+            R[row * kPad + qb] = y1;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    const int any = S.any;
+    __syncthreads();
+    if (!any) break;
+  }
+}
+
+}  // namespace mpsim_gpu
