@@ -34,6 +34,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// (256, 2): 124 registers, no spills. (256, 3) fits 80 registers with spills
+// and measured no faster at chi=512.
 __global__ void __launch_bounds__(256, 2) jacobi_round_dmma_kernel(
     const GateDesc* __restrict__ gates, cplx* __restrict__ ws, const int* __restrict__ active,
     int* __restrict__ rotated, int round, double tol, double tol_in, int max_in, const double* __restrict__ frob2,
@@ -60,68 +62,90 @@ __global__ void __launch_bounds__(256, 2) jacobi_round_dmma_kernel(
   double* Ti = S.u.t.Ti;
   // X_ext[e][c]: c < 32 -> Re, c >= 32 -> Im of vector c % 32
   auto xext = [&](int e, int c) -> double { return (c < kP ? Tr : Ti)[e * kPitch + (c & (kP - 1))]; };
-  // Register double-buffering: the next chunk's global loads are issued
-  // before the current chunk's DMMA work, so their latency overlaps compute.
-  constexpr int kPer = (kP * kE) / 256;
-  cplx pre[kPer];
-  auto fetch = [&](int e0) {
+  // (Register double-buffering of the next chunk was measured: no gain at
+  // chi=512, more spills; the chunk is loaded synchronously.)
+  auto load_chunk = [&](int e0) {
 #pragma unroll
-    for (int s = 0; s < kPer; ++s) pre[s] = vec((t + 256 * s) / kE)[e0 + (t + 256 * s) % kE];
-  };
-  auto stage = [&]() {
-#pragma unroll
-    for (int s = 0; s < kPer; ++s) {
+    for (int s = 0; s < (kP * kE) / 256; ++s) {
       const int idx = t + 256 * s;
       const int vi = idx / kE, ee = idx % kE;
-      Tr[ee * kPitch + vi] = pre[s].x;
-      Ti[ee * kPitch + vi] = pre[s].y;
+      const cplx v = vec(vi)[e0 + ee];
+      Tr[ee * kPitch + vi] = v.x;
+      Ti[ee * kPitch + vi] = v.y;
     }
   };
 
-  // ---- 1. Gram on DMMA: warp tile = rows [16*(warp/2), +16) x cols [32*(warp%2), +32) of G_ext
-  const int r0 = 16 * (warp / 2), c0 = 32 * (warp % 2);
+  // ---- 1. Gram on DMMA. Of the real 64x64 G_ext = [[A, B], [B^T, D]] only
+  // the upper 8x8 tiles of A and D and all of B are needed (36 of 64 tiles):
+  // Re G = A + D, Im G = B - B^T. Warps 0-3: tile row w of B (4 tiles);
+  // warps 4-7: tile row r of A plus tile row 3-r of D (5 tiles).
   const int fr = lane / 4, fk = lane % 4;  // A-fragment row / B-fragment col, and k index
-  double acc[2][4][2];
+  int trow[5], tcol[5];
+  int nt;
+  if (warp < 4) {
+    nt = 4;
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+    for (int i = 0; i < 4; ++i) {
+      trow[i] = warp;
+      tcol[i] = 4 + i;
+    }
+    trow[4] = tcol[4] = 0;
+  } else {
+    const int r = warp - 4;
+    nt = 0;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
-  fetch(0);
+    for (int i = 0; i < 5; ++i) {
+      // first 4 - r tiles: A row r, cols r..3 ; then r + 1 tiles: D row 3 - r, cols 3-r..3
+      const int na = 4 - r;
+      if (i < na) {
+        trow[i] = r;
+        tcol[i] = r + i;
+      } else {
+        trow[i] = 4 + (3 - r);
+        tcol[i] = 4 + (3 - r) + (i - na);
+      }
+    }
+    nt = 5;
+  }
+  double acc[5][2];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) acc[i][0] = acc[i][1] = 0.0;
   for (int e0 = 0; e0 < g.m_pad; e0 += kE) {
-    stage();
+    load_chunk(e0);
     __syncthreads();
-    if (e0 + kE < g.m_pad) fetch(e0 + kE);
 #pragma unroll 4
     for (int ks = 0; ks < kE / 4; ++ks) {
       const int e = 4 * ks + fk;
-      double av[2], bv[4];
+      double a_first = xext(e, 8 * trow[0] + fr), a_last = xext(e, 8 * trow[4] + fr);
 #pragma unroll
-      for (int a = 0; a < 2; ++a) av[a] = xext(e, r0 + 8 * a + fr);  // A[m = c][k = e] = X_ext[e][c]
-#pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = xext(e, c0 + 8 * b + fr);  // B[k = e][n = c'] = X_ext[e][c']
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) dmma(acc[a][b][0], acc[a][b][1], av[a], bv[b]);
+      for (int i = 0; i < 5; ++i) {
+        if (i < nt) {
+          const double av = trow[i] == trow[0] ? a_first : a_last;   // A[m = c][k = e] = X_ext[e][c]
+          const double bv = xext(e, 8 * tcol[i] + fr);                 // B[k = e][n = c'] = X_ext[e][c']
+          dmma(acc[i][0], acc[i][1], av, bv);
+        }
+      }
     }
     __syncthreads();
   }
-  // scatter the real 64x64 Gram (aliases the chunk planes), then combine
+  // scatter the computed tiles of G_ext (aliases the chunk planes), then combine
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
+  for (int i = 0; i < 5; ++i)
+    if (i < nt)
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
-        const int row = r0 + 8 * a + fr, col = c0 + 8 * b + fk * 2 + v;
-        S.u.Gx[row * 65 + col] = acc[a][b][v];
+        const int row = 8 * trow[i] + fr, col = 8 * tcol[i] + fk * 2 + v;
+        S.u.Gx[row * 65 + col] = acc[i][v];
       }
   __syncthreads();
   for (int idx = t; idx < kP * kP; idx += 256) {
     const int i = idx / kP, j = idx % kP;
+    if (i > j) continue;
     const double* Gx = S.u.Gx;
-    S.G[i * kPad + j] = make_double2(Gx[i * 65 + j] + Gx[(kP + i) * 65 + kP + j],
-                                     Gx[i * 65 + kP + j] - Gx[(kP + i) * 65 + j]);
+    const double re = Gx[i * 65 + j] + Gx[(kP + i) * 65 + kP + j];
+    const double im = Gx[i * 65 + kP + j] - Gx[j * 65 + kP + i];
+    S.G[i * kPad + j] = make_double2(re, i == j ? 0.0 : im);
+    if (i != j) S.G[j * kPad + i] = make_double2(re, -im);
   }
   __syncthreads();
 
@@ -129,7 +153,10 @@ __global__ void __launch_bounds__(256, 2) jacobi_round_dmma_kernel(
   const double tolg = tol * fmax(sqrt((double)g.m), (double)kP);
   const double floor2 = floor_rel2 * frob2[gi];
   if (!pair_needs_rotation(S.G, t, tolg, floor2)) return;
-  pair_evd(S.G, S.R, S.sc, t, tol_in, floor2, max_in);
+  // (16-thread parameters + fused block update, two barriers per step: the
+  // one-barrier variant with per-thread redundant parameters, pair_evd(), was
+  // measured 10 % slower at chi=512.)
+  pair_evd_v1(S.G, S.R, S.sc, t, tol_in, floor2, max_in);
 
   // ---- 4. rotation on DMMA: warp owns output column tile [8*warp, +8) of X_ext R_ext
   double bfrag[16];
@@ -146,11 +173,9 @@ __global__ void __launch_bounds__(256, 2) jacobi_round_dmma_kernel(
       bfrag[s] = v;
     }
   }
-  fetch(0);
   for (int e0 = 0; e0 < g.m_pad; e0 += kE) {
-    stage();
+    load_chunk(e0);
     __syncthreads();
-    if (e0 + kE < g.m_pad) fetch(e0 + kE);
     double o[kE / 8][2];
 #pragma unroll
     for (int rt = 0; rt < kE / 8; ++rt) o[rt][0] = o[rt][1] = 0.0;
