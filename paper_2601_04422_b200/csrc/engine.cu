@@ -30,7 +30,7 @@ int theta_tiles(int dl, int dr);
 void jacobi_init();
 void jacobi_dmma_init();
 void launch_jacobi_round_dmma(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, int,
-                              const double*, double, const int*, long long, cudaStream_t);
+                              const double*, double, const int*, long long, double*, cudaStream_t);
 // Jacobi round kernel: DMMA (FP64 tensor path) by default, MPSIM_JACOBI=simt
 // selects the DFMA kernel.
 static bool use_dmma() {
@@ -42,7 +42,7 @@ static bool use_dmma() {
 }
 size_t jacobi_smem_bytes();
 void launch_jacobi_round(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, int, const double*, double,
-                         const int*, long long, cudaStream_t);
+                         const int*, long long, double*, cudaStream_t);
 void launch_derijk(const GateDesc*, int, const cplx*, const int*, int*, long long, cudaStream_t);
 void launch_norms(const GateDesc*, int, int, const cplx*, double*, long long, cudaStream_t);
 void launch_truncate(const GateDesc*, int, double*, int*, long long, GateOut*, const double*, double, cudaStream_t);
@@ -75,6 +75,15 @@ std::string& last_error_slot() {
 static bool sync_debug() {
   static const bool on = [] {
     const char* v = std::getenv("MPSIM_SYNC_DEBUG");
+    return v != nullptr && v[0] == '1';
+  }();
+  return on;
+}
+
+// MPSIM_SWEEP_DEBUG=1 prints per-sweep Jacobi convergence to stderr.
+static bool sweep_debug() {
+  static const bool on = [] {
+    const char* v = std::getenv("MPSIM_SWEEP_DEBUG");
     return v != nullptr && v[0] == '1';
   }();
   return on;
@@ -184,9 +193,10 @@ State::~State() {
   DeviceGuard g(device);
   cudaStreamSynchronize(st);
   sites_buf.release();
-  for (DeviceBuf* b : {&ws, &d_gates, &d_out, &d_sigma, &d_order, &d_active, &d_rot, &d_frob, &d_perm, &d_g1, &q1, &q2, &q3, &q4, &qbits})
+  for (DeviceBuf* b : {&ws, &d_gates, &d_out, &d_sigma, &d_order, &d_active, &d_rot, &d_frob, &d_perm, &d_maxoff,
+                       &d_g1, &q1, &q2, &q3, &q4, &qbits})
     b->release();
-  for (PinnedBuf* b : {&h_gates, &h_out, &h_rot, &h_g1, &h_small}) b->release();
+  for (PinnedBuf* b : {&h_gates, &h_out, &h_rot, &h_g1, &h_small, &h_maxoff}) b->release();
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   cudaEventDestroy(evj0);
@@ -257,6 +267,9 @@ constexpr int kMaxSweeps = 60;
 constexpr double kEps = 2.220446049250313e-16;
 // Rounding-noise floor for Jacobi vectors: sigma^2 <= (64 eps)^2 ||theta||_F^2.
 constexpr double kFloorRel2 = (64.0 * kEps) * (64.0 * kEps);
+// Largest relative off-diagonal entering a sweep after which that sweep's
+// rotations are final (quadratic convergence; see run_two_chunk).
+constexpr double kQuadFinish = 1e-9;
 
 }  // namespace
 
@@ -325,8 +338,13 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   CK(cudaMemcpyAsync(s.d_active.p, h_rot, sizeof(int) * ng, cudaMemcpyHostToDevice, st));
   bool converged = false;
   std::vector<int> still(ng, 1);
+  s.d_maxoff.ensure(sizeof(double) * ng);
+  s.h_maxoff.ensure(sizeof(double) * ng);
+  double* h_maxoff = (double*)s.h_maxoff.p;
+  const bool dmma = use_dmma();
   for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
     CK(cudaMemsetAsync(s.d_rot.p, 0, sizeof(int) * ng, st));
+    CK(cudaMemsetAsync(s.d_maxoff.p, 0, sizeof(double) * ng, st));
     launch_derijk(dg, ng, ws, (const int*)s.d_active.p, (int*)s.d_perm.p, perm_stride, st);
     ++s.launches;
     CK(cudaEventRecord(s.evj0, st));
@@ -335,9 +353,9 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // outer iteration needs the same number of sweeps as with a fully
       // converged inner EVD (measured in emulation and on the B200), at a
       // fraction of the cost. Final orthogonality is at the tol level.
-      (use_dmma() ? launch_jacobi_round_dmma : launch_jacobi_round)(
+      (dmma ? launch_jacobi_round_dmma : launch_jacobi_round)(
           dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps, 2.0 * kEps, 1,
-          (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p, perm_stride, st);
+          (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p, perm_stride, (double*)s.d_maxoff.p, st);
       ++s.launches;
       ++s.jacobi_launches;
       if (sync_debug()) check_launch("jacobi_round_kernel");
@@ -346,15 +364,34 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     check_launch("jacobi_round_kernel");
     ++s.sweeps;
     CK(cudaMemcpyAsync(h_rot, s.d_rot.p, sizeof(int) * ng, cudaMemcpyDeviceToHost, st));
-    s.d2h_bytes += (long long)sizeof(int) * ng;
+    CK(cudaMemcpyAsync(h_maxoff, s.d_maxoff.p, sizeof(double) * ng, cudaMemcpyDeviceToHost, st));
+    s.d2h_bytes += (long long)(sizeof(int) + sizeof(double)) * ng;
     CK(cudaStreamSynchronize(st));
     {
       float ms = 0.f;
       CK(cudaEventElapsedTime(&ms, s.evj0, s.evj1));
       s.jacobi_ms += ms;
     }
+    // A gate is done when no pair rotated, or (DMMA kernel, which reports the
+    // largest relative off-diagonal it saw) when every pair entered this sweep
+    // with off <= kQuadFinish: cyclic Jacobi converges quadratically there, so
+    // the rotations of this sweep leave off ~ kQuadFinish^2 << tol and the
+    // otherwise Gram-only confirmation sweep is skipped.
+    if (sweep_debug()) {
+      double mx = 0.0, mn = 1e300;
+      int act = 0;
+      for (int i = 0; i < ng; ++i) {
+        mx = std::max(mx, h_maxoff[i]);
+        mn = std::min(mn, h_maxoff[i]);
+        act += h_rot[i];
+      }
+      std::fprintf(stderr, "[mpsim] sweep %d: %d/%d gates rotated, max rel off in [%.3e, %.3e], %.3f ms\n", sweep,
+                   act, ng, mn, mx, (double)0);
+    }
     bool any = false;
     for (int i = 0; i < ng; ++i) {
+      const bool quad_done = dmma && h_maxoff[i] <= kQuadFinish;
+      h_rot[i] = h_rot[i] && !quad_done;
       still[i] = h_rot[i];
       any = any || h_rot[i];
     }
@@ -362,7 +399,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       converged = true;
       break;
     }
-    CK(cudaMemcpyAsync(s.d_active.p, s.d_rot.p, sizeof(int) * ng, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(s.d_active.p, h_rot, sizeof(int) * ng, cudaMemcpyHostToDevice, st));
   }
   launch_norms(dg, ng, max_n, ws, (double*)s.d_sigma.p, sig_stride, st);
   check_launch("norms_kernel");

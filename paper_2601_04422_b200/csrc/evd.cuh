@@ -38,10 +38,14 @@ __device__ __forceinline__ void rr_pair(int step, int k, int M, int& a, int& b) 
 }
 
 // True if any off-diagonal |G_ij| > tolg sqrt(G_ii G_jj) among columns above
-// the noise floor. All 256 threads must call it.
-__device__ __forceinline__ bool pair_needs_rotation(const cplx* G, int t, double tolg, double floor2) {
+// the noise floor. All 256 threads must call it. If maxoff != nullptr the
+// largest relative off-diagonal of the block is folded into *maxoff
+// (atomicMax on the bit pattern: non-negative doubles order as integers).
+__device__ __forceinline__ bool pair_needs_rotation(const cplx* G, int t, double tolg, double floor2,
+                                                    double* maxoff = nullptr) {
   const int ip = t / 16, jp = t % 16;
   bool need = false;
+  double mx = 0.0;
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -50,9 +54,19 @@ __device__ __forceinline__ bool pair_needs_rotation(const cplx* G, int t, double
       if (i < j) {
         const double gij = sqrt(cabs2(G[i * kPad + j]));
         const double gii = G[i * kPad + i].x, gjj = G[j * kPad + j].x;
-        if (gij > 0.0 && gij > tolg * sqrt(gii * gjj) && fmin(gii, gjj) > floor2) need = true;
+        if (gij > 0.0 && fmin(gii, gjj) > floor2) {
+          const double rel = gij / sqrt(gii * gjj);
+          mx = fmax(mx, rel);
+          if (rel > tolg) need = true;
+        }
       }
     }
+  if (maxoff != nullptr) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((t & 31) == 0 && mx > 0.0)
+      atomicMax(reinterpret_cast<unsigned long long*>(maxoff), (unsigned long long)__double_as_longlong(mx));
+  }
   return __syncthreads_or(need);
 }
 

@@ -317,7 +317,7 @@ void jacobi_init() {
 void launch_jacobi_round(const GateDesc* d_gates, int n_gates, int max_pairs, cplx* ws,
                          const int* d_active, int* d_rotated, int round, double tol, double tol_in,
                          int max_in, const double* frob2, double floor_rel2, const int* perm,
-                         long long perm_stride, cudaStream_t st) {
+                         long long perm_stride, double* /*maxoff: DMMA kernel only*/, cudaStream_t st) {
   jacobi_round_kernel<<<dim3(max_pairs, n_gates), 256, sizeof(JacobiSmem), st>>>(
       d_gates, ws, d_active, d_rotated, round, tol, tol_in, max_in, frob2, floor_rel2, perm, perm_stride);
 }

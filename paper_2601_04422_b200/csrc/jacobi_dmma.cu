@@ -39,7 +39,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 __global__ void __launch_bounds__(256, 2) jacobi_round_dmma_kernel(
     const GateDesc* __restrict__ gates, cplx* __restrict__ ws, const int* __restrict__ active,
     int* __restrict__ rotated, int round, double tol, double tol_in, int max_in, const double* __restrict__ frob2,
-    double floor_rel2, const int* __restrict__ perm, long long perm_stride) {
+    double floor_rel2, const int* __restrict__ perm, long long perm_stride, double* __restrict__ maxoff) {
   const int gi = blockIdx.y;
   if (!active[gi]) return;
   const GateDesc& g = gates[gi];
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(256, 2) jacobi_round_dmma_kernel(
   // ---- 2. convergence test, 3. pair EVD (shared with the SIMT kernel)
   const double tolg = tol * fmax(sqrt((double)g.m), (double)kP);
   const double floor2 = floor_rel2 * frob2[gi];
-  if (!pair_needs_rotation(S.G, t, tolg, floor2)) return;
+  if (!pair_needs_rotation(S.G, t, tolg, floor2, maxoff + gi)) return;
   // (16-thread parameters + fused block update, two barriers per step: the
   // one-barrier variant with per-thread redundant parameters, pair_evd(), was
   // measured 10 % slower at chi=512.)
@@ -216,9 +216,10 @@ void jacobi_dmma_init() {
 
 void launch_jacobi_round_dmma(const GateDesc* d_gates, int n_gates, int max_pairs, cplx* ws, const int* d_active,
                               int* d_rotated, int round, double tol, double tol_in, int max_in, const double* frob2,
-                              double floor_rel2, const int* perm, long long perm_stride, cudaStream_t st) {
+                              double floor_rel2, const int* perm, long long perm_stride, double* maxoff,
+                              cudaStream_t st) {
   jacobi_round_dmma_kernel<<<dim3(max_pairs, n_gates), 256, sizeof(JacobiDmmaSmem), st>>>(
-      d_gates, ws, d_active, d_rotated, round, tol, tol_in, max_in, frob2, floor_rel2, perm, perm_stride);
+      d_gates, ws, d_active, d_rotated, round, tol, tol_in, max_in, frob2, floor_rel2, perm, perm_stride, maxoff);
 }
 
 }  // namespace mpsim_gpu
