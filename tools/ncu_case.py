@@ -4,7 +4,8 @@ sys.path.insert(0, '.')
 import numpy as np
 import paper_2601_04422_b200 as P
 exec(open('tools/perf_probe.py').read().split("chi = int")[0])
-chi, ngates = 512, 8
+import os
+chi, ngates = int(os.environ.get('CHI', '512')), int(os.environ.get('NGATES', '8'))
 rng = np.random.default_rng(1)
 lg = int(np.log2(chi)); n = 2 * (lg + 1) + 2 * ngates
 s, bonds = saturated_state(n, chi, rng)
