@@ -379,14 +379,21 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     // otherwise Gram-only confirmation sweep is skipped.
     if (sweep_debug()) {
       double mx = 0.0, mn = 1e300;
-      int act = 0;
+      long long act = 0, pairs = 0;
       for (int i = 0; i < ng; ++i) {
         mx = std::max(mx, h_maxoff[i]);
         mn = std::min(mn, h_maxoff[i]);
-        act += h_rot[i];
+        act += h_rot[i] > 0;
+        pairs += h_rot[i];
       }
-      std::fprintf(stderr, "[mpsim] sweep %d: %d/%d gates rotated, max rel off in [%.3e, %.3e], %.3f ms\n", sweep,
-                   act, ng, mn, mx, (double)0);
+      long long total = 0;
+      for (const GateDesc& d : descs) total += (long long)d.nb * (d.nb - 1) / 2;
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, s.evj0, s.evj1);
+      std::fprintf(stderr,
+                   "[mpsim] sweep %d: %lld/%d gates rotated, %lld/%lld pairs rotated, max rel off in [%.3e, %.3e], "
+                   "%.3f ms\n",
+                   sweep, act, ng, pairs, total, mn, mx, ms);
     }
     bool any = false;
     for (int i = 0; i < ng; ++i) {

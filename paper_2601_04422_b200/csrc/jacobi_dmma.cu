@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(256, 2) jacobi_round_dmma_kernel(
     }
     __syncthreads();
   }
-  if (t == 0) rotated[gi] = 1;
+  if (t == 0) atomicAdd(rotated + gi, 1);  // rotated pair count of this gate, this sweep
 }
 
 size_t jacobi_dmma_smem_bytes() { return sizeof(JacobiDmmaSmem); }
