@@ -80,6 +80,16 @@ static bool sync_debug() {
   return on;
 }
 
+// MPSIM_PHASE_PROBE=1|2 (profiling only): Jacobi rounds stop after the Gram
+// (1) or after the pair EVD (2), with a single sweep, to time the phases.
+static int phase_probe() {
+  static const int v = [] {
+    const char* e = std::getenv("MPSIM_PHASE_PROBE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 // MPSIM_SWEEP_DEBUG=1 prints per-sweep Jacobi convergence to stderr.
 static bool sweep_debug() {
   static const bool on = [] {
@@ -342,7 +352,8 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   s.h_maxoff.ensure(sizeof(double) * ng);
   double* h_maxoff = (double*)s.h_maxoff.p;
   const bool dmma = use_dmma();
-  for (int sweep = 0; sweep < kMaxSweeps; ++sweep) {
+  const int max_sweeps = phase_probe() ? 1 : kMaxSweeps;
+  for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     CK(cudaMemsetAsync(s.d_rot.p, 0, sizeof(int) * ng, st));
     CK(cudaMemsetAsync(s.d_maxoff.p, 0, sizeof(double) * ng, st));
     launch_derijk(dg, ng, ws, (const int*)s.d_active.p, (int*)s.d_perm.p, perm_stride, st);
@@ -354,7 +365,8 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // converged inner EVD (measured in emulation and on the B200), at a
       // fraction of the cost. Final orthogonality is at the tol level.
       (dmma ? launch_jacobi_round_dmma : launch_jacobi_round)(
-          dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps, 2.0 * kEps, 1,
+          dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps, 2.0 * kEps,
+          phase_probe() ? -phase_probe() : 1,
           (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p, perm_stride, (double*)s.d_maxoff.p, st);
       ++s.launches;
       ++s.jacobi_launches;

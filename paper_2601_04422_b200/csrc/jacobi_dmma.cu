@@ -156,52 +156,61 @@ __global__ void __launch_bounds__(256, 2) jacobi_round_dmma_kernel(
   // (16-thread parameters + fused block update, two barriers per step: the
   // one-barrier variant with per-thread redundant parameters, pair_evd(), was
   // measured 10 % slower at chi=512.)
-  pair_evd_v1(S.G, S.R, S.sc, t, tol_in, floor2, max_in);
+  // max_in < 0: phase-timing probes only (-1: stop after the Gram/test, -2: after the EVD).
+  if (max_in == -1) return;
+  pair_evd_v1(S.G, S.R, S.sc, t, tol_in, floor2, max_in < 0 ? 1 : max_in);
+  if (max_in == -2) return;
 
-  // ---- 4. rotation on DMMA: warp owns output column tile [8*warp, +8) of X_ext R_ext
-  double bfrag[16];
-  {
-    const int jext = 8 * warp + fr;  // B[k = c_ext][n = j_ext]: n = lane / 4
+  // ---- 4. rotation on DMMA. Warp w computes row tiles {2(w%4), 2(w%4)+1} of
+  // the chunk and complex column tiles {2(w/4), 2(w/4)+1}, i.e. the real column
+  // tiles cj (Re) and 4+cj (Im) for both: 8 output tiles, R_ext slice for its 4
+  // real column tiles held in registers (64 doubles), one A-fragment load per
+  // 4 DMMAs. Each thread then owns Re and Im of the same complex outputs and
+  // stores them straight to global (16-byte, 128-byte runs per 8 lanes).
+  const int rbase = 2 * (warp % 4), cbase = 2 * (warp / 4);
+  double bfrag[4][16];
+#pragma unroll
+  for (int ct = 0; ct < 4; ++ct) {
+    const int cj = cbase + (ct & 1);                  // complex column tile
+    const int jext = (ct < 2 ? 0 : kP) + 8 * cj + fr;  // Re tiles first, then Im tiles
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
-      const int cext = 4 * s + fk;
-      const int c = cext & (kP - 1), j = jext & (kP - 1);
-      const cplx r = S.R[c * kPad + j];
+      const int cext = 4 * s + fk;  // B[k = c_ext][n = j_ext]
+      const cplx r = S.R[(cext & (kP - 1)) * kPad + (jext & (kP - 1))];
       double v;
-      if (cext < kP) v = jext < kP ? r.x : r.y;   // [[Re R, Im R],
-      else v = jext < kP ? -r.y : r.x;            //  [-Im R, Re R]]
-      bfrag[s] = v;
+      if (cext < kP) v = jext < kP ? r.x : r.y;  // [[Re R, Im R],
+      else v = jext < kP ? -r.y : r.x;           //  [-Im R, Re R]]
+      bfrag[ct][s] = v;
     }
   }
   for (int e0 = 0; e0 < g.m_pad; e0 += kE) {
     load_chunk(e0);
     __syncthreads();
-    double o[kE / 8][2];
+    double o[2][4][2];
 #pragma unroll
-    for (int rt = 0; rt < kE / 8; ++rt) o[rt][0] = o[rt][1] = 0.0;
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o[a][c][0] = o[a][c][1] = 0.0;
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
 #pragma unroll
-      for (int rt = 0; rt < kE / 8; ++rt) {
-        const double av = xext(8 * rt + fr, 4 * s + fk);  // A[m = e][k = c_ext]
-        dmma(o[rt][0], o[rt][1], av, bfrag[s]);
+      for (int a = 0; a < 2; ++a) {
+        const double av = xext(8 * (rbase + a) + fr, 4 * s + fk);  // A[m = e][k = c_ext]
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dmma(o[a][c][0], o[a][c][1], av, bfrag[c][s]);
       }
     }
-    __syncthreads();
+    // C fragment: row e = 8 rt + lane/4, column 2 (lane%4) + v of each tile.
 #pragma unroll
-    for (int rt = 0; rt < kE / 8; ++rt)
+    for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int e = 8 * rt + fr, jext = 8 * warp + 2 * fk + v;
-        (jext < kP ? Tr : Ti)[e * kPitch + (jext & (kP - 1))] = o[rt][v];
-      }
-    __syncthreads();
+      for (int c = 0; c < 2; ++c)
 #pragma unroll
-    for (int s = 0; s < (kP * kE) / 256; ++s) {
-      const int idx = t + 256 * s;
-      const int vi = idx / kE, ee = idx % kE;
-      vec(vi)[e0 + ee] = make_double2(Tr[ee * kPitch + vi], Ti[ee * kPitch + vi]);
-    }
+        for (int v = 0; v < 2; ++v) {
+          const int e = 8 * (rbase + a) + fr;
+          const int j = 8 * (cbase + c) + 2 * fk + v;  // complex column within the pair
+          vec(j)[e0 + e] = make_double2(o[a][c][v], o[a][c + 2][v]);
+        }
     __syncthreads();
   }
   if (t == 0) atomicAdd(rotated + gi, 1);  // rotated pair count of this gate, this sweep
