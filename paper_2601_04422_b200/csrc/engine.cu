@@ -31,15 +31,21 @@ void jacobi_init();
 void jacobi_dmma_init();
 void launch_jacobi_round_dmma(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, int,
                               const double*, double, const int*, long long, double*, cudaStream_t);
-// Jacobi round kernel: DMMA (FP64 tensor path) by default, MPSIM_JACOBI=simt
-// selects the DFMA kernel.
-static bool use_dmma() {
-  static const bool on = [] {
+void jacobi_split_init();
+void launch_jacobi_round_split(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, const double*,
+                               double, const int*, long long, double*, int*, cplx*, cplx*, cudaStream_t);
+// Jacobi round implementation: "split" (default; Gram / EVD / rotation as three
+// launches, DMMA for both GEMMs), "dmma" (one fused DMMA kernel), "simt" (DFMA).
+static int jacobi_mode() {
+  static const int m = [] {
     const char* v = std::getenv("MPSIM_JACOBI");
-    return !(v != nullptr && std::string(v) == "simt");
+    if (v != nullptr && std::string(v) == "simt") return 0;
+    if (v != nullptr && std::string(v) == "dmma") return 1;
+    return 2;
   }();
-  return on;
+  return m;
 }
+static bool use_dmma() { return jacobi_mode() != 0; }
 size_t jacobi_smem_bytes();
 void launch_jacobi_round(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, int, const double*, double,
                          const int*, long long, double*, cudaStream_t);
@@ -175,6 +181,7 @@ State::State(int n_, long long chi_hint, int dev) : n(n_), device(dev) {
   if (!inited) {
     jacobi_init();
     jacobi_dmma_init();
+    jacobi_split_init();
     inited = true;
   }
   chi = next_pow2(std::max<long long>(2, std::min<long long>(chi_hint, 1 << 14)));
@@ -204,7 +211,7 @@ State::~State() {
   cudaStreamSynchronize(st);
   sites_buf.release();
   for (DeviceBuf* b : {&ws, &d_gates, &d_out, &d_sigma, &d_order, &d_active, &d_rot, &d_frob, &d_perm, &d_maxoff,
-                       &d_g1, &q1, &q2, &q3, &q4, &qbits})
+                       &d_g1, &q1, &q2, &q3, &q4, &qbits, &d_need, &d_gbuf, &d_rbuf})
     b->release();
   for (PinnedBuf* b : {&h_gates, &h_out, &h_rot, &h_g1, &h_small, &h_maxoff}) b->release();
   cudaEventDestroy(ev0);
@@ -349,6 +356,12 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   bool converged = false;
   std::vector<int> still(ng, 1);
   s.d_maxoff.ensure(sizeof(double) * ng);
+  if (jacobi_mode() == 2) {
+    const size_t slots = (size_t)ng * (max_nb / 2);
+    s.d_need.ensure(sizeof(int) * slots);
+    s.d_gbuf.ensure(sizeof(cplx) * slots * kP * kP);
+    s.d_rbuf.ensure(sizeof(cplx) * slots * kP * kP);
+  }
   s.h_maxoff.ensure(sizeof(double) * ng);
   double* h_maxoff = (double*)s.h_maxoff.p;
   const bool dmma = use_dmma();
@@ -364,10 +377,18 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // outer iteration needs the same number of sweeps as with a fully
       // converged inner EVD (measured in emulation and on the B200), at a
       // fraction of the cost. Final orthogonality is at the tol level.
-      (dmma ? launch_jacobi_round_dmma : launch_jacobi_round)(
-          dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps, 2.0 * kEps,
-          phase_probe() ? -phase_probe() : 1,
-          (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p, perm_stride, (double*)s.d_maxoff.p, st);
+      if (jacobi_mode() == 2) {
+        launch_jacobi_round_split(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round,
+                                  4.0 * kEps, 2.0 * kEps, (const double*)s.d_frob.p, kFloorRel2,
+                                  (const int*)s.d_perm.p, perm_stride, (double*)s.d_maxoff.p, (int*)s.d_need.p,
+                                  (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p, st);
+        s.launches += 2;  // three kernels per round (one more counted below)
+      } else {
+        (dmma ? launch_jacobi_round_dmma : launch_jacobi_round)(
+            dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps, 2.0 * kEps,
+            phase_probe() ? -phase_probe() : 1, (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p,
+            perm_stride, (double*)s.d_maxoff.p, st);
+      }
       ++s.launches;
       ++s.jacobi_launches;
       if (sync_debug()) check_launch("jacobi_round_kernel");
