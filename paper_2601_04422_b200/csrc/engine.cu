@@ -33,7 +33,17 @@ void launch_jacobi_round_dmma(const GateDesc*, int, int, cplx*, const int*, int*
                               const double*, double, const int*, long long, double*, cudaStream_t);
 void jacobi_split_init();
 void launch_jacobi_round_split(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, const double*,
-                               double, const int*, long long, double*, int*, cplx*, cplx*, cudaStream_t);
+                               double, const int*, long long, double*, int*, cplx*, cplx*, double*, cudaStream_t);
+// Cross-only pair EVDs (evd.cuh) in a sweep whose predecessor measured an rms
+// relative off-norm above this (the pre-asymptotic phase); MPSIM_CROSS=0 disables.
+constexpr double kCrossRms = 0.35;
+static bool cross_policy() {
+  static const bool on = [] {
+    const char* v = std::getenv("MPSIM_CROSS");
+    return !(v != nullptr && v[0] == '0');
+  }();
+  return on;
+}
 // Jacobi round implementation: "split" (default; Gram / EVD / rotation as three
 // launches, DMMA for both GEMMs), "dmma" (one fused DMMA kernel), "simt" (DFMA).
 static int jacobi_mode() {
@@ -364,11 +374,15 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   }
   s.h_maxoff.ensure(sizeof(double) * ng);
   double* h_maxoff = (double*)s.h_maxoff.p;
+  s.d_offsum.ensure(sizeof(double) * ng);
+  s.h_offsum.ensure(sizeof(double) * ng);
+  double* h_offsum = (double*)s.h_offsum.p;
   const bool dmma = use_dmma();
   const int max_sweeps = phase_probe() ? 1 : kMaxSweeps;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     CK(cudaMemsetAsync(s.d_rot.p, 0, sizeof(int) * ng, st));
     CK(cudaMemsetAsync(s.d_maxoff.p, 0, sizeof(double) * ng, st));
+    CK(cudaMemsetAsync(s.d_offsum.p, 0, sizeof(double) * ng, st));
     launch_derijk(dg, ng, ws, (const int*)s.d_active.p, (int*)s.d_perm.p, perm_stride, st);
     ++s.launches;
     CK(cudaEventRecord(s.evj0, st));
@@ -381,7 +395,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
         launch_jacobi_round_split(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round,
                                   4.0 * kEps, 2.0 * kEps, (const double*)s.d_frob.p, kFloorRel2,
                                   (const int*)s.d_perm.p, perm_stride, (double*)s.d_maxoff.p, (int*)s.d_need.p,
-                                  (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p, st);
+                                  (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p, (double*)s.d_offsum.p, st);
         s.launches += 2;  // three kernels per round (one more counted below)
       } else {
         (dmma ? launch_jacobi_round_dmma : launch_jacobi_round)(
@@ -398,7 +412,8 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     ++s.sweeps;
     CK(cudaMemcpyAsync(h_rot, s.d_rot.p, sizeof(int) * ng, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_maxoff, s.d_maxoff.p, sizeof(double) * ng, cudaMemcpyDeviceToHost, st));
-    s.d2h_bytes += (long long)(sizeof(int) + sizeof(double)) * ng;
+    CK(cudaMemcpyAsync(h_offsum, s.d_offsum.p, sizeof(double) * ng, cudaMemcpyDeviceToHost, st));
+    s.d2h_bytes += (long long)(sizeof(int) + 2 * sizeof(double)) * ng;
     CK(cudaStreamSynchronize(st));
     {
       float ms = 0.f;
@@ -425,8 +440,8 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       cudaEventElapsedTime(&ms, s.evj0, s.evj1);
       std::fprintf(stderr,
                    "[mpsim] sweep %d: %lld/%d gates rotated, %lld/%lld pairs rotated, max rel off in [%.3e, %.3e], "
-                   "%.3f ms\n",
-                   sweep, act, ng, pairs, total, mn, mx, ms);
+                   "rms off[0] %.3f, %.3f ms\n",
+                   sweep, act, ng, pairs, total, mn, mx, std::sqrt(2.0 * h_offsum[0] / std::max(1, descs[0].n)), ms);
     }
     bool any = false;
     for (int i = 0; i < ng; ++i) {
@@ -434,6 +449,10 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       h_rot[i] = h_rot[i] && !quad_done;
       still[i] = h_rot[i];
       any = any || h_rot[i];
+      // pre-asymptotic (rms relative off-norm of the sweep above kCrossRms):
+      // the next sweep's pair EVDs rotate the cross-block pairs only
+      const double rms = std::sqrt(2.0 * h_offsum[i] / std::max(1, descs[i].n));
+      if (h_rot[i] && jacobi_mode() == 2 && cross_policy() && rms > kCrossRms && h_maxoff[i] > 1e-3) h_rot[i] = 2;
     }
     if (!any) {
       converged = true;

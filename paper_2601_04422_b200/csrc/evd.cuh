@@ -262,8 +262,12 @@ __device__ __forceinline__ void pair_evd_2b(cplx* G, cplx* R, int t, double tol_
 }
 
 // (previous two-barrier-per-step version, kept for reference/A-B testing)
+// cross = true: one pass over the 256 pairs (i < W <= j) that straddle the two
+// blocks only, 16 steps of pairs (i, W + (i + step) % W) instead of 31 steps
+// over all 496 pairs. Used in the pre-asymptotic outer sweeps (engine.cu),
+// where the in-block pairs are near-orthogonal from their previous visits.
 __device__ __forceinline__ void pair_evd_v1(cplx* G, cplx* R, EvdScratch& S, int t, double tol_in, double floor2,
-                                            int max_in) {
+                                            int max_in, bool cross = false) {
   for (int idx = t; idx < kP * kP; idx += 256) {
     const int i = idx / kP, j = idx % kP;
     R[i * kPad + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
@@ -275,10 +279,16 @@ __device__ __forceinline__ void pair_evd_v1(cplx* G, cplx* R, EvdScratch& S, int
   for (int sweep = 0; sweep < max_in; ++sweep) {
     if (t == 0) S.any = 0;
     __syncthreads();
-    for (int step = 0; step < kP - 1; ++step) {
+    const int nsteps = cross ? kP / 2 : kP - 1;
+    for (int step = 0; step < nsteps; ++step) {
       if (t < kP / 2) {
         int p, q;
-        rr_pair(step, t, kP - 1, p, q);
+        if (cross) {
+          p = t;
+          q = kP / 2 + (t + step) % (kP / 2);
+        } else {
+          rr_pair(step, t, kP - 1, p, q);
+        }
         const double a = G[p * kPad + p].x, b = G[q * kPad + q].x;
         const cplx g = G[p * kPad + q];
         const double c2 = cabs2(g);

@@ -48,24 +48,52 @@ __device__ __forceinline__ bool pair_ctx(const GateDesc& g, int gi, int round, c
   return true;
 }
 
-__device__ __forceinline__ void load_chunk_planes(const PairCtx& c, int e0, double* Tr, double* Ti, int t) {
-#pragma unroll
-  for (int s = 0; s < (kP * kE) / 256; ++s) {
-    const int idx = t + 256 * s;
-    const int vi = idx / kE, ee = idx % kE;
-    const cplx v = c.vec(vi)[e0 + ee];
-    Tr[ee * kPitchS + vi] = v.x;
-    Ti[ee * kPitchS + vi] = v.y;
-  }
+// Chunks of kC rows x 32 vectors stream through shared memory as split Re/Im
+// planes [row][vector] (pitch 36), double-buffered with cp.async so the next
+// chunk's loads are in flight while the DMMAs consume the current one.
+constexpr int kC = 32;
+constexpr int kChunkPlane = kC * kPitchS;  // doubles per plane
+
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// Lane mapping: a half-warp covers 4 rows x 4 vectors, which puts its 16
+// 8-byte shared writes in 16 distinct bank pairs at pitch 36; a warp covers 8
+// consecutive rows (one 128-byte line) of 4 vectors.
+struct ChunkLoader {
+  const double* src;  // this thread's first element (as doubles)
+  int soff;           // this thread's first shared offset
+  __device__ __forceinline__ void init(const PairCtx& c, int t) {
+    const int lane = t & 31, warp = t >> 5;
+    const int e = (lane & 3) + 4 * (lane >> 4);
+    const int vi = 4 * warp + ((lane >> 2) & 3);
+    src = reinterpret_cast<const double*>(c.vec(vi) + e);
+    soff = e * kPitchS + vi;
+  }
+  // rows e0 .. e0 + kC of the pair -> buffer (Tr at buf, Ti at buf + kChunkPlane)
+  __device__ __forceinline__ void issue(double* buf, int e0) const {
+#pragma unroll
+    for (int s = 0; s < kC / 8; ++s) {
+      const double* g = src + 2 * (e0 + 8 * s);
+      double* d = buf + soff + 8 * s * kPitchS;
+      cp_async8(d, g);
+      cp_async8(d + kChunkPlane, g + 1);
+    }
+    cp_async_commit();
+  }
+};
 
 struct GramSmem {
   union {
-    struct {
-      double Tr[kE * kPitchS];
-      double Ti[kE * kPitchS];
-    } t;
-    double Gx[64 * 65];
+    double buf[2][2 * kChunkPlane];
+    double Gx[64 * 65];  // real 64x64 Gram (after the chunk loop)
   } u;
   cplx G[kP * kPad];
 };
@@ -77,7 +105,8 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __r
                                                              const double* __restrict__ frob2, double floor_rel2,
                                                              const int* __restrict__ perm, long long perm_stride,
                                                              double* __restrict__ maxoff, int* __restrict__ need,
-                                                             cplx* __restrict__ gbuf, int max_pairs) {
+                                                             cplx* __restrict__ gbuf, int max_pairs,
+                                                             double* __restrict__ offsum) {
   const int gi = blockIdx.y;
   const GateDesc& g = gates[gi];
   PairCtx c;
@@ -85,9 +114,8 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __r
   extern __shared__ __align__(16) unsigned char smem_raw[];
   GramSmem& S = *reinterpret_cast<GramSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t % 32, warp = t / 32;
-  double* Tr = S.u.t.Tr;
-  double* Ti = S.u.t.Ti;
-  auto xext = [&](int e, int col) -> double { return (col < kP ? Tr : Ti)[e * kPitchS + (col & (kP - 1))]; };
+  ChunkLoader ld;
+  ld.init(c, t);
   const int fr = lane / 4, fk = lane % 4;
   // tiles of G_ext = [[A, B], [B^T, D]]: upper A and D, all of B (see jacobi_dmma.cu)
   int trow[5], tcol[5], nt;
@@ -113,19 +141,33 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __r
     }
     nt = 5;
   }
+  // column offsets (plane + index) of this thread's fragments
+  auto coff = [&](int col) { return (col < kP ? 0 : kChunkPlane) + (col & (kP - 1)); };
+  const int oa0 = coff(8 * trow[0] + fr), oa4 = coff(8 * trow[4] + fr);
+  int ob[5];
+#pragma unroll
+  for (int i = 0; i < 5; ++i) ob[i] = coff(8 * tcol[i] + fr);
   double acc[5][2];
 #pragma unroll
   for (int i = 0; i < 5; ++i) acc[i][0] = acc[i][1] = 0.0;
-  for (int e0 = 0; e0 < g.m_pad; e0 += kE) {
-    load_chunk_planes(c, e0, Tr, Ti, t);
+  const int nchunks = g.m_pad / kC;
+  ld.issue(S.u.buf[0], 0);
+  for (int k = 0; k < nchunks; ++k) {
+    if (k + 1 < nchunks) {
+      ld.issue(S.u.buf[(k + 1) & 1], (k + 1) * kC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
-#pragma unroll 4
-    for (int ks = 0; ks < kE / 4; ++ks) {
-      const int e = 4 * ks + fk;
-      const double a_first = xext(e, 8 * trow[0] + fr), a_last = xext(e, 8 * trow[4] + fr);
+    const double* B = S.u.buf[k & 1];
+#pragma unroll
+    for (int ks = 0; ks < kC / 4; ++ks) {
+      const int row = (4 * ks + fk) * kPitchS;
+      const double a_first = B[row + oa0], a_last = B[row + oa4];
 #pragma unroll
       for (int i = 0; i < 5; ++i)
-        if (i < nt) dmma_s(acc[i][0], acc[i][1], trow[i] == trow[0] ? a_first : a_last, xext(e, 8 * tcol[i] + fr));
+        if (i < nt) dmma_s(acc[i][0], acc[i][1], trow[i] == trow[0] ? a_first : a_last, B[row + ob[i]]);
     }
     __syncthreads();
   }
@@ -147,6 +189,16 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __r
   __syncthreads();
   const double tolg = tol * fmax(sqrt((double)g.m), (double)kP);
   const double floor2 = floor_rel2 * frob2[gi];
+  {
+    // sum of squared relative off-diagonals between the two blocks: the host
+    // turns it into the sweep's rms off-norm (cross-only EVD policy)
+    const int i = t >> 4, j = kW + (t & 15);
+    const double gii = S.G[i * kPad + i].x, gjj = S.G[j * kPad + j].x;
+    double r = (fmin(gii, gjj) > floor2) ? cabs2(S.G[i * kPad + j]) / (gii * gjj) : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (lane == 0 && r > 0.0) atomicAdd(offsum + gi, r);
+  }
   const bool nd = pair_needs_rotation(S.G, t, tolg, floor2, maxoff + gi);
   const long long slot = (long long)gi * max_pairs + blockIdx.x;
   if (t == 0) need[slot] = nd ? 1 : 0;
@@ -178,18 +230,24 @@ __global__ void __launch_bounds__(256, 6) jacobi_evd_kernel(const GateDesc* __re
   const cplx* gin = gbuf + slot * (kP * kP);
   for (int idx = t; idx < kP * kP; idx += 256) S.G[(idx / kP) * kPad + idx % kP] = gin[idx];
   __syncthreads();
-  pair_evd_v1(S.G, S.R, S.sc, t, tol_in, floor_rel2 * frob2[gi], 1);
+  pair_evd_v1(S.G, S.R, S.sc, t, tol_in, floor_rel2 * frob2[gi], 1, active[gi] == 2);
   __syncthreads();
   cplx* rout = rbuf + slot * (kP * kP);
   for (int idx = t; idx < kP * kP; idx += 256) rout[idx] = S.R[(idx / kP) * kPad + idx % kP];
 }
 
+constexpr int kPitchR = 68;  // R_ext row pitch (== 4 mod 16: conflict-free B fragments)
+
 struct RotSmem {
-  double Tr[kE * kPitchS];
-  double Ti[kE * kPitchS];
+  double buf[2][2 * kChunkPlane];
+  double Rx[2 * kP * kPitchR];  // R_ext[c_ext][j_ext] = [[Re R, Im R], [-Im R, Re R]]
 };
 
-__global__ void __launch_bounds__(256, 2) jacobi_rot_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
+// 3 CTAs x 72 KB per SM. Warp w computes row tiles {2(w&1), +1} of the chunk
+// and complex column tile w/2 (real column tiles w/2 and 4 + w/2): per k-step
+// two A and two B fragment loads feed four DMMAs, and each thread ends up
+// with Re and Im of the same complex outputs (16-byte global stores).
+__global__ void __launch_bounds__(256, 3) jacobi_rot_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
                                                             const int* __restrict__ active, int* __restrict__ rotated,
                                                             int round, const int* __restrict__ perm,
                                                             long long perm_stride, const int* __restrict__ need,
@@ -204,55 +262,55 @@ __global__ void __launch_bounds__(256, 2) jacobi_rot_kernel(const GateDesc* __re
   RotSmem& S = *reinterpret_cast<RotSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t % 32, warp = t / 32;
   const int fr = lane / 4, fk = lane % 4;
+  ChunkLoader ld;
+  ld.init(c, t);
+  const int nchunks = g.m_pad / kC;
+  ld.issue(S.buf[0], 0);
   const cplx* R = rbuf + slot * (kP * kP);
-  // warp: row tiles {2(w%4), +1}, complex column tiles {2(w/4), +1} (Re and Im)
-  const int rbase = 2 * (warp % 4), cbase = 2 * (warp / 4);
-  double bfrag[4][16];
-#pragma unroll
-  for (int ct = 0; ct < 4; ++ct) {
-    const int cj = cbase + (ct & 1);
-    const int jext = (ct < 2 ? 0 : kP) + 8 * cj + fr;
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {
-      const int cext = 4 * s + fk;
-      const cplx r = R[(cext & (kP - 1)) * kP + (jext & (kP - 1))];
-      double v;
-      if (cext < kP) v = jext < kP ? r.x : r.y;
-      else v = jext < kP ? -r.y : r.x;
-      bfrag[ct][s] = v;
-    }
+  for (int idx = t; idx < kP * kP; idx += 256) {
+    const int i = idx / kP, j = idx % kP;
+    const cplx r = R[idx];
+    S.Rx[i * kPitchR + j] = r.x;
+    S.Rx[i * kPitchR + kP + j] = r.y;
+    S.Rx[(kP + i) * kPitchR + j] = -r.y;
+    S.Rx[(kP + i) * kPitchR + kP + j] = r.x;
   }
-  double* Tr = S.Tr;
-  double* Ti = S.Ti;
-  for (int e0 = 0; e0 < g.m_pad; e0 += kE) {
-    load_chunk_planes(c, e0, Tr, Ti, t);
+  const int rbase = 2 * (warp & 1), cj = warp >> 1;
+  const int bre = 8 * cj + fr, bim = kP + 8 * cj + fr;
+  for (int k = 0; k < nchunks; ++k) {
+    if (k + 1 < nchunks) {
+      ld.issue(S.buf[(k + 1) & 1], (k + 1) * kC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
-    double o[2][4][2];
+    const double* B = S.buf[k & 1];
+    double o[2][2][2];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) o[a][q][0] = o[a][q][1] = 0.0;
+      for (int q = 0; q < 2; ++q) o[a][q][0] = o[a][q][1] = 0.0;
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
       const int cext = 4 * s + fk;
-#pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        const int e = 8 * (rbase + a) + fr;
-        const double av = (cext < kP ? Tr : Ti)[e * kPitchS + (cext & (kP - 1))];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) dmma_s(o[a][q][0], o[a][q][1], av, bfrag[q][s]);
-      }
+      const double* plane = B + (cext < kP ? 0 : kChunkPlane) + (cext & (kP - 1));
+      const double a0 = plane[(8 * rbase + fr) * kPitchS], a1 = plane[(8 * (rbase + 1) + fr) * kPitchS];
+      const double b0 = S.Rx[cext * kPitchR + bre], b1 = S.Rx[cext * kPitchR + bim];
+      dmma_s(o[0][0][0], o[0][0][1], a0, b0);
+      dmma_s(o[0][1][0], o[0][1][1], a0, b1);
+      dmma_s(o[1][0][0], o[1][0][1], a1, b0);
+      dmma_s(o[1][1][0], o[1][1][1], a1, b1);
     }
+    const int e0 = k * kC;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int q = 0; q < 2; ++q)
-#pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int e = 8 * (rbase + a) + fr;
-          const int j = 8 * (cbase + q) + 2 * fk + v;
-          c.vec(j)[e0 + e] = make_double2(o[a][q][v], o[a][q + 2][v]);
-        }
+      for (int v = 0; v < 2; ++v) {
+        const int e = 8 * (rbase + a) + fr;
+        const int j = 8 * cj + 2 * fk + v;
+        c.vec(j)[e0 + e] = make_double2(o[a][0][v], o[a][1][v]);
+      }
     __syncthreads();
   }
   if (t == 0) atomicAdd(rotated + gi, 1);
@@ -267,10 +325,10 @@ void jacobi_split_init() {
 void launch_jacobi_round_split(const GateDesc* d_gates, int n_gates, int max_pairs, cplx* ws, const int* d_active,
                                int* d_rotated, int round, double tol, double tol_in, const double* frob2,
                                double floor_rel2, const int* perm, long long perm_stride, double* maxoff, int* need,
-                               cplx* gbuf, cplx* rbuf, cudaStream_t st) {
+                               cplx* gbuf, cplx* rbuf, double* offsum, cudaStream_t st) {
   const dim3 grid(max_pairs, n_gates);
   jacobi_gram_kernel<<<grid, 256, sizeof(GramSmem), st>>>(d_gates, ws, d_active, round, tol, frob2, floor_rel2, perm,
-                                                           perm_stride, maxoff, need, gbuf, max_pairs);
+                                                           perm_stride, maxoff, need, gbuf, max_pairs, offsum);
   jacobi_evd_kernel<<<grid, 256, sizeof(EvdSmem), st>>>(d_gates, d_active, round, tol_in, frob2, floor_rel2, need,
                                                          gbuf, rbuf, max_pairs);
   jacobi_rot_kernel<<<grid, 256, sizeof(RotSmem), st>>>(d_gates, ws, d_active, d_rotated, round, perm, perm_stride,
