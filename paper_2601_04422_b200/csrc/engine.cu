@@ -33,7 +33,8 @@ void launch_jacobi_round_dmma(const GateDesc*, int, int, cplx*, const int*, int*
                               const double*, double, const int*, long long, double*, cudaStream_t);
 void jacobi_split_init();
 void launch_jacobi_round_split(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, const double*,
-                               double, const int*, long long, double*, int*, cplx*, cplx*, double*, cudaStream_t);
+                               double, const int*, long long, double*, int*, cplx*, cplx*, double*, bool,
+                               cudaStream_t);
 // Cross-only pair EVDs (evd.cuh) in a sweep whose predecessor measured an rms
 // relative off-norm above this (the pre-asymptotic phase); MPSIM_CROSS=0 disables.
 constexpr double kCrossRms = 0.35;
@@ -44,14 +45,16 @@ static bool cross_policy() {
   }();
   return on;
 }
-// Jacobi round implementation: "split" (default; Gram / EVD / rotation as three
-// launches, DMMA for both GEMMs), "dmma" (one fused DMMA kernel), "simt" (DFMA).
+// Jacobi round implementation: default = Gram + pair EVD in one kernel and the
+// rotation in a second (DMMA for both GEMMs); "split3" (Gram / EVD / rotation
+// as three launches), "dmma" (one fused DMMA kernel), "simt" (DFMA).
 static int jacobi_mode() {
   static const int m = [] {
     const char* v = std::getenv("MPSIM_JACOBI");
     if (v != nullptr && std::string(v) == "simt") return 0;
     if (v != nullptr && std::string(v) == "dmma") return 1;
-    return 2;
+    if (v != nullptr && std::string(v) == "split3") return 2;
+    return 3;
   }();
   return m;
 }
@@ -366,7 +369,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   bool converged = false;
   std::vector<int> still(ng, 1);
   s.d_maxoff.ensure(sizeof(double) * ng);
-  if (jacobi_mode() == 2) {
+  if (jacobi_mode() >= 2) {
     const size_t slots = (size_t)ng * (max_nb / 2);
     s.d_need.ensure(sizeof(int) * slots);
     s.d_gbuf.ensure(sizeof(cplx) * slots * kP * kP);
@@ -391,12 +394,12 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // outer iteration needs the same number of sweeps as with a fully
       // converged inner EVD (measured in emulation and on the B200), at a
       // fraction of the cost. Final orthogonality is at the tol level.
-      if (jacobi_mode() == 2) {
+      if (jacobi_mode() >= 2) {
         launch_jacobi_round_split(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round,
                                   4.0 * kEps, 2.0 * kEps, (const double*)s.d_frob.p, kFloorRel2,
                                   (const int*)s.d_perm.p, perm_stride, (double*)s.d_maxoff.p, (int*)s.d_need.p,
-                                  (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p, (double*)s.d_offsum.p, st);
-        s.launches += 2;  // three kernels per round (one more counted below)
+                                  (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p, (double*)s.d_offsum.p, jacobi_mode() == 3, st);
+        s.launches += jacobi_mode() == 3 ? 1 : 2;  // kernels per round beyond the one counted below
       } else {
         (dmma ? launch_jacobi_round_dmma : launch_jacobi_round)(
             dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps, 2.0 * kEps,
@@ -452,7 +455,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // pre-asymptotic (rms relative off-norm of the sweep above kCrossRms):
       // the next sweep's pair EVDs rotate the cross-block pairs only
       const double rms = std::sqrt(2.0 * h_offsum[i] / std::max(1, descs[i].n));
-      if (h_rot[i] && jacobi_mode() == 2 && cross_policy() && rms > kCrossRms && h_maxoff[i] > 1e-3) h_rot[i] = 2;
+      if (h_rot[i] && jacobi_mode() >= 2 && cross_policy() && rms > kCrossRms && h_maxoff[i] > 1e-3) h_rot[i] = 2;
     }
     if (!any) {
       converged = true;

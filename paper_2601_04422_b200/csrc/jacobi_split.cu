@@ -97,16 +97,25 @@ struct GramSmem {
   } u;
   cplx G[kP * kPad];
 };
+// Gram + pair EVD in one CTA (the EVD of one CTA overlaps the DMMA Gram of the
+// others on its SM)
+struct GramEvdSmem {
+  GramSmem g;
+  cplx R[kP * kPad];
+  EvdScratch sc;
+};
 
 }  // namespace
 
+template <bool kFuseEvd>
 __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
                                                              const int* __restrict__ active, int round, double tol,
                                                              const double* __restrict__ frob2, double floor_rel2,
                                                              const int* __restrict__ perm, long long perm_stride,
                                                              double* __restrict__ maxoff, int* __restrict__ need,
                                                              cplx* __restrict__ gbuf, int max_pairs,
-                                                             double* __restrict__ offsum) {
+                                                             double* __restrict__ offsum, cplx* __restrict__ rbuf,
+                                                             double tol_in) {
   const int gi = blockIdx.y;
   const GateDesc& g = gates[gi];
   PairCtx c;
@@ -203,8 +212,16 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __r
   const long long slot = (long long)gi * max_pairs + blockIdx.x;
   if (t == 0) need[slot] = nd ? 1 : 0;
   if (!nd) return;
-  cplx* gout = gbuf + slot * (kP * kP);
-  for (int idx = t; idx < kP * kP; idx += 256) gout[idx] = S.G[(idx / kP) * kPad + idx % kP];
+  if constexpr (kFuseEvd) {
+    GramEvdSmem& SE = *reinterpret_cast<GramEvdSmem*>(smem_raw);
+    pair_evd_v1(S.G, SE.R, SE.sc, t, tol_in, floor2, 1, active[gi] == 2);
+    __syncthreads();
+    cplx* rout = rbuf + slot * (kP * kP);
+    for (int idx = t; idx < kP * kP; idx += 256) rout[idx] = SE.R[(idx / kP) * kPad + idx % kP];
+  } else {
+    cplx* gout = gbuf + slot * (kP * kP);
+    for (int idx = t; idx < kP * kP; idx += 256) gout[idx] = S.G[(idx / kP) * kPad + idx % kP];
+  }
 }
 
 struct EvdSmem {
@@ -317,7 +334,9 @@ __global__ void __launch_bounds__(256, 3) jacobi_rot_kernel(const GateDesc* __re
 }
 
 void jacobi_split_init() {
-  cudaFuncSetAttribute(jacobi_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GramSmem));
+  cudaFuncSetAttribute(jacobi_gram_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GramSmem));
+  cudaFuncSetAttribute(jacobi_gram_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(GramEvdSmem));
   cudaFuncSetAttribute(jacobi_evd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EvdSmem));
   cudaFuncSetAttribute(jacobi_rot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RotSmem));
 }
@@ -325,12 +344,19 @@ void jacobi_split_init() {
 void launch_jacobi_round_split(const GateDesc* d_gates, int n_gates, int max_pairs, cplx* ws, const int* d_active,
                                int* d_rotated, int round, double tol, double tol_in, const double* frob2,
                                double floor_rel2, const int* perm, long long perm_stride, double* maxoff, int* need,
-                               cplx* gbuf, cplx* rbuf, double* offsum, cudaStream_t st) {
+                               cplx* gbuf, cplx* rbuf, double* offsum, bool fuse_evd, cudaStream_t st) {
   const dim3 grid(max_pairs, n_gates);
-  jacobi_gram_kernel<<<grid, 256, sizeof(GramSmem), st>>>(d_gates, ws, d_active, round, tol, frob2, floor_rel2, perm,
-                                                           perm_stride, maxoff, need, gbuf, max_pairs, offsum);
-  jacobi_evd_kernel<<<grid, 256, sizeof(EvdSmem), st>>>(d_gates, d_active, round, tol_in, frob2, floor_rel2, need,
-                                                         gbuf, rbuf, max_pairs);
+  if (fuse_evd) {
+    jacobi_gram_kernel<true><<<grid, 256, sizeof(GramEvdSmem), st>>>(d_gates, ws, d_active, round, tol, frob2,
+                                                                     floor_rel2, perm, perm_stride, maxoff, need,
+                                                                     gbuf, max_pairs, offsum, rbuf, tol_in);
+  } else {
+    jacobi_gram_kernel<false><<<grid, 256, sizeof(GramSmem), st>>>(d_gates, ws, d_active, round, tol, frob2,
+                                                                   floor_rel2, perm, perm_stride, maxoff, need, gbuf,
+                                                                   max_pairs, offsum, rbuf, tol_in);
+    jacobi_evd_kernel<<<grid, 256, sizeof(EvdSmem), st>>>(d_gates, d_active, round, tol_in, frob2, floor_rel2, need,
+                                                           gbuf, rbuf, max_pairs);
+  }
   jacobi_rot_kernel<<<grid, 256, sizeof(RotSmem), st>>>(d_gates, ws, d_active, d_rotated, round, perm, perm_stride,
                                                          need, rbuf, max_pairs);
 }
