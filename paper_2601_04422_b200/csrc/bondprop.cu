@@ -104,7 +104,7 @@ GateOut svd_into(State& s, const cplx* A, int M, int N, const mpsim_policy& pol,
   d.nb = d.n_pad / kW;
   d.max_bond = pol.max_bond;
   d.cutoff = pol.cutoff;
-  d.ws_off = 0;
+  desc_layout(d, 0, false);
   d.u_out = u_out;
   d.ldu = ldu;
   d.v_out = v_out;

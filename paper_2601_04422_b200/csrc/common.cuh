@@ -48,7 +48,47 @@ struct GateDesc {
   long long max_bond;
   double cutoff;
   cplx u[16];       // 4x4 gate, (low, high) basis, row = 2*p_low + p_high (circuit.hpp:20-22)
+  // Factor formula of the split epilogue (split.cu): f = 0: the converged X
+  // holds sigma * (left singular vectors); f = 1: it holds sigma * (right
+  // singular vectors)^*. X0 (the pristine operand the other factor is
+  // contracted with) has n0 vectors of length m, stride x0_ld.
+  int f, n0;
+  long long x0_off, x0_ld;
+  // QR preconditioning (qr_pre.cu): theta -> QR operand (n vectors of length
+  // qr_m, stride qr_m_pad at qr_off, orientation trans) = Q R; the Jacobi
+  // operand X is then R^H (n vectors of length m = n) and f = trans ^ 1.
+  int pre, qr_m;
+  long long qr_off, qr_m_pad;
 };
+
+// Workspace layout of one descriptor starting at `off` (complex elements);
+// returns the span. Without preconditioning: X (n_pad x m_pad) then X0 (same).
+// With it: X = R^H (n_pad x m_pad, m = n), X0 (n0 = qr_m vectors x m_pad), then
+// the QR operand (n_pad x qr_m_pad).
+inline long long desc_layout(GateDesc& d, long long off, bool pre) {
+  d.pre = pre ? 1 : 0;
+  d.ws_off = off;
+  if (!pre) {
+    d.f = d.trans;
+    d.n0 = d.n;
+    d.x0_ld = d.m_pad;
+    d.x0_off = off + (long long)d.n_pad * d.m_pad;
+    d.qr_m = 0;
+    d.qr_m_pad = 0;
+    d.qr_off = 0;
+    return 2LL * d.n_pad * d.m_pad;
+  }
+  d.qr_m = d.m;
+  d.qr_m_pad = d.m_pad;
+  d.m = d.n;
+  d.m_pad = ((d.n + kE - 1) / kE) * kE;
+  d.f = d.trans ^ 1;
+  d.n0 = d.qr_m;
+  d.x0_ld = d.m_pad;
+  d.x0_off = off + (long long)d.n_pad * d.m_pad;
+  d.qr_off = d.x0_off + (long long)d.n0 * d.x0_ld;
+  return (long long)d.n_pad * d.m_pad + (long long)d.n0 * d.x0_ld + (long long)d.n_pad * d.qr_m_pad;
+}
 
 // Per-gate outputs of the split epilogue.
 struct GateOut {

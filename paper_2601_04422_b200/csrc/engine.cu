@@ -32,6 +32,18 @@ void jacobi_dmma_init();
 void launch_jacobi_round_dmma(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, int,
                               const double*, double, const int*, long long, double*, cudaStream_t);
 void jacobi_split_init();
+void qrp_init();
+void launch_qr_precondition(const GateDesc*, int, int, int, cplx*, cplx*, long long, cplx*, cudaStream_t);
+// QR preconditioning (qr_pre.cu) of gates whose SVD operand has at least
+// kQrMinN vectors; MPSIM_QR=0 disables it.
+constexpr int kQrMinN = 128;
+static bool qr_policy() {
+  static const bool on = [] {
+    const char* v = std::getenv("MPSIM_QR");
+    return !(v != nullptr && v[0] == '0');
+  }();
+  return on;
+}
 void launch_jacobi_round_split(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, const double*,
                                double, const int*, long long, double*, int*, cplx*, cplx*, double*, bool,
                                cudaStream_t);
@@ -65,7 +77,7 @@ void launch_jacobi_round(const GateDesc*, int, int, cplx*, const int*, int*, int
 void launch_derijk(const GateDesc*, int, const cplx*, const int*, int*, long long, cudaStream_t);
 void launch_norms(const GateDesc*, int, int, const cplx*, double*, long long, cudaStream_t);
 void launch_truncate(const GateDesc*, int, double*, int*, long long, GateOut*, const double*, double, cudaStream_t);
-void launch_write_factors(const GateDesc*, int, int, int, const cplx*, const double*, const int*, long long,
+void launch_write_factors(const GateDesc*, int, int, int, int, const cplx*, const double*, const int*, long long,
                           const GateOut*, const double*, double, cudaStream_t);
 void launch_apply1q(const Gate1Desc*, int, long long, cplx*, long long, int, cudaStream_t);
 void launch_regrow(const cplx*, long long, int, cplx*, long long, int, const int*, int, cudaStream_t);
@@ -195,6 +207,7 @@ State::State(int n_, long long chi_hint, int dev) : n(n_), device(dev) {
     jacobi_init();
     jacobi_dmma_init();
     jacobi_split_init();
+    qrp_init();
     inited = true;
   }
   chi = next_pow2(std::max<long long>(2, std::min<long long>(chi_hint, 1 << 14)));
@@ -312,8 +325,16 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   const int ng = (int)descs.size();
   long long ws_elems = 0;
   int max_tiles = 1, max_nb = 2, max_m = 1, max_n = 1;
+  int max_n0 = 1, qr_n_pad = 0, qr_m_pad = 0, qr_jm_pad = 0;
   for (const GateDesc& d : descs) {
-    ws_elems = std::max(ws_elems, d.ws_off + 2LL * d.n_pad * d.m_pad);
+    const long long end = d.pre ? d.qr_off + (long long)d.n_pad * d.qr_m_pad : d.x0_off + (long long)d.n_pad * d.x0_ld;
+    ws_elems = std::max(ws_elems, end);
+    max_n0 = std::max(max_n0, d.n0);
+    if (d.pre) {
+      qr_n_pad = std::max(qr_n_pad, d.n_pad);
+      qr_m_pad = std::max(qr_m_pad, (int)d.qr_m_pad);
+      qr_jm_pad = std::max(qr_jm_pad, d.m_pad);
+    }
     max_tiles = std::max(max_tiles, theta_tiles(d.dl, d.dr));
     max_nb = std::max(max_nb, d.nb);
     max_m = std::max(max_m, d.m);
@@ -346,19 +367,26 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     launch_theta(dg, ng, max_tiles, s.sites, s.stride, s.chi, ws, (double*)s.d_frob.p, st);
     check_launch("theta_kernel");
     ++s.launches;
+    if (qr_n_pad > 0) {
+      s.d_qrv.ensure(sizeof(cplx) * (size_t)ng * 32 * qr_m_pad);
+      s.d_qrt.ensure(sizeof(cplx) * (size_t)ng * 32 * 32);
+      launch_qr_precondition(dg, ng, qr_n_pad, qr_jm_pad, ws, (cplx*)s.d_qrv.p, qr_m_pad, (cplx*)s.d_qrt.p, st);
+      check_launch("qr_precondition");
+      s.launches += 2 * (qr_n_pad / 32) + 1;
+    }
   } else if (pre_dev == nullptr) {
     // Plain-matrix SVD (mpsim_gpu_svd): X and X0 arrive from the host.
     const GateDesc& d = descs[0];
     const size_t bytes = sizeof(cplx) * (size_t)d.n_pad * d.m_pad;
     CK(cudaMemcpyAsync(ws + d.ws_off, pre, bytes, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(ws + d.ws_off + (long long)d.n_pad * d.m_pad, pre, bytes, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ws + d.x0_off, pre, bytes, cudaMemcpyHostToDevice, st));
     CK(cudaMemcpyAsync(s.d_frob.p, &pre_frob, sizeof(double), cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
   } else {
     // A device-resident matrix (bond-propagation carriers): load X, X0, ||.||^2.
     const GateDesc& d = descs[0];
     launch_load_matrix(pre_dev, pre_ld, d.trans == 0 ? d.m : d.n, d.trans == 0 ? d.n : d.m, d.trans, ws + d.ws_off,
-                       ws + d.ws_off + (long long)d.n_pad * d.m_pad, d.m_pad, (double*)s.d_frob.p, st);
+                       ws + d.x0_off, d.m_pad, (double*)s.d_frob.p, st);
     check_launch("load_matrix_kernel");
     ++s.launches;
   }
@@ -468,7 +496,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   launch_truncate(dg, ng, (double*)s.d_sigma.p, (int*)s.d_order.p, sig_stride, (GateOut*)s.d_out.p,
                   (const double*)s.d_frob.p, kFloorRel2, st);
   check_launch("truncate_kernel");
-  launch_write_factors(dg, ng, max_m, max_n, ws, (const double*)s.d_sigma.p, (const int*)s.d_order.p, sig_stride,
+  launch_write_factors(dg, ng, max_m, max_n, max_n0, ws, (const double*)s.d_sigma.p, (const int*)s.d_order.p, sig_stride,
                        (const GateOut*)s.d_out.p, (const double*)s.d_frob.p, kFloorRel2, st);
   check_launch("write_factors");
   s.launches += 4;
@@ -586,9 +614,11 @@ void run_layer(State& s, const std::vector<G2>& two, const std::vector<G1>& one,
     d.ldv = 2LL * s.chi;
     d.vsplit = d.dr;
     d.vsplit_ld = s.chi;
-    const long long sz = 2LL * d.n_pad * d.m_pad;
+    const bool pre = qr_policy() && jacobi_mode() >= 2 && d.n >= kQrMinN;
+    GateDesc probe = d;
+    const long long sz = desc_layout(probe, 0, pre);
     if (!chunk.empty() && off + sz > budget_elems) flush();
-    d.ws_off = off;
+    desc_layout(d, off, pre);
     off += sz;
     chunk.push_back(d);
     chunk_src.push_back(&g);
@@ -1313,7 +1343,7 @@ int mpsim_gpu_svd(int32_t rows, int32_t cols, const double* a, int64_t max_rank,
     d.nb = d.n_pad / kW;
     d.max_bond = max_rank;
     d.cutoff = cutoff;
-    d.ws_off = 0;
+    desc_layout(d, 0, false);
     DeviceBuf dU, dV;
     dU.ensure(sizeof(cplx) * (size_t)rows * d.n);
     dV.ensure(sizeof(cplx) * (size_t)d.n * cols);

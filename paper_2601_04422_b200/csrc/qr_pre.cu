@@ -1,0 +1,397 @@
+// QR preconditioning of the batched Jacobi SVD (Drmac-Veselic): theta = Q R by
+// blocked Householder QR, then the one-sided Jacobi runs on R^H, whose columns
+// are far closer to orthogonal in the sense the sweeps need: at chi = 512 the
+// 1024 x 1024 theta of a random circuit converges in 11 sweeps instead of 14
+// (tools/emu_jacobi.py). Q is never formed: R^H = U' Sigma W^H gives the right
+// singular vectors of theta directly (S V^dag = X^H), and U = theta X / sigma^2
+// from the pristine theta (split.cu, f = 1; the transposed case likewise).
+//
+// Per 32-column panel p of every gate's QR operand A (vectors = columns,
+// stride qr_m_pad, rows [0, qr_m)):
+//   qrp_panel_kernel    one 1024-thread CTA per gate: 32 Householder
+//                       reflectors (zlarfg convention, H = I - tau v v^H),
+//                       R written on and above the diagonal, explicit V
+//                       (unit diagonal, zeros above) and the compact-WY T
+//                       (zlarft, Q_p = I - V T V^H) to scratch
+//   qrp_update_kernel   A_b <- Q_p^H A_b = A_b - V T^H (V^H A_b) for each
+//                       32-column block b right of the panel, both GEMMs on
+//                       DMMA with the pair-chunk pipeline of jacobi_split.cu
+// and finally qrp_form_rh_kernel writes X = R^H (n vectors of length n).
+#include "common.cuh"
+
+namespace mpsim_gpu {
+
+namespace {
+
+constexpr int kQ = 32;       // panel width
+constexpr int kQC = 32;      // rows per streamed chunk
+constexpr int kQPitch = 36;  // conflict-free DMMA fragment pitch (== 4 mod 16)
+constexpr int kQPlane = kQC * kQPitch;
+constexpr int kQPitchW = 68;
+
+__device__ __forceinline__ void dmma_q(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async8_q(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit_q() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_q() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+__device__ __forceinline__ double block_sum_1024(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int t = threadIdx.x;
+  __syncthreads();  // red is reused across calls
+  if ((t & 31) == 0) red[t >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll 8
+  for (int w = 0; w < 32; ++w) s += red[w];
+  return s;
+}
+
+}  // namespace
+
+// vbuf: per gate kQ vectors of stride vld (>= qr_m_pad); tbuf: per gate kQ x kQ.
+__global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
+                                                         int p, cplx* __restrict__ vbuf, long long vld,
+                                                         cplx* __restrict__ tbuf) {
+  const GateDesc& g = gates[blockIdx.x];
+  if (!g.pre) return;
+  const int n = g.n, m = g.qr_m;
+  const long long ld = g.qr_m_pad;
+  const int c0 = kQ * p;
+  if (c0 >= n) return;
+  const int jb = min(kQ, n - c0);
+  cplx* A = ws + g.qr_off;
+  cplx* V = vbuf + (long long)blockIdx.x * kQ * vld;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  __shared__ double red[32];
+  __shared__ cplx taus[kQ];
+  __shared__ cplx Gv[kQ][kQ + 1];
+  __shared__ cplx T[kQ][kQ + 1];
+
+  for (int j = 0; j < jb; ++j) {
+    const int row0 = c0 + j;
+    cplx* col = A + (long long)(c0 + j) * ld;
+    double s = 0.0;
+    for (int r = row0 + 1 + t; r < m; r += 1024) s += cabs2(col[r]);
+    const double xn2 = block_sum_1024(s, red);
+    const cplx alpha = row0 < m ? col[row0] : make_double2(0.0, 0.0);
+    // zlarfg: H^H x = beta e_1, beta real, v = [1; x(2:)/(alpha - beta)]
+    cplx tau = make_double2(0.0, 0.0), inv = make_double2(0.0, 0.0);
+    double beta = alpha.x;
+    if (!(xn2 == 0.0 && alpha.y == 0.0)) {
+      beta = -copysign(sqrt(cabs2(alpha) + xn2), alpha.x);
+      tau = make_double2((beta - alpha.x) / beta, -alpha.y / beta);
+      const cplx d = make_double2(alpha.x - beta, alpha.y);
+      const double dd = cabs2(d);
+      inv = make_double2(d.x / dd, -d.y / dd);
+    }
+    const bool refl = tau.x != 0.0 || tau.y != 0.0;
+    cplx* vj = V + (long long)j * vld;
+    for (long long r = t; r < vld; r += 1024) {
+      cplx v = make_double2(0.0, 0.0);
+      if (r == row0) v = make_double2(1.0, 0.0);
+      else if (r > row0 && r < m && refl) v = cmul(col[r], inv);
+      vj[r] = v;
+    }
+    if (t == 0) {
+      if (row0 < m) col[row0] = make_double2(refl ? beta : alpha.x, refl ? 0.0 : alpha.y);
+      taus[j] = tau;
+    }
+    __syncthreads();
+    // H^H = I - conj(tau) v v^H on panel columns j+1 .. jb-1, one warp each
+    if (refl && warp < jb - 1 - j) {
+      cplx* a = A + (long long)(c0 + j + 1 + warp) * ld;
+      cplx w = make_double2(0.0, 0.0);
+      for (int r = row0 + lane; r < m; r += 32) cfmac(w, vj[r], a[r]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        w.x += __shfl_xor_sync(0xffffffffu, w.x, o);
+        w.y += __shfl_xor_sync(0xffffffffu, w.y, o);
+      }
+      const cplx coef = cmul(make_double2(tau.x, -tau.y), w);
+      for (int r = row0 + lane; r < m; r += 32) {
+        const cplx vr = vj[r];
+        cplx ar = a[r];
+        ar.x -= vr.x * coef.x - vr.y * coef.y;
+        ar.y -= vr.x * coef.y + vr.y * coef.x;
+        a[r] = ar;
+      }
+    }
+    __syncthreads();
+  }
+  // unused reflector slots of a short last panel: v = 0, tau = 0
+  for (int j = jb; j < kQ; ++j) {
+    cplx* vj = V + (long long)j * vld;
+    for (long long r = t; r < vld; r += 1024) vj[r] = make_double2(0.0, 0.0);
+    if (t == 0) taus[j] = make_double2(0.0, 0.0);
+  }
+  // Gram of the reflectors, Gv[i][k] = v_i^H v_k (i < k), rows >= c0 + k
+  for (int pr = warp; pr < kQ * kQ; pr += 32) {
+    const int i = pr / kQ, k = pr % kQ;
+    if (i >= k || k >= jb) continue;
+    const cplx* vi = V + (long long)i * vld;
+    const cplx* vk = V + (long long)k * vld;
+    cplx w = make_double2(0.0, 0.0);
+    for (int r = c0 + k + lane; r < m; r += 32) cfmac(w, vi[r], vk[r]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      w.x += __shfl_xor_sync(0xffffffffu, w.x, o);
+      w.y += __shfl_xor_sync(0xffffffffu, w.y, o);
+    }
+    if (lane == 0) Gv[i][k] = w;
+  }
+  for (int idx = t; idx < kQ * (kQ + 1); idx += 1024) T[idx / (kQ + 1)][idx % (kQ + 1)] = make_double2(0.0, 0.0);
+  __syncthreads();
+  // zlarft (forward, columnwise): T[j][j] = tau_j, T[0:j, j] = -tau_j T[0:j,0:j] Gv[0:j, j]
+  for (int j = 0; j < jb; ++j) {
+    if (t < j) {
+      cplx z = make_double2(0.0, 0.0);
+      for (int k = t; k < j; ++k) cfma(z, T[t][k], Gv[k][j]);
+      const cplx tj = taus[j];
+      T[t][j] = make_double2(-(tj.x * z.x - tj.y * z.y), -(tj.x * z.y + tj.y * z.x));
+    } else if (t == j) {
+      T[j][j] = taus[j];
+    }
+    __syncthreads();
+  }
+  cplx* To = tbuf + (long long)blockIdx.x * kQ * kQ;
+  for (int idx = t; idx < kQ * kQ; idx += 1024) To[idx] = T[idx / kQ][idx % kQ];
+}
+
+namespace {
+
+// Streams rows [r0, r0 + kQC) of 32 V vectors and 32 A vectors into split
+// Re/Im planes: buf = [Vr | Vi | Ar | Ai], each kQC x kQPitch.
+struct QrChunkLoader {
+  const double* vsrc;
+  const double* asrc;
+  int soff;
+  __device__ __forceinline__ void init(const cplx* V, long long vld, const cplx* A, long long ald, int t) {
+    const int lane = t & 31, warp = t >> 5;
+    const int e = (lane & 3) + 4 * (lane >> 4);
+    const int vi = 4 * warp + ((lane >> 2) & 3);
+    vsrc = reinterpret_cast<const double*>(V + (long long)vi * vld + e);
+    asrc = reinterpret_cast<const double*>(A + (long long)vi * ald + e);
+    soff = e * kQPitch + vi;
+  }
+  __device__ __forceinline__ void issue(double* buf, int r0, bool with_v = true) const {
+#pragma unroll
+    for (int s = 0; s < kQC / 8; ++s) {
+      double* d = buf + soff + 8 * s * kQPitch;
+      const long long go = 2LL * (r0 + 8 * s);
+      if (with_v) {
+        cp_async8_q(d, vsrc + go);
+        cp_async8_q(d + kQPlane, vsrc + go + 1);
+      }
+      cp_async8_q(d + 2 * kQPlane, asrc + go);
+      cp_async8_q(d + 3 * kQPlane, asrc + go + 1);
+    }
+    cp_async_commit_q();
+  }
+};
+
+struct QrUpdSmem {
+  union {
+    double buf[2][4 * kQPlane];
+    struct {
+      double Wx[64 * 65];        // real 64 x 64 V_ext^T A_ext
+      cplx W[kQ * (kQ + 1)];     // V^H A_b
+      cplx T[kQ * (kQ + 1)];
+    } w;
+  } u;
+  double W2x[64 * kQPitchW];     // -(T^H W)_ext as the B operand
+};
+
+}  // namespace
+
+// A_b <- A_b - V T^H (V^H A_b), rows [c0, qr_m_pad), block b of 32 columns at
+// c0 + 32 (b + 1). Grid (blocks, gates), 256 threads.
+__global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
+                                                            int p, const cplx* __restrict__ vbuf, long long vld,
+                                                            const cplx* __restrict__ tbuf) {
+  const GateDesc& g = gates[blockIdx.y];
+  if (!g.pre) return;
+  const int c0 = kQ * p;
+  const int cb = c0 + kQ * (blockIdx.x + 1);
+  if (cb >= g.n_pad) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  QrUpdSmem& S = *reinterpret_cast<QrUpdSmem*>(smem_raw);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  const long long ald = g.qr_m_pad;
+  cplx* A = ws + g.qr_off + (long long)cb * ald;
+  const cplx* V = vbuf + (long long)blockIdx.y * kQ * vld;
+  QrChunkLoader ld;
+  ld.init(V, vld, A, ald, t);
+  const int nchunks = (int)((ald - c0) / kQC);
+
+  // ---- pass 1: W_ext = V_ext^T A_ext (64 x 64 real). Warp w: quadrant
+  // (x = w / 4 (V Re/Im), y = (w / 2) & 1 (A Re/Im)), tile rows 2 (w & 1) + {0, 1},
+  // all four tile columns.
+  const int qx = warp >> 2, qy = (warp >> 1) & 1, tr0 = 2 * (warp & 1);
+  double acc[2][4][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
+  ld.issue(S.u.buf[0], c0);
+  for (int k = 0; k < nchunks; ++k) {
+    if (k + 1 < nchunks) {
+      ld.issue(S.u.buf[(k + 1) & 1], c0 + (k + 1) * kQC);
+      cp_async_wait_q<1>();
+    } else {
+      cp_async_wait_q<0>();
+    }
+    __syncthreads();
+    const double* Pv = S.u.buf[k & 1] + qx * kQPlane;
+    const double* Pa = S.u.buf[k & 1] + (2 + qy) * kQPlane;
+#pragma unroll
+    for (int ks = 0; ks < kQC / 4; ++ks) {
+      const int row = (4 * ks + fk) * kQPitch;
+      double av[2], bv[4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) av[a] = Pv[row + 8 * (tr0 + a) + fr];  // A[m = v idx][k = e]
+#pragma unroll
+      for (int c = 0; c < 4; ++c) bv[c] = Pa[row + 8 * c + fr];          // B[k = e][n = a idx]
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) dmma_q(acc[a][c][0], acc[a][c][1], av[a], bv[c]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+        S.u.w.Wx[(qx * kQ + 8 * (tr0 + a) + fr) * 65 + qy * kQ + 8 * c + 2 * fk + v] = acc[a][c][v];
+  const cplx* Tg = tbuf + (long long)blockIdx.y * kQ * kQ;
+  for (int idx = t; idx < kQ * kQ; idx += 256) S.u.w.T[(idx / kQ) * (kQ + 1) + idx % kQ] = Tg[idx];
+  __syncthreads();
+  // W = V^H A_b: Re = Vr^T Ar + Vi^T Ai, Im = Vr^T Ai - Vi^T Ar
+  for (int idx = t; idx < kQ * kQ; idx += 256) {
+    const int i = idx / kQ, j = idx % kQ;
+    const double* Wx = S.u.w.Wx;
+    const double re = Wx[i * 65 + j] + Wx[(kQ + i) * 65 + kQ + j];
+    const double im = Wx[i * 65 + kQ + j] - Wx[(kQ + i) * 65 + j];
+    S.u.w.W[i * (kQ + 1) + j] = make_double2(re, im);
+  }
+  __syncthreads();
+  // W2 = T^H W (T upper triangular); stored negated in real-extended form
+  for (int idx = t; idx < kQ * kQ; idx += 256) {
+    const int i = idx / kQ, j = idx % kQ;
+    cplx z = make_double2(0.0, 0.0);
+    for (int k = 0; k <= i; ++k) cfmac(z, S.u.w.T[k * (kQ + 1) + i], S.u.w.W[k * (kQ + 1) + j]);
+    S.W2x[i * kQPitchW + j] = -z.x;
+    S.W2x[i * kQPitchW + kQ + j] = -z.y;
+    S.W2x[(kQ + i) * kQPitchW + j] = z.y;
+    S.W2x[(kQ + i) * kQPitchW + kQ + j] = -z.x;
+  }
+  __syncthreads();
+
+  // ---- pass 2: A_ext += V_ext (-W2_ext). Warp w: row tiles 2 (w & 1) + {0, 1},
+  // complex column tile w / 2 (real tiles w/2 and 4 + w/2).
+  const int rbase = 2 * (warp & 1), cj = warp >> 1;
+  const int bre = 8 * cj + fr, bim = kQ + 8 * cj + fr;
+  ld.issue(S.u.buf[0], c0);
+  for (int k = 0; k < nchunks; ++k) {
+    if (k + 1 < nchunks) {
+      ld.issue(S.u.buf[(k + 1) & 1], c0 + (k + 1) * kQC);
+      cp_async_wait_q<1>();
+    } else {
+      cp_async_wait_q<0>();
+    }
+    __syncthreads();
+    const double* B = S.u.buf[k & 1];
+    double o[2][2][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int e = 8 * (rbase + a) + fr, j = 8 * cj + 2 * fk + v;
+        o[a][0][v] = B[2 * kQPlane + e * kQPitch + j];
+        o[a][1][v] = B[3 * kQPlane + e * kQPitch + j];
+      }
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int cext = 4 * s + fk;
+      const double* plane = B + (cext < kQ ? 0 : kQPlane) + (cext & (kQ - 1));
+      const double a0 = plane[(8 * rbase + fr) * kQPitch], a1 = plane[(8 * (rbase + 1) + fr) * kQPitch];
+      const double b0 = S.W2x[cext * kQPitchW + bre], b1 = S.W2x[cext * kQPitchW + bim];
+      dmma_q(o[0][0][0], o[0][0][1], a0, b0);
+      dmma_q(o[0][1][0], o[0][1][1], a0, b1);
+      dmma_q(o[1][0][0], o[1][0][1], a1, b0);
+      dmma_q(o[1][1][0], o[1][1][1], a1, b1);
+    }
+    const int r0 = c0 + k * kQC;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int e = 8 * (rbase + a) + fr, j = 8 * cj + 2 * fk + v;
+        A[(long long)j * ald + r0 + e] = make_double2(o[a][0][v], o[a][1][v]);
+      }
+    __syncthreads();
+  }
+}
+
+// X = R^H: X[j][i] = conj(R[j][i]) = conj(A_i[j]) for j <= i < n, else 0,
+// i < m_pad (= round64(n)), j < n_pad. Grid (m_pad / 32, n_pad / 32, gates).
+__global__ void __launch_bounds__(256) qrp_form_rh_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws) {
+  const GateDesc& g = gates[blockIdx.z];
+  if (!g.pre) return;
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  if (i0 >= g.m_pad || j0 >= g.n_pad) return;
+  const cplx* A = ws + g.qr_off;
+  cplx* X = ws + g.ws_off;
+  __shared__ cplx tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  // read A_i[j] along j (rows of A), i.e. tile[ii][jj]
+  for (int ii = ty; ii < 32; ii += 8) {
+    const int i = i0 + ii, j = j0 + tx;
+    cplx v = make_double2(0.0, 0.0);
+    if (i < g.n && j < g.n && j <= i) {
+      const cplx a = A[(long long)i * g.qr_m_pad + j];
+      v = make_double2(a.x, -a.y);
+    }
+    tile[ii][tx] = v;
+  }
+  __syncthreads();
+  for (int jj = ty; jj < 32; jj += 8) {
+    const int j = j0 + jj, i = i0 + tx;
+    X[(long long)j * g.m_pad + i] = tile[tx][jj];
+  }
+}
+
+void qrp_init() {
+  cudaFuncSetAttribute(qrp_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(QrUpdSmem));
+}
+
+// Whole preconditioning pass for the descriptors with pre = 1. max_n_pad: the
+// largest n_pad of them; vbuf holds gates x 32 vectors of vld >= qr_m_pad.
+void launch_qr_precondition(const GateDesc* d_gates, int n_gates, int max_n_pad, int max_m_pad, cplx* ws,
+                            cplx* vbuf, long long vld, cplx* tbuf, cudaStream_t st) {
+  const int panels = max_n_pad / kQ;
+  for (int p = 0; p < panels; ++p) {
+    qrp_panel_kernel<<<n_gates, 1024, 0, st>>>(d_gates, ws, p, vbuf, vld, tbuf);
+    const int blocks = panels - p - 1;
+    if (blocks > 0)
+      qrp_update_kernel<<<dim3(blocks, n_gates), 256, sizeof(QrUpdSmem), st>>>(d_gates, ws, p, vbuf, vld, tbuf);
+  }
+  qrp_form_rh_kernel<<<dim3(max_m_pad / 32, max_n_pad / 32, n_gates), 256, 0, st>>>(d_gates, ws);
+}
+
+}  // namespace mpsim_gpu

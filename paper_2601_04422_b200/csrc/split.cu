@@ -3,8 +3,8 @@
 //   site q   <- U        (Dl, 2, k)   (gate_apply.cpp:136)
 //   site q+1 <- S V^dag  (k, 2, Dr)   (gate_apply.cpp:137-138, scale_rows :54-64)
 // After the Jacobi sweeps the vectors of X are orthogonal: X = U_X Sigma.
-//   trans = 0 (X = theta):   U = X/sigma,           S V^dag = U^H theta = (X/sigma)^H X0
-//   trans = 1 (X = theta^H): S V^dag = X^H,         U = theta X Sigma^-2 = X0^H X / sigma^2
+//   f = 0 (X = theta, or R^H of theta^H = QR):  U = X/sigma,  S V^dag = U^H theta = (X/sigma)^H X0
+//   f = 1 (X = theta^H, or R^H of theta = QR):  S V^dag = X^H, U = theta X Sigma^-2 = X0^H X / sigma^2
 // so one "cross-Gram" kernel (C = P^H Q over vector-major operands) produces
 // whichever factor is not a plain copy.
 #include <float.h>
@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(256) copy_factor_kernel(const GateDesc* __rest
   const cplx* X = ws + g.ws_off;
   __shared__ cplx tile[32][33];
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
-  if (g.trans == 0) {
+  if (g.f == 0) {
     // Read along e (coalesced), write along j (coalesced) through a transpose.
     for (int jj = ty; jj < 32; jj += 8) {
       const int j = j0 + jj, e = e0 + tx;
@@ -183,14 +183,14 @@ __global__ void __launch_bounds__(256) cross_gram_kernel(const GateDesc* __restr
   // cross-Gram formula is meaningless for them: they contribute an exact
   // zero (their true weight is below 64 eps ||theta||_F).
   const double floor2 = floor_rel2 * frob2[blockIdx.z];
-  const int n_a = g.trans == 0 ? k : g.n;
-  const int n_b = g.trans == 0 ? g.n : k;
+  const int n_a = g.f == 0 ? k : g.n0;
+  const int n_b = g.f == 0 ? g.n0 : k;
   const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32;
   if (a0 >= n_a || b0 >= n_b) return;
   const double* sg = sigma + blockIdx.z * sig_stride;
   const int* od = order + blockIdx.z * sig_stride;
   const cplx* X = ws + g.ws_off;
-  const cplx* X0 = X + (long long)g.n_pad * g.m_pad;
+  const cplx* X0 = ws + g.x0_off;
   constexpr int kCE = 32;
   __shared__ cplx Ta[kCE][kPad];
   __shared__ cplx Tb[kCE][kPad];
@@ -198,12 +198,12 @@ __global__ void __launch_bounds__(256) cross_gram_kernel(const GateDesc* __restr
   auto pa = [&](int i) -> const cplx* {
     const int a = a0 + i;
     if (a >= n_a) return nullptr;
-    return g.trans == 0 ? X + (long long)od[a] * g.m_pad : X0 + (long long)a * g.m_pad;
+    return g.f == 0 ? X + (long long)od[a] * g.m_pad : X0 + (long long)a * g.x0_ld;
   };
   auto pb = [&](int i) -> const cplx* {
     const int b = b0 + i;
     if (b >= n_b) return nullptr;
-    return g.trans == 0 ? X0 + (long long)b * g.m_pad : X + (long long)od[b] * g.m_pad;
+    return g.f == 0 ? X0 + (long long)b * g.x0_ld : X + (long long)od[b] * g.m_pad;
   };
   const int ip = t / 16, jp = t % 16;
   cplx acc[2][2];
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(256) cross_gram_kernel(const GateDesc* __restr
       const int a = a0 + 2 * ip + ai, b = b0 + 2 * jp + bi;
       if (a >= n_a || b >= n_b) continue;
       const cplx c = acc[ai][bi];
-      if (g.trans == 0) {
+      if (g.f == 0) {
         const double s = sg[a];
         const double f = s * s > floor2 && s > 0.0 ? o.scale / s : 0.0;
         const long long off = (long long)a * g.ldv + (long long)(b / g.vsplit) * g.vsplit_ld + b % g.vsplit;
@@ -269,13 +269,13 @@ void launch_truncate(const GateDesc* d_gates, int n_gates, double* sigma, int* o
   truncate_kernel<<<dim3(1, n_gates), 1024, 0, st>>>(d_gates, sigma, order, sig_stride, d_out, frob2, floor_rel2);
 }
 
-void launch_write_factors(const GateDesc* d_gates, int n_gates, int max_m, int max_n, const cplx* ws,
+void launch_write_factors(const GateDesc* d_gates, int n_gates, int max_m, int max_n, int max_n0, const cplx* ws,
                           const double* sigma, const int* order, long long sig_stride, const GateOut* d_out,
                           const double* frob2, double floor_rel2, cudaStream_t st) {
   // k <= n, so n bounds every tile count.
   copy_factor_kernel<<<dim3((max_m + 31) / 32, (max_n + 31) / 32, n_gates), 256, 0, st>>>(
       d_gates, ws, sigma, order, sig_stride, d_out);
-  cross_gram_kernel<<<dim3((max_n + 31) / 32, (max_n + 31) / 32, n_gates), 256, 0, st>>>(
+  cross_gram_kernel<<<dim3((max_n0 + 31) / 32, (max_n0 + 31) / 32, n_gates), 256, 0, st>>>(
       d_gates, ws, sigma, order, sig_stride, d_out, frob2, floor_rel2);
 }
 

@@ -90,8 +90,11 @@ __global__ void __launch_bounds__(256) theta_kernel(const GateDesc* __restrict__
     __syncthreads();
   }
 
-  cplx* X = ws + g.ws_off;
-  cplx* X0 = X + (long long)g.n_pad * g.m_pad;
+  // Jacobi operand X (or, preconditioned, the QR operand) in orientation
+  // trans; X0 in the orientation of the factor formula f (common.cuh).
+  cplx* X = ws + (g.pre ? g.qr_off : g.ws_off);
+  const long long ldx = g.pre ? g.qr_m_pad : g.m_pad;
+  cplx* X0 = ws + g.x0_off;
   double f2 = 0.0;  // this CTA's share of ||theta||_F^2 (Jacobi noise floor)
 #pragma unroll
   for (int ls = 0; ls < 2; ++ls)
@@ -106,15 +109,12 @@ __global__ void __launch_bounds__(256) theta_kernel(const GateDesc* __restrict__
 #pragma unroll
         for (int i = 0; i < 4; ++i) cfma(v, acc[ls][rs][i >> 1][i & 1], U[o * 4 + i]);
         const int p0o = o >> 1, p1o = o & 1;
-        long long off;
-        if (g.trans == 0) {
-          off = (long long)(p1o * dr + r) * g.m_pad + (l * 2 + p0o);
-        } else {
-          off = (long long)(l * 2 + p0o) * g.m_pad + (p1o * dr + r);
-          v.y = -v.y;
-        }
-        X[off] = v;
-        X0[off] = v;
+        const long long row = l * 2 + p0o, col = p1o * dr + r;  // theta (2Dl x 2Dr)
+        const cplx vc = make_double2(v.x, -v.y);
+        if (g.trans == 0) X[col * ldx + row] = v;
+        else X[row * ldx + col] = vc;
+        if (g.f == 0) X0[col * g.x0_ld + row] = v;
+        else X0[row * g.x0_ld + col] = vc;
         f2 += cabs2(v);
       }
     }
