@@ -45,11 +45,21 @@ static bool qr_policy() {
   return on;
 }
 void launch_jacobi_round_split(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, const double*,
-                               double, const int*, long long, double*, int*, cplx*, cplx*, double*, bool,
+                               double, const int*, long long, double*, int*, cplx*, cplx*, double*, int, cplx*,
                                cudaStream_t);
 // Cross-only pair EVDs (evd.cuh) in a sweep whose predecessor measured an rms
 // relative off-norm above this (the pre-asymptotic phase); MPSIM_CROSS=0 disables.
 constexpr double kCrossRms = 0.35;
+// Stored in-block Grams while the previous sweep's largest relative
+// off-diagonal exceeds this; MPSIM_INBLOCK=0 disables.
+constexpr double kInblockMaxoff = 1e-4;
+static bool inblock_policy() {
+  static const bool on = [] {
+    const char* v = std::getenv("MPSIM_INBLOCK");
+    return !(v != nullptr && v[0] == '0');
+  }();
+  return on;
+}
 static bool cross_policy() {
   static const bool on = [] {
     const char* v = std::getenv("MPSIM_CROSS");
@@ -66,7 +76,8 @@ static int jacobi_mode() {
     if (v != nullptr && std::string(v) == "simt") return 0;
     if (v != nullptr && std::string(v) == "dmma") return 1;
     if (v != nullptr && std::string(v) == "split3") return 2;
-    return 3;
+    if (v != nullptr && std::string(v) == "split2") return 3;
+    return 4;
   }();
   return m;
 }
@@ -402,6 +413,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     s.d_need.ensure(sizeof(int) * slots);
     s.d_gbuf.ensure(sizeof(cplx) * slots * kP * kP);
     s.d_rbuf.ensure(sizeof(cplx) * slots * kP * kP);
+    s.d_gblk.ensure(sizeof(cplx) * slots * 2 * kW * kW);
   }
   s.h_maxoff.ensure(sizeof(double) * ng);
   double* h_maxoff = (double*)s.h_maxoff.p;
@@ -426,8 +438,9 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
         launch_jacobi_round_split(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round,
                                   4.0 * kEps, 2.0 * kEps, (const double*)s.d_frob.p, kFloorRel2,
                                   (const int*)s.d_perm.p, perm_stride, (double*)s.d_maxoff.p, (int*)s.d_need.p,
-                                  (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p, (double*)s.d_offsum.p, jacobi_mode() == 3, st);
-        s.launches += jacobi_mode() == 3 ? 1 : 2;  // kernels per round beyond the one counted below
+                                  (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p, (double*)s.d_offsum.p, jacobi_mode() - 2,
+                                  (cplx*)s.d_gblk.p, st);
+        s.launches += 4 - jacobi_mode();  // kernels per round beyond the one counted below
       } else {
         (dmma ? launch_jacobi_round_dmma : launch_jacobi_round)(
             dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps, 2.0 * kEps,
@@ -483,7 +496,10 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // pre-asymptotic (rms relative off-norm of the sweep above kCrossRms):
       // the next sweep's pair EVDs rotate the cross-block pairs only
       const double rms = std::sqrt(2.0 * h_offsum[i] / std::max(1, descs[i].n));
-      if (h_rot[i] && jacobi_mode() >= 2 && cross_policy() && rms > kCrossRms && h_maxoff[i] > 1e-3) h_rot[i] = 2;
+      if (h_rot[i] && jacobi_mode() >= 2 && cross_policy() && rms > kCrossRms && h_maxoff[i] > 1e-3) h_rot[i] |= 2;
+      // pre-asymptotic and early asymptotic sweeps reuse the in-block Grams the
+      // pair EVDs leave behind (jacobi_split.cu); the closing sweeps recompute all
+      if (h_rot[i] && jacobi_mode() >= 3 && inblock_policy() && h_maxoff[i] > kInblockMaxoff) h_rot[i] |= 4;
     }
     if (!any) {
       converged = true;

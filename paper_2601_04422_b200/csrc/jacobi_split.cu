@@ -90,24 +90,90 @@ struct ChunkLoader {
   }
 };
 
-struct GramSmem {
+constexpr int kPitchR = 68;  // R_ext row pitch (== 4 mod 16: conflict-free B fragments)
+
+// Gram (+ pair EVD (+ rotation)) of one block pair in one CTA. R aliases the
+// chunk buffers / Gx, dead once G is built; R_ext aliases G, dead once the
+// in-block Grams are stored: 72 KB per CTA, three CTAs per SM.
+struct PairSmem {
   union {
     double buf[2][2 * kChunkPlane];
     double Gx[64 * 65];  // real 64x64 Gram (after the chunk loop)
   } u;
-  cplx G[kP * kPad];
-};
-// Gram + pair EVD in one CTA (the EVD of one CTA overlaps the DMMA Gram of the
-// others on its SM)
-struct GramEvdSmem {
-  GramSmem g;
-  cplx R[kP * kPad];
+  union {
+    cplx G[kP * kPad];
+    double Rx[2 * kP * kPitchR];  // R_ext[c_ext][j_ext] = [[Re R, Im R], [-Im R, Re R]]
+  } v;
   EvdScratch sc;
 };
+static_assert(sizeof(cplx) * kP * kPad <= sizeof(PairSmem::u), "R must fit in the chunk buffers");
+
+// X_P <- X_P R_ext over all chunks (R_ext in shared memory). Warp w computes
+// row tiles {2(w&1), +1} of a chunk and complex column tile w/2 (real column
+// tiles w/2 and 4 + w/2): per k-step two A and two B fragment loads feed four
+// DMMAs, and each thread ends up with Re and Im of the same complex outputs
+// (16-byte global stores).
+__device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader& ld, double (*buf)[2 * kChunkPlane],
+                                            const double* Rx, int nchunks, int t) {
+  const int lane = t % 32, warp = t / 32;
+  const int fr = lane / 4, fk = lane % 4;
+  const int rbase = 2 * (warp & 1), cj = warp >> 1;
+  const int bre = 8 * cj + fr, bim = kP + 8 * cj + fr;
+  for (int k = 0; k < nchunks; ++k) {
+    if (k + 1 < nchunks) {
+      ld.issue(buf[(k + 1) & 1], (k + 1) * kC);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double* B = buf[k & 1];
+    double o[2][2][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) o[a][q][0] = o[a][q][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+      const int cext = 4 * s + fk;
+      const double* plane = B + (cext < kP ? 0 : kChunkPlane) + (cext & (kP - 1));
+      const double a0 = plane[(8 * rbase + fr) * kPitchS], a1 = plane[(8 * (rbase + 1) + fr) * kPitchS];
+      const double b0 = Rx[cext * kPitchR + bre], b1 = Rx[cext * kPitchR + bim];
+      dmma_s(o[0][0][0], o[0][0][1], a0, b0);
+      dmma_s(o[0][1][0], o[0][1][1], a0, b1);
+      dmma_s(o[1][0][0], o[1][0][1], a1, b0);
+      dmma_s(o[1][1][0], o[1][1][1], a1, b1);
+    }
+    const int e0 = k * kC;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int e = 8 * (rbase + a) + fr;
+        const int j = 8 * cj + 2 * fk + v;
+        c.vec(j)[e0 + e] = make_double2(o[a][0][v], o[a][1][v]);
+      }
+    __syncthreads();
+  }
+}
+
+// R (complex, pitch kPad) -> R_ext
+__device__ __forceinline__ void expand_rotation(const cplx* R, long long rpitch, double* Rx, int t) {
+  for (int idx = t; idx < kP * kP; idx += 256) {
+    const int i = idx / kP, j = idx % kP;
+    const cplx r = R[i * rpitch + j];
+    Rx[i * kPitchR + j] = r.x;
+    Rx[i * kPitchR + kP + j] = r.y;
+    Rx[(kP + i) * kPitchR + j] = -r.y;
+    Rx[(kP + i) * kPitchR + kP + j] = r.x;
+  }
+}
 
 }  // namespace
 
-template <bool kFuseEvd>
+// kMode 0: Gram only (G -> gbuf); 1: Gram + pair EVD (R -> rbuf); 2: the whole
+// pair visit, Gram + EVD + rotation, in one CTA.
+template <int kMode>
 __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
                                                              const int* __restrict__ active, int round, double tol,
                                                              const double* __restrict__ frob2, double floor_rel2,
@@ -115,20 +181,39 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __r
                                                              double* __restrict__ maxoff, int* __restrict__ need,
                                                              cplx* __restrict__ gbuf, int max_pairs,
                                                              double* __restrict__ offsum, cplx* __restrict__ rbuf,
-                                                             double tol_in) {
+                                                             double tol_in, cplx* __restrict__ gblk,
+                                                             int* __restrict__ rotated) {
+  constexpr bool kFuseEvd = kMode >= 1;
   const int gi = blockIdx.y;
   const GateDesc& g = gates[gi];
   PairCtx c;
   if (!pair_ctx(g, gi, round, active, ws, perm, perm_stride, c)) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  GramSmem& S = *reinterpret_cast<GramSmem*>(smem_raw);
+  PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
+  cplx* const SG = S.v.G;
   const int t = threadIdx.x, lane = t % 32, warp = t / 32;
   ChunkLoader ld;
   ld.init(c, t);
   const int fr = lane / 4, fk = lane % 4;
+  // Stored in-block Grams (active bit 4, rounds > 0 of a pre-asymptotic
+  // sweep): the in-block 16 x 16 Grams of both blocks are those the pair EVD
+  // left at the blocks' previous visit this sweep (R^H G R, exact up to
+  // rounding: the blocks have not changed since), so only the cross block
+  // X_a^H X_b is computed: 16 of the 36 DMMA tiles.
+  const bool approx = kFuseEvd && (active[gi] & 4) && round > 0;
+  cplx* const gblk_a = gblk + ((long long)gi * 2 * max_pairs + c.ba) * (kW * kW);
+  cplx* const gblk_b = gblk + ((long long)gi * 2 * max_pairs + c.bb) * (kW * kW);
   // tiles of G_ext = [[A, B], [B^T, D]]: upper A and D, all of B (see jacobi_dmma.cu)
   int trow[5], tcol[5], nt;
-  if (warp < 4) {
+  if (approx) {
+    // cross block: rows Re_a / Im_a (tiles 0, 1, 4, 5), cols Re_b / Im_b (2, 3, 6, 7)
+    const int r = warp >> 1, c = 2 * (warp & 1);
+    nt = 2;
+    trow[0] = trow[1] = r + (r >= 2 ? 2 : 0);
+    tcol[0] = c + (c >= 2 ? 4 : 2);
+    tcol[1] = tcol[0] + 1;
+    trow[2] = trow[3] = trow[4] = tcol[2] = tcol[3] = tcol[4] = 0;
+  } else if (warp < 4) {
     nt = 4;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -186,14 +271,26 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __r
 #pragma unroll
       for (int v = 0; v < 2; ++v) S.u.Gx[(8 * trow[i] + fr) * 65 + 8 * tcol[i] + fk * 2 + v] = acc[i][v];
   __syncthreads();
-  for (int idx = t; idx < kP * kP; idx += 256) {
-    const int i = idx / kP, j = idx % kP;
-    if (i > j) continue;
+  if (approx) {
     const double* Gx = S.u.Gx;
+    const int i = t >> 4, j = kW + (t & 15);
     const double re = Gx[i * 65 + j] + Gx[(kP + i) * 65 + kP + j];
-    const double im = Gx[i * 65 + kP + j] - Gx[j * 65 + kP + i];
-    S.G[i * kPad + j] = make_double2(re, i == j ? 0.0 : im);
-    if (i != j) S.G[j * kPad + i] = make_double2(re, -im);
+    const double im = Gx[i * 65 + kP + j] - Gx[(kP + i) * 65 + j];
+    SG[i * kPad + j] = make_double2(re, im);
+    SG[j * kPad + i] = make_double2(re, -im);
+    const int r = t >> 4, q = t & 15;
+    SG[r * kPad + q] = gblk_a[t];
+    SG[(kW + r) * kPad + kW + q] = gblk_b[t];
+  } else {
+    for (int idx = t; idx < kP * kP; idx += 256) {
+      const int i = idx / kP, j = idx % kP;
+      if (i > j) continue;
+      const double* Gx = S.u.Gx;
+      const double re = Gx[i * 65 + j] + Gx[(kP + i) * 65 + kP + j];
+      const double im = Gx[i * 65 + kP + j] - Gx[j * 65 + kP + i];
+      SG[i * kPad + j] = make_double2(re, i == j ? 0.0 : im);
+      if (i != j) SG[j * kPad + i] = make_double2(re, -im);
+    }
   }
   __syncthreads();
   const double tolg = tol * fmax(sqrt((double)g.m), (double)kP);
@@ -202,25 +299,43 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __r
     // sum of squared relative off-diagonals between the two blocks: the host
     // turns it into the sweep's rms off-norm (cross-only EVD policy)
     const int i = t >> 4, j = kW + (t & 15);
-    const double gii = S.G[i * kPad + i].x, gjj = S.G[j * kPad + j].x;
-    double r = (fmin(gii, gjj) > floor2) ? cabs2(S.G[i * kPad + j]) / (gii * gjj) : 0.0;
+    const double gii = SG[i * kPad + i].x, gjj = SG[j * kPad + j].x;
+    double r = (fmin(gii, gjj) > floor2) ? cabs2(SG[i * kPad + j]) / (gii * gjj) : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
     if (lane == 0 && r > 0.0) atomicAdd(offsum + gi, r);
   }
-  const bool nd = pair_needs_rotation(S.G, t, tolg, floor2, maxoff + gi);
+  const bool nd = pair_needs_rotation(SG, t, tolg, floor2, maxoff + gi);
   const long long slot = (long long)gi * max_pairs + blockIdx.x;
   if (t == 0) need[slot] = nd ? 1 : 0;
-  if (!nd) return;
+  auto store_inblock = [&]() {  // the in-block Grams for this sweep's later visits
+    const int r = t >> 4, q = t & 15;
+    gblk_a[t] = SG[r * kPad + q];
+    gblk_b[t] = SG[(kW + r) * kPad + kW + q];
+  };
+  if (!nd) {
+    if (kFuseEvd && !approx) store_inblock();
+    return;
+  }
   if constexpr (kFuseEvd) {
-    GramEvdSmem& SE = *reinterpret_cast<GramEvdSmem*>(smem_raw);
-    pair_evd_v1(S.G, SE.R, SE.sc, t, tol_in, floor2, 1, active[gi] == 2);
+    cplx* R = reinterpret_cast<cplx*>(S.u.buf);
+    pair_evd_v1(SG, R, S.sc, t, tol_in, floor2, 1, (active[gi] & 2) != 0);
     __syncthreads();
-    cplx* rout = rbuf + slot * (kP * kP);
-    for (int idx = t; idx < kP * kP; idx += 256) rout[idx] = SE.R[(idx / kP) * kPad + idx % kP];
+    store_inblock();
+    if constexpr (kMode == 1) {
+      cplx* rout = rbuf + slot * (kP * kP);
+      for (int idx = t; idx < kP * kP; idx += 256) rout[idx] = R[(idx / kP) * kPad + idx % kP];
+    } else {
+      __syncthreads();  // G (aliased by R_ext) has been stored
+      expand_rotation(R, kPad, S.v.Rx, t);
+      __syncthreads();  // R (aliased by the chunk buffers) has been read
+      ld.issue(S.u.buf[0], 0);
+      rotate_pair(c, ld, S.u.buf, S.v.Rx, nchunks, t);
+      if (t == 0) atomicAdd(rotated + gi, 1);
+    }
   } else {
     cplx* gout = gbuf + slot * (kP * kP);
-    for (int idx = t; idx < kP * kP; idx += 256) gout[idx] = S.G[(idx / kP) * kPad + idx % kP];
+    for (int idx = t; idx < kP * kP; idx += 256) gout[idx] = SG[(idx / kP) * kPad + idx % kP];
   }
 }
 
@@ -247,23 +362,18 @@ __global__ void __launch_bounds__(256, 6) jacobi_evd_kernel(const GateDesc* __re
   const cplx* gin = gbuf + slot * (kP * kP);
   for (int idx = t; idx < kP * kP; idx += 256) S.G[(idx / kP) * kPad + idx % kP] = gin[idx];
   __syncthreads();
-  pair_evd_v1(S.G, S.R, S.sc, t, tol_in, floor_rel2 * frob2[gi], 1, active[gi] == 2);
+  pair_evd_v1(S.G, S.R, S.sc, t, tol_in, floor_rel2 * frob2[gi], 1, (active[gi] & 2) != 0);
   __syncthreads();
   cplx* rout = rbuf + slot * (kP * kP);
   for (int idx = t; idx < kP * kP; idx += 256) rout[idx] = S.R[(idx / kP) * kPad + idx % kP];
 }
 
-constexpr int kPitchR = 68;  // R_ext row pitch (== 4 mod 16: conflict-free B fragments)
-
 struct RotSmem {
   double buf[2][2 * kChunkPlane];
-  double Rx[2 * kP * kPitchR];  // R_ext[c_ext][j_ext] = [[Re R, Im R], [-Im R, Re R]]
+  double Rx[2 * kP * kPitchR];
 };
 
-// 3 CTAs x 72 KB per SM. Warp w computes row tiles {2(w&1), +1} of the chunk
-// and complex column tile w/2 (real column tiles w/2 and 4 + w/2): per k-step
-// two A and two B fragment loads feed four DMMAs, and each thread ends up
-// with Re and Im of the same complex outputs (16-byte global stores).
+// 3 CTAs x 72 KB per SM.
 __global__ void __launch_bounds__(256, 3) jacobi_rot_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
                                                             const int* __restrict__ active, int* __restrict__ rotated,
                                                             int round, const int* __restrict__ perm,
@@ -277,83 +387,45 @@ __global__ void __launch_bounds__(256, 3) jacobi_rot_kernel(const GateDesc* __re
   if (!need[slot]) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   RotSmem& S = *reinterpret_cast<RotSmem*>(smem_raw);
-  const int t = threadIdx.x, lane = t % 32, warp = t / 32;
-  const int fr = lane / 4, fk = lane % 4;
+  const int t = threadIdx.x;
   ChunkLoader ld;
   ld.init(c, t);
   const int nchunks = g.m_pad / kC;
   ld.issue(S.buf[0], 0);
-  const cplx* R = rbuf + slot * (kP * kP);
-  for (int idx = t; idx < kP * kP; idx += 256) {
-    const int i = idx / kP, j = idx % kP;
-    const cplx r = R[idx];
-    S.Rx[i * kPitchR + j] = r.x;
-    S.Rx[i * kPitchR + kP + j] = r.y;
-    S.Rx[(kP + i) * kPitchR + j] = -r.y;
-    S.Rx[(kP + i) * kPitchR + kP + j] = r.x;
-  }
-  const int rbase = 2 * (warp & 1), cj = warp >> 1;
-  const int bre = 8 * cj + fr, bim = kP + 8 * cj + fr;
-  for (int k = 0; k < nchunks; ++k) {
-    if (k + 1 < nchunks) {
-      ld.issue(S.buf[(k + 1) & 1], (k + 1) * kC);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
-    __syncthreads();
-    const double* B = S.buf[k & 1];
-    double o[2][2][2];
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int q = 0; q < 2; ++q) o[a][q][0] = o[a][q][1] = 0.0;
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {
-      const int cext = 4 * s + fk;
-      const double* plane = B + (cext < kP ? 0 : kChunkPlane) + (cext & (kP - 1));
-      const double a0 = plane[(8 * rbase + fr) * kPitchS], a1 = plane[(8 * (rbase + 1) + fr) * kPitchS];
-      const double b0 = S.Rx[cext * kPitchR + bre], b1 = S.Rx[cext * kPitchR + bim];
-      dmma_s(o[0][0][0], o[0][0][1], a0, b0);
-      dmma_s(o[0][1][0], o[0][1][1], a0, b1);
-      dmma_s(o[1][0][0], o[1][0][1], a1, b0);
-      dmma_s(o[1][1][0], o[1][1][1], a1, b1);
-    }
-    const int e0 = k * kC;
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int e = 8 * (rbase + a) + fr;
-        const int j = 8 * cj + 2 * fk + v;
-        c.vec(j)[e0 + e] = make_double2(o[a][0][v], o[a][1][v]);
-      }
-    __syncthreads();
-  }
+  expand_rotation(rbuf + slot * (kP * kP), kP, S.Rx, t);
+  rotate_pair(c, ld, S.buf, S.Rx, nchunks, t);
   if (t == 0) atomicAdd(rotated + gi, 1);
 }
 
 void jacobi_split_init() {
-  cudaFuncSetAttribute(jacobi_gram_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(GramSmem));
-  cudaFuncSetAttribute(jacobi_gram_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(GramEvdSmem));
+  cudaFuncSetAttribute(jacobi_gram_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem));
+  cudaFuncSetAttribute(jacobi_gram_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem));
+  cudaFuncSetAttribute(jacobi_gram_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem));
   cudaFuncSetAttribute(jacobi_evd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EvdSmem));
   cudaFuncSetAttribute(jacobi_rot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RotSmem));
 }
 
+// fuse: 0 = three launches, 1 = Gram+EVD / rotation, 2 = one launch per round.
 void launch_jacobi_round_split(const GateDesc* d_gates, int n_gates, int max_pairs, cplx* ws, const int* d_active,
                                int* d_rotated, int round, double tol, double tol_in, const double* frob2,
                                double floor_rel2, const int* perm, long long perm_stride, double* maxoff, int* need,
-                               cplx* gbuf, cplx* rbuf, double* offsum, bool fuse_evd, cudaStream_t st) {
+                               cplx* gbuf, cplx* rbuf, double* offsum, int fuse, cplx* gblk, cudaStream_t st) {
   const dim3 grid(max_pairs, n_gates);
-  if (fuse_evd) {
-    jacobi_gram_kernel<true><<<grid, 256, sizeof(GramEvdSmem), st>>>(d_gates, ws, d_active, round, tol, frob2,
-                                                                     floor_rel2, perm, perm_stride, maxoff, need,
-                                                                     gbuf, max_pairs, offsum, rbuf, tol_in);
+  const size_t sm = sizeof(PairSmem);
+  if (fuse == 2) {
+    jacobi_gram_kernel<2><<<grid, 256, sm, st>>>(d_gates, ws, d_active, round, tol, frob2, floor_rel2, perm,
+                                                 perm_stride, maxoff, need, gbuf, max_pairs, offsum, rbuf, tol_in,
+                                                 gblk, d_rotated);
+    return;
+  }
+  if (fuse == 1) {
+    jacobi_gram_kernel<1><<<grid, 256, sm, st>>>(d_gates, ws, d_active, round, tol, frob2, floor_rel2, perm,
+                                                 perm_stride, maxoff, need, gbuf, max_pairs, offsum, rbuf, tol_in,
+                                                 gblk, d_rotated);
   } else {
-    jacobi_gram_kernel<false><<<grid, 256, sizeof(GramSmem), st>>>(d_gates, ws, d_active, round, tol, frob2,
-                                                                   floor_rel2, perm, perm_stride, maxoff, need, gbuf,
-                                                                   max_pairs, offsum, rbuf, tol_in);
+    jacobi_gram_kernel<0><<<grid, 256, sm, st>>>(d_gates, ws, d_active, round, tol, frob2, floor_rel2, perm,
+                                                 perm_stride, maxoff, need, gbuf, max_pairs, offsum, rbuf, tol_in,
+                                                 gblk, d_rotated);
     jacobi_evd_kernel<<<grid, 256, sizeof(EvdSmem), st>>>(d_gates, d_active, round, tol_in, frob2, floor_rel2, need,
                                                            gbuf, rbuf, max_pairs);
   }
