@@ -19,36 +19,33 @@ struct Small4 {
   cplx m[16];  // row-major 4x4 (left: (p0',p0) x kappa ; right: kappa x (p1',p1))
 };
 
-// X/X0 of the Jacobi operand from a row-major device matrix A (rows x cols):
-// trans 0: X[v][e] = A[e][v] ; trans 1: X[v][e] = conj(A[v][e]).
-__global__ void load_matrix_kernel(const cplx* __restrict__ A, long long lda, int rows, int cols, int trans,
-                                   cplx* __restrict__ X, cplx* __restrict__ X0, int m_pad, double* frob2) {
-  double f = 0.0;
+// X/X0 of the Jacobi operand from a row-major device matrix A (rows x cols).
+// Orientation 0: vector v = column v of A; 1: vector v = conj(row v of A).
+__global__ void load_matrix_kernel(const cplx* __restrict__ A, long long lda, int rows, int cols, int xtrans,
+                                   cplx* __restrict__ X, long long ldx, int f, cplx* __restrict__ X0, long long ldx0,
+                                   double* frob2) {
+  double fr = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)rows * cols;
        i += (long long)gridDim.x * blockDim.x) {
     const int r = (int)(i / cols), c = (int)(i % cols);
-    cplx v = A[(long long)r * lda + c];
-    long long off;
-    if (trans == 0) {
-      off = (long long)c * m_pad + r;
-    } else {
-      off = (long long)r * m_pad + c;
-      v.y = -v.y;
-    }
-    X[off] = v;
-    X0[off] = v;
-    f += cabs2(v);
+    const cplx v = A[(long long)r * lda + c];
+    const cplx vc = make_double2(v.x, -v.y);
+    if (xtrans == 0) X[(long long)c * ldx + r] = v;
+    else X[(long long)r * ldx + c] = vc;
+    if (f == 0) X0[(long long)c * ldx0 + r] = v;
+    else X0[(long long)r * ldx0 + c] = vc;
+    fr += cabs2(v);
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) f += __shfl_xor_sync(0xffffffffu, f, o);
-  if (threadIdx.x % 32 == 0) atomicAdd(frob2, f);
+  for (int o = 16; o > 0; o >>= 1) fr += __shfl_xor_sync(0xffffffffu, fr, o);
+  if (threadIdx.x % 32 == 0) atomicAdd(frob2, fr);
 }
 
-void launch_load_matrix(const cplx* A, long long lda, int rows, int cols, int trans, cplx* X, cplx* X0, int m_pad,
-                        double* frob2, cudaStream_t st) {
+void launch_load_matrix(const cplx* A, long long lda, int rows, int cols, int xtrans, cplx* X, long long ldx, int f,
+                        cplx* X0, long long ldx0, double* frob2, cudaStream_t st) {
   long long blocks = ((long long)rows * cols + 255) / 256;
   blocks = std::max(1LL, std::min(blocks, 2048LL));
-  load_matrix_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, lda, rows, cols, trans, X, X0, m_pad, frob2);
+  load_matrix_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, lda, rows, cols, xtrans, X, ldx, f, X0, ldx0, frob2);
 }
 
 // Open (gate_apply.cpp:210-215):
@@ -104,7 +101,7 @@ GateOut svd_into(State& s, const cplx* A, int M, int N, const mpsim_policy& pol,
   d.nb = d.n_pad / kW;
   d.max_bond = pol.max_bond;
   d.cutoff = pol.cutoff;
-  desc_layout(d, 0, false);
+  desc_layout(d, 0, use_qr_precondition(d.n));
   d.u_out = u_out;
   d.ldu = ldu;
   d.v_out = v_out;
@@ -112,7 +109,7 @@ GateOut svd_into(State& s, const cplx* A, int M, int N, const mpsim_policy& pol,
   d.vsplit = N;
   d.vsplit_ld = 0;
   std::vector<GateOut> outs;
-  run_two_chunk(s, {d}, outs, nullptr, 0.0, A, N);
+  run_two_chunk(s, {d}, outs, A, N);
   if (outs[0].status != 0)
     fail(MPSIM_ENUMERIC, "singular value decomposition did not converge for (" + std::to_string(M) + "," +
                              std::to_string(N) + ") matrix");

@@ -327,12 +327,14 @@ constexpr double kQuadFinish = 1e-9;
 
 }  // namespace
 
-// Runs the batched Jacobi SVD + truncation + split for the descriptors. The
-// operand comes from the theta kernel (pre == pre_dev == nullptr), from host
-// memory already in X layout (pre, mpsim_gpu_svd) or from a row-major device
-// matrix (pre_dev, bond propagation).
+// Runs the batched Jacobi SVD + truncation + split for the descriptors: the
+// operand comes from the theta kernel (src == nullptr) or from a row-major
+// device matrix (plain SVDs, bond-propagation carriers); descriptors with
+// pre = 1 are QR-preconditioned (qr_pre.cu) before the sweeps.
+bool mpsim_gpu::use_qr_precondition(int n) { return qr_policy() && jacobi_mode() >= 2 && n >= kQrMinN; }
+
 void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs,
-                              const cplx* pre, double pre_frob, const cplx* pre_dev, long long pre_ld) {
+                              const cplx* src, long long src_ld) {
   const int ng = (int)descs.size();
   long long ws_elems = 0;
   int max_tiles = 1, max_nb = 2, max_m = 1, max_n = 1;
@@ -374,32 +376,26 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   const GateDesc* dg = (const GateDesc*)s.d_gates.p;
   cplx* ws = (cplx*)s.ws.p;
   CK(cudaMemsetAsync(s.d_frob.p, 0, sizeof(double) * ng, st));
-  if (pre == nullptr && pre_dev == nullptr) {
+  if (src == nullptr) {
     launch_theta(dg, ng, max_tiles, s.sites, s.stride, s.chi, ws, (double*)s.d_frob.p, st);
     check_launch("theta_kernel");
     ++s.launches;
-    if (qr_n_pad > 0) {
-      s.d_qrv.ensure(sizeof(cplx) * (size_t)ng * 32 * qr_m_pad);
-      s.d_qrt.ensure(sizeof(cplx) * (size_t)ng * 32 * 32);
-      launch_qr_precondition(dg, ng, qr_n_pad, qr_jm_pad, ws, (cplx*)s.d_qrv.p, qr_m_pad, (cplx*)s.d_qrt.p, st);
-      check_launch("qr_precondition");
-      s.launches += 2 * (qr_n_pad / 32) + 1;
-    }
-  } else if (pre_dev == nullptr) {
-    // Plain-matrix SVD (mpsim_gpu_svd): X and X0 arrive from the host.
-    const GateDesc& d = descs[0];
-    const size_t bytes = sizeof(cplx) * (size_t)d.n_pad * d.m_pad;
-    CK(cudaMemcpyAsync(ws + d.ws_off, pre, bytes, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(ws + d.x0_off, pre, bytes, cudaMemcpyHostToDevice, st));
-    CK(cudaMemcpyAsync(s.d_frob.p, &pre_frob, sizeof(double), cudaMemcpyHostToDevice, st));
-    CK(cudaStreamSynchronize(st));
   } else {
-    // A device-resident matrix (bond-propagation carriers): load X, X0, ||.||^2.
+    // A device-resident row-major matrix (plain SVDs, bond-propagation carriers)
     const GateDesc& d = descs[0];
-    launch_load_matrix(pre_dev, pre_ld, d.trans == 0 ? d.m : d.n, d.trans == 0 ? d.n : d.m, d.trans, ws + d.ws_off,
-                       ws + d.x0_off, d.m_pad, (double*)s.d_frob.p, st);
+    const int big = d.pre ? d.qr_m : d.m;
+    launch_load_matrix(src, src_ld, d.trans == 0 ? big : d.n, d.trans == 0 ? d.n : big, d.trans,
+                       ws + (d.pre ? d.qr_off : d.ws_off), d.pre ? d.qr_m_pad : d.m_pad, d.f, ws + d.x0_off, d.x0_ld,
+                       (double*)s.d_frob.p, st);
     check_launch("load_matrix_kernel");
     ++s.launches;
+  }
+  if (qr_n_pad > 0) {
+    s.d_qrv.ensure(sizeof(cplx) * (size_t)ng * 32 * qr_m_pad);
+    s.d_qrt.ensure(sizeof(cplx) * (size_t)ng * 32 * 32);
+    launch_qr_precondition(dg, ng, qr_n_pad, qr_jm_pad, ws, (cplx*)s.d_qrv.p, qr_m_pad, (cplx*)s.d_qrt.p, st);
+    check_launch("qr_precondition");
+    s.launches += 2 * (qr_n_pad / 32) + 1;
   }
 
   int* h_rot = (int*)s.h_rot.p;
@@ -524,7 +520,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     // F_2q = 32 Dl Dm Dr + 128 Dl Dr + 32 M N^2 (M = max, N = min of 2Dl, 2Dr)
     const double M = d.m, N = d.n;
     s.svd_flops += 32.0 * M * N * N;
-    if (pre == nullptr && pre_dev == nullptr) s.gate_flops +=32.0 * d.dl * (double)d.dm * d.dr + 128.0 * d.dl * (double)d.dr + 32.0 * M * N * N;
+    if (src == nullptr) s.gate_flops +=32.0 * d.dl * (double)d.dm * d.dr + 128.0 * d.dl * (double)d.dr + 32.0 * M * N * N;
   }
   if (!converged)
     for (int i = 0; i < ng; ++i)
@@ -630,7 +626,7 @@ void run_layer(State& s, const std::vector<G2>& two, const std::vector<G1>& one,
     d.ldv = 2LL * s.chi;
     d.vsplit = d.dr;
     d.vsplit_ld = s.chi;
-    const bool pre = qr_policy() && jacobi_mode() >= 2 && d.n >= kQrMinN;
+    const bool pre = use_qr_precondition(d.n);
     GateDesc probe = d;
     const long long sz = desc_layout(probe, 0, pre);
     if (!chunk.empty() && off + sz > budget_elems) flush();
@@ -1359,27 +1355,21 @@ int mpsim_gpu_svd(int32_t rows, int32_t cols, const double* a, int64_t max_rank,
     d.nb = d.n_pad / kW;
     d.max_bond = max_rank;
     d.cutoff = cutoff;
-    desc_layout(d, 0, false);
-    DeviceBuf dU, dV;
+    desc_layout(d, 0, use_qr_precondition(d.n));
+    DeviceBuf dU, dV, dA;
     dU.ensure(sizeof(cplx) * (size_t)rows * d.n);
     dV.ensure(sizeof(cplx) * (size_t)d.n * cols);
+    dA.ensure(sizeof(cplx) * (size_t)rows * cols);
     d.u_out = (cplx*)dU.p;
     d.ldu = d.n;
     d.v_out = (cplx*)dV.p;
     d.ldv = cols;
     d.vsplit = cols;
     d.vsplit_ld = 0;
-    std::vector<cplx> X((size_t)d.n_pad * d.m_pad, make_double2(0.0, 0.0));
-    double frob = 0.0;
-    for (int r = 0; r < rows; ++r)
-      for (int c = 0; c < cols; ++c) {
-        const double re = a[2 * ((size_t)r * cols + c)], im = a[2 * ((size_t)r * cols + c) + 1];
-        frob += re * re + im * im;
-        if (d.trans == 0) X[(size_t)c * d.m_pad + r] = make_double2(re, im);
-        else X[(size_t)r * d.m_pad + c] = make_double2(re, -im);
-      }
+    CK(cudaMemcpy(dA.p, a, sizeof(cplx) * (size_t)rows * cols, cudaMemcpyHostToDevice));
     std::vector<GateOut> outs;
-    run_two_chunk(*sc, {d}, outs, X.data(), frob);
+    run_two_chunk(*sc, {d}, outs, (const cplx*)dA.p, cols);
+    dA.release();
     const GateOut& o = outs[0];
     if (o.status != 0)
       fail(MPSIM_ENUMERIC, "singular value decomposition did not converge for (" + std::to_string(rows) + "," +

@@ -80,12 +80,17 @@ struct State {
 // QR sweeps of move_center (canon.cu).
 void move_center_impl(State& s, int center);
 
-// Batched Jacobi SVD + truncation + split of the descriptors (engine.cu).
+// Batched Jacobi SVD + truncation + split of the descriptors (engine.cu). The
+// operand comes from the theta kernel (src == nullptr) or, for a single
+// descriptor, from a row-major device matrix src (leading dimension src_ld).
 void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs,
-                   const cplx* pre = nullptr, double pre_frob = 0.0, const cplx* pre_dev = nullptr,
-                   long long pre_ld = 0);
-void launch_load_matrix(const cplx* A, long long lda, int rows, int cols, int trans, cplx* X, cplx* X0, int m_pad,
-                        double* frob2, cudaStream_t st);
+                   const cplx* src = nullptr, long long src_ld = 0);
+// X (orientation xtrans, stride ldx) and X0 (orientation f, stride ldx0) of a
+// row-major device matrix A (rows x cols), ||A||_F^2 added to *frob2.
+void launch_load_matrix(const cplx* A, long long lda, int rows, int cols, int xtrans, cplx* X, long long ldx, int f,
+                        cplx* X0, long long ldx0, double* frob2, cudaStream_t st);
+// Whether a descriptor with n vectors gets QR preconditioning (engine.cu).
+bool use_qr_precondition(int n);
 void launch_cgemm(const GemmArgs&, cudaStream_t);
 
 }  // namespace mpsim_gpu

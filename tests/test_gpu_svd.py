@@ -27,12 +27,17 @@ def test_reconstruct_isometric_sorted(gpu, shape):
         k = len(s)
         assert k == min(shape) and w == 0.0
         assert np.linalg.norm(u @ np.diag(s) @ vd - m) / np.linalg.norm(m) <= 1e-12
-        assert np.abs(u.conj().T @ u - np.eye(k)).max() <= 1e-12
-        # V^dag = S^-1 U^H A inherits U's residual non-orthogonality (<= the
-        # Jacobi tolerance) amplified by (s_max / s_i)(s_max / s_j); the
-        # reference's own case (6x5, test_tensor.cpp:247-277) meets 1e-12.
+        # One factor is the converged Jacobi operand (orthonormal to the
+        # Jacobi tolerance); the other is contracted from A (V^dag = S^-1 U^H A,
+        # or U = A V S^-1 when the sweeps ran on the QR-preconditioned A^H
+        # side) and inherits that residual amplified by (s_max / s_i)(s_max /
+        # s_j). The reference's own case (6x5, test_tensor.cpp:247-277) meets
+        # 1e-12 on both.
         kappa2 = (s[0] / s[-1]) ** 2
-        assert np.abs(vd @ vd.conj().T - np.eye(k)).max() <= 1e-12 * max(1.0, kappa2 / 100)
+        eu = np.abs(u.conj().T @ u - np.eye(k)).max()
+        ev = np.abs(vd @ vd.conj().T - np.eye(k)).max()
+        assert min(eu, ev) <= 1e-12
+        assert max(eu, ev) <= 1e-12 * max(1.0, kappa2 / 100)
         assert np.all(np.diff(s) <= 0) and s[-1] >= 0
         assert np.abs(s - np.linalg.svd(m, compute_uv=False)).max() <= 1e-13 * s[0]
 
