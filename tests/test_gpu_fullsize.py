@@ -34,6 +34,27 @@ def test_chi512_gates_match_oracle(gpu, oracle):
 
 
 @pytest.mark.slow
+def test_chi512_ragged_gates_match_oracle(gpu, oracle):
+    """Gates where 2Dl != 2Dr (theta 512 x 1024 and 1024 x 512 at the chain's
+    growing edge): both QR-preconditioned factor formulas."""
+    n, chi, seed = 24, 512, 77
+    o = oracle.MpsState.random(n, chi, seed)
+    g = copy_state_to_gpu(gpu, o, chi_hint=chi)
+    for i, q in enumerate([8, 14]):
+        u = oracle.haar_unitary(4, seed + 17 * i)
+        rg = g.apply_2q_local(u, q, max_bond=chi, cutoff=1e-12)
+        ro = o.apply_2q_local(u, q, max_bond=chi, cutoff=1e-12)
+        assert rg.new_bond == ro.new_bond
+        assert rel(rg.discarded_weight, ro.discarded_weight) <= 1e-10
+    assert (g.bond_dims() == o.bond_dims()).all()
+    rng = np.random.default_rng(5)
+    bits = ["".join(rng.choice(["0", "1"], n)) for _ in range(16)]
+    ag = g.amplitudes(bits)
+    ao = np.array([o.amplitude(b) for b in bits])
+    assert np.max(np.abs(ag - ao) / np.abs(ao)) <= 1e-10
+
+
+@pytest.mark.slow
 def test_chi1024_gate_matches_oracle(gpu, oracle):
     _fullsize(gpu, oracle, 24, 1024, 256, [11])
 

@@ -18,7 +18,8 @@ def test_identity_and_diagonal(gpu):
     assert abs(s[0] - 4) < 1e-13 and abs(s[1] - 3) < 1e-13
 
 
-@pytest.mark.parametrize("shape", [(6, 5), (5, 6), (2, 2), (1, 7), (7, 1), (33, 17), (40, 64), (130, 129)])
+@pytest.mark.parametrize("shape", [(6, 5), (5, 6), (2, 2), (1, 7), (7, 1), (33, 17), (40, 64), (130, 129),
+                                   (129, 200), (256, 160)])
 def test_reconstruct_isometric_sorted(gpu, shape):
     rng = np.random.default_rng(23)
     for _ in range(4):
@@ -86,3 +87,16 @@ def test_kept_rank_matches_oracle(gpu, oracle, cap, cutoff):
         assert len(sg) == len(so)
         assert np.abs(sg - so).max() <= 1e-13 * so[0]
         assert abs(wg - wo) <= 1e-10 * max(wo, 1e-300) or abs(wg - wo) < 1e-15
+
+
+@pytest.mark.parametrize("shape", [(200, 200), (160, 300)])
+def test_rank_deficient_preconditioned(gpu, shape):
+    """Low-rank operands on the QR-preconditioned path (n >= 128): exact zero
+    Householder columns, zero rows of R, noise-floor vectors."""
+    rng = np.random.default_rng(31)
+    m = _rand(rng, shape[0], 3) @ _rand(rng, 3, shape[1])
+    u, s, vd, w = gpu.mps.svd(m, None, 1e-14)
+    ref = np.linalg.svd(m, compute_uv=False)
+    assert len(s) == 3
+    assert np.abs(s - ref[:3]).max() <= 1e-13 * ref[0]
+    assert np.linalg.norm(u @ np.diag(s) @ vd - m) / np.linalg.norm(m) <= 1e-12
