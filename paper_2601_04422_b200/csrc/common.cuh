@@ -54,21 +54,27 @@ struct GateDesc {
   // contracted with) has n0 vectors of length m, stride x0_ld.
   int f, n0;
   long long x0_off, x0_ld;
-  // QR preconditioning (qr_pre.cu): theta -> QR operand (n vectors of length
-  // qr_m, stride qr_m_pad at qr_off, orientation trans) = Q R; the Jacobi
-  // operand X is then R^H (n vectors of length m = n) and f = trans ^ 1.
+  // QR preconditioning (qr_pre.cu), pre = 1: theta -> QR operand (n vectors
+  // of length qr_m, stride qr_m_pad at qr_off, orientation trans) = Q R; the
+  // Jacobi operand X is R^H (n vectors of length m = n) and f = trans ^ 1.
+  // pre = 2: a second step R^H = Q2 R2 (in the y2 area), Jacobi on R2^H, then
+  // Z = Q1 [X; 0] in the QR area holds sigma * (left vectors): f = trans.
   int pre, qr_m;
-  long long qr_off, qr_m_pad;
+  long long qr_off, qr_m_pad, y2_off;
 };
 
 // Workspace layout of one descriptor starting at `off` (complex elements);
 // returns the span. Without preconditioning: X (n_pad x m_pad) then X0 (same).
-// With it: X = R^H (n_pad x m_pad, m = n), X0 (n0 = qr_m vectors x m_pad), then
-// the QR operand (n_pad x qr_m_pad).
-inline long long desc_layout(GateDesc& d, long long off, bool pre) {
-  d.pre = pre ? 1 : 0;
+// pre = 1: X = R^H (n_pad x m_pad, m = n), X0 (n0 = qr_m vectors x m_pad), the
+// QR operand (n_pad x qr_m_pad). pre = 2: X = R2^H (n_pad x m_pad, m = n), X0
+// (n vectors x qr_m_pad, orientation trans), the QR operand / Z, the y2 area.
+// The descriptor holds the Jacobi-phase view; phase_desc() (engine.cu) derives
+// the others.
+inline long long desc_layout(GateDesc& d, long long off, int pre) {
+  d.pre = pre;
   d.ws_off = off;
-  if (!pre) {
+  d.y2_off = 0;
+  if (pre == 0) {
     d.f = d.trans;
     d.n0 = d.n;
     d.x0_ld = d.m_pad;
@@ -82,12 +88,20 @@ inline long long desc_layout(GateDesc& d, long long off, bool pre) {
   d.qr_m_pad = d.m_pad;
   d.m = d.n;
   d.m_pad = ((d.n + kE - 1) / kE) * kE;
-  d.f = d.trans ^ 1;
-  d.n0 = d.qr_m;
-  d.x0_ld = d.m_pad;
   d.x0_off = off + (long long)d.n_pad * d.m_pad;
-  d.qr_off = d.x0_off + (long long)d.n0 * d.x0_ld;
-  return (long long)d.n_pad * d.m_pad + (long long)d.n0 * d.x0_ld + (long long)d.n_pad * d.qr_m_pad;
+  if (pre == 1) {
+    d.f = d.trans ^ 1;
+    d.n0 = d.qr_m;
+    d.x0_ld = d.m_pad;
+    d.qr_off = d.x0_off + (long long)d.n0 * d.x0_ld;
+    return (long long)d.n_pad * d.m_pad + (long long)d.n0 * d.x0_ld + (long long)d.n_pad * d.qr_m_pad;
+  }
+  d.f = d.trans;
+  d.n0 = d.n;
+  d.x0_ld = d.qr_m_pad;
+  d.qr_off = d.x0_off + (long long)d.n_pad * d.x0_ld;
+  d.y2_off = d.qr_off + (long long)d.n_pad * d.qr_m_pad;
+  return 2LL * d.n_pad * d.m_pad + 2LL * d.n_pad * d.qr_m_pad;
 }
 
 // Per-gate outputs of the split epilogue.

@@ -33,16 +33,19 @@ void launch_jacobi_round_dmma(const GateDesc*, int, int, cplx*, const int*, int*
                               const double*, double, const int*, long long, double*, cudaStream_t);
 void jacobi_split_init();
 void qrp_init();
-void launch_qr_precondition(const GateDesc*, int, int, int, cplx*, cplx*, long long, cplx*, cudaStream_t);
+void launch_qr_factor(const GateDesc*, int, int, int, cplx*, cplx*, long long, cplx*, int, cudaStream_t);
+void launch_qr_apply(const GateDesc*, int, int, int, cplx*, const cplx*, long long, const cplx*, int, cudaStream_t);
 // QR preconditioning (qr_pre.cu) of gates whose SVD operand has at least
-// kQrMinN vectors; MPSIM_QR=0 disables it.
+// kQrMinN vectors: MPSIM_QR=2 (default) two QR steps, 1 one, 0 none.
 constexpr int kQrMinN = 128;
-static bool qr_policy() {
-  static const bool on = [] {
-    const char* v = std::getenv("MPSIM_QR");
-    return !(v != nullptr && v[0] == '0');
+static int qr_policy() {
+  static const int v = [] {
+    const char* e = std::getenv("MPSIM_QR");
+    if (e == nullptr) return 2;
+    const int x = std::atoi(e);
+    return x < 0 ? 0 : (x > 2 ? 2 : x);
   }();
-  return on;
+  return v;
 }
 void launch_jacobi_round_split(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, const double*,
                                double, const int*, long long, double*, int*, cplx*, cplx*, double*, int, cplx*,
@@ -331,16 +334,43 @@ constexpr double kQuadFinish = 1e-9;
 // operand comes from the theta kernel (src == nullptr) or from a row-major
 // device matrix (plain SVDs, bond-propagation carriers); descriptors with
 // pre = 1 are QR-preconditioned (qr_pre.cu) before the sweeps.
-bool mpsim_gpu::use_qr_precondition(int n) { return qr_policy() && jacobi_mode() >= 2 && n >= kQrMinN; }
+int mpsim_gpu::use_qr_precondition(int n) { return (jacobi_mode() >= 2 && n >= kQrMinN) ? qr_policy() : 0; }
+
+// The descriptor as each phase of run_two_chunk sees it (desc_layout holds the
+// Jacobi-phase view): 0 theta / load + first QR (R^H -> y2 for pre = 2),
+// 1 second QR (pre = 2 only), 2 Jacobi sweeps, 3 Z = Q1 [X; 0] (pre = 2 only),
+// 4 split epilogue.
+static GateDesc phase_desc(const GateDesc& d, int phase) {
+  GateDesc e = d;
+  if (d.pre == 2) {
+    if (phase == 0) {
+      e.ws_off = d.y2_off;
+    } else if (phase == 1) {
+      e.qr_off = d.y2_off;
+      e.qr_m = d.n;
+      e.qr_m_pad = d.m_pad;
+    } else if (phase == 4) {
+      e.ws_off = d.qr_off;
+      e.m = d.qr_m;
+      e.m_pad = (int)d.qr_m_pad;
+    }
+  } else if (phase == 1 || phase == 3) {
+    e.pre = 0;
+  }
+  return e;
+}
 
 void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs,
                               const cplx* src, long long src_ld) {
   const int ng = (int)descs.size();
   long long ws_elems = 0;
   int max_tiles = 1, max_nb = 2, max_m = 1, max_n = 1;
-  int max_n0 = 1, qr_n_pad = 0, qr_m_pad = 0, qr_jm_pad = 0;
+  int max_n0 = 1, qr_n_pad = 0, qr_m_pad = 0, qr_jm_pad = 0, max_out_m = 1;
+  bool any_pre2 = false;
   for (const GateDesc& d : descs) {
-    const long long end = d.pre ? d.qr_off + (long long)d.n_pad * d.qr_m_pad : d.x0_off + (long long)d.n_pad * d.x0_ld;
+    long long end = d.x0_off + (long long)d.n_pad * d.x0_ld;
+    if (d.pre == 1) end = d.qr_off + (long long)d.n_pad * d.qr_m_pad;
+    if (d.pre == 2) end = d.y2_off + (long long)d.n_pad * d.m_pad;
     ws_elems = std::max(ws_elems, end);
     max_n0 = std::max(max_n0, d.n0);
     if (d.pre) {
@@ -348,41 +378,48 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       qr_m_pad = std::max(qr_m_pad, (int)d.qr_m_pad);
       qr_jm_pad = std::max(qr_jm_pad, d.m_pad);
     }
+    any_pre2 = any_pre2 || d.pre == 2;
     max_tiles = std::max(max_tiles, theta_tiles(d.dl, d.dr));
     max_nb = std::max(max_nb, d.nb);
     max_m = std::max(max_m, d.m);
     max_n = std::max(max_n, d.n);
+    max_out_m = std::max(max_out_m, phase_desc(d, 4).m);
   }
   const long long sig_stride = ((max_n + 31) / 32) * 32;
   long long perm_stride = 32;
   for (const GateDesc& d : descs) perm_stride = std::max<long long>(perm_stride, d.n_pad);
   s.d_perm.ensure(sizeof(int) * perm_stride * ng);
   s.ws.ensure((size_t)ws_elems * sizeof(cplx));
-  s.d_gates.ensure(sizeof(GateDesc) * ng);
+  s.d_gates.ensure(sizeof(GateDesc) * 5 * ng);
   s.d_out.ensure(sizeof(GateOut) * ng);
   s.d_sigma.ensure(sizeof(double) * sig_stride * ng);
   s.d_order.ensure(sizeof(int) * sig_stride * ng);
   s.d_active.ensure(sizeof(int) * ng);
   s.d_rot.ensure(sizeof(int) * ng);
   s.d_frob.ensure(sizeof(double) * ng);
-  s.h_gates.ensure(sizeof(GateDesc) * ng);
+  s.h_gates.ensure(sizeof(GateDesc) * 5 * ng);
   s.h_out.ensure(sizeof(GateOut) * ng);
   s.h_rot.ensure(sizeof(int) * ng);
-  std::memcpy(s.h_gates.p, descs.data(), sizeof(GateDesc) * ng);
+  {
+    GateDesc* h = (GateDesc*)s.h_gates.p;
+    for (int ph = 0; ph < 5; ++ph)
+      for (int i = 0; i < ng; ++i) h[ph * ng + i] = phase_desc(descs[i], ph);
+  }
   cudaStream_t st = s.st;
-  CK(cudaMemcpyAsync(s.d_gates.p, s.h_gates.p, sizeof(GateDesc) * ng, cudaMemcpyHostToDevice, st));
-  s.h2d_bytes += (long long)sizeof(GateDesc) * ng + (long long)sizeof(int) * ng;
+  CK(cudaMemcpyAsync(s.d_gates.p, s.h_gates.p, sizeof(GateDesc) * 5 * ng, cudaMemcpyHostToDevice, st));
+  s.h2d_bytes += (long long)sizeof(GateDesc) * 5 * ng + (long long)sizeof(int) * ng;
   CK(cudaMemsetAsync(s.ws.p, 0, (size_t)ws_elems * sizeof(cplx), st));
-  const GateDesc* dg = (const GateDesc*)s.d_gates.p;
+  const GateDesc* dph = (const GateDesc*)s.d_gates.p;
+  const GateDesc* dg = dph + 2 * ng;  // Jacobi phase
   cplx* ws = (cplx*)s.ws.p;
   CK(cudaMemsetAsync(s.d_frob.p, 0, sizeof(double) * ng, st));
   if (src == nullptr) {
-    launch_theta(dg, ng, max_tiles, s.sites, s.stride, s.chi, ws, (double*)s.d_frob.p, st);
+    launch_theta(dph, ng, max_tiles, s.sites, s.stride, s.chi, ws, (double*)s.d_frob.p, st);
     check_launch("theta_kernel");
     ++s.launches;
   } else {
     // A device-resident row-major matrix (plain SVDs, bond-propagation carriers)
-    const GateDesc& d = descs[0];
+    const GateDesc d = phase_desc(descs[0], 0);
     const int big = d.pre ? d.qr_m : d.m;
     launch_load_matrix(src, src_ld, d.trans == 0 ? big : d.n, d.trans == 0 ? d.n : big, d.trans,
                        ws + (d.pre ? d.qr_off : d.ws_off), d.pre ? d.qr_m_pad : d.m_pad, d.f, ws + d.x0_off, d.x0_ld,
@@ -390,12 +427,22 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     check_launch("load_matrix_kernel");
     ++s.launches;
   }
+  const int npan = qr_n_pad / 32;
   if (qr_n_pad > 0) {
-    s.d_qrv.ensure(sizeof(cplx) * (size_t)ng * 32 * qr_m_pad);
-    s.d_qrt.ensure(sizeof(cplx) * (size_t)ng * 32 * 32);
-    launch_qr_precondition(dg, ng, qr_n_pad, qr_jm_pad, ws, (cplx*)s.d_qrv.p, qr_m_pad, (cplx*)s.d_qrt.p, st);
-    check_launch("qr_precondition");
-    s.launches += 2 * (qr_n_pad / 32) + 1;
+    // first QR (its reflectors stay in d_qrv / d_qrt for Z = Q1 [X; 0])
+    s.d_qrv.ensure(sizeof(cplx) * (size_t)ng * npan * 32 * qr_m_pad);
+    s.d_qrt.ensure(sizeof(cplx) * (size_t)ng * npan * 32 * 32);
+    launch_qr_factor(dph, ng, qr_n_pad, qr_jm_pad, ws, (cplx*)s.d_qrv.p, qr_m_pad, (cplx*)s.d_qrt.p, npan, st);
+    check_launch("qr_factor");
+    s.launches += 2 * npan;
+  }
+  if (any_pre2) {
+    s.d_qrv2.ensure(sizeof(cplx) * (size_t)ng * npan * 32 * qr_jm_pad);
+    s.d_qrt2.ensure(sizeof(cplx) * (size_t)ng * npan * 32 * 32);
+    launch_qr_factor(dph + ng, ng, qr_n_pad, qr_jm_pad, ws, (cplx*)s.d_qrv2.p, qr_jm_pad, (cplx*)s.d_qrt2.p, npan,
+                     st);
+    check_launch("qr_factor (second step)");
+    s.launches += 2 * npan;
   }
 
   int* h_rot = (int*)s.h_rot.p;
@@ -503,12 +550,19 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     }
     CK(cudaMemcpyAsync(s.d_active.p, h_rot, sizeof(int) * ng, cudaMemcpyHostToDevice, st));
   }
-  launch_norms(dg, ng, max_n, ws, (double*)s.d_sigma.p, sig_stride, st);
+  if (any_pre2) {
+    launch_qr_apply(dph + 3 * ng, ng, qr_n_pad, qr_m_pad, ws, (const cplx*)s.d_qrv.p, qr_m_pad,
+                    (const cplx*)s.d_qrt.p, npan, st);
+    check_launch("qr_apply");
+    s.launches += 1 + npan;
+  }
+  const GateDesc* dout = dph + 4 * ng;
+  launch_norms(dout, ng, max_n, ws, (double*)s.d_sigma.p, sig_stride, st);
   check_launch("norms_kernel");
-  launch_truncate(dg, ng, (double*)s.d_sigma.p, (int*)s.d_order.p, sig_stride, (GateOut*)s.d_out.p,
+  launch_truncate(dout, ng, (double*)s.d_sigma.p, (int*)s.d_order.p, sig_stride, (GateOut*)s.d_out.p,
                   (const double*)s.d_frob.p, kFloorRel2, st);
   check_launch("truncate_kernel");
-  launch_write_factors(dg, ng, max_m, max_n, max_n0, ws, (const double*)s.d_sigma.p, (const int*)s.d_order.p, sig_stride,
+  launch_write_factors(dout, ng, max_out_m, max_n, max_n0, ws, (const double*)s.d_sigma.p, (const int*)s.d_order.p, sig_stride,
                        (const GateOut*)s.d_out.p, (const double*)s.d_frob.p, kFloorRel2, st);
   check_launch("write_factors");
   s.launches += 4;
@@ -518,7 +572,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   outs.assign((GateOut*)s.h_out.p, (GateOut*)s.h_out.p + ng);
   for (const GateDesc& d : descs) {
     // F_2q = 32 Dl Dm Dr + 128 Dl Dr + 32 M N^2 (M = max, N = min of 2Dl, 2Dr)
-    const double M = d.m, N = d.n;
+    const double M = d.pre ? d.qr_m : d.m, N = d.n;
     s.svd_flops += 32.0 * M * N * N;
     if (src == nullptr) s.gate_flops +=32.0 * d.dl * (double)d.dm * d.dr + 128.0 * d.dl * (double)d.dr + 32.0 * M * N * N;
   }
@@ -626,7 +680,7 @@ void run_layer(State& s, const std::vector<G2>& two, const std::vector<G1>& one,
     d.ldv = 2LL * s.chi;
     d.vsplit = d.dr;
     d.vsplit_ld = s.chi;
-    const bool pre = use_qr_precondition(d.n);
+    const int pre = use_qr_precondition(d.n);
     GateDesc probe = d;
     const long long sz = desc_layout(probe, 0, pre);
     if (!chunk.empty() && off + sz > budget_elems) flush();

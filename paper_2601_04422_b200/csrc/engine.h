@@ -56,7 +56,7 @@ struct State {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // workspaces
   DeviceBuf ws, d_gates, d_out, d_sigma, d_order, d_active, d_rot, d_frob, d_perm, d_maxoff, d_g1, q1, q2, q3, q4,
-      qbits, d_need, d_gbuf, d_rbuf, d_offsum, d_qrv, d_qrt, d_gblk;
+      qbits, d_need, d_gbuf, d_rbuf, d_offsum, d_qrv, d_qrt, d_gblk, d_qrv2, d_qrt2;
   PinnedBuf h_gates, h_out, h_rot, h_g1, h_small, h_maxoff, h_offsum;
   // instrumentation
   long long launches = 0;
@@ -89,8 +89,8 @@ void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<Gat
 // row-major device matrix A (rows x cols), ||A||_F^2 added to *frob2.
 void launch_load_matrix(const cplx* A, long long lda, int rows, int cols, int xtrans, cplx* X, long long ldx, int f,
                         cplx* X0, long long ldx0, double* frob2, cudaStream_t st);
-// Whether a descriptor with n vectors gets QR preconditioning (engine.cu).
-bool use_qr_precondition(int n);
+// QR preconditioning steps (0, 1, 2) for a descriptor with n vectors (engine.cu).
+int use_qr_precondition(int n);
 void launch_cgemm(const GemmArgs&, cudaStream_t);
 
 }  // namespace mpsim_gpu

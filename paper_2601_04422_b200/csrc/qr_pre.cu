@@ -6,6 +6,12 @@
 // singular vectors of theta directly (S V^dag = X^H), and U = theta X / sigma^2
 // from the pristine theta (split.cu, f = 1; the transposed case likewise).
 //
+// Two-step variant (pre = 2): R^H = Q2 R2 again and the Jacobi runs on R2^H
+// (9 instead of 11 sweeps at chi = 512); R2^H = U'' S W^H gives theta =
+// Q1 U'' S (Q2 W)^H, so the converged X is mapped back through the stored
+// block reflectors of the first QR, Z = Q1 [X; 0] (qrp_update_kernel<true>), and the
+// epilogue proceeds as without preconditioning (f = trans).
+//
 // Per 32-column panel p of every gate's QR operand A (vectors = columns,
 // stride qr_m_pad, rows [0, qr_m)):
 //   qrp_panel_kernel    one 1024-thread CTA per gate: 32 Householder
@@ -60,10 +66,11 @@ __device__ __forceinline__ double block_sum_1024(double v, double* red) {
 
 }  // namespace
 
-// vbuf: per gate kQ vectors of stride vld (>= qr_m_pad); tbuf: per gate kQ x kQ.
+// vbuf: per gate and panel kQ vectors of stride vld (>= qr_m_pad); tbuf: per
+// gate and panel kQ x kQ; npan panel slots per gate (all kept for Q1 [X; 0]).
 __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
                                                          int p, cplx* __restrict__ vbuf, long long vld,
-                                                         cplx* __restrict__ tbuf) {
+                                                         cplx* __restrict__ tbuf, int npan) {
   const GateDesc& g = gates[blockIdx.x];
   if (!g.pre) return;
   const int n = g.n, m = g.qr_m;
@@ -72,7 +79,7 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
   if (c0 >= n) return;
   const int jb = min(kQ, n - c0);
   cplx* A = ws + g.qr_off;
-  cplx* V = vbuf + (long long)blockIdx.x * kQ * vld;
+  cplx* V = vbuf + ((long long)blockIdx.x * npan + p) * kQ * vld;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   __shared__ double red[32];
   __shared__ cplx taus[kQ];
@@ -165,7 +172,7 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
     }
     __syncthreads();
   }
-  cplx* To = tbuf + (long long)blockIdx.x * kQ * kQ;
+  cplx* To = tbuf + ((long long)blockIdx.x * npan + p) * kQ * kQ;
   for (int idx = t; idx < kQ * kQ; idx += 1024) To[idx] = T[idx / kQ][idx % kQ];
 }
 
@@ -215,15 +222,20 @@ struct QrUpdSmem {
 
 }  // namespace
 
-// A_b <- A_b - V T^H (V^H A_b), rows [c0, qr_m_pad), block b of 32 columns at
-// c0 + 32 (b + 1). Grid (blocks, gates), 256 threads.
+// kApply = false: A_b <- Q_p^H A_b = A_b - V T^H (V^H A_b) for the 32-column
+// block b at c0 + 32 (b + 1) (trailing update of the factorisation);
+// kApply = true:  A_b <- Q_p A_b = A_b - V T (V^H A_b) for block b at 32 b
+// (Z = Q1 [X; 0], panels applied last to first). Rows [c0, qr_m_pad).
+// Grid (blocks, gates), 256 threads.
+template <bool kApply>
 __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
                                                             int p, const cplx* __restrict__ vbuf, long long vld,
-                                                            const cplx* __restrict__ tbuf) {
+                                                            const cplx* __restrict__ tbuf, int npan) {
   const GateDesc& g = gates[blockIdx.y];
   if (!g.pre) return;
   const int c0 = kQ * p;
-  const int cb = c0 + kQ * (blockIdx.x + 1);
+  if (kApply && c0 >= g.n) return;
+  const int cb = kApply ? kQ * blockIdx.x : c0 + kQ * (blockIdx.x + 1);
   if (cb >= g.n_pad) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   QrUpdSmem& S = *reinterpret_cast<QrUpdSmem*>(smem_raw);
@@ -231,7 +243,7 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
   const int fr = lane >> 2, fk = lane & 3;
   const long long ald = g.qr_m_pad;
   cplx* A = ws + g.qr_off + (long long)cb * ald;
-  const cplx* V = vbuf + (long long)blockIdx.y * kQ * vld;
+  const cplx* V = vbuf + ((long long)blockIdx.y * npan + p) * kQ * vld;
   QrChunkLoader ld;
   ld.init(V, vld, A, ald, t);
   const int nchunks = (int)((ald - c0) / kQC);
@@ -278,7 +290,7 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
 #pragma unroll
       for (int v = 0; v < 2; ++v)
         S.u.w.Wx[(qx * kQ + 8 * (tr0 + a) + fr) * 65 + qy * kQ + 8 * c + 2 * fk + v] = acc[a][c][v];
-  const cplx* Tg = tbuf + (long long)blockIdx.y * kQ * kQ;
+  const cplx* Tg = tbuf + ((long long)blockIdx.y * npan + p) * kQ * kQ;
   for (int idx = t; idx < kQ * kQ; idx += 256) S.u.w.T[(idx / kQ) * (kQ + 1) + idx % kQ] = Tg[idx];
   __syncthreads();
   // W = V^H A_b: Re = Vr^T Ar + Vi^T Ai, Im = Vr^T Ai - Vi^T Ar
@@ -290,11 +302,16 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
     S.u.w.W[i * (kQ + 1) + j] = make_double2(re, im);
   }
   __syncthreads();
-  // W2 = T^H W (T upper triangular); stored negated in real-extended form
+  // W2 = T^H W (factorisation) or T W (apply), T upper triangular; stored
+  // negated in real-extended form
   for (int idx = t; idx < kQ * kQ; idx += 256) {
     const int i = idx / kQ, j = idx % kQ;
     cplx z = make_double2(0.0, 0.0);
-    for (int k = 0; k <= i; ++k) cfmac(z, S.u.w.T[k * (kQ + 1) + i], S.u.w.W[k * (kQ + 1) + j]);
+    if (kApply) {
+      for (int k = i; k < kQ; ++k) cfma(z, S.u.w.T[i * (kQ + 1) + k], S.u.w.W[k * (kQ + 1) + j]);
+    } else {
+      for (int k = 0; k <= i; ++k) cfmac(z, S.u.w.T[k * (kQ + 1) + i], S.u.w.W[k * (kQ + 1) + j]);
+    }
     S.W2x[i * kQPitchW + j] = -z.x;
     S.W2x[i * kQPitchW + kQ + j] = -z.y;
     S.W2x[(kQ + i) * kQPitchW + j] = z.y;
@@ -376,22 +393,51 @@ __global__ void __launch_bounds__(256) qrp_form_rh_kernel(const GateDesc* __rest
   }
 }
 
-void qrp_init() {
-  cudaFuncSetAttribute(qrp_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(QrUpdSmem));
+// Z[j][r] = X[j][r] for r < n (X: stride m_pad, the converged R2^H side),
+// 0 for n <= r < qr_m_pad. Grid (qr_m_pad / 256, n_pad, gates).
+__global__ void __launch_bounds__(256) qrp_zinit_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws) {
+  const GateDesc& g = gates[blockIdx.z];
+  if (!g.pre) return;
+  const long long r = blockIdx.x * 256LL + threadIdx.x;
+  const int j = blockIdx.y;
+  if (r >= g.qr_m_pad || j >= g.n_pad) return;
+  const cplx* X = ws + g.ws_off + (long long)j * g.m_pad;
+  cplx* Z = ws + g.qr_off + (long long)j * g.qr_m_pad;
+  Z[r] = r < g.n ? X[r] : make_double2(0.0, 0.0);
 }
 
-// Whole preconditioning pass for the descriptors with pre = 1. max_n_pad: the
-// largest n_pad of them; vbuf holds gates x 32 vectors of vld >= qr_m_pad.
-void launch_qr_precondition(const GateDesc* d_gates, int n_gates, int max_n_pad, int max_m_pad, cplx* ws,
-                            cplx* vbuf, long long vld, cplx* tbuf, cudaStream_t st) {
+void qrp_init() {
+  cudaFuncSetAttribute(qrp_update_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(QrUpdSmem));
+  cudaFuncSetAttribute(qrp_update_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(QrUpdSmem));
+}
+
+// Householder QR of every descriptor with pre != 0 (panels, trailing
+// updates), then X = R^H (qrp_form_rh_kernel: from qr_off into ws_off).
+// max_n_pad: largest n_pad; max_x_pad: largest X stride; vbuf / tbuf hold
+// npan panel slots per gate.
+void launch_qr_factor(const GateDesc* d_gates, int n_gates, int max_n_pad, int max_x_pad, cplx* ws, cplx* vbuf,
+                      long long vld, cplx* tbuf, int npan, cudaStream_t st) {
   const int panels = max_n_pad / kQ;
   for (int p = 0; p < panels; ++p) {
-    qrp_panel_kernel<<<n_gates, 1024, 0, st>>>(d_gates, ws, p, vbuf, vld, tbuf);
+    qrp_panel_kernel<<<n_gates, 1024, 0, st>>>(d_gates, ws, p, vbuf, vld, tbuf, npan);
     const int blocks = panels - p - 1;
     if (blocks > 0)
-      qrp_update_kernel<<<dim3(blocks, n_gates), 256, sizeof(QrUpdSmem), st>>>(d_gates, ws, p, vbuf, vld, tbuf);
+      qrp_update_kernel<false><<<dim3(blocks, n_gates), 256, sizeof(QrUpdSmem), st>>>(d_gates, ws, p, vbuf, vld,
+                                                                                      tbuf, npan);
   }
-  qrp_form_rh_kernel<<<dim3(max_m_pad / 32, max_n_pad / 32, n_gates), 256, 0, st>>>(d_gates, ws);
+  qrp_form_rh_kernel<<<dim3(max_x_pad / 32, max_n_pad / 32, n_gates), 256, 0, st>>>(d_gates, ws);
+}
+
+// Z = Q1 [X; 0] with the reflectors kept by launch_qr_factor.
+void launch_qr_apply(const GateDesc* d_gates, int n_gates, int max_n_pad, int max_qr_m_pad, cplx* ws,
+                     const cplx* vbuf, long long vld, const cplx* tbuf, int npan, cudaStream_t st) {
+  qrp_zinit_kernel<<<dim3((max_qr_m_pad + 255) / 256, max_n_pad, n_gates), 256, 0, st>>>(d_gates, ws);
+  const int panels = max_n_pad / kQ;
+  for (int p = panels - 1; p >= 0; --p)
+    qrp_update_kernel<true><<<dim3(panels, n_gates), 256, sizeof(QrUpdSmem), st>>>(d_gates, ws, p, vbuf, vld, tbuf,
+                                                                                  npan);
 }
 
 }  // namespace mpsim_gpu
