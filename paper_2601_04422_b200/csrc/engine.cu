@@ -34,7 +34,8 @@ void launch_jacobi_round_dmma(const GateDesc*, int, int, cplx*, const int*, int*
 void jacobi_split_init();
 void qrp_init();
 void launch_qr_factor(const GateDesc*, int, int, int, cplx*, cplx*, long long, cplx*, int, cudaStream_t);
-void launch_qr_apply(const GateDesc*, int, int, int, cplx*, const cplx*, long long, const cplx*, int, cudaStream_t);
+void launch_qr_apply(const GateDesc*, int, int, int, cplx*, const cplx*, long long, const cplx*, int, const int*,
+                     long long, const GateOut*, cudaStream_t);
 // QR preconditioning (qr_pre.cu) of gates whose SVD operand has at least
 // kQrMinN vectors: MPSIM_QR=2 (default) two QR steps, 1 one, 0 none.
 constexpr int kQrMinN = 128;
@@ -550,18 +551,19 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     }
     CK(cudaMemcpyAsync(s.d_active.p, h_rot, sizeof(int) * ng, cudaMemcpyHostToDevice, st));
   }
+  launch_norms(dg, ng, max_n, ws, (double*)s.d_sigma.p, sig_stride, st);
+  check_launch("norms_kernel");
+  launch_truncate(dg, ng, (double*)s.d_sigma.p, (int*)s.d_order.p, sig_stride, (GateOut*)s.d_out.p,
+                  (const double*)s.d_frob.p, kFloorRel2, st);
+  check_launch("truncate_kernel");
   if (any_pre2) {
     launch_qr_apply(dph + 3 * ng, ng, qr_n_pad, qr_m_pad, ws, (const cplx*)s.d_qrv.p, qr_m_pad,
-                    (const cplx*)s.d_qrt.p, npan, st);
+                    (const cplx*)s.d_qrt.p, npan, (const int*)s.d_order.p, sig_stride, (const GateOut*)s.d_out.p,
+                    st);
     check_launch("qr_apply");
     s.launches += 1 + npan;
   }
   const GateDesc* dout = dph + 4 * ng;
-  launch_norms(dout, ng, max_n, ws, (double*)s.d_sigma.p, sig_stride, st);
-  check_launch("norms_kernel");
-  launch_truncate(dout, ng, (double*)s.d_sigma.p, (int*)s.d_order.p, sig_stride, (GateOut*)s.d_out.p,
-                  (const double*)s.d_frob.p, kFloorRel2, st);
-  check_launch("truncate_kernel");
   launch_write_factors(dout, ng, max_out_m, max_n, max_n0, ws, (const double*)s.d_sigma.p, (const int*)s.d_order.p, sig_stride,
                        (const GateOut*)s.d_out.p, (const double*)s.d_frob.p, kFloorRel2, st);
   check_launch("write_factors");

@@ -9,8 +9,9 @@
 // Two-step variant (pre = 2): R^H = Q2 R2 again and the Jacobi runs on R2^H
 // (9 instead of 11 sweeps at chi = 512); R2^H = U'' S W^H gives theta =
 // Q1 U'' S (Q2 W)^H, so the converged X is mapped back through the stored
-// block reflectors of the first QR, Z = Q1 [X; 0] (qrp_update_kernel<true>), and the
-// epilogue proceeds as without preconditioning (f = trans).
+// block reflectors of the first QR, Z = Q1 [X; 0] (qrp_update_kernel<true>,
+// kept columns only, after the truncation), and the epilogue writes the
+// factors as without preconditioning (f = trans).
 //
 // Per 32-column panel p of every gate's QR operand A (vectors = columns,
 // stride qr_m_pad, rows [0, qr_m)):
@@ -230,13 +231,15 @@ struct QrUpdSmem {
 template <bool kApply>
 __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
                                                             int p, const cplx* __restrict__ vbuf, long long vld,
-                                                            const cplx* __restrict__ tbuf, int npan) {
+                                                            const cplx* __restrict__ tbuf, int npan,
+                                                            const GateOut* __restrict__ out) {
   const GateDesc& g = gates[blockIdx.y];
   if (!g.pre) return;
   const int c0 = kQ * p;
   if (kApply && c0 >= g.n) return;
   const int cb = kApply ? kQ * blockIdx.x : c0 + kQ * (blockIdx.x + 1);
   if (cb >= g.n_pad) return;
+  if (kApply && cb >= out[blockIdx.y].k) return;  // only the kept columns are mapped back
   extern __shared__ __align__(16) unsigned char smem_raw[];
   QrUpdSmem& S = *reinterpret_cast<QrUpdSmem*>(smem_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -393,15 +396,18 @@ __global__ void __launch_bounds__(256) qrp_form_rh_kernel(const GateDesc* __rest
   }
 }
 
-// Z[j][r] = X[j][r] for r < n (X: stride m_pad, the converged R2^H side),
-// 0 for n <= r < qr_m_pad. Grid (qr_m_pad / 256, n_pad, gates).
-__global__ void __launch_bounds__(256) qrp_zinit_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws) {
+// Z[j][r] = X[order[j]][r] for r < n (X: stride m_pad, the converged R2^H
+// side, order: the truncation's descending-sigma order), 0 for n <= r <
+// qr_m_pad; kept columns j < k only. Grid (qr_m_pad / 256, n_pad, gates).
+__global__ void __launch_bounds__(256) qrp_zinit_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
+                                                        const int* __restrict__ order, long long sig_stride,
+                                                        const GateOut* __restrict__ out) {
   const GateDesc& g = gates[blockIdx.z];
   if (!g.pre) return;
   const long long r = blockIdx.x * 256LL + threadIdx.x;
   const int j = blockIdx.y;
-  if (r >= g.qr_m_pad || j >= g.n_pad) return;
-  const cplx* X = ws + g.ws_off + (long long)j * g.m_pad;
+  if (r >= g.qr_m_pad || j >= out[blockIdx.z].k) return;
+  const cplx* X = ws + g.ws_off + (long long)order[blockIdx.z * sig_stride + j] * g.m_pad;
   cplx* Z = ws + g.qr_off + (long long)j * g.qr_m_pad;
   Z[r] = r < g.n ? X[r] : make_double2(0.0, 0.0);
 }
@@ -425,19 +431,22 @@ void launch_qr_factor(const GateDesc* d_gates, int n_gates, int max_n_pad, int m
     const int blocks = panels - p - 1;
     if (blocks > 0)
       qrp_update_kernel<false><<<dim3(blocks, n_gates), 256, sizeof(QrUpdSmem), st>>>(d_gates, ws, p, vbuf, vld,
-                                                                                      tbuf, npan);
+                                                                                      tbuf, npan, nullptr);
   }
   qrp_form_rh_kernel<<<dim3(max_x_pad / 32, max_n_pad / 32, n_gates), 256, 0, st>>>(d_gates, ws);
 }
 
-// Z = Q1 [X; 0] with the reflectors kept by launch_qr_factor.
+// Z = Q1 [X_kept; 0] (kept columns in descending-sigma order) with the
+// reflectors kept by launch_qr_factor; runs after the truncation.
 void launch_qr_apply(const GateDesc* d_gates, int n_gates, int max_n_pad, int max_qr_m_pad, cplx* ws,
-                     const cplx* vbuf, long long vld, const cplx* tbuf, int npan, cudaStream_t st) {
-  qrp_zinit_kernel<<<dim3((max_qr_m_pad + 255) / 256, max_n_pad, n_gates), 256, 0, st>>>(d_gates, ws);
+                     const cplx* vbuf, long long vld, const cplx* tbuf, int npan, const int* order,
+                     long long sig_stride, const GateOut* out, cudaStream_t st) {
+  qrp_zinit_kernel<<<dim3((max_qr_m_pad + 255) / 256, max_n_pad, n_gates), 256, 0, st>>>(d_gates, ws, order,
+                                                                                        sig_stride, out);
   const int panels = max_n_pad / kQ;
   for (int p = panels - 1; p >= 0; --p)
     qrp_update_kernel<true><<<dim3(panels, n_gates), 256, sizeof(QrUpdSmem), st>>>(d_gates, ws, p, vbuf, vld, tbuf,
-                                                                                  npan);
+                                                                                  npan, out);
 }
 
 }  // namespace mpsim_gpu

@@ -6,7 +6,8 @@
 //   f = 0 (X = theta, or R^H of theta^H = QR):  U = X/sigma,  S V^dag = U^H theta = (X/sigma)^H X0
 //   f = 1 (X = theta^H, or R^H of theta = QR):  S V^dag = X^H, U = theta X Sigma^-2 = X0^H X / sigma^2
 // so one "cross-Gram" kernel (C = P^H Q over vector-major operands) produces
-// whichever factor is not a plain copy.
+// whichever factor is not a plain copy. With two-step QR preconditioning
+// (pre = 2) X is Z = Q1 [X_kept; 0], already in descending-sigma order.
 #include <float.h>
 
 #include "common.cuh"
@@ -141,7 +142,7 @@ __global__ void __launch_bounds__(256) copy_factor_kernel(const GateDesc* __rest
       if (j < k && e < g.m) {
         const double s = sg[j];
         if (s > 0.0) {
-          const cplx x = X[(long long)od[j] * g.m_pad + e];
+          const cplx x = X[(long long)(g.pre == 2 ? j : od[j]) * g.m_pad + e];
           v = make_double2(x.x / s, x.y / s);
         } else {
           v = make_double2(e == j ? 1.0 : 0.0, 0.0);  // zero matrix: any unit column
@@ -158,7 +159,7 @@ __global__ void __launch_bounds__(256) copy_factor_kernel(const GateDesc* __rest
     for (int jj = ty; jj < 32; jj += 8) {
       const int j = j0 + jj, e = e0 + tx;
       if (j < k && e < g.m) {
-        const cplx x = X[(long long)od[j] * g.m_pad + e];
+        const cplx x = X[(long long)(g.pre == 2 ? j : od[j]) * g.m_pad + e];
         const long long off = (long long)j * g.ldv + (long long)(e / g.vsplit) * g.vsplit_ld + e % g.vsplit;
         g.v_out[off] = make_double2(o.scale * x.x, -o.scale * x.y);
       }
@@ -198,12 +199,12 @@ __global__ void __launch_bounds__(256) cross_gram_kernel(const GateDesc* __restr
   auto pa = [&](int i) -> const cplx* {
     const int a = a0 + i;
     if (a >= n_a) return nullptr;
-    return g.f == 0 ? X + (long long)od[a] * g.m_pad : X0 + (long long)a * g.x0_ld;
+    return g.f == 0 ? X + (long long)(g.pre == 2 ? a : od[a]) * g.m_pad : X0 + (long long)a * g.x0_ld;
   };
   auto pb = [&](int i) -> const cplx* {
     const int b = b0 + i;
     if (b >= n_b) return nullptr;
-    return g.f == 0 ? X0 + (long long)b * g.x0_ld : X + (long long)od[b] * g.m_pad;
+    return g.f == 0 ? X0 + (long long)b * g.x0_ld : X + (long long)(g.pre == 2 ? b : od[b]) * g.m_pad;
   };
   const int ip = t / 16, jp = t % 16;
   cplx acc[2][2];

@@ -8,7 +8,7 @@ GPU's convergence test (all relative off-diagonals <= 4 eps * 32).
     VARIANT: plain   Jacobi on theta's columns
              qr      Jacobi on R^H, theta = Q R (what qr_pre.cu does)
              qrcp    Jacobi on R^H of a column-pivoted QR
-             qr2     Jacobi on R2^H, R^H = Q2 R2 (two QR steps)
+             qr2     Jacobi on R2^H, R^H = Q2 R2 (two QR steps); qr3, qr4 likewise
              cross   plain, cross-block-only inner sweeps while the measured
                      rms relative off-norm of the previous sweep > 0.35
 Measured (chi = 512, theta 1024 x 1024 from a saturated random MPS):
@@ -114,7 +114,7 @@ def main():
         X = sl.qr(th, pivoting=True, mode='economic')[1].conj().T.copy()
     else:
         X = np.linalg.qr(th)[1].conj().T.copy()
-        if variant == "qr2":
+        for _ in range({"qr2": 1, "qr3": 2, "qr4": 3}.get(variant, 0)):
             X = np.linalg.qr(X)[1].conj().T.copy()
     sweeps = run(X, fro2, cross_policy=variant == "cross")
     print(f"{variant}: converged after {sweeps} rotating sweeps")
