@@ -33,6 +33,8 @@ void launch_jacobi_round_dmma(const GateDesc*, int, int, cplx*, const int*, int*
                               const double*, double, const int*, long long, double*, cudaStream_t);
 void jacobi_split_init();
 void qrp_init();
+void split_init();
+void theta_init();
 void launch_qr_factor(const GateDesc*, int, int, int, cplx*, cplx*, long long, cplx*, int, cudaStream_t);
 void launch_qr_apply(const GateDesc*, int, int, int, cplx*, const cplx*, long long, const cplx*, int, const int*,
                      long long, const GateOut*, cudaStream_t);
@@ -223,6 +225,8 @@ State::State(int n_, long long chi_hint, int dev) : n(n_), device(dev) {
     jacobi_dmma_init();
     jacobi_split_init();
     qrp_init();
+    split_init();
+    theta_init();
     inited = true;
   }
   chi = next_pow2(std::max<long long>(2, std::min<long long>(chi_hint, 1 << 14)));

@@ -25,32 +25,17 @@
 //                       DMMA with the pair-chunk pipeline of jacobi_split.cu
 // and finally qrp_form_rh_kernel writes X = R^H (n vectors of length n).
 #include "common.cuh"
+#include "pair_gemm.cuh"
 
 namespace mpsim_gpu {
 
 namespace {
 
-constexpr int kQ = 32;       // panel width
-constexpr int kQC = 32;      // rows per streamed chunk
-constexpr int kQPitch = 36;  // conflict-free DMMA fragment pitch (== 4 mod 16)
-constexpr int kQPlane = kQC * kQPitch;
+constexpr int kQ = 32;                  // panel width
+constexpr int kQC = pg::kC;             // rows per streamed chunk
+constexpr int kQPitch = pg::kPitch;     // conflict-free DMMA fragment pitch (== 4 mod 16)
+constexpr int kQPlane = pg::kPlane;
 constexpr int kQPitchW = 68;
-
-__device__ __forceinline__ void dmma_q(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ void cp_async8_q(double* smem, const double* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_commit_q() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait_q() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
 
 __device__ __forceinline__ double block_sum_1024(double v, double* red) {
 #pragma unroll
@@ -179,40 +164,10 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
 
 namespace {
 
-// Streams rows [r0, r0 + kQC) of 32 V vectors and 32 A vectors into split
-// Re/Im planes: buf = [Vr | Vi | Ar | Ai], each kQC x kQPitch.
-struct QrChunkLoader {
-  const double* vsrc;
-  const double* asrc;
-  int soff;
-  __device__ __forceinline__ void init(const cplx* V, long long vld, const cplx* A, long long ald, int t) {
-    const int lane = t & 31, warp = t >> 5;
-    const int e = (lane & 3) + 4 * (lane >> 4);
-    const int vi = 4 * warp + ((lane >> 2) & 3);
-    vsrc = reinterpret_cast<const double*>(V + (long long)vi * vld + e);
-    asrc = reinterpret_cast<const double*>(A + (long long)vi * ald + e);
-    soff = e * kQPitch + vi;
-  }
-  __device__ __forceinline__ void issue(double* buf, int r0, bool with_v = true) const {
-#pragma unroll
-    for (int s = 0; s < kQC / 8; ++s) {
-      double* d = buf + soff + 8 * s * kQPitch;
-      const long long go = 2LL * (r0 + 8 * s);
-      if (with_v) {
-        cp_async8_q(d, vsrc + go);
-        cp_async8_q(d + kQPlane, vsrc + go + 1);
-      }
-      cp_async8_q(d + 2 * kQPlane, asrc + go);
-      cp_async8_q(d + 3 * kQPlane, asrc + go + 1);
-    }
-    cp_async_commit_q();
-  }
-};
-
 struct QrUpdSmem {
   union {
-    double buf[2][4 * kQPlane];
-    struct {
+    double buf[2][pg::kBuf];
+    struct {                     // after pass 1 (the chunk buffers are dead)
       double Wx[64 * 65];        // real 64 x 64 V_ext^T A_ext
       cplx W[kQ * (kQ + 1)];     // V^H A_b
       cplx T[kQ * (kQ + 1)];
@@ -247,63 +202,14 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
   const long long ald = g.qr_m_pad;
   cplx* A = ws + g.qr_off + (long long)cb * ald;
   const cplx* V = vbuf + ((long long)blockIdx.y * npan + p) * kQ * vld;
-  QrChunkLoader ld;
-  ld.init(V, vld, A, ald, t);
+  pg::Loader ld;
+  ld.init(V + (long long)pg::loader_vector(t) * vld, A + (long long)pg::loader_vector(t) * ald, t);
   const int nchunks = (int)((ald - c0) / kQC);
 
-  // ---- pass 1: W_ext = V_ext^T A_ext (64 x 64 real). Warp w: quadrant
-  // (x = w / 4 (V Re/Im), y = (w / 2) & 1 (A Re/Im)), tile rows 2 (w & 1) + {0, 1},
-  // all four tile columns.
-  const int qx = warp >> 2, qy = (warp >> 1) & 1, tr0 = 2 * (warp & 1);
-  double acc[2][4][2];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[a][c][0] = acc[a][c][1] = 0.0;
-  ld.issue(S.u.buf[0], c0);
-  for (int k = 0; k < nchunks; ++k) {
-    if (k + 1 < nchunks) {
-      ld.issue(S.u.buf[(k + 1) & 1], c0 + (k + 1) * kQC);
-      cp_async_wait_q<1>();
-    } else {
-      cp_async_wait_q<0>();
-    }
-    __syncthreads();
-    const double* Pv = S.u.buf[k & 1] + qx * kQPlane;
-    const double* Pa = S.u.buf[k & 1] + (2 + qy) * kQPlane;
-#pragma unroll
-    for (int ks = 0; ks < kQC / 4; ++ks) {
-      const int row = (4 * ks + fk) * kQPitch;
-      double av[2], bv[4];
-#pragma unroll
-      for (int a = 0; a < 2; ++a) av[a] = Pv[row + 8 * (tr0 + a) + fr];  // A[m = v idx][k = e]
-#pragma unroll
-      for (int c = 0; c < 4; ++c) bv[c] = Pa[row + 8 * c + fr];          // B[k = e][n = a idx]
-#pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) dmma_q(acc[a][c][0], acc[a][c][1], av[a], bv[c]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-      for (int v = 0; v < 2; ++v)
-        S.u.w.Wx[(qx * kQ + 8 * (tr0 + a) + fr) * 65 + qy * kQ + 8 * c + 2 * fk + v] = acc[a][c][v];
+  // ---- pass 1: W = V^H A_b (pair_gemm.cuh), then T
+  pg::cross_gram(ld, S.u.buf, S.u.w.Wx, S.u.w.W, kQ + 1, c0, ald, t);
   const cplx* Tg = tbuf + ((long long)blockIdx.y * npan + p) * kQ * kQ;
   for (int idx = t; idx < kQ * kQ; idx += 256) S.u.w.T[(idx / kQ) * (kQ + 1) + idx % kQ] = Tg[idx];
-  __syncthreads();
-  // W = V^H A_b: Re = Vr^T Ar + Vi^T Ai, Im = Vr^T Ai - Vi^T Ar
-  for (int idx = t; idx < kQ * kQ; idx += 256) {
-    const int i = idx / kQ, j = idx % kQ;
-    const double* Wx = S.u.w.Wx;
-    const double re = Wx[i * 65 + j] + Wx[(kQ + i) * 65 + kQ + j];
-    const double im = Wx[i * 65 + kQ + j] - Wx[(kQ + i) * 65 + j];
-    S.u.w.W[i * (kQ + 1) + j] = make_double2(re, im);
-  }
   __syncthreads();
   // W2 = T^H W (factorisation) or T W (apply), T upper triangular; stored
   // negated in real-extended form
@@ -330,9 +236,9 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
   for (int k = 0; k < nchunks; ++k) {
     if (k + 1 < nchunks) {
       ld.issue(S.u.buf[(k + 1) & 1], c0 + (k + 1) * kQC);
-      cp_async_wait_q<1>();
+      pg::wait<1>();
     } else {
-      cp_async_wait_q<0>();
+      pg::wait<0>();
     }
     __syncthreads();
     const double* B = S.u.buf[k & 1];
@@ -351,10 +257,10 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
       const double* plane = B + (cext < kQ ? 0 : kQPlane) + (cext & (kQ - 1));
       const double a0 = plane[(8 * rbase + fr) * kQPitch], a1 = plane[(8 * (rbase + 1) + fr) * kQPitch];
       const double b0 = S.W2x[cext * kQPitchW + bre], b1 = S.W2x[cext * kQPitchW + bim];
-      dmma_q(o[0][0][0], o[0][0][1], a0, b0);
-      dmma_q(o[0][1][0], o[0][1][1], a0, b1);
-      dmma_q(o[1][0][0], o[1][0][1], a1, b0);
-      dmma_q(o[1][1][0], o[1][1][1], a1, b1);
+      pg::dmma(o[0][0][0], o[0][0][1], a0, b0);
+      pg::dmma(o[0][1][0], o[0][1][1], a0, b1);
+      pg::dmma(o[1][0][0], o[1][0][1], a1, b0);
+      pg::dmma(o[1][1][0], o[1][1][1], a1, b1);
     }
     const int r0 = c0 + k * kQC;
 #pragma unroll

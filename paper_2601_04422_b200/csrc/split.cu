@@ -11,6 +11,7 @@
 #include <float.h>
 
 #include "common.cuh"
+#include "pair_gemm.cuh"
 
 namespace mpsim_gpu {
 
@@ -167,15 +168,24 @@ __global__ void __launch_bounds__(256) copy_factor_kernel(const GateDesc* __rest
   }
 }
 
-// ---- cross-Gram factor, C[a][b] = sum_e conj(P_a[e]) Q_b[e].
-//  trans 0: a = j (X, ordered), b = v (X0):  site q+1[(j*2+p1)*chi + r] = scale/sigma_j * C, v = p1*dr + r
-//  trans 1: a = v (X0), b = j (X, ordered):  site q  [v*chi + j]        = C / sigma_j^2
-__global__ void __launch_bounds__(256) cross_gram_kernel(const GateDesc* __restrict__ gates,
-                                                         const cplx* __restrict__ ws,
-                                                         const double* __restrict__ sigma,
-                                                         const int* __restrict__ order, long long sig_stride,
-                                                         const GateOut* __restrict__ out,
-                                                         const double* __restrict__ frob2, double floor_rel2) {
+// ---- cross-Gram factor, C[a][b] = sum_e conj(P_a[e]) Q_b[e], on DMMA
+// (pair_gemm.cuh), one 32 x 32 block of C per CTA.
+//  f = 0: a = j (X, sigma order), b = v (X0): site q+1[(j*2+p1)*chi + r] = scale/sigma_j * C, v = p1*dr + r
+//  f = 1: a = v (X0), b = j (X, sigma order): site q  [v*chi + j]        = C / sigma_j^2
+struct CrossSmem {
+  union {
+    double buf[2][pg::kBuf];
+    double Wx[64 * 65];
+  } u;
+  cplx W[32 * 33];
+};
+
+__global__ void __launch_bounds__(256, 2) cross_gram_kernel(const GateDesc* __restrict__ gates,
+                                                            const cplx* __restrict__ ws,
+                                                            const double* __restrict__ sigma,
+                                                            const int* __restrict__ order, long long sig_stride,
+                                                            const GateOut* __restrict__ out,
+                                                            const double* __restrict__ frob2, double floor_rel2) {
   const GateDesc& g = gates[blockIdx.z];
   const GateOut o = out[blockIdx.z];
   const int k = o.k;
@@ -188,76 +198,45 @@ __global__ void __launch_bounds__(256) cross_gram_kernel(const GateDesc* __restr
   const int n_b = g.f == 0 ? g.n0 : k;
   const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32;
   if (a0 >= n_a || b0 >= n_b) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CrossSmem& S = *reinterpret_cast<CrossSmem*>(smem_raw);
   const double* sg = sigma + blockIdx.z * sig_stride;
   const int* od = order + blockIdx.z * sig_stride;
   const cplx* X = ws + g.ws_off;
   const cplx* X0 = ws + g.x0_off;
-  constexpr int kCE = 32;
-  __shared__ cplx Ta[kCE][kPad];
-  __shared__ cplx Tb[kCE][kPad];
   const int t = threadIdx.x;
-  auto pa = [&](int i) -> const cplx* {
-    const int a = a0 + i;
-    if (a >= n_a) return nullptr;
-    return g.f == 0 ? X + (long long)(g.pre == 2 ? a : od[a]) * g.m_pad : X0 + (long long)a * g.x0_ld;
-  };
-  auto pb = [&](int i) -> const cplx* {
-    const int b = b0 + i;
-    if (b >= n_b) return nullptr;
-    return g.f == 0 ? X0 + (long long)b * g.x0_ld : X + (long long)(g.pre == 2 ? b : od[b]) * g.m_pad;
-  };
-  const int ip = t / 16, jp = t % 16;
-  cplx acc[2][2];
-#pragma unroll
-  for (int a = 0; a < 2; ++a)
-#pragma unroll
-    for (int b = 0; b < 2; ++b) acc[a][b] = make_double2(0.0, 0.0);
-  for (int e0 = 0; e0 < g.m_pad; e0 += kCE) {
-#pragma unroll
-    for (int s = 0; s < (32 * kCE) / 256; ++s) {
-      const int idx = t + 256 * s;
-      const int vi = idx / kCE, ee = idx % kCE;
-      const cplx* xa = pa(vi);
-      const cplx* xb = pb(vi);
-      Ta[ee][vi] = xa ? xa[e0 + ee] : make_double2(0.0, 0.0);
-      Tb[ee][vi] = xb ? xb[e0 + ee] : make_double2(0.0, 0.0);
-    }
-    __syncthreads();
-#pragma unroll 8
-    for (int ee = 0; ee < kCE; ++ee) {
-      const cplx x0 = Ta[ee][2 * ip], x1 = Ta[ee][2 * ip + 1];
-      const cplx y0 = Tb[ee][2 * jp], y1 = Tb[ee][2 * jp + 1];
-      cfmac(acc[0][0], x0, y0);
-      cfmac(acc[0][1], x0, y1);
-      cfmac(acc[1][0], x1, y0);
-      cfmac(acc[1][1], x1, y1);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int ai = 0; ai < 2; ++ai)
-#pragma unroll
-    for (int bi = 0; bi < 2; ++bi) {
-      const int a = a0 + 2 * ip + ai, b = b0 + 2 * jp + bi;
-      if (a >= n_a || b >= n_b) continue;
-      const cplx c = acc[ai][bi];
-      if (g.f == 0) {
-        const double s = sg[a];
-        const double f = s * s > floor2 && s > 0.0 ? o.scale / s : 0.0;
-        const long long off = (long long)a * g.ldv + (long long)(b / g.vsplit) * g.vsplit_ld + b % g.vsplit;
-        g.v_out[off] = make_double2(f * c.x, f * c.y);
+  auto xvec = [&](int j) { return X + (long long)(g.pre == 2 ? j : od[j]) * g.m_pad; };
+  auto x0vec = [&](int v) { return X0 + (long long)v * g.x0_ld; };
+  const int vi = pg::loader_vector(t);
+  const int a = min(a0 + vi, n_a - 1), b = min(b0 + vi, n_b - 1);  // padding lanes load a valid vector
+  pg::Loader ld;
+  ld.init(g.f == 0 ? xvec(a) : x0vec(a), g.f == 0 ? x0vec(b) : xvec(b), t);
+  pg::cross_gram(ld, S.u.buf, S.u.Wx, S.W, 33, 0, g.m_pad, t);
+  for (int idx = t; idx < 32 * 32; idx += 256) {
+    const int ai = a0 + idx / 32, bi = b0 + idx % 32;
+    if (ai >= n_a || bi >= n_b) continue;
+    const cplx c = S.W[(idx / 32) * 33 + idx % 32];
+    if (g.f == 0) {
+      const double s = sg[ai];
+      const double f = s * s > floor2 && s > 0.0 ? o.scale / s : 0.0;
+      const long long off = (long long)ai * g.ldv + (long long)(bi / g.vsplit) * g.vsplit_ld + bi % g.vsplit;
+      g.v_out[off] = make_double2(f * c.x, f * c.y);
+    } else {
+      const double s = sg[bi];
+      cplx v;
+      if (s * s > floor2 && s > 0.0) {
+        const double f = 1.0 / (s * s);
+        v = make_double2(f * c.x, f * c.y);
       } else {
-        const double s = sg[b];
-        cplx v;
-        if (s * s > floor2 && s > 0.0) {
-          const double f = 1.0 / (s * s);
-          v = make_double2(f * c.x, f * c.y);
-        } else {
-          v = make_double2(s == 0.0 && a == b ? 1.0 : 0.0, 0.0);
-        }
-        g.u_out[(long long)a * g.ldu + b] = v;
+        v = make_double2(s == 0.0 && ai == bi ? 1.0 : 0.0, 0.0);
       }
+      g.u_out[(long long)ai * g.ldu + bi] = v;
     }
+  }
+}
+
+void split_init() {
+  cudaFuncSetAttribute(cross_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CrossSmem));
 }
 
 void launch_norms(const GateDesc* d_gates, int n_gates, int max_n, const cplx* ws, double* sigma,
@@ -276,7 +255,7 @@ void launch_write_factors(const GateDesc* d_gates, int n_gates, int max_m, int m
   // k <= n, so n bounds every tile count.
   copy_factor_kernel<<<dim3((max_m + 31) / 32, (max_n + 31) / 32, n_gates), 256, 0, st>>>(
       d_gates, ws, sigma, order, sig_stride, d_out);
-  cross_gram_kernel<<<dim3((max_n0 + 31) / 32, (max_n0 + 31) / 32, n_gates), 256, 0, st>>>(
+  cross_gram_kernel<<<dim3((max_n0 + 31) / 32, (max_n0 + 31) / 32, n_gates), 256, sizeof(CrossSmem), st>>>(
       d_gates, ws, sigma, order, sig_stride, d_out, frob2, floor_rel2);
 }
 

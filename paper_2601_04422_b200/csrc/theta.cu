@@ -8,6 +8,9 @@
 // Here the three steps are one kernel: each CTA owns a 32(l) x 32(r) tile for
 // all four (p0,p1) physical combinations, so the gate mix is a register-level
 // epilogue of the merge GEMM and theta is never materialised in site order.
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 
 namespace mpsim_gpu {
@@ -130,10 +133,198 @@ __global__ void __launch_bounds__(256) theta_kernel(const GateDesc* __restrict__
   }
 }
 
+// ---- DMMA variant (default). Same tile (32 l x 32 r x all (p0, p1)) as a
+// complex GEMM C (64 x 64) = A (64 x Dm) B (Dm x 64), rows (l, p0), cols
+// (p1, r), on mma.sync.m8n8k4.f64 in real-extended form with the complex
+// interleave as the K index: k = 2 m + c,
+//   A_ext[row][2m + c] = (Re, Im)[c] A[row][m]        (the smem layout as loaded)
+//   Re C: B_ext[2m + c][j] = (Re B, -Im B)[c],  Im C: B_ext[2m + c][j] = (Im B, Re B)[c]
+// so one 16-byte B load feeds the Re and the Im tile. 16 m per stage, two
+// stages in flight with cp.async (zero-filled outside the tensors).
+namespace {
+constexpr int kTM = 16;          // m per stage
+constexpr int kPA = 2 * kTM + 4; // A row pitch (doubles): == 4 mod 16, conflict-free fragments
+constexpr int kPB = 2 * 64 + 4;  // B row pitch (doubles)
+struct ThetaSmem {
+  union {
+    struct {
+      double A[2][64 * kPA];
+      double B[2][kTM * kPB];
+    } st;
+    cplx C[64 * 65];  // epilogue staging
+  } u;
+  cplx U[16];
+};
+__device__ __forceinline__ void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void dmma_t(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+}  // namespace
+
+__global__ void __launch_bounds__(256, 2) theta_dmma_kernel(const GateDesc* __restrict__ gates,
+                                                            const cplx* __restrict__ sites, long long site_stride,
+                                                            int chi, cplx* __restrict__ ws,
+                                                            double* __restrict__ frob2) {
+  const GateDesc& g = gates[blockIdx.y];
+  const int tiles_r = (g.dr + kTR - 1) / kTR;
+  const int tiles_l = (g.dl + kTL - 1) / kTL;
+  const int tl = blockIdx.x / tiles_r, tr = blockIdx.x % tiles_r;
+  if (tl >= tiles_l) return;
+  const int l0 = tl * kTL, r0 = tr * kTR;
+  const int dl = g.dl, dm = g.dm, dr = g.dr;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ThetaSmem& S = *reinterpret_cast<ThetaSmem*>(smem_raw);
+  const cplx* A = sites + (long long)g.q * site_stride;
+  const cplx* B = sites + (long long)(g.q + 1) * site_stride;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  if (t < 16) S.U[t] = g.u[t];
+
+  auto issue = [&](int buf, int m0) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int idx = t + 256 * s;
+      {  // A: row i = (l, p0), 16 m
+        const int i = idx / kTM, mm = idx % kTM;
+        const int l = l0 + i / 2, m = m0 + mm;
+        const bool ok = l < dl && m < dm;
+        cp_async16_zfill(&S.u.st.A[buf][i * kPA + 2 * mm], ok ? (const void*)(A + (long long)(2 * l0 + i) * chi + m)
+                                                              : (const void*)A, ok);
+      }
+      {  // B: 16 m x 64 cols (p1, r)
+        const int mm = idx / 64, j = idx % 64;
+        const int p1 = j / kTR, r = r0 + j % kTR, m = m0 + mm;
+        const bool ok = m < dm && r < dr;
+        cp_async16_zfill(&S.u.st.B[buf][mm * kPB + 2 * j],
+                         ok ? (const void*)(B + (long long)(m * 2 + p1) * chi + r) : (const void*)B, ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+
+  // warp w: row tiles 2 (w >> 1) + {0, 1}, complex column tiles 4 (w & 1) + {0..3}
+  const int rt0 = 2 * (warp >> 1), ct0 = 4 * (warp & 1);
+  double acc[2][4][2][2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) acc[a][c][q][0] = acc[a][c][q][1] = 0.0;
+  const int nk = (dm + kTM - 1) / kTM;
+  const bool im_lane = (fk & 1) != 0;  // c of this lane's k index
+  issue(0, 0);
+  for (int kc = 0; kc < nk; ++kc) {
+    if (kc + 1 < nk) {
+      issue((kc + 1) & 1, (kc + 1) * kTM);
+      asm volatile("cp.async.wait_group 1;\n" ::);
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::);
+    }
+    __syncthreads();
+    const double* As = S.u.st.A[kc & 1];
+    const double* Bs = S.u.st.B[kc & 1];
+#pragma unroll
+    for (int ks = 0; ks < 2 * kTM / 4; ++ks) {
+      const int kk = 4 * ks + fk;  // = 2 m + c
+      double av[2];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) av[a] = As[(8 * (rt0 + a) + fr) * kPA + kk];
+      const int mm = kk >> 1;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const double2 b = *reinterpret_cast<const double2*>(&Bs[mm * kPB + 2 * (8 * (ct0 + c) + fr)]);
+        const double bre = im_lane ? -b.y : b.x;  // Re C tile
+        const double bim = im_lane ? b.x : b.y;   // Im C tile
+#pragma unroll
+        for (int a = 0; a < 2; ++a) {
+          dmma_t(acc[a][c][0][0], acc[a][c][0][1], av[a], bre);
+          dmma_t(acc[a][c][1][0], acc[a][c][1][1], av[a], bim);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // stage C (rows (l, p0), cols (p1, r)) for the gate-mix epilogue
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int v = 0; v < 2; ++v)
+        S.u.C[(8 * (rt0 + a) + fr) * 65 + 8 * (ct0 + c) + 2 * fk + v] = make_double2(acc[a][c][0][v], acc[a][c][1][v]);
+  __syncthreads();
+
+  cplx* X = ws + (g.pre ? g.qr_off : g.ws_off);
+  const long long ldx = g.pre ? g.qr_m_pad : g.m_pad;
+  cplx* X0 = ws + g.x0_off;
+  const int tx = t % 16, ty = t / 16;
+  double f2 = 0.0;
+#pragma unroll
+  for (int ls = 0; ls < 2; ++ls)
+#pragma unroll
+    for (int rs = 0; rs < 2; ++rs) {
+      const int li = ty + 16 * ls, ri = tx + 16 * rs;
+      const int l = l0 + li, r = r0 + ri;
+      if (l >= dl || r >= dr) continue;
+      cplx T[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) T[i] = S.u.C[(2 * li + (i >> 1)) * 65 + (i & 1) * kTR + ri];
+#pragma unroll
+      for (int o = 0; o < 4; ++o) {
+        // theta'[p0',p1'] = sum_{p0,p1} u[2p0'+p1', 2p0+p1] T[p0][p1]  (gate_apply.cpp:127-128)
+        cplx v = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cfma(v, T[i], S.U[o * 4 + i]);
+        const int p0o = o >> 1, p1o = o & 1;
+        const long long row = l * 2 + p0o, col = p1o * dr + r;  // theta (2Dl x 2Dr)
+        const cplx vc = make_double2(v.x, -v.y);
+        if (g.trans == 0) X[col * ldx + row] = v;
+        else X[row * ldx + col] = vc;
+        if (g.f == 0) X0[col * g.x0_ld + row] = v;
+        else X0[row * g.x0_ld + col] = vc;
+        f2 += cabs2(v);
+      }
+    }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) f2 += __shfl_xor_sync(0xffffffffu, f2, o);
+  __shared__ double red[8];
+  if (lane == 0) red[warp] = f2;
+  __syncthreads();
+  if (t == 0) {
+    double sum = 0.0;
+    for (int i = 0; i < 8; ++i) sum += red[i];
+    atomicAdd(frob2 + blockIdx.y, sum);
+  }
+}
+
+void theta_init() {
+  cudaFuncSetAttribute(theta_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(ThetaSmem));
+}
+
+// MPSIM_THETA=simt selects the DFMA kernel (A/B only).
+static bool theta_simt() {
+  static const bool v = [] {
+    const char* e = std::getenv("MPSIM_THETA");
+    return e != nullptr && std::string(e) == "simt";
+  }();
+  return v;
+}
+
 void launch_theta(const GateDesc* d_gates, int n_gates, int max_tiles, const cplx* sites,
                   long long site_stride, int chi, cplx* ws, double* frob2, cudaStream_t st) {
   if (n_gates == 0) return;
-  theta_kernel<<<dim3(max_tiles, n_gates), 256, 0, st>>>(d_gates, sites, site_stride, chi, ws, frob2);
+  if (theta_simt())
+    theta_kernel<<<dim3(max_tiles, n_gates), 256, 0, st>>>(d_gates, sites, site_stride, chi, ws, frob2);
+  else
+    theta_dmma_kernel<<<dim3(max_tiles, n_gates), 256, sizeof(ThetaSmem), st>>>(d_gates, sites, site_stride, chi,
+                                                                                 ws, frob2);
 }
 
 int theta_tiles(int dl, int dr) { return ((dl + kTL - 1) / kTL) * ((dr + kTR - 1) / kTR); }
