@@ -24,6 +24,11 @@
 //                       32-column block b right of the panel, both GEMMs on
 //                       DMMA with the pair-chunk pipeline of jacobi_split.cu
 // and finally qrp_form_rh_kernel writes X = R^H (n vectors of length n).
+#include <cooperative_groups.h>
+
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 #include "pair_gemm.cuh"
 
@@ -54,6 +59,9 @@ __device__ __forceinline__ double block_sum_1024(double v, double* red) {
 
 // vbuf: per gate and panel kQ vectors of stride vld (>= qr_m_pad); tbuf: per
 // gate and panel kQ x kQ; npan panel slots per gate (all kept for Q1 [X; 0]).
+// The current reflector is also staged in shared memory (dynamic, qr_m_pad
+// complex) and the per-warp column loops keep 8 independent loads in flight:
+// the panel is latency-bound (32 dependent reflectors), not bandwidth-bound.
 __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
                                                          int p, cplx* __restrict__ vbuf, long long vld,
                                                          cplx* __restrict__ tbuf, int npan) {
@@ -71,6 +79,8 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
   __shared__ cplx taus[kQ];
   __shared__ cplx Gv[kQ][kQ + 1];
   __shared__ cplx T[kQ][kQ + 1];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* vs = reinterpret_cast<cplx*>(smem_raw);  // current reflector, rows [0, qr_m_pad)
 
   for (int j = 0; j < jb; ++j) {
     const int row0 = c0 + j;
@@ -96,29 +106,95 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
       if (r == row0) v = make_double2(1.0, 0.0);
       else if (r > row0 && r < m && refl) v = cmul(col[r], inv);
       vj[r] = v;
+      if (r < ld) vs[r] = v;
     }
     if (t == 0) {
       if (row0 < m) col[row0] = make_double2(refl ? beta : alpha.x, refl ? 0.0 : alpha.y);
       taus[j] = tau;
     }
     __syncthreads();
-    // H^H = I - conj(tau) v v^H on panel columns j+1 .. jb-1, one warp each
-    if (refl && warp < jb - 1 - j) {
-      cplx* a = A + (long long)(c0 + j + 1 + warp) * ld;
-      cplx w = make_double2(0.0, 0.0);
-      for (int r = row0 + lane; r < m; r += 32) cfmac(w, vj[r], a[r]);
+    // warps [jb-1-j, jb-1): Gv[i][j] = v_i^H v_j, i < j (for zlarft), while
+    // warps [0, jb-1-j) apply H^H = I - conj(tau) v v^H to panel columns
+    // j+1 .. jb-1, one column each
+    if (warp >= jb - 1 - j && warp < jb - 1) {
+      const int i = warp - (jb - 1 - j);
+      const cplx* vi = V + (long long)i * vld;
+      constexpr int kU = 4;
+      cplx w[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) w[u] = make_double2(0.0, 0.0);
+      for (int rb = row0; rb < m; rb += 32 * kU) {
+        cplx xv[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int r = rb + 32 * u + lane;
+          xv[u] = r < m ? vi[r] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int r = rb + 32 * u + lane;
+          if (r < m) cfmac(w[u], xv[u], vs[r]);
+        }
+      }
+#pragma unroll
+      for (int u = 1; u < kU; ++u) {
+        w[0].x += w[u].x;
+        w[0].y += w[u].y;
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        w.x += __shfl_xor_sync(0xffffffffu, w.x, o);
-        w.y += __shfl_xor_sync(0xffffffffu, w.y, o);
+        w[0].x += __shfl_xor_sync(0xffffffffu, w[0].x, o);
+        w[0].y += __shfl_xor_sync(0xffffffffu, w[0].y, o);
       }
-      const cplx coef = cmul(make_double2(tau.x, -tau.y), w);
-      for (int r = row0 + lane; r < m; r += 32) {
-        const cplx vr = vj[r];
-        cplx ar = a[r];
-        ar.x -= vr.x * coef.x - vr.y * coef.y;
-        ar.y -= vr.x * coef.y + vr.y * coef.x;
-        a[r] = ar;
+      if (lane == 0) Gv[i][j] = w[0];
+    }
+    if (refl && warp < jb - 1 - j) {
+      cplx* a = A + (long long)(c0 + j + 1 + warp) * ld;
+      constexpr int kU = 4;
+      cplx w[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) w[u] = make_double2(0.0, 0.0);
+      for (int rb = row0; rb < m; rb += 32 * kU) {
+        cplx av[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int r = rb + 32 * u + lane;
+          av[u] = r < m ? a[r] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int r = rb + 32 * u + lane;
+          if (r < m) cfmac(w[u], vs[r], av[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 1; u < kU; ++u) {
+        w[0].x += w[u].x;
+        w[0].y += w[u].y;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        w[0].x += __shfl_xor_sync(0xffffffffu, w[0].x, o);
+        w[0].y += __shfl_xor_sync(0xffffffffu, w[0].y, o);
+      }
+      const cplx coef = cmul(make_double2(tau.x, -tau.y), w[0]);
+      for (int rb = row0; rb < m; rb += 32 * kU) {
+        cplx av[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int r = rb + 32 * u + lane;
+          av[u] = r < m ? a[r] : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int r = rb + 32 * u + lane;
+          if (r < m) {
+            const cplx vr = vs[r];
+            av[u].x -= vr.x * coef.x - vr.y * coef.y;
+            av[u].y -= vr.x * coef.y + vr.y * coef.x;
+            a[r] = av[u];
+          }
+        }
       }
     }
     __syncthreads();
@@ -128,21 +204,6 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
     cplx* vj = V + (long long)j * vld;
     for (long long r = t; r < vld; r += 1024) vj[r] = make_double2(0.0, 0.0);
     if (t == 0) taus[j] = make_double2(0.0, 0.0);
-  }
-  // Gram of the reflectors, Gv[i][k] = v_i^H v_k (i < k), rows >= c0 + k
-  for (int pr = warp; pr < kQ * kQ; pr += 32) {
-    const int i = pr / kQ, k = pr % kQ;
-    if (i >= k || k >= jb) continue;
-    const cplx* vi = V + (long long)i * vld;
-    const cplx* vk = V + (long long)k * vld;
-    cplx w = make_double2(0.0, 0.0);
-    for (int r = c0 + k + lane; r < m; r += 32) cfmac(w, vi[r], vk[r]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      w.x += __shfl_xor_sync(0xffffffffu, w.x, o);
-      w.y += __shfl_xor_sync(0xffffffffu, w.y, o);
-    }
-    if (lane == 0) Gv[i][k] = w;
   }
   for (int idx = t; idx < kQ * (kQ + 1); idx += 1024) T[idx / (kQ + 1)][idx % (kQ + 1)] = make_double2(0.0, 0.0);
   __syncthreads();
@@ -160,6 +221,189 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
   }
   cplx* To = tbuf + ((long long)blockIdx.x * npan + p) * kQ * kQ;
   for (int idx = t; idx < kQ * kQ; idx += 1024) To[idx] = T[idx / kQ][idx % kQ];
+}
+
+// ---- Cluster-resident panel (default for qr_m_pad <= 256 * 8): the 32
+// panel columns live in registers, spread over a cluster of cs = qr_m_pad /
+// 256 CTAs of 32 warps: warp w of CTA k holds rows [256 k, 256 k + 256) of
+// panel column w, 8 rows per lane. A reflector costs two cluster barriers:
+// (1) partial norms -> every CTA forms beta / tau redundantly; (2) partial
+// v^H a_c (and v_i^H v_j for zlarft) -> every CTA updates its rows. The
+// previous kernel (qrp_panel_kernel) streamed the columns through L2 on every
+// reflector and spent 10 us per reflector waiting on those loads.
+namespace cgp = cooperative_groups;
+constexpr int kPR = 256;  // panel rows per CTA
+constexpr int kPL = kPR / 32;
+
+struct PanelSmem {
+  cplx vs[kQ][kPR];       // this CTA's rows of every reflector
+  double pn[2];           // partial ||x(2:)||^2 (double-buffered by reflector parity)
+  cplx pal[2];            // alpha, written by the CTA owning the diagonal row
+  cplx pw[2][kQ];         // partial v_j^H a_c (c > j) and v_i^H v_j (i < j)
+  cplx taus[kQ];
+  cplx Gv[kQ][kQ + 1];
+  cplx T[kQ][kQ + 1];
+  cplx tau, inv, alpha;  // this reflector's zlarfg results (thread 0 forms them)
+  double beta;
+};
+
+__global__ void __launch_bounds__(1024, 1) qrp_panel_cluster_kernel(const GateDesc* __restrict__ gates,
+                                                                    cplx* __restrict__ ws, int p,
+                                                                    cplx* __restrict__ vbuf, long long vld,
+                                                                    cplx* __restrict__ tbuf, int npan) {
+  cgp::cluster_group cl = cgp::this_cluster();
+  const int rank = (int)cl.block_rank(), cs = (int)cl.num_blocks();
+  const GateDesc& g = gates[blockIdx.y];
+  // whole clusters skip together (no barrier is ever left waiting)
+  if (!g.pre) return;
+  const int n = g.n, m = g.qr_m;
+  const long long ld = g.qr_m_pad;
+  const int c0 = kQ * p;
+  if (c0 >= n) return;
+  const int jb = min(kQ, n - c0);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PanelSmem& S = *reinterpret_cast<PanelSmem*>(smem_raw);
+  cplx* A = ws + g.qr_off;
+  cplx* V = vbuf + ((long long)blockIdx.y * npan + p) * kQ * vld;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int rbase = kPR * rank;
+  // this warp's column slice: rows rbase + lane + 32 s
+  cplx a[kPL];
+  cplx* acol = A + (long long)(c0 + warp) * ld;
+#pragma unroll
+  for (int s2 = 0; s2 < kPL; ++s2) {
+    const int r = rbase + lane + 32 * s2;
+    a[s2] = (warp < jb && r < m) ? acol[r] : make_double2(0.0, 0.0);
+  }
+  for (int j = 0; j < jb; ++j) {
+    const int row0 = c0 + j, buf = j & 1;
+    // (1) partial norm of column j below the diagonal, and alpha
+    if (warp == j) {
+      double sn = 0.0;
+#pragma unroll
+      for (int s2 = 0; s2 < kPL; ++s2) {
+        const int r = rbase + lane + 32 * s2;
+        if (r > row0 && r < m) sn += cabs2(a[s2]);
+        if (r == row0) S.pal[buf] = a[s2];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sn += __shfl_xor_sync(0xffffffffu, sn, o);
+      if (lane == 0) S.pn[buf] = sn;
+    }
+    cl.sync();
+    if (t == 0) {  // one thread per CTA gathers the partials and forms zlarfg
+      double xn2 = 0.0;
+      for (int k = 0; k < cs; ++k) xn2 += *cl.map_shared_rank(&S.pn[buf], k);
+      const int owner = row0 / kPR;
+      const cplx al = row0 < m ? *cl.map_shared_rank(&S.pal[buf], owner) : make_double2(0.0, 0.0);
+      // zlarfg: H^H x = beta e_1, beta real, v = [1; x(2:)/(alpha - beta)]
+      cplx ta = make_double2(0.0, 0.0), iv = make_double2(0.0, 0.0);
+      double be = al.x;
+      if (!(xn2 == 0.0 && al.y == 0.0)) {
+        be = -copysign(sqrt(cabs2(al) + xn2), al.x);
+        ta = make_double2((be - al.x) / be, -al.y / be);
+        const cplx d = make_double2(al.x - be, al.y);
+        const double dd = cabs2(d);
+        iv = make_double2(d.x / dd, -d.y / dd);
+      }
+      S.tau = ta;
+      S.inv = iv;
+      S.alpha = al;
+      S.beta = be;
+    }
+    __syncthreads();
+    const cplx tau = S.tau, inv = S.inv, alpha = S.alpha;
+    const double beta = S.beta;
+    const bool refl = tau.x != 0.0 || tau.y != 0.0;
+    if (warp == j) {
+#pragma unroll
+      for (int s2 = 0; s2 < kPL; ++s2) {
+        const int r = rbase + lane + 32 * s2;
+        cplx v = make_double2(0.0, 0.0);
+        if (r == row0) {
+          v = make_double2(1.0, 0.0);
+          a[s2] = make_double2(refl ? beta : alpha.x, refl ? 0.0 : alpha.y);  // R diagonal
+        } else if (r > row0 && r < m && refl) {
+          v = cmul(a[s2], inv);
+        }
+        S.vs[j][lane + 32 * s2] = v;
+      }
+      if (t == 32 * j) S.taus[j] = tau;
+    }
+    __syncthreads();
+    // (2) partial v^H a_c for the columns right of j, v_i^H v_j for i < j
+    cplx w = make_double2(0.0, 0.0);
+    if (warp != j) {
+#pragma unroll
+      for (int s2 = 0; s2 < kPL; ++s2) {
+        const cplx v = S.vs[j][lane + 32 * s2];
+        if (warp > j) cfmac(w, v, a[s2]);
+        else cfmac(w, S.vs[warp][lane + 32 * s2], v);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        w.x += __shfl_xor_sync(0xffffffffu, w.x, o);
+        w.y += __shfl_xor_sync(0xffffffffu, w.y, o);
+      }
+      if (lane == 0) S.pw[buf][warp] = w;
+    }
+    cl.sync();
+    if (warp != j && warp < jb) {
+      cplx x = make_double2(0.0, 0.0);
+      if (lane < cs) x = *cl.map_shared_rank(&S.pw[buf][warp], lane);  // one remote read per lane
+#pragma unroll
+      for (int o = 4; o > 0; o >>= 1) {
+        x.x += __shfl_xor_sync(0xffffffffu, x.x, o);
+        x.y += __shfl_xor_sync(0xffffffffu, x.y, o);
+      }
+      const cplx tot = make_double2(__shfl_sync(0xffffffffu, x.x, 0), __shfl_sync(0xffffffffu, x.y, 0));
+      if (warp > j) {
+        if (refl) {
+          const cplx coef = cmul(make_double2(tau.x, -tau.y), tot);
+#pragma unroll
+          for (int s2 = 0; s2 < kPL; ++s2) {
+            const int r = rbase + lane + 32 * s2;
+            if (r >= row0 && r < m) {
+              const cplx v = S.vs[j][lane + 32 * s2];
+              a[s2].x -= v.x * coef.x - v.y * coef.y;
+              a[s2].y -= v.x * coef.y + v.y * coef.x;
+            }
+          }
+        }
+      } else if (lane == 0) {
+        S.Gv[warp][j] = tot;
+      }
+    }
+  }
+  // write back R (and whatever lies below the diagonal) and the reflectors
+#pragma unroll
+  for (int s2 = 0; s2 < kPL; ++s2) {
+    const int r = rbase + lane + 32 * s2;
+    if (warp < jb && r < ld) acol[r] = a[s2];
+  }
+  for (int idx = t; idx < kQ * kPR; idx += 1024) {
+    const int jj = idx / kPR, rr = idx % kPR, r = rbase + rr;
+    if (r < vld) V[(long long)jj * vld + r] = jj < jb ? S.vs[jj][rr] : make_double2(0.0, 0.0);
+  }
+  if (rank == 0) {
+    // zlarft (forward, columnwise): T[j][j] = tau_j, T[0:j, j] = -tau_j T[0:j,0:j] Gv[0:j, j]
+    for (int idx = t; idx < kQ * (kQ + 1); idx += 1024) S.T[idx / (kQ + 1)][idx % (kQ + 1)] = make_double2(0.0, 0.0);
+    __syncthreads();
+    for (int j = 0; j < jb; ++j) {
+      if (t < j) {
+        cplx z = make_double2(0.0, 0.0);
+        for (int k = t; k < j; ++k) cfma(z, S.T[t][k], S.Gv[k][j]);
+        const cplx tj = S.taus[j];
+        S.T[t][j] = make_double2(-(tj.x * z.x - tj.y * z.y), -(tj.x * z.y + tj.y * z.x));
+      } else if (t == j) {
+        S.T[j][j] = S.taus[j];
+      }
+      __syncthreads();
+    }
+    cplx* To = tbuf + ((long long)blockIdx.y * npan + p) * kQ * kQ;
+    for (int idx = t; idx < kQ * kQ; idx += 1024) To[idx] = S.T[idx / kQ][idx % kQ];
+  }
+  cl.sync();  // no CTA leaves while its shared memory may still be read remotely
 }
 
 namespace {
@@ -318,7 +562,18 @@ __global__ void __launch_bounds__(256) qrp_zinit_kernel(const GateDesc* __restri
   Z[r] = r < g.n ? X[r] : make_double2(0.0, 0.0);
 }
 
+// MPSIM_PANEL=legacy selects the L2-streaming panel kernel (A/B only).
+static bool panel_legacy() {
+  static const bool v = [] {
+    const char* e = std::getenv("MPSIM_PANEL");
+    return e != nullptr && std::string(e) == "legacy";
+  }();
+  return v;
+}
+
 void qrp_init() {
+  cudaFuncSetAttribute(qrp_panel_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PanelSmem));
+  cudaFuncSetAttribute(qrp_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   cudaFuncSetAttribute(qrp_update_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(QrUpdSmem));
   cudaFuncSetAttribute(qrp_update_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -332,8 +587,25 @@ void qrp_init() {
 void launch_qr_factor(const GateDesc* d_gates, int n_gates, int max_n_pad, int max_x_pad, cplx* ws, cplx* vbuf,
                       long long vld, cplx* tbuf, int npan, cudaStream_t st) {
   const int panels = max_n_pad / kQ;
+  const int cs = (int)((vld + kPR - 1) / kPR);
   for (int p = 0; p < panels; ++p) {
-    qrp_panel_kernel<<<n_gates, 1024, 0, st>>>(d_gates, ws, p, vbuf, vld, tbuf, npan);
+    if (cs <= 8 && !panel_legacy()) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cs, n_gates);
+      cfg.blockDim = dim3(1024);
+      cfg.dynamicSmemBytes = sizeof(PanelSmem);
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, qrp_panel_cluster_kernel, d_gates, ws, p, vbuf, vld, tbuf, npan);
+    } else {
+      qrp_panel_kernel<<<n_gates, 1024, sizeof(cplx) * vld, st>>>(d_gates, ws, p, vbuf, vld, tbuf, npan);
+    }
     const int blocks = panels - p - 1;
     if (blocks > 0)
       qrp_update_kernel<false><<<dim3(blocks, n_gates), 256, sizeof(QrUpdSmem), st>>>(d_gates, ws, p, vbuf, vld,
