@@ -588,8 +588,14 @@ void launch_qr_factor(const GateDesc* d_gates, int n_gates, int max_n_pad, int m
                       long long vld, cplx* tbuf, int npan, cudaStream_t st) {
   const int panels = max_n_pad / kQ;
   const int cs = (int)((vld + kPR - 1) / kPR);
+  // The cluster kernel holds one SM per CTA (128 KB of reflector slices): use
+  // it while all clusters fit in one wave, else one streaming CTA per gate.
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool cluster = cs <= 8 && (long long)cs * n_gates <= sms && !panel_legacy();
   for (int p = 0; p < panels; ++p) {
-    if (cs <= 8 && !panel_legacy()) {
+    if (cluster) {
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(cs, n_gates);
       cfg.blockDim = dim3(1024);
