@@ -52,7 +52,7 @@ static int qr_policy() {
 }
 void launch_jacobi_round_split(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, const double*,
                                double, const int*, long long, double*, int*, cplx*, cplx*, double*, int, cplx*,
-                               cudaStream_t);
+                               int, cudaStream_t);
 // Cross-only pair EVDs (evd.cuh) in a sweep whose predecessor measured an rms
 // relative off-norm above this (the pre-asymptotic phase); MPSIM_CROSS=0 disables.
 constexpr double kCrossRms = 0.35;
@@ -487,7 +487,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
                                   4.0 * kEps, 2.0 * kEps, (const double*)s.d_frob.p, kFloorRel2,
                                   (const int*)s.d_perm.p, perm_stride, (double*)s.d_maxoff.p, (int*)s.d_need.p,
                                   (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p, (double*)s.d_offsum.p, jacobi_mode() - 2,
-                                  (cplx*)s.d_gblk.p, st);
+                                  (cplx*)s.d_gblk.p, phase_probe(), st);
         s.launches += 4 - jacobi_mode();  // kernels per round beyond the one counted below
       } else {
         (dmma ? launch_jacobi_round_dmma : launch_jacobi_round)(

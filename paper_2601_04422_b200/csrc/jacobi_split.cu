@@ -182,7 +182,7 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __r
                                                              cplx* __restrict__ gbuf, int max_pairs,
                                                              double* __restrict__ offsum, cplx* __restrict__ rbuf,
                                                              double tol_in, cplx* __restrict__ gblk,
-                                                             int* __restrict__ rotated) {
+                                                             int* __restrict__ rotated, int probe) {
   constexpr bool kFuseEvd = kMode >= 1;
   const int gi = blockIdx.y;
   const GateDesc& g = gates[gi];
@@ -317,9 +317,11 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __r
     if (kFuseEvd && !approx) store_inblock();
     return;
   }
+  if (probe == 1) return;  // profiling (MPSIM_PHASE_PROBE): Gram only
   if constexpr (kFuseEvd) {
     cplx* R = reinterpret_cast<cplx*>(S.u.buf);
     pair_evd_v1(SG, R, S.sc, t, tol_in, floor2, 1, (active[gi] & 2) != 0);
+    if (probe == 2) return;  // Gram + EVD
     __syncthreads();
     store_inblock();
     if constexpr (kMode == 1) {
@@ -409,23 +411,24 @@ void jacobi_split_init() {
 void launch_jacobi_round_split(const GateDesc* d_gates, int n_gates, int max_pairs, cplx* ws, const int* d_active,
                                int* d_rotated, int round, double tol, double tol_in, const double* frob2,
                                double floor_rel2, const int* perm, long long perm_stride, double* maxoff, int* need,
-                               cplx* gbuf, cplx* rbuf, double* offsum, int fuse, cplx* gblk, cudaStream_t st) {
+                               cplx* gbuf, cplx* rbuf, double* offsum, int fuse, cplx* gblk, int probe,
+                               cudaStream_t st) {
   const dim3 grid(max_pairs, n_gates);
   const size_t sm = sizeof(PairSmem);
   if (fuse == 2) {
     jacobi_gram_kernel<2><<<grid, 256, sm, st>>>(d_gates, ws, d_active, round, tol, frob2, floor_rel2, perm,
                                                  perm_stride, maxoff, need, gbuf, max_pairs, offsum, rbuf, tol_in,
-                                                 gblk, d_rotated);
+                                                 gblk, d_rotated, probe);
     return;
   }
   if (fuse == 1) {
     jacobi_gram_kernel<1><<<grid, 256, sm, st>>>(d_gates, ws, d_active, round, tol, frob2, floor_rel2, perm,
                                                  perm_stride, maxoff, need, gbuf, max_pairs, offsum, rbuf, tol_in,
-                                                 gblk, d_rotated);
+                                                 gblk, d_rotated, probe);
   } else {
     jacobi_gram_kernel<0><<<grid, 256, sm, st>>>(d_gates, ws, d_active, round, tol, frob2, floor_rel2, perm,
                                                  perm_stride, maxoff, need, gbuf, max_pairs, offsum, rbuf, tol_in,
-                                                 gblk, d_rotated);
+                                                 gblk, d_rotated, probe);
     jacobi_evd_kernel<<<grid, 256, sizeof(EvdSmem), st>>>(d_gates, d_active, round, tol_in, frob2, floor_rel2, need,
                                                            gbuf, rbuf, max_pairs);
   }
