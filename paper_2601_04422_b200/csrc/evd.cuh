@@ -70,198 +70,7 @@ __device__ __forceinline__ bool pair_needs_rotation(const cplx* G, int t, double
   return __syncthreads_or(need);
 }
 
-// Rotation parameters for the pair (p, q) of the current G (see the header
-// comment for the FP32-angle / FP64-unitary split). Returns false for J = I.
-__device__ __forceinline__ bool rotation_params(const cplx* G, int p, int q, double tol2, double floor2, double& cs,
-                                                double& sn, cplx& ph) {
-  const double a = G[p * kPad + p].x, b = G[q * kPad + q].x;
-  const cplx g = G[p * kPad + q];
-  const double c2 = cabs2(g);
-  cs = 1.0;
-  sn = 0.0;
-  ph = make_double2(1.0, 0.0);
-  if (!(c2 > 0.0 && c2 > tol2 * fabs(a * b) && fmin(a, b) > floor2)) return false;
-  const double inv_c = rsqrt(c2);
-  ph = make_double2(g.x * inv_c, -g.y * inv_c);  // e^{-i phi}, |ph| = 1 to rounding
-  const float zf = (float)((b - a) * 0.5 * inv_c);
-  const float az = fabsf(zf);
-  const float tf = copysignf(1.0f, zf) / (az > 1e18f ? 2.0f * az : az + sqrtf(1.0f + zf * zf));
-  const double tt = (double)tf;
-  cs = rsqrt(1.0 + tt * tt);
-  sn = cs * tt;
-  return sn != 0.0;
-}
-
-// R <- eigenvectors of the Hermitian G, max_in cyclic sweeps. Every thread
-// derives the parameters of its two pairs itself (redundantly) and writes its
-// updated block into the other G buffer (G2), so a step needs one barrier.
-// G and G2 are both clobbered.
-__device__ __forceinline__ void pair_evd(cplx* G, cplx* G2, cplx* R, int t, double tol_in, double floor2,
-                                         int max_in) {
-  for (int idx = t; idx < kP * kP; idx += 256) {
-    const int i = idx / kP, j = idx % kP;
-    R[i * kPad + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-  }
-  if (t < kP) G[t * kPad + t].y = 0.0;
-  const double tol2 = tol_in * tol_in;
-  const int ba = t / (kP / 2), bb = t % (kP / 2);  // this thread's (row pair, column pair)
-  __syncthreads();
-  cplx* Gc = G;
-  cplx* Gn = G2;
-  for (int sweep = 0; sweep < max_in; ++sweep) {
-    int any = 0;
-    for (int step = 0; step < kP - 1; ++step) {
-      int pa, qa, pb, qb;
-      rr_pair(step, ba, kP - 1, pa, qa);
-      rr_pair(step, bb, kP - 1, pb, qb);
-      double csa, sna, csb, snb;
-      cplx pha, phb;
-      const bool ra = rotation_params(Gc, pa, qa, tol2, floor2, csa, sna, pha);
-      bool rb;
-      if (ba == bb) {
-        rb = ra;
-        csb = csa;
-        snb = sna;
-        phb = pha;
-      } else {
-        rb = rotation_params(Gc, pb, qb, tol2, floor2, csb, snb, phb);
-      }
-      any |= ra;
-      cplx n00 = Gc[pa * kPad + pb], n01 = Gc[pa * kPad + qb], n10 = Gc[qa * kPad + pb], n11 = Gc[qa * kPad + qb];
-      if (ra || rb) {
-        const cplx jb_qp = make_double2(-phb.x * snb, -phb.y * snb), jb_qq = make_double2(phb.x * csb, phb.y * csb);
-        const cplx ca_qp = make_double2(-pha.x * sna, pha.y * sna), ca_qq = make_double2(pha.x * csa, -pha.y * csa);
-        cplx m00 = make_double2(csa * n00.x, csa * n00.y), m01 = make_double2(csa * n01.x, csa * n01.y);
-        cplx m10 = make_double2(sna * n00.x, sna * n00.y), m11 = make_double2(sna * n01.x, sna * n01.y);
-        cfma(m00, ca_qp, n10);
-        cfma(m01, ca_qp, n11);
-        cfma(m10, ca_qq, n10);
-        cfma(m11, ca_qq, n11);
-        n00 = make_double2(csb * m00.x, csb * m00.y);
-        n01 = make_double2(snb * m00.x, snb * m00.y);
-        n10 = make_double2(csb * m10.x, csb * m10.y);
-        n11 = make_double2(snb * m10.x, snb * m10.y);
-        cfma(n00, m01, jb_qp);
-        cfma(n01, m01, jb_qq);
-        cfma(n10, m11, jb_qp);
-        cfma(n11, m11, jb_qq);
-        if (ba == bb) {
-          n00.y = 0.0;
-          n11.y = 0.0;
-          n01 = make_double2(0.0, 0.0);
-          n10 = make_double2(0.0, 0.0);
-        }
-        if (rb) {  // R <- R J_b on this thread's own block (in place: no other reader)
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const int row = r == 0 ? pa : qa;
-            const cplx x0 = R[row * kPad + pb], x1 = R[row * kPad + qb];
-            cplx y0 = make_double2(csb * x0.x, csb * x0.y), y1 = make_double2(snb * x0.x, snb * x0.y);
-            cfma(y0, x1, jb_qp);
-            cfma(y1, x1, jb_qq);
-            R[row * kPad + pb] = y0;
-            R[row * kPad + qb] = y1;
-          }
-        }
-      }
-      Gn[pa * kPad + pb] = n00;
-      Gn[pa * kPad + qb] = n01;
-      Gn[qa * kPad + pb] = n10;
-      Gn[qa * kPad + qb] = n11;
-      __syncthreads();
-      cplx* tmp = Gc;
-      Gc = Gn;
-      Gn = tmp;
-    }
-    if (!__syncthreads_or(any)) break;
-  }
-}
-
-// (two-barrier in-place variant, kept for A/B testing)
-__device__ __forceinline__ void pair_evd_2b(cplx* G, cplx* R, int t, double tol_in, double floor2, int max_in) {
-  for (int idx = t; idx < kP * kP; idx += 256) {
-    const int i = idx / kP, j = idx % kP;
-    R[i * kPad + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
-  }
-  if (t < kP) G[t * kPad + t].y = 0.0;
-  const double tol2 = tol_in * tol_in;
-  const int ba = t / (kP / 2), bb = t % (kP / 2);  // this thread's (row pair, column pair)
-  __syncthreads();
-  for (int sweep = 0; sweep < max_in; ++sweep) {
-    int any = 0;
-    for (int step = 0; step < kP - 1; ++step) {
-      int pa, qa, pb, qb;
-      rr_pair(step, ba, kP - 1, pa, qa);
-      rr_pair(step, bb, kP - 1, pb, qb);
-      double csa, sna, csb, snb;
-      cplx pha, phb;
-      const bool ra = rotation_params(G, pa, qa, tol2, floor2, csa, sna, pha);
-      const bool rb = ba == bb ? ra : rotation_params(G, pb, qb, tol2, floor2, csb, snb, phb);
-      if (ba == bb) {
-        csb = csa;
-        snb = sna;
-        phb = pha;
-      }
-      any |= ra;
-      cplx n00, n01, n10, n11, y[2][2];
-      if (ra || rb) {
-        const cplx jb_qp = make_double2(-phb.x * snb, -phb.y * snb), jb_qq = make_double2(phb.x * csb, phb.y * csb);
-        const cplx ca_qp = make_double2(-pha.x * sna, pha.y * sna), ca_qq = make_double2(pha.x * csa, -pha.y * csa);
-        const cplx b00 = G[pa * kPad + pb], b01 = G[pa * kPad + qb], b10 = G[qa * kPad + pb], b11 = G[qa * kPad + qb];
-        cplx m00 = make_double2(csa * b00.x, csa * b00.y), m01 = make_double2(csa * b01.x, csa * b01.y);
-        cplx m10 = make_double2(sna * b00.x, sna * b00.y), m11 = make_double2(sna * b01.x, sna * b01.y);
-        cfma(m00, ca_qp, b10);
-        cfma(m01, ca_qp, b11);
-        cfma(m10, ca_qq, b10);
-        cfma(m11, ca_qq, b11);
-        n00 = make_double2(csb * m00.x, csb * m00.y);
-        n01 = make_double2(snb * m00.x, snb * m00.y);
-        n10 = make_double2(csb * m10.x, csb * m10.y);
-        n11 = make_double2(snb * m10.x, snb * m10.y);
-        cfma(n00, m01, jb_qp);
-        cfma(n01, m01, jb_qq);
-        cfma(n10, m11, jb_qp);
-        cfma(n11, m11, jb_qq);
-        if (ba == bb) {
-          n00.y = 0.0;
-          n11.y = 0.0;
-          n01 = make_double2(0.0, 0.0);
-          n10 = make_double2(0.0, 0.0);
-        }
-        if (rb) {
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const int row = r == 0 ? pa : qa;
-            const cplx x0 = R[row * kPad + pb], x1 = R[row * kPad + qb];
-            y[r][0] = make_double2(csb * x0.x, csb * x0.y);
-            y[r][1] = make_double2(snb * x0.x, snb * x0.y);
-            cfma(y[r][0], x1, jb_qp);
-            cfma(y[r][1], x1, jb_qq);
-          }
-        }
-      }
-      // every thread has read its inputs (G entries of pairs a/b may be read
-      // by other threads for their parameters): write after the barrier
-      __syncthreads();
-      if (ra || rb) {
-        G[pa * kPad + pb] = n00;
-        G[pa * kPad + qb] = n01;
-        G[qa * kPad + pb] = n10;
-        G[qa * kPad + qb] = n11;
-        if (rb) {
-          R[pa * kPad + pb] = y[0][0];
-          R[pa * kPad + qb] = y[0][1];
-          R[qa * kPad + pb] = y[1][0];
-          R[qa * kPad + qb] = y[1][1];
-        }
-      }
-      __syncthreads();
-    }
-    if (!__syncthreads_or(any)) break;
-  }
-}
-
-// (previous two-barrier-per-step version, kept for reference/A-B testing)
+// Two barriers per step: 16 threads form the parameters, then all 256 update.
 // cross = true: one pass over the 256 pairs (i < W <= j) that straddle the two
 // blocks only, 16 steps of pairs (i, W + (i + step) % W) instead of 31 steps
 // over all 496 pairs. Used in the pre-asymptotic outer sweeps (engine.cu),
