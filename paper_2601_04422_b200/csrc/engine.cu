@@ -32,6 +32,17 @@ void jacobi_dmma_init();
 void launch_jacobi_round_dmma(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, int,
                               const double*, double, const int*, long long, double*, cudaStream_t);
 void jacobi_split_init();
+void launch_jacobi_sweep(const GateDesc*, int, int, cplx*, const int*, int*, double, double, const double*, double,
+                         const int*, long long, double*, int*, cplx*, cplx*, double*, cplx*, int*, cudaStream_t);
+// One persistent launch per sweep (jacobi_split.cu); MPSIM_SWEEP=rounds selects
+// one launch per tournament round.
+static bool sweep_policy() {
+  static const bool on = [] {
+    const char* v = std::getenv("MPSIM_SWEEP");
+    return !(v != nullptr && std::string(v) == "rounds");
+  }();
+  return on;
+}
 void qrp_init();
 void split_init();
 void theta_init();
@@ -477,11 +488,22 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     launch_derijk(dg, ng, ws, (const int*)s.d_active.p, (int*)s.d_perm.p, perm_stride, st);
     ++s.launches;
     CK(cudaEventRecord(s.evj0, st));
-    for (int round = 0; round < max_nb - 1; ++round) {
-      // One cyclic sweep of the inner 2W x 2W eigensolver per pair visit: the
-      // outer iteration needs the same number of sweeps as with a fully
-      // converged inner EVD (measured in emulation and on the B200), at a
-      // fraction of the cost. Final orthogonality is at the tol level.
+    // One cyclic sweep of the inner 2W x 2W eigensolver per pair visit: the
+    // outer iteration needs the same number of sweeps as with a fully
+    // converged inner EVD (measured in emulation and on the B200), at a
+    // fraction of the cost. Final orthogonality is at the tol level.
+    const bool persistent = jacobi_mode() == 4 && !phase_probe() && sweep_policy();
+    if (persistent) {
+      s.d_sweepctl.ensure(sizeof(int) * (1 + (size_t)ng * max_nb));
+      launch_jacobi_sweep(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, 4.0 * kEps, 2.0 * kEps,
+                          (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p, perm_stride,
+                          (double*)s.d_maxoff.p, (int*)s.d_need.p, (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p,
+                          (double*)s.d_offsum.p, (cplx*)s.d_gblk.p, (int*)s.d_sweepctl.p, st);
+      s.launches += 1;
+      ++s.jacobi_launches;
+    }
+    for (int round = 0; round < (persistent ? 0 : max_nb - 1); ++round) {
+      // (per-round launches: A/B and phase probes)
       if (jacobi_mode() >= 2) {
         launch_jacobi_round_split(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round,
                                   4.0 * kEps, 2.0 * kEps, (const double*)s.d_frob.p, kFloorRel2,

@@ -37,11 +37,11 @@ struct PairCtx {
 
 // Returns false if this CTA has no pair in this round.
 __device__ __forceinline__ bool pair_ctx(const GateDesc& g, int gi, int round, const int* active, cplx* ws,
-                                         const int* perm, long long perm_stride, PairCtx& c) {
+                                         const int* perm, long long perm_stride, PairCtx& c, int k) {
   if (!active[gi]) return false;
   const int nb = g.nb;
-  if (round >= nb - 1 || (int)blockIdx.x >= nb / 2) return false;
-  rr_pair(round, blockIdx.x, nb - 1, c.ba, c.bb);
+  if (round >= nb - 1 || k >= nb / 2) return false;
+  rr_pair(round, k, nb - 1, c.ba, c.bb);
   c.X = ws + g.ws_off;
   c.pm = perm + gi * perm_stride;
   c.mp = g.m_pad;
@@ -173,23 +173,50 @@ __device__ __forceinline__ void expand_rotation(const cplx* R, long long rpitch,
 
 // kMode 0: Gram only (G -> gbuf); 1: Gram + pair EVD (R -> rbuf); 2: the whole
 // pair visit, Gram + EVD + rotation, in one CTA.
+struct RoundArgs {
+  const GateDesc* gates;
+  cplx* ws;
+  const int* active;
+  double tol;
+  const double* frob2;
+  double floor_rel2;
+  const int* perm;
+  long long perm_stride;
+  double* maxoff;
+  int* need;
+  cplx* gbuf;
+  int max_pairs;
+  double* offsum;
+  cplx* rbuf;
+  double tol_in;
+  cplx* gblk;
+  int* rotated;
+  int probe;
+};
+
+// One pair visit (block pair k of gate gi in tournament round `round`).
 template <int kMode>
-__global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
-                                                             const int* __restrict__ active, int round, double tol,
-                                                             const double* __restrict__ frob2, double floor_rel2,
-                                                             const int* __restrict__ perm, long long perm_stride,
-                                                             double* __restrict__ maxoff, int* __restrict__ need,
-                                                             cplx* __restrict__ gbuf, int max_pairs,
-                                                             double* __restrict__ offsum, cplx* __restrict__ rbuf,
-                                                             double tol_in, cplx* __restrict__ gblk,
-                                                             int* __restrict__ rotated, int probe) {
+__device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round, int k, PairSmem& S) {
   constexpr bool kFuseEvd = kMode >= 1;
-  const int gi = blockIdx.y;
+  const GateDesc* __restrict__ gates = A.gates;
+  cplx* __restrict__ ws = A.ws;
+  const int* __restrict__ active = A.active;
+  const double tol = A.tol, floor_rel2 = A.floor_rel2, tol_in = A.tol_in;
+  const double* __restrict__ frob2 = A.frob2;
+  const int* __restrict__ perm = A.perm;
+  const long long perm_stride = A.perm_stride;
+  double* __restrict__ maxoff = A.maxoff;
+  int* __restrict__ need = A.need;
+  cplx* __restrict__ gbuf = A.gbuf;
+  const int max_pairs = A.max_pairs;
+  double* __restrict__ offsum = A.offsum;
+  cplx* __restrict__ rbuf = A.rbuf;
+  cplx* __restrict__ gblk = A.gblk;
+  int* __restrict__ rotated = A.rotated;
+  const int probe = A.probe;
   const GateDesc& g = gates[gi];
   PairCtx c;
-  if (!pair_ctx(g, gi, round, active, ws, perm, perm_stride, c)) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
+  if (!pair_ctx(g, gi, round, active, ws, perm, perm_stride, c, k)) return;
   cplx* const SG = S.v.G;
   const int t = threadIdx.x, lane = t % 32, warp = t / 32;
   ChunkLoader ld;
@@ -306,7 +333,7 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __r
     if (lane == 0 && r > 0.0) atomicAdd(offsum + gi, r);
   }
   const bool nd = pair_needs_rotation(SG, t, tolg, floor2, maxoff + gi);
-  const long long slot = (long long)gi * max_pairs + blockIdx.x;
+  const long long slot = (long long)gi * max_pairs + k;
   if (t == 0) need[slot] = nd ? 1 : 0;
   auto store_inblock = [&]() {  // the in-block Grams for this sweep's later visits
     const int r = t >> 4, q = t & 15;
@@ -338,6 +365,69 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(const GateDesc* __r
   } else {
     cplx* gout = gbuf + slot * (kP * kP);
     for (int idx = t; idx < kP * kP; idx += 256) gout[idx] = SG[(idx / kP) * kPad + idx % kP];
+  }
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(RoundArgs A, int round) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  pair_visit<kMode>(A, blockIdx.y, round, blockIdx.x, *reinterpret_cast<PairSmem*>(smem_raw));
+}
+
+// A whole sweep in one persistent launch: CTAs claim pair visits in
+// (round, gate, pair) order from a global counter and start a visit as soon
+// as both of its blocks have finished the previous round (per-block round
+// counters, release/acquire at gpu scope) instead of waiting for the whole
+// round: no per-round launch and tail, and CTAs drift out of phase, so one
+// CTA's pair EVD overlaps the DMMA phases of its neighbours. Deadlock-free:
+// a visit only waits on visits claimed before it, all of which are held by
+// running CTAs.
+__global__ void __launch_bounds__(256, 3) jacobi_sweep_kernel(RoundArgs A, int n_gates, int max_rounds,
+                                                              int* __restrict__ ctl) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
+  __shared__ int s_item;
+  int* counter = ctl;
+  int* ready = ctl + 1;  // [gate][block]: rounds completed this sweep
+  const int per_round = n_gates * A.max_pairs;
+  const long long total = (long long)per_round * max_rounds;
+  const int t = threadIdx.x;
+  for (;;) {
+    __syncthreads();  // shared memory of the previous visit is free
+    if (t == 0) s_item = atomicAdd(counter, 1);
+    __syncthreads();
+    const int item = s_item;
+    if (item >= total) break;
+    const int round = item / per_round, rem = item % per_round;
+    const int gi = rem / A.max_pairs, k = rem % A.max_pairs;
+    const GateDesc& g = A.gates[gi];
+    const int nb = g.nb;
+    if (!A.active[gi] || round >= nb - 1 || k >= nb / 2) continue;
+    int ba, bb;
+    rr_pair(round, k, nb - 1, ba, bb);
+    int* ra = ready + gi * 2 * A.max_pairs + ba;
+    int* rb = ready + gi * 2 * A.max_pairs + bb;
+    if (t == 0) {
+      int v;
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ra) : "memory");
+        if (v >= round) break;
+        __nanosleep(64);
+      }
+      for (;;) {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(rb) : "memory");
+        if (v >= round) break;
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+    pair_visit<2>(A, gi, round, k, S);
+    __syncthreads();  // every thread's writes of this visit are issued
+    if (t == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ra), "r"(round + 1) : "memory");
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(rb), "r"(round + 1) : "memory");
+    }
   }
 }
 
@@ -384,7 +474,7 @@ __global__ void __launch_bounds__(256, 3) jacobi_rot_kernel(const GateDesc* __re
   const int gi = blockIdx.y;
   const GateDesc& g = gates[gi];
   PairCtx c;
-  if (!pair_ctx(g, gi, round, active, ws, perm, perm_stride, c)) return;
+  if (!pair_ctx(g, gi, round, active, ws, perm, perm_stride, c, blockIdx.x)) return;
   const long long slot = (long long)gi * max_pairs + blockIdx.x;
   if (!need[slot]) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -403,8 +493,35 @@ void jacobi_split_init() {
   cudaFuncSetAttribute(jacobi_gram_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem));
   cudaFuncSetAttribute(jacobi_gram_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem));
   cudaFuncSetAttribute(jacobi_gram_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem));
+  cudaFuncSetAttribute(jacobi_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem));
   cudaFuncSetAttribute(jacobi_evd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EvdSmem));
   cudaFuncSetAttribute(jacobi_rot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RotSmem));
+}
+
+static RoundArgs make_args(const GateDesc* d_gates, cplx* ws, const int* d_active, int* d_rotated, double tol,
+                           double tol_in, const double* frob2, double floor_rel2, const int* perm,
+                           long long perm_stride, double* maxoff, int* need, cplx* gbuf, cplx* rbuf, double* offsum,
+                           int max_pairs, cplx* gblk, int probe) {
+  RoundArgs a;
+  a.gates = d_gates;
+  a.ws = ws;
+  a.active = d_active;
+  a.tol = tol;
+  a.frob2 = frob2;
+  a.floor_rel2 = floor_rel2;
+  a.perm = perm;
+  a.perm_stride = perm_stride;
+  a.maxoff = maxoff;
+  a.need = need;
+  a.gbuf = gbuf;
+  a.max_pairs = max_pairs;
+  a.offsum = offsum;
+  a.rbuf = rbuf;
+  a.tol_in = tol_in;
+  a.gblk = gblk;
+  a.rotated = d_rotated;
+  a.probe = probe;
+  return a;
 }
 
 // fuse: 0 = three launches, 1 = Gram+EVD / rotation, 2 = one launch per round.
@@ -415,25 +532,41 @@ void launch_jacobi_round_split(const GateDesc* d_gates, int n_gates, int max_pai
                                cudaStream_t st) {
   const dim3 grid(max_pairs, n_gates);
   const size_t sm = sizeof(PairSmem);
+  const RoundArgs a = make_args(d_gates, ws, d_active, d_rotated, tol, tol_in, frob2, floor_rel2, perm, perm_stride,
+                                maxoff, need, gbuf, rbuf, offsum, max_pairs, gblk, probe);
   if (fuse == 2) {
-    jacobi_gram_kernel<2><<<grid, 256, sm, st>>>(d_gates, ws, d_active, round, tol, frob2, floor_rel2, perm,
-                                                 perm_stride, maxoff, need, gbuf, max_pairs, offsum, rbuf, tol_in,
-                                                 gblk, d_rotated, probe);
+    jacobi_gram_kernel<2><<<grid, 256, sm, st>>>(a, round);
     return;
   }
   if (fuse == 1) {
-    jacobi_gram_kernel<1><<<grid, 256, sm, st>>>(d_gates, ws, d_active, round, tol, frob2, floor_rel2, perm,
-                                                 perm_stride, maxoff, need, gbuf, max_pairs, offsum, rbuf, tol_in,
-                                                 gblk, d_rotated, probe);
+    jacobi_gram_kernel<1><<<grid, 256, sm, st>>>(a, round);
   } else {
-    jacobi_gram_kernel<0><<<grid, 256, sm, st>>>(d_gates, ws, d_active, round, tol, frob2, floor_rel2, perm,
-                                                 perm_stride, maxoff, need, gbuf, max_pairs, offsum, rbuf, tol_in,
-                                                 gblk, d_rotated, probe);
+    jacobi_gram_kernel<0><<<grid, 256, sm, st>>>(a, round);
     jacobi_evd_kernel<<<grid, 256, sizeof(EvdSmem), st>>>(d_gates, d_active, round, tol_in, frob2, floor_rel2, need,
                                                            gbuf, rbuf, max_pairs);
   }
   jacobi_rot_kernel<<<grid, 256, sizeof(RotSmem), st>>>(d_gates, ws, d_active, d_rotated, round, perm, perm_stride,
                                                          need, rbuf, max_pairs);
+}
+
+// One whole sweep (all rounds) as a persistent dataflow launch. ctl: 1 +
+// n_gates * 2 * max_pairs ints, zeroed here.
+void launch_jacobi_sweep(const GateDesc* d_gates, int n_gates, int max_pairs, cplx* ws, const int* d_active,
+                         int* d_rotated, double tol, double tol_in, const double* frob2, double floor_rel2,
+                         const int* perm, long long perm_stride, double* maxoff, int* need, cplx* gbuf, cplx* rbuf,
+                         double* offsum, cplx* gblk, int* ctl, cudaStream_t st) {
+  static int ctas = 0;
+  if (ctas == 0) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_sweep_kernel, 256, sizeof(PairSmem));
+    ctas = sms * (per_sm > 0 ? per_sm : 1);
+  }
+  cudaMemsetAsync(ctl, 0, sizeof(int) * (1 + (size_t)n_gates * 2 * max_pairs), st);
+  const RoundArgs a = make_args(d_gates, ws, d_active, d_rotated, tol, tol_in, frob2, floor_rel2, perm, perm_stride,
+                                maxoff, need, gbuf, rbuf, offsum, max_pairs, gblk, 0);
+  jacobi_sweep_kernel<<<ctas, 256, sizeof(PairSmem), st>>>(a, n_gates, 2 * max_pairs - 1, ctl);
 }
 
 }  // namespace mpsim_gpu
