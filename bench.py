@@ -54,31 +54,51 @@ def layer_gates(n, parity, rng, lo=0, hi=None):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region through
+    NVML in-process (the nvidia-smi CLI, spawned every 0.2 s by every rank,
+    stalls the driver enough to cost ~30 % at 4 GPUs). Rank 0 samples every
+    GPU of the run; other ranks do not sample."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40, "sw_power_cap": 0x4}
 
-    def __init__(self, device):
-        self.device = device
+    def __init__(self, devices, interval=0.25):
+        self.devices = list(devices)
+        self.interval = interval
         self.rows = []
         self._stop = threading.Event()
         self._t = None
 
     def _run(self):
-        while not self._stop.is_set():
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+        except Exception:
+            return
+        handles = []
+        for d in self.devices:  # CUDA ordinal -> NVML handle by UUID (CUDA_VISIBLE_DEVICES-safe)
             try:
-                out = subprocess.run(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                      "-i", str(self.device)], capture_output=True, text=True, timeout=5).stdout
-                self.rows.append([x.strip() for x in out.strip().split(",")])
+                import torch
+                handles.append(nv.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(d).uuid)))
             except Exception:
-                pass
-            self._stop.wait(0.2)
+                try:
+                    handles.append(nv.nvmlDeviceGetHandleByIndex(d))
+                except Exception:
+                    pass
+        while not self._stop.is_set():
+            for h in handles:
+                try:
+                    sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                    mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                    rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.rows.append((float(sm), float(mx), int(rs)))
+                except Exception:
+                    pass
+            self._stop.wait(self.interval)
 
     def __enter__(self):
-        self._t = threading.Thread(target=self._run, daemon=True)
-        self._t.start()
+        if self.devices:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
         return self
 
     def __exit__(self, *a):
@@ -87,21 +107,11 @@ class ClockSampler:
             self._t.join(timeout=10)
 
     def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in self.rows:
-            try:
-                sm.append(float(r[0]))
-                mx.append(float(r[1]))
-                for nm, v in zip(names, r[3:7]):
-                    if v.lower() == "active":
-                        reasons.add(nm)
-            except (ValueError, IndexError):
-                continue
-        if not sm:
+        if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        reasons = sorted({nm for _, _, rs in self.rows for nm, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "gpus": len(self.devices), "source": "NVML"}
 
 
 def fp64_peak():
@@ -230,7 +240,7 @@ def main():
     chain.reset_counters()
     dev_ms, wall, ngates = [], [], 0
     torch = chain._torch
-    with ClockSampler(local) as clk:
+    with ClockSampler(range(world) if rank == 0 else []) as clk:
         chain.barrier()
         for s in range(args.warmup, args.warmup + args.steps):
             if torch is not None:
