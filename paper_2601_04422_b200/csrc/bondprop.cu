@@ -22,16 +22,18 @@ struct Small4 {
 // X/X0 of the Jacobi operand from a row-major device matrix A (rows x cols).
 // Orientation 0: vector v = column v of A; 1: vector v = conj(row v of A).
 __global__ void load_matrix_kernel(const cplx* __restrict__ A, long long lda, int rows, int cols, int xtrans,
-                                   cplx* __restrict__ X, long long ldx, int f, cplx* __restrict__ X0, long long ldx0,
-                                   double* frob2) {
+                                   cplx* __restrict__ X, long long ldx, int xsplit, int f, cplx* __restrict__ X0,
+                                   long long ldx0, double* frob2) {
   double fr = 0.0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)rows * cols;
        i += (long long)gridDim.x * blockDim.x) {
     const int r = (int)(i / cols), c = (int)(i % cols);
     const cplx v = A[(long long)r * lda + c];
     const cplx vc = make_double2(v.x, -v.y);
-    if (xtrans == 0) X[(long long)c * ldx + r] = v;
-    else X[(long long)r * ldx + c] = vc;
+    const long long xv = xtrans == 0 ? c : r, xe = xtrans == 0 ? r : c;
+    const cplx xval = xtrans == 0 ? v : vc;
+    if (xsplit) xs_set(X + xv * ldx, ldx, xe, xval);  // the Jacobi operand (split planes)
+    else X[xv * ldx + xe] = xval;
     if (f == 0) X0[(long long)c * ldx0 + r] = v;
     else X0[(long long)r * ldx0 + c] = vc;
     fr += cabs2(v);
@@ -41,11 +43,12 @@ __global__ void load_matrix_kernel(const cplx* __restrict__ A, long long lda, in
   if (threadIdx.x % 32 == 0) atomicAdd(frob2, fr);
 }
 
-void launch_load_matrix(const cplx* A, long long lda, int rows, int cols, int xtrans, cplx* X, long long ldx, int f,
-                        cplx* X0, long long ldx0, double* frob2, cudaStream_t st) {
+void launch_load_matrix(const cplx* A, long long lda, int rows, int cols, int xtrans, cplx* X, long long ldx,
+                        int xsplit, int f, cplx* X0, long long ldx0, double* frob2, cudaStream_t st) {
   long long blocks = ((long long)rows * cols + 255) / 256;
   blocks = std::max(1LL, std::min(blocks, 2048LL));
-  load_matrix_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, lda, rows, cols, xtrans, X, ldx, f, X0, ldx0, frob2);
+  load_matrix_kernel<<<(unsigned)blocks, 256, 0, st>>>(A, lda, rows, cols, xtrans, X, ldx, xsplit, f, X0, ldx0,
+                                                       frob2);
 }
 
 // Open (gate_apply.cpp:210-215):

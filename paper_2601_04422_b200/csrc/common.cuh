@@ -160,4 +160,18 @@ __device__ __forceinline__ void cmac_rn(cplx& acc, cplx a, cplx b) {
 __device__ __forceinline__ cplx conjc(cplx a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double cabs2(cplx a) { return a.x * a.x + a.y * a.y; }
 
+// The Jacobi operand X keeps each vector as split planes inside its m_pad-
+// complex slot: Re in doubles [0, m_pad), Im in [m_pad, 2 m_pad) (16-byte
+// cp.async of two rows of one plane into vector-major shared memory,
+// jacobi_split.cu). X0, the QR operand and Z (pre = 2) are interleaved complex.
+__device__ __forceinline__ cplx xs_get(const cplx* vec, long long m_pad, long long e) {
+  const double* d = reinterpret_cast<const double*>(vec);
+  return make_double2(d[e], d[m_pad + e]);
+}
+__device__ __forceinline__ void xs_set(cplx* vec, long long m_pad, long long e, cplx v) {
+  double* d = reinterpret_cast<double*>(vec);
+  d[e] = v.x;
+  d[m_pad + e] = v.y;
+}
+
 }  // namespace mpsim_gpu

@@ -27,10 +27,6 @@ namespace mpsim_gpu {
 // ---- launchers implemented in the kernel translation units
 void launch_theta(const GateDesc*, int, int, const cplx*, long long, int, cplx*, double*, cudaStream_t);
 int theta_tiles(int dl, int dr);
-void jacobi_init();
-void jacobi_dmma_init();
-void launch_jacobi_round_dmma(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, int,
-                              const double*, double, const int*, long long, double*, cudaStream_t);
 void jacobi_split_init();
 void launch_jacobi_sweep(const GateDesc*, int, int, cplx*, const int*, int*, double, double, const double*, double,
                          const int*, long long, double*, int*, cplx*, cplx*, double*, cplx*, int*, cudaStream_t);
@@ -46,7 +42,7 @@ static bool sweep_policy() {
 void qrp_init();
 void split_init();
 void theta_init();
-void launch_qr_factor(const GateDesc*, int, int, int, cplx*, cplx*, long long, cplx*, int, cudaStream_t);
+void launch_qr_factor(const GateDesc*, int, int, int, cplx*, cplx*, long long, cplx*, int, int, cudaStream_t);
 void launch_qr_apply(const GateDesc*, int, int, int, cplx*, const cplx*, long long, const cplx*, int, const int*,
                      long long, const GateOut*, cudaStream_t);
 // QR preconditioning (qr_pre.cu) of gates whose SVD operand has at least
@@ -84,24 +80,18 @@ static bool cross_policy() {
   }();
   return on;
 }
-// Jacobi round implementation: default = Gram + pair EVD in one kernel and the
-// rotation in a second (DMMA for both GEMMs); "split3" (Gram / EVD / rotation
-// as three launches), "dmma" (one fused DMMA kernel), "simt" (DFMA).
+// Jacobi round implementation: default = the whole pair visit in one kernel
+// (one persistent launch per sweep, see sweep_policy); "split2" (Gram + pair
+// EVD / rotation) and "split3" (Gram / EVD / rotation) launch per round (A/B).
 static int jacobi_mode() {
   static const int m = [] {
     const char* v = std::getenv("MPSIM_JACOBI");
-    if (v != nullptr && std::string(v) == "simt") return 0;
-    if (v != nullptr && std::string(v) == "dmma") return 1;
     if (v != nullptr && std::string(v) == "split3") return 2;
     if (v != nullptr && std::string(v) == "split2") return 3;
     return 4;
   }();
   return m;
 }
-static bool use_dmma() { return jacobi_mode() != 0; }
-size_t jacobi_smem_bytes();
-void launch_jacobi_round(const GateDesc*, int, int, cplx*, const int*, int*, int, double, double, int, const double*, double,
-                         const int*, long long, double*, cudaStream_t);
 void launch_derijk(const GateDesc*, int, const cplx*, const int*, int*, long long, cudaStream_t);
 void launch_norms(const GateDesc*, int, int, const cplx*, double*, long long, cudaStream_t);
 void launch_truncate(const GateDesc*, int, double*, int*, long long, GateOut*, const double*, double, cudaStream_t);
@@ -232,8 +222,6 @@ State::State(int n_, long long chi_hint, int dev) : n(n_), device(dev) {
   CK(cudaEventCreate(&evj1));
   static bool inited = false;
   if (!inited) {
-    jacobi_init();
-    jacobi_dmma_init();
     jacobi_split_init();
     qrp_init();
     split_init();
@@ -350,7 +338,7 @@ constexpr double kQuadFinish = 1e-9;
 // operand comes from the theta kernel (src == nullptr) or from a row-major
 // device matrix (plain SVDs, bond-propagation carriers); descriptors with
 // pre = 1 are QR-preconditioned (qr_pre.cu) before the sweeps.
-int mpsim_gpu::use_qr_precondition(int n) { return (jacobi_mode() >= 2 && n >= kQrMinN) ? qr_policy() : 0; }
+int mpsim_gpu::use_qr_precondition(int n) { return n >= kQrMinN ? qr_policy() : 0; }
 
 // The descriptor as each phase of run_two_chunk sees it (desc_layout holds the
 // Jacobi-phase view): 0 theta / load + first QR (R^H -> y2 for pre = 2),
@@ -438,7 +426,8 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     const GateDesc d = phase_desc(descs[0], 0);
     const int big = d.pre ? d.qr_m : d.m;
     launch_load_matrix(src, src_ld, d.trans == 0 ? big : d.n, d.trans == 0 ? d.n : big, d.trans,
-                       ws + (d.pre ? d.qr_off : d.ws_off), d.pre ? d.qr_m_pad : d.m_pad, d.f, ws + d.x0_off, d.x0_ld,
+                       ws + (d.pre ? d.qr_off : d.ws_off), d.pre ? d.qr_m_pad : d.m_pad, d.pre ? 0 : 1, d.f,
+                       ws + d.x0_off, d.x0_ld,
                        (double*)s.d_frob.p, st);
     check_launch("load_matrix_kernel");
     ++s.launches;
@@ -448,7 +437,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     // first QR (its reflectors stay in d_qrv / d_qrt for Z = Q1 [X; 0])
     s.d_qrv.ensure(sizeof(cplx) * (size_t)ng * npan * 32 * qr_m_pad);
     s.d_qrt.ensure(sizeof(cplx) * (size_t)ng * npan * 32 * 32);
-    launch_qr_factor(dph, ng, qr_n_pad, qr_jm_pad, ws, (cplx*)s.d_qrv.p, qr_m_pad, (cplx*)s.d_qrt.p, npan, st);
+    launch_qr_factor(dph, ng, qr_n_pad, qr_jm_pad, ws, (cplx*)s.d_qrv.p, qr_m_pad, (cplx*)s.d_qrt.p, npan, 0, st);
     check_launch("qr_factor");
     s.launches += 2 * npan;
   }
@@ -456,7 +445,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     s.d_qrv2.ensure(sizeof(cplx) * (size_t)ng * npan * 32 * qr_jm_pad);
     s.d_qrt2.ensure(sizeof(cplx) * (size_t)ng * npan * 32 * 32);
     launch_qr_factor(dph + ng, ng, qr_n_pad, qr_jm_pad, ws, (cplx*)s.d_qrv2.p, qr_jm_pad, (cplx*)s.d_qrt2.p, npan,
-                     st);
+                     1, st);
     check_launch("qr_factor (second step)");
     s.launches += 2 * npan;
   }
@@ -467,7 +456,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   bool converged = false;
   std::vector<int> still(ng, 1);
   s.d_maxoff.ensure(sizeof(double) * ng);
-  if (jacobi_mode() >= 2) {
+  {
     const size_t slots = (size_t)ng * (max_nb / 2);
     s.d_need.ensure(sizeof(int) * slots);
     s.d_gbuf.ensure(sizeof(cplx) * slots * kP * kP);
@@ -479,7 +468,6 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   s.d_offsum.ensure(sizeof(double) * ng);
   s.h_offsum.ensure(sizeof(double) * ng);
   double* h_offsum = (double*)s.h_offsum.p;
-  const bool dmma = use_dmma();
   const int max_sweeps = phase_probe() ? 1 : kMaxSweeps;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     CK(cudaMemsetAsync(s.d_rot.p, 0, sizeof(int) * ng, st));
@@ -504,18 +492,13 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     }
     for (int round = 0; round < (persistent ? 0 : max_nb - 1); ++round) {
       // (per-round launches: A/B and phase probes)
-      if (jacobi_mode() >= 2) {
+      {
         launch_jacobi_round_split(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round,
                                   4.0 * kEps, 2.0 * kEps, (const double*)s.d_frob.p, kFloorRel2,
                                   (const int*)s.d_perm.p, perm_stride, (double*)s.d_maxoff.p, (int*)s.d_need.p,
                                   (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p, (double*)s.d_offsum.p, jacobi_mode() - 2,
                                   (cplx*)s.d_gblk.p, phase_probe(), st);
         s.launches += 4 - jacobi_mode();  // kernels per round beyond the one counted below
-      } else {
-        (dmma ? launch_jacobi_round_dmma : launch_jacobi_round)(
-            dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round, 4.0 * kEps, 2.0 * kEps,
-            phase_probe() ? -phase_probe() : 1, (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p,
-            perm_stride, (double*)s.d_maxoff.p, st);
       }
       ++s.launches;
       ++s.jacobi_launches;
@@ -559,14 +542,14 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     }
     bool any = false;
     for (int i = 0; i < ng; ++i) {
-      const bool quad_done = dmma && h_maxoff[i] <= kQuadFinish;
+      const bool quad_done = h_maxoff[i] <= kQuadFinish;
       h_rot[i] = h_rot[i] && !quad_done;
       still[i] = h_rot[i];
       any = any || h_rot[i];
       // pre-asymptotic (rms relative off-norm of the sweep above kCrossRms):
       // the next sweep's pair EVDs rotate the cross-block pairs only
       const double rms = std::sqrt(2.0 * h_offsum[i] / std::max(1, descs[i].n));
-      if (h_rot[i] && jacobi_mode() >= 2 && cross_policy() && rms > kCrossRms && h_maxoff[i] > 1e-3) h_rot[i] |= 2;
+      if (h_rot[i] && cross_policy() && rms > kCrossRms && h_maxoff[i] > 1e-3) h_rot[i] |= 2;
       // pre-asymptotic and early asymptotic sweeps reuse the in-block Grams the
       // pair EVDs leave behind (jacobi_split.cu); the closing sweeps recompute all
       if (h_rot[i] && jacobi_mode() >= 3 && inblock_policy() && h_maxoff[i] > kInblockMaxoff) h_rot[i] |= 4;

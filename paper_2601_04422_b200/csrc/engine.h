@@ -85,10 +85,10 @@ void move_center_impl(State& s, int center);
 // descriptor, from a row-major device matrix src (leading dimension src_ld).
 void run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs,
                    const cplx* src = nullptr, long long src_ld = 0);
-// X (orientation xtrans, stride ldx) and X0 (orientation f, stride ldx0) of a
+// X (orientation xtrans, stride ldx, split planes if xsplit) and X0 (orientation f, stride ldx0) of a
 // row-major device matrix A (rows x cols), ||A||_F^2 added to *frob2.
-void launch_load_matrix(const cplx* A, long long lda, int rows, int cols, int xtrans, cplx* X, long long ldx, int f,
-                        cplx* X0, long long ldx0, double* frob2, cudaStream_t st);
+void launch_load_matrix(const cplx* A, long long lda, int rows, int cols, int xtrans, cplx* X, long long ldx,
+                        int xsplit, int f, cplx* X0, long long ldx0, double* frob2, cudaStream_t st);
 // QR preconditioning steps (0, 1, 2) for a descriptor with n vectors (engine.cu).
 int use_qr_precondition(int n);
 void launch_cgemm(const GemmArgs&, cudaStream_t);

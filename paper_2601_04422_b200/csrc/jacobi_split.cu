@@ -1,14 +1,16 @@
-// Block one-sided Jacobi round split into three launches, each shaped for its
-// own bound (the fused jacobi_dmma.cu kernel serialises them inside one CTA,
-// so a CTA's latency-bound EVD stalls the FP64 tensor pipe):
-//   A  jacobi_gram_kernel  — DMMA Gram of every block pair of the round, the
-//                            relative convergence test, G -> global (16 KB/pair)
-//   B  jacobi_evd_kernel   — one cyclic complex Jacobi sweep of each 32x32 G
-//                            that needs it, R -> global; small footprint, so
-//                            many CTAs per SM overlap its barrier-bound steps
-//   C  jacobi_rot_kernel   — X_P <- X_P R on DMMA, R_ext slice in registers,
-//                            results stored straight to global
-// Algorithm, tolerances and numerics are those of jacobi_dmma.cu.
+// Block one-sided Jacobi on the FP64 tensor path: the visit of one block pair
+// (2W = 32 vectors) of a tournament round —
+//   1. Gram G = X_P^H X_P on DMMA (36 tiles of the real-extended 64 x 64 Gram,
+//      or the 16 cross-block tiles when the in-block Grams are reused),
+//   2. the relative convergence test,
+//   3. one cyclic complex Jacobi sweep of the 32 x 32 G (evd.cuh) -> R,
+//   4. X_P <- X_P R on DMMA —
+// as one persistent launch per sweep (jacobi_sweep_kernel, default), one
+// launch per round (jacobi_gram_kernel<2>), or split into Gram+EVD / rotation
+// or Gram / EVD / rotation launches (A/B). The Jacobi operand X lives in
+// global memory as split planes per vector (Re[0, m_pad) then Im[0, m_pad),
+// common.cuh), so 32-row chunks stream into vector-major shared planes with
+// 16-byte cp.async.
 #include "common.cuh"
 #include "evd.cuh"
 
@@ -29,9 +31,10 @@ struct PairCtx {
   const int* pm;
   long long mp;
   int ba, bb;
-  __device__ __forceinline__ cplx* vec(int i) const {
+  // vector i of the pair as split planes: Re at [0, mp), Im at [mp, 2 mp)
+  __device__ __forceinline__ double* vec(int i) const {
     const int slot = i < kW ? ba * kW + i : bb * kW + (i - kW);
-    return X + (long long)pm[slot] * mp;
+    return reinterpret_cast<double*>(X + (long long)pm[slot] * mp);
   }
 };
 
@@ -49,14 +52,14 @@ __device__ __forceinline__ bool pair_ctx(const GateDesc& g, int gi, int round, c
 }
 
 // Chunks of kC rows x 32 vectors stream through shared memory as split Re/Im
-// planes [row][vector] (pitch 36), double-buffered with cp.async so the next
+// planes [vector][row] (pitch 36), double-buffered with cp.async so the next
 // chunk's loads are in flight while the DMMAs consume the current one.
 constexpr int kC = 32;
-constexpr int kChunkPlane = kC * kPitchS;  // doubles per plane
+constexpr int kChunkPlane = kP * kPitchS;  // doubles per plane
 
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -64,28 +67,24 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// Lane mapping: a half-warp covers 4 rows x 4 vectors, which puts its 16
-// 8-byte shared writes in 16 distinct bank pairs at pitch 36; a warp covers 8
-// consecutive rows (one 128-byte line) of 4 vectors.
+// Per chunk and thread four 16-byte copies (two rows of one plane of one
+// vector): in copy s, warp w moves vector w + 8 s, lanes 0-15 its Re rows and
+// lanes 16-31 its Im rows, 256 contiguous bytes each (full lines from global,
+// conflict-free in shared memory).
 struct ChunkLoader {
-  const double* src;  // this thread's first element (as doubles)
-  int soff;           // this thread's first shared offset
+  const double* src[4];  // this thread's plane of vectors w + 8 s, at its row pair
+  int soff;              // shared offset of vector w, plane, row pair
   __device__ __forceinline__ void init(const PairCtx& c, int t) {
     const int lane = t & 31, warp = t >> 5;
-    const int e = (lane & 3) + 4 * (lane >> 4);
-    const int vi = 4 * warp + ((lane >> 2) & 3);
-    src = reinterpret_cast<const double*>(c.vec(vi) + e);
-    soff = e * kPitchS + vi;
+    const int rp = lane & 15, plane = lane >> 4;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) src[s] = c.vec(warp + 8 * s) + plane * c.mp + 2 * rp;
+    soff = plane * kChunkPlane + warp * kPitchS + 2 * rp;
   }
-  // rows e0 .. e0 + kC of the pair -> buffer (Tr at buf, Ti at buf + kChunkPlane)
+  // rows e0 .. e0 + kC of the pair -> buffer (Re plane at buf, Im at buf + kChunkPlane)
   __device__ __forceinline__ void issue(double* buf, int e0) const {
 #pragma unroll
-    for (int s = 0; s < kC / 8; ++s) {
-      const double* g = src + 2 * (e0 + 8 * s);
-      double* d = buf + soff + 8 * s * kPitchS;
-      cp_async8(d, g);
-      cp_async8(d + kChunkPlane, g + 1);
-    }
+    for (int s = 0; s < 4; ++s) cp_async16(buf + soff + 8 * s * kPitchS, src[s] + e0);
     cp_async_commit();
   }
 };
@@ -136,8 +135,8 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
       const int cext = 4 * s + fk;
-      const double* plane = B + (cext < kP ? 0 : kChunkPlane) + (cext & (kP - 1));
-      const double a0 = plane[(8 * rbase + fr) * kPitchS], a1 = plane[(8 * (rbase + 1) + fr) * kPitchS];
+      const double* plane = B + (cext < kP ? 0 : kChunkPlane) + (cext & (kP - 1)) * kPitchS;
+      const double a0 = plane[8 * rbase + fr], a1 = plane[8 * (rbase + 1) + fr];
       const double b0 = Rx[cext * kPitchR + bre], b1 = Rx[cext * kPitchR + bim];
       dmma_s(o[0][0][0], o[0][0][1], a0, b0);
       dmma_s(o[0][1][0], o[0][1][1], a0, b1);
@@ -151,7 +150,9 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
       for (int v = 0; v < 2; ++v) {
         const int e = 8 * (rbase + a) + fr;
         const int j = 8 * cj + 2 * fk + v;
-        c.vec(j)[e0 + e] = make_double2(o[a][0][v], o[a][1][v]);
+        double* xj = c.vec(j);
+        xj[e0 + e] = o[a][0][v];
+        xj[c.mp + e0 + e] = o[a][1][v];
       }
     __syncthreads();
   }
@@ -230,7 +231,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
   const bool approx = kFuseEvd && (active[gi] & 4) && round > 0;
   cplx* const gblk_a = gblk + ((long long)gi * 2 * max_pairs + c.ba) * (kW * kW);
   cplx* const gblk_b = gblk + ((long long)gi * 2 * max_pairs + c.bb) * (kW * kW);
-  // tiles of G_ext = [[A, B], [B^T, D]]: upper A and D, all of B (see jacobi_dmma.cu)
+  // tiles of G_ext = [[A, B], [B^T, D]]: upper A and D, all of B (Re G = A + D, Im G = B - B^T)
   int trow[5], tcol[5], nt;
   if (approx) {
     // cross block: rows Re_a / Im_a (tiles 0, 1, 4, 5), cols Re_b / Im_b (2, 3, 6, 7)
@@ -263,7 +264,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
     nt = 5;
   }
   // column offsets (plane + index) of this thread's fragments
-  auto coff = [&](int col) { return (col < kP ? 0 : kChunkPlane) + (col & (kP - 1)); };
+  auto coff = [&](int col) { return (col < kP ? 0 : kChunkPlane) + (col & (kP - 1)) * kPitchS; };
   const int oa0 = coff(8 * trow[0] + fr), oa4 = coff(8 * trow[4] + fr);
   int ob[5];
 #pragma unroll
@@ -284,7 +285,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
     const double* B = S.u.buf[k & 1];
 #pragma unroll
     for (int ks = 0; ks < kC / 4; ++ks) {
-      const int row = (4 * ks + fk) * kPitchS;
+      const int row = 4 * ks + fk;
       const double a_first = B[row + oa0], a_last = B[row + oa4];
 #pragma unroll
       for (int i = 0; i < 5; ++i)

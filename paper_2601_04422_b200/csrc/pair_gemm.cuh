@@ -41,27 +41,36 @@ __device__ __forceinline__ void wait() {
 __device__ __forceinline__ int loader_vector(int t) { return 4 * (t >> 5) + (((t & 31) >> 2) & 3); }
 
 struct Loader {
-  const double* p;  // this thread's P vector (as doubles), first row
+  const double* p;  // this thread's P vector (as doubles), Re of its first row
   const double* q;
+  int ps, qs;       // doubles per row: 2 (interleaved complex) or 1 (split planes)
+  long long pi, qi; // offset of Im from Re: 1 (interleaved) or m_pad (split planes)
   int soff;
   // pvec / qvec: the vectors of index loader_vector(t) (any valid address for
-  // padding vectors whose results are discarded)
-  __device__ __forceinline__ void init(const cplx* pvec, const cplx* qvec, int t) {
+  // padding vectors whose results are discarded); psplit / qsplit: 0 for
+  // interleaved complex vectors, else the m_pad of split-plane vectors
+  // (common.cuh, the Jacobi operand)
+  __device__ __forceinline__ void init(const cplx* pvec, const cplx* qvec, int t, long long psplit = 0,
+                                       long long qsplit = 0) {
     const int lane = t & 31;
     const int e = (lane & 3) + 4 * (lane >> 4);
-    p = reinterpret_cast<const double*>(pvec + e);
-    q = reinterpret_cast<const double*>(qvec + e);
+    ps = psplit ? 1 : 2;
+    qs = qsplit ? 1 : 2;
+    pi = psplit ? psplit : 1;
+    qi = qsplit ? qsplit : 1;
+    p = reinterpret_cast<const double*>(pvec) + ps * e;
+    q = reinterpret_cast<const double*>(qvec) + qs * e;
     soff = e * kPitch + loader_vector(t);
   }
   __device__ __forceinline__ void issue(double* buf, long long r0) const {
 #pragma unroll
     for (int s = 0; s < kC / 8; ++s) {
       double* d = buf + soff + 8 * s * kPitch;
-      const long long go = 2 * (r0 + 8 * s);
-      cp_async8(d, p + go);
-      cp_async8(d + kPlane, p + go + 1);
-      cp_async8(d + 2 * kPlane, q + go);
-      cp_async8(d + 3 * kPlane, q + go + 1);
+      const long long gp = ps * (r0 + 8 * s), gq = qs * (r0 + 8 * s);
+      cp_async8(d, p + gp);
+      cp_async8(d + kPlane, p + gp + pi);
+      cp_async8(d + 2 * kPlane, q + gq);
+      cp_async8(d + 3 * kPlane, q + gq + qi);
     }
     commit();
   }

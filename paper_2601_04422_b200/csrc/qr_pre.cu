@@ -520,7 +520,12 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
 
 // X = R^H: X[j][i] = conj(R[j][i]) = conj(A_i[j]) for j <= i < n, else 0,
 // i < m_pad (= round64(n)), j < n_pad. Grid (m_pad / 32, n_pad / 32, gates).
-__global__ void __launch_bounds__(256) qrp_form_rh_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws) {
+// second_step: this is the second QR of pre = 2 (R2^H -> the Jacobi operand).
+// The target is the Jacobi operand (split planes, common.cuh) for pre = 1 and
+// for the second step, else (R1^H of pre = 2, the second QR's operand)
+// interleaved.
+__global__ void __launch_bounds__(256) qrp_form_rh_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
+                                                          int second_step) {
   const GateDesc& g = gates[blockIdx.z];
   if (!g.pre) return;
   const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
@@ -542,7 +547,8 @@ __global__ void __launch_bounds__(256) qrp_form_rh_kernel(const GateDesc* __rest
   __syncthreads();
   for (int jj = ty; jj < 32; jj += 8) {
     const int j = j0 + jj, i = i0 + tx;
-    X[(long long)j * g.m_pad + i] = tile[tx][jj];
+    if (second_step || g.pre == 1) xs_set(X + (long long)j * g.m_pad, g.m_pad, i, tile[tx][jj]);
+    else X[(long long)j * g.m_pad + i] = tile[tx][jj];
   }
 }
 
@@ -559,7 +565,7 @@ __global__ void __launch_bounds__(256) qrp_zinit_kernel(const GateDesc* __restri
   if (r >= g.qr_m_pad || j >= out[blockIdx.z].k) return;
   const cplx* X = ws + g.ws_off + (long long)order[blockIdx.z * sig_stride + j] * g.m_pad;
   cplx* Z = ws + g.qr_off + (long long)j * g.qr_m_pad;
-  Z[r] = r < g.n ? X[r] : make_double2(0.0, 0.0);
+  Z[r] = r < g.n ? xs_get(X, g.m_pad, r) : make_double2(0.0, 0.0);
 }
 
 // MPSIM_PANEL=legacy selects the L2-streaming panel kernel (A/B only).
@@ -585,7 +591,7 @@ void qrp_init() {
 // max_n_pad: largest n_pad; max_x_pad: largest X stride; vbuf / tbuf hold
 // npan panel slots per gate.
 void launch_qr_factor(const GateDesc* d_gates, int n_gates, int max_n_pad, int max_x_pad, cplx* ws, cplx* vbuf,
-                      long long vld, cplx* tbuf, int npan, cudaStream_t st) {
+                      long long vld, cplx* tbuf, int npan, int second_step, cudaStream_t st) {
   const int panels = max_n_pad / kQ;
   const int cs = (int)((vld + kPR - 1) / kPR);
   // The cluster kernel holds one SM per CTA (128 KB of reflector slices): use
@@ -617,7 +623,7 @@ void launch_qr_factor(const GateDesc* d_gates, int n_gates, int max_n_pad, int m
       qrp_update_kernel<false><<<dim3(blocks, n_gates), 256, sizeof(QrUpdSmem), st>>>(d_gates, ws, p, vbuf, vld,
                                                                                       tbuf, npan, nullptr);
   }
-  qrp_form_rh_kernel<<<dim3(max_x_pad / 32, max_n_pad / 32, n_gates), 256, 0, st>>>(d_gates, ws);
+  qrp_form_rh_kernel<<<dim3(max_x_pad / 32, max_n_pad / 32, n_gates), 256, 0, st>>>(d_gates, ws, second_step);
 }
 
 // Z = Q1 [X_kept; 0] (kept columns in descending-sigma order) with the

@@ -25,7 +25,7 @@ __global__ void __launch_bounds__(256) norms_kernel(const GateDesc* __restrict__
   if (v >= g.n) return;
   const cplx* x = ws + g.ws_off + (long long)v * g.m_pad;
   double s = 0.0;
-  for (int e = lane; e < g.m; e += 32) s += cabs2(x[e]);
+  for (int e = lane; e < g.m; e += 32) s += cabs2(xs_get(x, g.m_pad, e));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (lane == 0) sigma[blockIdx.y * sig_stride + v] = sqrt(s);
@@ -117,6 +117,13 @@ __global__ void __launch_bounds__(1024) truncate_kernel(const GateDesc* __restri
   }
 }
 
+// Element e of vector j of the converged operand: the Jacobi X (split planes)
+// or, with two-step QR preconditioning, Z = Q1 [X; 0] (interleaved).
+__device__ __forceinline__ cplx x_elem(const GateDesc& g, const cplx* X, int j, int e) {
+  const cplx* v = X + (long long)j * g.m_pad;
+  return g.pre == 2 ? v[e] : xs_get(v, g.m_pad, e);
+}
+
 // ---- plain-copy factor.
 //  trans 0: site q   [e*chi + j]                 = X[o_j][e] / sigma_j   (e < m = 2dl, j < k)
 //  trans 1: site q+1 [j*2chi + p1*chi + r]       = scale * conj(X[o_j][e]), e = p1*dr + r
@@ -143,7 +150,7 @@ __global__ void __launch_bounds__(256) copy_factor_kernel(const GateDesc* __rest
       if (j < k && e < g.m) {
         const double s = sg[j];
         if (s > 0.0) {
-          const cplx x = X[(long long)(g.pre == 2 ? j : od[j]) * g.m_pad + e];
+          const cplx x = x_elem(g, X, g.pre == 2 ? j : od[j], e);
           v = make_double2(x.x / s, x.y / s);
         } else {
           v = make_double2(e == j ? 1.0 : 0.0, 0.0);  // zero matrix: any unit column
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(256) copy_factor_kernel(const GateDesc* __rest
     for (int jj = ty; jj < 32; jj += 8) {
       const int j = j0 + jj, e = e0 + tx;
       if (j < k && e < g.m) {
-        const cplx x = X[(long long)(g.pre == 2 ? j : od[j]) * g.m_pad + e];
+        const cplx x = x_elem(g, X, g.pre == 2 ? j : od[j], e);
         const long long off = (long long)j * g.ldv + (long long)(e / g.vsplit) * g.vsplit_ld + e % g.vsplit;
         g.v_out[off] = make_double2(o.scale * x.x, -o.scale * x.y);
       }
@@ -210,7 +217,9 @@ __global__ void __launch_bounds__(256, 2) cross_gram_kernel(const GateDesc* __re
   const int vi = pg::loader_vector(t);
   const int a = min(a0 + vi, n_a - 1), b = min(b0 + vi, n_b - 1);  // padding lanes load a valid vector
   pg::Loader ld;
-  ld.init(g.f == 0 ? xvec(a) : x0vec(a), g.f == 0 ? x0vec(b) : xvec(b), t);
+  const bool xsplit = g.pre != 2;  // X: split planes (Jacobi operand) or Z (interleaved)
+  if (g.f == 0) ld.init(xvec(a), x0vec(b), t, xsplit ? g.m_pad : 0, 0);
+  else ld.init(x0vec(a), xvec(b), t, 0, xsplit ? g.m_pad : 0);
   pg::cross_gram(ld, S.u.buf, S.u.Wx, S.W, 33, 0, g.m_pad, t);
   for (int idx = t; idx < 32 * 32; idx += 256) {
     const int ai = a0 + idx / 32, bi = b0 + idx % 32;
