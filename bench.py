@@ -133,7 +133,7 @@ def ncu_traffic():
         return None
     with open(p) as f:
         d = json.load(f)
-    return d.get("jacobi_gram_kernel", {}).get("dram_bytes_per_launch")
+    return d.get("jacobi_sweep_kernel", {}).get("dram_bytes_per_launch")
 
 
 # ---------------------------------------------------------------- CPU reference path
@@ -276,10 +276,12 @@ def main():
         "roofline": {
             "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved / peak, "traffic": ncu_traffic(),
-            "kernel": "jacobi_gram_kernel<2> (one Jacobi tournament round: Gram + pair EVD + rotation)",
+            "kernel": "jacobi_sweep_kernel (one persistent launch per Jacobi sweep: every pair visit = DMMA "
+                      "Gram + pair EVD + DMMA rotation)",
             "definition": "algorithmic SVD flops 32*M*N^2 per decomposed theta (SURVEY 8(d)) / CUDA-event "
-                          "time of all Jacobi round launches on the library stream (QR preconditioning, "
-                          "theta and the split epilogue excluded; see jacobi_share_of_step)",
+                          "time of all Jacobi sweep launches on the library stream (QR preconditioning, "
+                          "theta and the split epilogue excluded; see jacobi_share_of_step); traffic = DRAM "
+                          "bytes of one sweep launch (64 gates) from profiles/ncu_summary.json",
             "peak_source": peak_src,
             "jacobi_share_of_step": jac_ms / sum(dev_ms) if sum(dev_ms) > 0 else None,
             "step_algorithmic_tflops": c["gate_flops"] / dev_total / 1e12,
