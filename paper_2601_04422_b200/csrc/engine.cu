@@ -63,6 +63,7 @@ void launch_jacobi_round_split(const GateDesc*, int, int, cplx*, const int*, int
 // Cross-only pair EVDs (evd.cuh) in a sweep whose predecessor measured an rms
 // relative off-norm above this (the pre-asymptotic phase); MPSIM_CROSS=0 disables.
 constexpr double kCrossRms = 0.35;
+constexpr int kCrossSweeps = 4;  // cross-only EVDs in sweeps 1 .. kCrossSweeps - 1 at most
 // Stored in-block Grams while the previous sweep's largest relative
 // off-diagonal exceeds this; MPSIM_INBLOCK=0 disables.
 constexpr double kInblockMaxoff = 1e-4;
@@ -549,7 +550,13 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // pre-asymptotic (rms relative off-norm of the sweep above kCrossRms):
       // the next sweep's pair EVDs rotate the cross-block pairs only
       const double rms = std::sqrt(2.0 * h_offsum[i] / std::max(1, descs[i].n));
-      if (h_rot[i] && cross_policy() && rms > kCrossRms && h_maxoff[i] > 1e-3) h_rot[i] |= 2;
+      // (bounded: at most kCrossSweeps sweeps and only with >= 8 blocks, where the
+      // de Rijk reordering keeps reshuffling the blocks; with few blocks two
+      // nearly parallel vectors could share a block for good and a cross-only
+      // EVD would never rotate them — measured on a SWAP-routed 32 x 32 theta)
+      if (h_rot[i] && cross_policy() && rms > kCrossRms && h_maxoff[i] > 1e-3 && sweep < kCrossSweeps &&
+          descs[i].nb >= 8)
+        h_rot[i] |= 2;
       // pre-asymptotic and early asymptotic sweeps reuse the in-block Grams the
       // pair EVDs leave behind (jacobi_split.cu); the closing sweeps recompute all
       if (h_rot[i] && jacobi_mode() >= 3 && inblock_policy() && h_maxoff[i] > kInblockMaxoff) h_rot[i] |= 4;
