@@ -89,11 +89,11 @@ struct ChunkLoader {
   }
 };
 
-constexpr int kPitchR = 68;  // R_ext row pitch (== 4 mod 16: conflict-free B fragments)
+constexpr int kPitchR = 34;  // complex R row pitch (== 2 mod 8: conflict-free 16-byte B fragments)
 
 // Gram (+ pair EVD (+ rotation)) of one block pair in one CTA. R aliases the
-// chunk buffers / Gx, dead once G is built; R_ext aliases G, dead once the
-// in-block Grams are stored: 72 KB per CTA, three CTAs per SM.
+// chunk buffers / Gx, dead once G is built; the rotation's copy of R aliases G,
+// dead once the in-block Grams are stored: 55 KB per CTA.
 struct PairSmem {
   union {
     double buf[2][2 * kChunkPlane];
@@ -101,23 +101,25 @@ struct PairSmem {
   } u;
   union {
     cplx G[kP * kPad];
-    double Rx[2 * kP * kPitchR];  // R_ext[c_ext][j_ext] = [[Re R, Im R], [-Im R, Re R]]
+    cplx Rs[kP * kPitchR];  // R for the rotation
   } v;
   EvdScratch sc;
 };
 static_assert(sizeof(cplx) * kP * kPad <= sizeof(PairSmem::u), "R must fit in the chunk buffers");
 
-// X_P <- X_P R_ext over all chunks (R_ext in shared memory). Warp w computes
-// row tiles {2(w&1), +1} of a chunk and complex column tile w/2 (real column
-// tiles w/2 and 4 + w/2): per k-step two A and two B fragment loads feed four
-// DMMAs, and each thread ends up with Re and Im of the same complex outputs
-// (16-byte global stores).
+// X_P <- X_P R over all chunks, on DMMA in real-extended form
+// X_ext R_ext with R_ext = [[Re R, Im R], [-Im R, Re R]] formed on the fly:
+// one 16-byte load of R[c][j] gives both B fragments (Re and Im output tiles)
+// of a k-step. Warp w computes row tiles {2(w&1), +1} of a chunk and complex
+// column tile w/2 (real column tiles w/2 and 4 + w/2): per k-step two A loads
+// and one B load feed four DMMAs, and each thread ends up with Re and Im of the
+// same complex outputs.
 __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader& ld, double (*buf)[2 * kChunkPlane],
-                                            const double* Rx, int nchunks, int t) {
+                                            const cplx* Rs, int nchunks, int t) {
   const int lane = t % 32, warp = t / 32;
   const int fr = lane / 4, fk = lane % 4;
   const int rbase = 2 * (warp & 1), cj = warp >> 1;
-  const int bre = 8 * cj + fr, bim = kP + 8 * cj + fr;
+  const int jb = 8 * cj + fr;
   for (int k = 0; k < nchunks; ++k) {
     if (k + 1 < nchunks) {
       ld.issue(buf[(k + 1) & 1], (k + 1) * kC);
@@ -134,10 +136,12 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
       for (int q = 0; q < 2; ++q) o[a][q][0] = o[a][q][1] = 0.0;
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
-      const int cext = 4 * s + fk;
-      const double* plane = B + (cext < kP ? 0 : kChunkPlane) + (cext & (kP - 1)) * kPitchS;
+      const int cext = 4 * s + fk, cc = cext & (kP - 1);
+      const double* plane = B + (s < 8 ? 0 : kChunkPlane) + cc * kPitchS;
       const double a0 = plane[8 * rbase + fr], a1 = plane[8 * (rbase + 1) + fr];
-      const double b0 = Rx[cext * kPitchR + bre], b1 = Rx[cext * kPitchR + bim];
+      const cplx r = Rs[cc * kPitchR + jb];
+      const double b0 = s < 8 ? r.x : -r.y;  // [[Re R, Im R],
+      const double b1 = s < 8 ? r.y : r.x;   //  [-Im R, Re R]]
       dmma_s(o[0][0][0], o[0][0][1], a0, b0);
       dmma_s(o[0][1][0], o[0][1][1], a0, b1);
       dmma_s(o[1][0][0], o[1][0][1], a1, b0);
@@ -158,15 +162,11 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
   }
 }
 
-// R (complex, pitch kPad) -> R_ext
-__device__ __forceinline__ void expand_rotation(const cplx* R, long long rpitch, double* Rx, int t) {
+// R (complex, pitch rpitch) -> Rs (pitch kPitchR)
+__device__ __forceinline__ void copy_rotation(const cplx* R, long long rpitch, cplx* Rs, int t) {
   for (int idx = t; idx < kP * kP; idx += 256) {
     const int i = idx / kP, j = idx % kP;
-    const cplx r = R[i * rpitch + j];
-    Rx[i * kPitchR + j] = r.x;
-    Rx[i * kPitchR + kP + j] = r.y;
-    Rx[(kP + i) * kPitchR + j] = -r.y;
-    Rx[(kP + i) * kPitchR + kP + j] = r.x;
+    Rs[i * kPitchR + j] = R[i * rpitch + j];
   }
 }
 
@@ -357,10 +357,10 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
       for (int idx = t; idx < kP * kP; idx += 256) rout[idx] = R[(idx / kP) * kPad + idx % kP];
     } else {
       __syncthreads();  // G (aliased by R_ext) has been stored
-      expand_rotation(R, kPad, S.v.Rx, t);
+      copy_rotation(R, kPad, S.v.Rs, t);
       __syncthreads();  // R (aliased by the chunk buffers) has been read
       ld.issue(S.u.buf[0], 0);
-      rotate_pair(c, ld, S.u.buf, S.v.Rx, nchunks, t);
+      rotate_pair(c, ld, S.u.buf, S.v.Rs, nchunks, t);
       if (t == 0) atomicAdd(rotated + gi, 1);
     }
   } else {
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(RoundArgs A, int ro
 // CTA's pair EVD overlaps the DMMA phases of its neighbours. Deadlock-free:
 // a visit only waits on visits claimed before it, all of which are held by
 // running CTAs.
-__global__ void __launch_bounds__(256, 3) jacobi_sweep_kernel(RoundArgs A, int n_gates, int max_rounds,
+__global__ void __launch_bounds__(256, 4) jacobi_sweep_kernel(RoundArgs A, int n_gates, int max_rounds,
                                                               int* __restrict__ ctl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
@@ -463,7 +463,7 @@ __global__ void __launch_bounds__(256, 6) jacobi_evd_kernel(const GateDesc* __re
 
 struct RotSmem {
   double buf[2][2 * kChunkPlane];
-  double Rx[2 * kP * kPitchR];
+  cplx Rs[kP * kPitchR];
 };
 
 // 3 CTAs x 72 KB per SM.
@@ -485,8 +485,8 @@ __global__ void __launch_bounds__(256, 3) jacobi_rot_kernel(const GateDesc* __re
   ld.init(c, t);
   const int nchunks = g.m_pad / kC;
   ld.issue(S.buf[0], 0);
-  expand_rotation(rbuf + slot * (kP * kP), kP, S.Rx, t);
-  rotate_pair(c, ld, S.buf, S.Rx, nchunks, t);
+  copy_rotation(rbuf + slot * (kP * kP), kP, S.Rs, t);
+  rotate_pair(c, ld, S.buf, S.Rs, nchunks, t);
   if (t == 0) atomicAdd(rotated + gi, 1);
 }
 
