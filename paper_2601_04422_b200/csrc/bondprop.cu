@@ -32,10 +32,10 @@ __global__ void load_matrix_kernel(const cplx* __restrict__ A, long long lda, in
     const cplx vc = make_double2(v.x, -v.y);
     const long long xv = xtrans == 0 ? c : r, xe = xtrans == 0 ? r : c;
     const cplx xval = xtrans == 0 ? v : vc;
-    if (xsplit) xs_set(X + xv * ldx, ldx, xe, xval);  // the Jacobi operand (split planes)
-    else X[xv * ldx + xe] = xval;
-    if (f == 0) X0[(long long)c * ldx0 + r] = v;
-    else X0[(long long)r * ldx0 + c] = vc;
+    (void)xsplit;  // every workspace operand is split planes (common.cuh)
+    xs_set(X + xv * ldx, ldx, xe, xval);
+    if (f == 0) xs_set(X0 + (long long)c * ldx0, ldx0, r, v);
+    else xs_set(X0 + (long long)r * ldx0, ldx0, c, vc);
     fr += cabs2(v);
   }
 #pragma unroll

@@ -160,10 +160,11 @@ __device__ __forceinline__ void cmac_rn(cplx& acc, cplx a, cplx b) {
 __device__ __forceinline__ cplx conjc(cplx a) { return make_double2(a.x, -a.y); }
 __device__ __forceinline__ double cabs2(cplx a) { return a.x * a.x + a.y * a.y; }
 
-// The Jacobi operand X keeps each vector as split planes inside its m_pad-
-// complex slot: Re in doubles [0, m_pad), Im in [m_pad, 2 m_pad) (16-byte
-// cp.async of two rows of one plane into vector-major shared memory,
-// jacobi_split.cu). X0, the QR operand and Z (pre = 2) are interleaved complex.
+// Every workspace operand (the Jacobi X, X0, the QR operand / Z, the y2 area,
+// the QR reflectors) keeps each vector as split planes inside its m_pad-complex
+// slot: Re in doubles [0, m_pad), Im in [m_pad, 2 m_pad) — so two rows of one
+// plane are one 16-byte cp.async into vector-major shared memory
+// (jacobi_split.cu, pair_gemm.cuh).
 __device__ __forceinline__ cplx xs_get(const cplx* vec, long long m_pad, long long e) {
   const double* d = reinterpret_cast<const double*>(vec);
   return make_double2(d[e], d[m_pad + e]);

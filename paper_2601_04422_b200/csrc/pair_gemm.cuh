@@ -3,8 +3,8 @@
 //   [Pr | Pi]^T [Qr | Qi] = [[Pr^T Qr, Pr^T Qi], [Pi^T Qr, Pi^T Qi]]  (64 x 64)
 //   Re W = Pr^T Qr + Pi^T Qi,  Im W = Pr^T Qi - Pi^T Qr
 // with the chunk pipeline of the Jacobi pair kernel (jacobi_split.cu): 32-row
-// chunks as split Re/Im planes [row][vector] of pitch 36 (conflict-free DMMA
-// fragments), double-buffered with cp.async. Used by the QR trailing update
+// chunks as vector-major split Re/Im planes of pitch 36 (conflict-free DMMA
+// fragments), double-buffered with 16-byte cp.async. Used by the QR trailing update
 // (V^H A, qr_pre.cu) and the split epilogue (U^H X0 / X0^H X, split.cu).
 // 256-thread CTAs.
 #pragma once
@@ -24,54 +24,42 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }
-__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
-}
 __device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
-// The vector a thread streams: vi = 4 warp + ((lane >> 2) & 3), rows
-// (lane & 3) + 4 (lane >> 4) + 8 s; a half-warp covers 4 rows x 4 vectors, so
-// its 8-byte shared writes hit 16 distinct bank pairs; a warp reads full
-// 128-byte lines.
-__device__ __forceinline__ int loader_vector(int t) { return 4 * (t >> 5) + (((t & 31) >> 2) & 3); }
+// Operands are split-plane vectors (common.cuh): Re in doubles [0, m),
+// Im in [m, 2 m) of each vector's slot. Per chunk and thread eight 16-byte
+// copies (two rows of one plane of one vector): in copy s, warp w moves
+// vector w + 8 (s & 3) of P (s < 4) or Q, lanes 0-15 its Re rows and lanes
+// 16-31 its Im rows, 256 contiguous bytes each; shared planes are vector-major
+// [vector][row] with pitch 36 (conflict-free DMMA fragments).
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
 
 struct Loader {
-  const double* p;  // this thread's P vector (as doubles), Re of its first row
-  const double* q;
-  int ps, qs;       // doubles per row: 2 (interleaved complex) or 1 (split planes)
-  long long pi, qi; // offset of Im from Re: 1 (interleaved) or m_pad (split planes)
+  const double* src[8];  // this thread's plane of its 8 vectors, at its row pair
   int soff;
-  // pvec / qvec: the vectors of index loader_vector(t) (any valid address for
-  // padding vectors whose results are discarded); psplit / qsplit: 0 for
-  // interleaved complex vectors, else the m_pad of split-plane vectors
-  // (common.cuh, the Jacobi operand)
-  __device__ __forceinline__ void init(const cplx* pvec, const cplx* qvec, int t, long long psplit = 0,
-                                       long long qsplit = 0) {
-    const int lane = t & 31;
-    const int e = (lane & 3) + 4 * (lane >> 4);
-    ps = psplit ? 1 : 2;
-    qs = qsplit ? 1 : 2;
-    pi = psplit ? psplit : 1;
-    qi = qsplit ? qsplit : 1;
-    p = reinterpret_cast<const double*>(pvec) + ps * e;
-    q = reinterpret_cast<const double*>(qvec) + qs * e;
-    soff = e * kPitch + loader_vector(t);
+  // pvec(v) / qvec(v): vector v (0..31) of P / Q (any valid vector for padding
+  // vectors whose results are discarded); pm / qm: their plane offsets (m_pad)
+  template <class PF, class QF>
+  __device__ __forceinline__ void init(PF pvec, QF qvec, long long pm, long long qm, int t) {
+    const int lane = t & 31, warp = t >> 5;
+    const int rp = lane & 15, plane = lane >> 4;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      src[s] = reinterpret_cast<const double*>(pvec(warp + 8 * s)) + plane * pm + 2 * rp;
+      src[4 + s] = reinterpret_cast<const double*>(qvec(warp + 8 * s)) + plane * qm + 2 * rp;
+    }
+    soff = plane * kPlane + warp * kPitch + 2 * rp;
   }
   __device__ __forceinline__ void issue(double* buf, long long r0) const {
 #pragma unroll
-    for (int s = 0; s < kC / 8; ++s) {
-      double* d = buf + soff + 8 * s * kPitch;
-      const long long gp = ps * (r0 + 8 * s), gq = qs * (r0 + 8 * s);
-      cp_async8(d, p + gp);
-      cp_async8(d + kPlane, p + gp + pi);
-      cp_async8(d + 2 * kPlane, q + gq);
-      cp_async8(d + 3 * kPlane, q + gq + qi);
-    }
+    for (int s = 0; s < 8; ++s) cp_async16(buf + (s >> 2) * 2 * kPlane + soff + 8 * (s & 3) * kPitch, src[s] + r0);
     commit();
   }
 };
@@ -105,12 +93,12 @@ __device__ __forceinline__ void cross_gram(const Loader& ld, double (*buf)[kBuf]
     const double* Pa = buf[k & 1] + (2 + qy) * kPlane;
 #pragma unroll
     for (int ks = 0; ks < kC / 4; ++ks) {
-      const int row = (4 * ks + fk) * kPitch;
+      const int row = 4 * ks + fk;
       double av[2], bv[4];
 #pragma unroll
-      for (int a = 0; a < 2; ++a) av[a] = Pv[row + 8 * (tr0 + a) + fr];  // A[m = p idx][k = e]
+      for (int a = 0; a < 2; ++a) av[a] = Pv[(8 * (tr0 + a) + fr) * kPitch + row];  // A[m = p idx][k = e]
 #pragma unroll
-      for (int c = 0; c < 4; ++c) bv[c] = Pa[row + 8 * c + fr];          // B[k = e][n = q idx]
+      for (int c = 0; c < 4; ++c) bv[c] = Pa[(8 * c + fr) * kPitch + row];          // B[k = e][n = q idx]
 #pragma unroll
       for (int a = 0; a < 2; ++a)
 #pragma unroll

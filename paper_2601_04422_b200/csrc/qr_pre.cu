@@ -40,7 +40,7 @@ constexpr int kQ = 32;                  // panel width
 constexpr int kQC = pg::kC;             // rows per streamed chunk
 constexpr int kQPitch = pg::kPitch;     // conflict-free DMMA fragment pitch (== 4 mod 16)
 constexpr int kQPlane = pg::kPlane;
-constexpr int kQPitchW = 68;
+constexpr int kQPitchW = 34;  // complex W2 pitch (== 2 mod 8: conflict-free 16-byte B fragments)
 
 __device__ __forceinline__ double block_sum_1024(double v, double* red) {
 #pragma unroll
@@ -86,9 +86,9 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
     const int row0 = c0 + j;
     cplx* col = A + (long long)(c0 + j) * ld;
     double s = 0.0;
-    for (int r = row0 + 1 + t; r < m; r += 1024) s += cabs2(col[r]);
+    for (int r = row0 + 1 + t; r < m; r += 1024) s += cabs2(xs_get(col, ld, r));
     const double xn2 = block_sum_1024(s, red);
-    const cplx alpha = row0 < m ? col[row0] : make_double2(0.0, 0.0);
+    const cplx alpha = row0 < m ? xs_get(col, ld, row0) : make_double2(0.0, 0.0);
     // zlarfg: H^H x = beta e_1, beta real, v = [1; x(2:)/(alpha - beta)]
     cplx tau = make_double2(0.0, 0.0), inv = make_double2(0.0, 0.0);
     double beta = alpha.x;
@@ -104,12 +104,12 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
     for (long long r = t; r < vld; r += 1024) {
       cplx v = make_double2(0.0, 0.0);
       if (r == row0) v = make_double2(1.0, 0.0);
-      else if (r > row0 && r < m && refl) v = cmul(col[r], inv);
-      vj[r] = v;
+      else if (r > row0 && r < m && refl) v = cmul(xs_get(col, ld, r), inv);
+      xs_set(vj, vld, r, v);
       if (r < ld) vs[r] = v;
     }
     if (t == 0) {
-      if (row0 < m) col[row0] = make_double2(refl ? beta : alpha.x, refl ? 0.0 : alpha.y);
+      if (row0 < m) xs_set(col, ld, row0, make_double2(refl ? beta : alpha.x, refl ? 0.0 : alpha.y));
       taus[j] = tau;
     }
     __syncthreads();
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const int r = rb + 32 * u + lane;
-          xv[u] = r < m ? vi[r] : make_double2(0.0, 0.0);
+          xv[u] = r < m ? xs_get(vi, vld, r) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const int r = rb + 32 * u + lane;
-          av[u] = r < m ? a[r] : make_double2(0.0, 0.0);
+          av[u] = r < m ? xs_get(a, ld, r) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -183,7 +183,7 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
           const int r = rb + 32 * u + lane;
-          av[u] = r < m ? a[r] : make_double2(0.0, 0.0);
+          av[u] = r < m ? xs_get(a, ld, r) : make_double2(0.0, 0.0);
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
             const cplx vr = vs[r];
             av[u].x -= vr.x * coef.x - vr.y * coef.y;
             av[u].y -= vr.x * coef.y + vr.y * coef.x;
-            a[r] = av[u];
+            xs_set(a, ld, r, av[u]);
           }
         }
       }
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(1024) qrp_panel_kernel(const GateDesc* __restr
   // unused reflector slots of a short last panel: v = 0, tau = 0
   for (int j = jb; j < kQ; ++j) {
     cplx* vj = V + (long long)j * vld;
-    for (long long r = t; r < vld; r += 1024) vj[r] = make_double2(0.0, 0.0);
+    for (long long r = t; r < vld; r += 1024) xs_set(vj, vld, r, make_double2(0.0, 0.0));
     if (t == 0) taus[j] = make_double2(0.0, 0.0);
   }
   for (int idx = t; idx < kQ * (kQ + 1); idx += 1024) T[idx / (kQ + 1)][idx % (kQ + 1)] = make_double2(0.0, 0.0);
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(1024, 1) qrp_panel_cluster_kernel(const GateDe
 #pragma unroll
   for (int s2 = 0; s2 < kPL; ++s2) {
     const int r = rbase + lane + 32 * s2;
-    a[s2] = (warp < jb && r < m) ? acol[r] : make_double2(0.0, 0.0);
+    a[s2] = (warp < jb && r < m) ? xs_get(acol, ld, r) : make_double2(0.0, 0.0);
   }
   for (int j = 0; j < jb; ++j) {
     const int row0 = c0 + j, buf = j & 1;
@@ -379,11 +379,11 @@ __global__ void __launch_bounds__(1024, 1) qrp_panel_cluster_kernel(const GateDe
 #pragma unroll
   for (int s2 = 0; s2 < kPL; ++s2) {
     const int r = rbase + lane + 32 * s2;
-    if (warp < jb && r < ld) acol[r] = a[s2];
+    if (warp < jb && r < ld) xs_set(acol, ld, r, a[s2]);
   }
   for (int idx = t; idx < kQ * kPR; idx += 1024) {
     const int jj = idx / kPR, rr = idx % kPR, r = rbase + rr;
-    if (r < vld) V[(long long)jj * vld + r] = jj < jb ? S.vs[jj][rr] : make_double2(0.0, 0.0);
+    if (r < vld) xs_set(V + (long long)jj * vld, vld, r, jj < jb ? S.vs[jj][rr] : make_double2(0.0, 0.0));
   }
   if (rank == 0) {
     // zlarft (forward, columnwise): T[j][j] = tau_j, T[0:j, j] = -tau_j T[0:j,0:j] Gv[0:j, j]
@@ -417,7 +417,7 @@ struct QrUpdSmem {
       cplx T[kQ * (kQ + 1)];
     } w;
   } u;
-  double W2x[64 * kQPitchW];     // -(T^H W)_ext as the B operand
+  cplx W2[kQ * kQPitchW];        // -(T^H W) (or -(T W)), complex, pitch 34
 };
 
 }  // namespace
@@ -447,7 +447,7 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
   cplx* A = ws + g.qr_off + (long long)cb * ald;
   const cplx* V = vbuf + ((long long)blockIdx.y * npan + p) * kQ * vld;
   pg::Loader ld;
-  ld.init(V + (long long)pg::loader_vector(t) * vld, A + (long long)pg::loader_vector(t) * ald, t);
+  ld.init([&](int v) { return V + (long long)v * vld; }, [&](int v) { return A + (long long)v * ald; }, vld, ald, t);
   const int nchunks = (int)((ald - c0) / kQC);
 
   // ---- pass 1: W = V^H A_b (pair_gemm.cuh), then T
@@ -465,17 +465,15 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
     } else {
       for (int k = 0; k <= i; ++k) cfmac(z, S.u.w.T[k * (kQ + 1) + i], S.u.w.W[k * (kQ + 1) + j]);
     }
-    S.W2x[i * kQPitchW + j] = -z.x;
-    S.W2x[i * kQPitchW + kQ + j] = -z.y;
-    S.W2x[(kQ + i) * kQPitchW + j] = z.y;
-    S.W2x[(kQ + i) * kQPitchW + kQ + j] = -z.x;
+    S.W2[i * kQPitchW + j] = make_double2(-z.x, -z.y);
   }
   __syncthreads();
 
-  // ---- pass 2: A_ext += V_ext (-W2_ext). Warp w: row tiles 2 (w & 1) + {0, 1},
-  // complex column tile w / 2 (real tiles w/2 and 4 + w/2).
+  // ---- pass 2: A_ext += V_ext (-W2_ext), -W2_ext = [[Re, Im], [-Im, Re]] of -W2
+  // formed from one 16-byte load per k-step. Warp w: row tiles 2 (w & 1) +
+  // {0, 1}, complex column tile w / 2 (real tiles w/2 and 4 + w/2).
   const int rbase = 2 * (warp & 1), cj = warp >> 1;
-  const int bre = 8 * cj + fr, bim = kQ + 8 * cj + fr;
+  const int jb = 8 * cj + fr;
   ld.issue(S.u.buf[0], c0);
   for (int k = 0; k < nchunks; ++k) {
     if (k + 1 < nchunks) {
@@ -492,15 +490,16 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int e = 8 * (rbase + a) + fr, j = 8 * cj + 2 * fk + v;
-        o[a][0][v] = B[2 * kQPlane + e * kQPitch + j];
-        o[a][1][v] = B[3 * kQPlane + e * kQPitch + j];
+        o[a][0][v] = B[2 * kQPlane + j * kQPitch + e];
+        o[a][1][v] = B[3 * kQPlane + j * kQPitch + e];
       }
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
-      const int cext = 4 * s + fk;
-      const double* plane = B + (cext < kQ ? 0 : kQPlane) + (cext & (kQ - 1));
-      const double a0 = plane[(8 * rbase + fr) * kQPitch], a1 = plane[(8 * (rbase + 1) + fr) * kQPitch];
-      const double b0 = S.W2x[cext * kQPitchW + bre], b1 = S.W2x[cext * kQPitchW + bim];
+      const int cc = (4 * s + fk) & (kQ - 1);
+      const double* plane = B + (s < 8 ? 0 : kQPlane) + cc * kQPitch;
+      const double a0 = plane[8 * rbase + fr], a1 = plane[8 * (rbase + 1) + fr];
+      const cplx w2 = S.W2[cc * kQPitchW + jb];
+      const double b0 = s < 8 ? w2.x : -w2.y, b1 = s < 8 ? w2.y : w2.x;
       pg::dmma(o[0][0][0], o[0][0][1], a0, b0);
       pg::dmma(o[0][1][0], o[0][1][1], a0, b1);
       pg::dmma(o[1][0][0], o[1][0][1], a1, b0);
@@ -512,7 +511,9 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int e = 8 * (rbase + a) + fr, j = 8 * cj + 2 * fk + v;
-        A[(long long)j * ald + r0 + e] = make_double2(o[a][0][v], o[a][1][v]);
+        double* aj = reinterpret_cast<double*>(A + (long long)j * ald);
+        aj[r0 + e] = o[a][0][v];
+        aj[ald + r0 + e] = o[a][1][v];
       }
     __syncthreads();
   }
@@ -520,10 +521,8 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
 
 // X = R^H: X[j][i] = conj(R[j][i]) = conj(A_i[j]) for j <= i < n, else 0,
 // i < m_pad (= round64(n)), j < n_pad. Grid (m_pad / 32, n_pad / 32, gates).
-// second_step: this is the second QR of pre = 2 (R2^H -> the Jacobi operand).
-// The target is the Jacobi operand (split planes, common.cuh) for pre = 1 and
-// for the second step, else (R1^H of pre = 2, the second QR's operand)
-// interleaved.
+// second_step: this is the second QR of pre = 2 (R2^H -> the Jacobi operand);
+// either way the target is split planes (common.cuh).
 __global__ void __launch_bounds__(256) qrp_form_rh_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
                                                           int second_step) {
   const GateDesc& g = gates[blockIdx.z];
@@ -539,7 +538,7 @@ __global__ void __launch_bounds__(256) qrp_form_rh_kernel(const GateDesc* __rest
     const int i = i0 + ii, j = j0 + tx;
     cplx v = make_double2(0.0, 0.0);
     if (i < g.n && j < g.n && j <= i) {
-      const cplx a = A[(long long)i * g.qr_m_pad + j];
+      const cplx a = xs_get(A + (long long)i * g.qr_m_pad, g.qr_m_pad, j);
       v = make_double2(a.x, -a.y);
     }
     tile[ii][tx] = v;
@@ -547,8 +546,7 @@ __global__ void __launch_bounds__(256) qrp_form_rh_kernel(const GateDesc* __rest
   __syncthreads();
   for (int jj = ty; jj < 32; jj += 8) {
     const int j = j0 + jj, i = i0 + tx;
-    if (second_step || g.pre == 1) xs_set(X + (long long)j * g.m_pad, g.m_pad, i, tile[tx][jj]);
-    else X[(long long)j * g.m_pad + i] = tile[tx][jj];
+    xs_set(X + (long long)j * g.m_pad, g.m_pad, i, tile[tx][jj]);
   }
 }
 
@@ -565,7 +563,7 @@ __global__ void __launch_bounds__(256) qrp_zinit_kernel(const GateDesc* __restri
   if (r >= g.qr_m_pad || j >= out[blockIdx.z].k) return;
   const cplx* X = ws + g.ws_off + (long long)order[blockIdx.z * sig_stride + j] * g.m_pad;
   cplx* Z = ws + g.qr_off + (long long)j * g.qr_m_pad;
-  Z[r] = r < g.n ? xs_get(X, g.m_pad, r) : make_double2(0.0, 0.0);
+  xs_set(Z, g.qr_m_pad, r, r < g.n ? xs_get(X, g.m_pad, r) : make_double2(0.0, 0.0));
 }
 
 // MPSIM_PANEL=legacy selects the L2-streaming panel kernel (A/B only).

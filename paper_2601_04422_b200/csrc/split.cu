@@ -117,11 +117,10 @@ __global__ void __launch_bounds__(1024) truncate_kernel(const GateDesc* __restri
   }
 }
 
-// Element e of vector j of the converged operand: the Jacobi X (split planes)
-// or, with two-step QR preconditioning, Z = Q1 [X; 0] (interleaved).
+// Element e of vector j of the converged operand: the Jacobi X or, with
+// two-step QR preconditioning, Z = Q1 [X; 0] (both split planes).
 __device__ __forceinline__ cplx x_elem(const GateDesc& g, const cplx* X, int j, int e) {
-  const cplx* v = X + (long long)j * g.m_pad;
-  return g.pre == 2 ? v[e] : xs_get(v, g.m_pad, e);
+  return xs_get(X + (long long)j * g.m_pad, g.m_pad, e);
 }
 
 // ---- plain-copy factor.
@@ -214,12 +213,11 @@ __global__ void __launch_bounds__(256, 2) cross_gram_kernel(const GateDesc* __re
   const int t = threadIdx.x;
   auto xvec = [&](int j) { return X + (long long)(g.pre == 2 ? j : od[j]) * g.m_pad; };
   auto x0vec = [&](int v) { return X0 + (long long)v * g.x0_ld; };
-  const int vi = pg::loader_vector(t);
-  const int a = min(a0 + vi, n_a - 1), b = min(b0 + vi, n_b - 1);  // padding lanes load a valid vector
+  // padding vectors (beyond n_a / n_b) load a valid vector, results discarded
+  auto pa = [&](int v) { const int a = min(a0 + v, n_a - 1); return g.f == 0 ? xvec(a) : x0vec(a); };
+  auto qb = [&](int v) { const int b = min(b0 + v, n_b - 1); return g.f == 0 ? x0vec(b) : xvec(b); };
   pg::Loader ld;
-  const bool xsplit = g.pre != 2;  // X: split planes (Jacobi operand) or Z (interleaved)
-  if (g.f == 0) ld.init(xvec(a), x0vec(b), t, xsplit ? g.m_pad : 0, 0);
-  else ld.init(x0vec(a), xvec(b), t, 0, xsplit ? g.m_pad : 0);
+  ld.init(pa, qb, g.f == 0 ? g.m_pad : g.x0_ld, g.f == 0 ? g.x0_ld : g.m_pad, t);
   pg::cross_gram(ld, S.u.buf, S.u.Wx, S.W, 33, 0, g.m_pad, t);
   for (int idx = t; idx < 32 * 32; idx += 256) {
     const int ai = a0 + idx / 32, bi = b0 + idx % 32;

@@ -114,15 +114,11 @@ __global__ void __launch_bounds__(256) theta_kernel(const GateDesc* __restrict__
         const int p0o = o >> 1, p1o = o & 1;
         const long long row = l * 2 + p0o, col = p1o * dr + r;  // theta (2Dl x 2Dr)
         const cplx vc = make_double2(v.x, -v.y);
-        if (g.pre) {  // QR operand: interleaved
-          if (g.trans == 0) X[col * ldx + row] = v;
-          else X[row * ldx + col] = vc;
-        } else {  // Jacobi operand: split planes
-          if (g.trans == 0) xs_set(X + col * ldx, ldx, row, v);
-          else xs_set(X + row * ldx, ldx, col, vc);
-        }
-        if (g.f == 0) X0[col * g.x0_ld + row] = v;
-        else X0[row * g.x0_ld + col] = vc;
+        // split planes (common.cuh): the Jacobi / QR operand and X0
+        if (g.trans == 0) xs_set(X + col * ldx, ldx, row, v);
+        else xs_set(X + row * ldx, ldx, col, vc);
+        if (g.f == 0) xs_set(X0 + col * g.x0_ld, g.x0_ld, row, v);
+        else xs_set(X0 + row * g.x0_ld, g.x0_ld, col, vc);
         f2 += cabs2(v);
       }
     }
@@ -290,15 +286,11 @@ __global__ void __launch_bounds__(256, 2) theta_dmma_kernel(const GateDesc* __re
         const int p0o = o >> 1, p1o = o & 1;
         const long long row = l * 2 + p0o, col = p1o * dr + r;  // theta (2Dl x 2Dr)
         const cplx vc = make_double2(v.x, -v.y);
-        if (g.pre) {  // QR operand: interleaved
-          if (g.trans == 0) X[col * ldx + row] = v;
-          else X[row * ldx + col] = vc;
-        } else {  // Jacobi operand: split planes
-          if (g.trans == 0) xs_set(X + col * ldx, ldx, row, v);
-          else xs_set(X + row * ldx, ldx, col, vc);
-        }
-        if (g.f == 0) X0[col * g.x0_ld + row] = v;
-        else X0[row * g.x0_ld + col] = vc;
+        // split planes (common.cuh): the Jacobi / QR operand and X0
+        if (g.trans == 0) xs_set(X + col * ldx, ldx, row, v);
+        else xs_set(X + row * ldx, ldx, col, vc);
+        if (g.f == 0) xs_set(X0 + col * g.x0_ld, g.x0_ld, row, v);
+        else xs_set(X0 + row * g.x0_ld, g.x0_ld, col, vc);
         f2 += cabs2(v);
       }
     }
