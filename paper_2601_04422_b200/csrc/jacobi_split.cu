@@ -120,9 +120,11 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
   const int fr = lane / 4, fk = lane % 4;
   const int rbase = 2 * (warp & 1), cj = warp >> 1;
   const int jb = 8 * cj + fr;
+  // chunks last to first: the rows the Gram pass read last are the likeliest
+  // still in L2 (the caller issues chunk nchunks - 1 into buffer 0)
   for (int k = 0; k < nchunks; ++k) {
     if (k + 1 < nchunks) {
-      ld.issue(buf[(k + 1) & 1], (k + 1) * kC);
+      ld.issue(buf[(k + 1) & 1], (nchunks - 2 - k) * kC);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -147,7 +149,7 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
       dmma_s(o[1][0][0], o[1][0][1], a1, b0);
       dmma_s(o[1][1][0], o[1][1][1], a1, b1);
     }
-    const int e0 = k * kC;
+    const int e0 = (nchunks - 1 - k) * kC;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -359,7 +361,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
       __syncthreads();  // G (aliased by R_ext) has been stored
       copy_rotation(R, kPad, S.v.Rs, t);
       __syncthreads();  // R (aliased by the chunk buffers) has been read
-      ld.issue(S.u.buf[0], 0);
+      ld.issue(S.u.buf[0], (nchunks - 1) * kC);
       rotate_pair(c, ld, S.u.buf, S.v.Rs, nchunks, t);
       if (t == 0) atomicAdd(rotated + gi, 1);
     }
@@ -484,7 +486,7 @@ __global__ void __launch_bounds__(256, 3) jacobi_rot_kernel(const GateDesc* __re
   ChunkLoader ld;
   ld.init(c, t);
   const int nchunks = g.m_pad / kC;
-  ld.issue(S.buf[0], 0);
+  ld.issue(S.buf[0], (nchunks - 1) * kC);
   copy_rotation(rbuf + slot * (kP * kP), kP, S.Rs, t);
   rotate_pair(c, ld, S.buf, S.Rs, nchunks, t);
   if (t == 0) atomicAdd(rotated + gi, 1);
