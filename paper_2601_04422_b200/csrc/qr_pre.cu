@@ -474,10 +474,11 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
   // {0, 1}, complex column tile w / 2 (real tiles w/2 and 4 + w/2).
   const int rbase = 2 * (warp & 1), cj = warp >> 1;
   const int jb = 8 * cj + fr;
-  ld.issue(S.u.buf[0], c0);
+  // chunks last to first (L2 reuse of pass 1's most recent rows)
+  ld.issue(S.u.buf[0], c0 + (nchunks - 1) * kQC);
   for (int k = 0; k < nchunks; ++k) {
     if (k + 1 < nchunks) {
-      ld.issue(S.u.buf[(k + 1) & 1], c0 + (k + 1) * kQC);
+      ld.issue(S.u.buf[(k + 1) & 1], c0 + (nchunks - 2 - k) * kQC);
       pg::wait<1>();
     } else {
       pg::wait<0>();
@@ -505,7 +506,7 @@ __global__ void __launch_bounds__(256, 2) qrp_update_kernel(const GateDesc* __re
       pg::dmma(o[1][0][0], o[1][0][1], a1, b0);
       pg::dmma(o[1][1][0], o[1][1][1], a1, b1);
     }
-    const int r0 = c0 + k * kQC;
+    const int r0 = c0 + (nchunks - 1 - k) * kQC;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
