@@ -62,8 +62,23 @@ void launch_jacobi_round_split(const GateDesc*, int, int, cplx*, const int*, int
                                int, cudaStream_t);
 // Cross-only pair EVDs (evd.cuh) in a sweep whose predecessor measured an rms
 // relative off-norm above this (the pre-asymptotic phase); MPSIM_CROSS=0 disables.
-constexpr double kCrossRms = 0.35;
-constexpr int kCrossSweeps = 4;  // cross-only EVDs in sweeps 1 .. kCrossSweeps - 1 at most
+constexpr double kCrossRmsDefault = 0.35;
+constexpr int kCrossSweepsDefault = 4;  // cross-only EVDs in sweeps 1 .. kCrossSweeps - 1 at most
+// (MPSIM_CROSS_RMS / MPSIM_CROSS_SWEEPS override both, A/B only)
+static double cross_rms() {
+  static const double v = [] {
+    const char* e = std::getenv("MPSIM_CROSS_RMS");
+    return e ? std::atof(e) : kCrossRmsDefault;
+  }();
+  return v;
+}
+static int cross_sweeps() {
+  static const int v = [] {
+    const char* e = std::getenv("MPSIM_CROSS_SWEEPS");
+    return e ? std::atoi(e) : kCrossSweepsDefault;
+  }();
+  return v;
+}
 // Stored in-block Grams while the previous sweep's largest relative
 // off-diagonal exceeds this; MPSIM_INBLOCK=0 disables.
 constexpr double kInblockMaxoff = 1e-4;
@@ -554,7 +569,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // de Rijk reordering keeps reshuffling the blocks; with few blocks two
       // nearly parallel vectors could share a block for good and a cross-only
       // EVD would never rotate them — measured on a SWAP-routed 32 x 32 theta)
-      if (h_rot[i] && cross_policy() && rms > kCrossRms && h_maxoff[i] > 1e-3 && sweep < kCrossSweeps &&
+      if (h_rot[i] && cross_policy() && rms > cross_rms() && h_maxoff[i] > 1e-3 && sweep < cross_sweeps() &&
           descs[i].nb >= 8)
         h_rot[i] |= 2;
       // pre-asymptotic and early asymptotic sweeps reuse the in-block Grams the
