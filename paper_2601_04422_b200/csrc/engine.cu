@@ -48,6 +48,7 @@ void launch_qr_apply(const GateDesc*, int, int, int, cplx*, const cplx*, long lo
 // QR preconditioning (qr_pre.cu) of gates whose SVD operand has at least
 // kQrMinN vectors: MPSIM_QR=2 (default) two QR steps, 1 one, 0 none.
 constexpr int kQrMinN = 128;
+constexpr int kMaxSvdN = 2048;  // derijk_kernel / truncate_kernel: one 1024-thread CTA, 2048 keys
 static int qr_policy() {
   static const int v = [] {
     const char* e = std::getenv("MPSIM_QR");
@@ -383,6 +384,10 @@ static GateDesc phase_desc(const GateDesc& d, int phase) {
 void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs,
                               const cplx* src, long long src_ld) {
   const int ng = (int)descs.size();
+  for (const GateDesc& d : descs)
+    if (d.n_pad > kMaxSvdN)  // de Rijk / truncation sort one gate's vectors in one CTA
+      fail(MPSIM_EINVAL, "SVD operand with " + std::to_string(d.n) + " vectors (min dimension) exceeds the " +
+                             std::to_string(kMaxSvdN) + " this build supports (bond dimension <= 1024)");
   long long ws_elems = 0;
   int max_tiles = 1, max_nb = 2, max_m = 1, max_n = 1;
   int max_n0 = 1, qr_n_pad = 0, qr_m_pad = 0, qr_jm_pad = 0, max_out_m = 1;
