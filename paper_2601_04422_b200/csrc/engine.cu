@@ -29,7 +29,7 @@ void launch_theta(const GateDesc*, int, int, const cplx*, long long, int, cplx*,
 int theta_tiles(int dl, int dr);
 void jacobi_split_init();
 void launch_jacobi_sweep(const GateDesc*, int, int, cplx*, const int*, int*, double, double, const double*, double,
-                         const int*, long long, double*, int*, cplx*, cplx*, double*, cplx*, int*, cudaStream_t);
+                         const int*, long long, double*, int*, cplx*, cplx*, double*, cplx*, int*, int, cudaStream_t);
 // One persistent launch per sweep (jacobi_split.cu); MPSIM_SWEEP=rounds selects
 // one launch per tournament round.
 static bool sweep_policy() {
@@ -501,13 +501,14 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     // outer iteration needs the same number of sweeps as with a fully
     // converged inner EVD (measured in emulation and on the B200), at a
     // fraction of the cost. Final orthogonality is at the tol level.
-    const bool persistent = jacobi_mode() == 4 && !phase_probe() && sweep_policy();
+    // (phase probes 1-2 run per round; probe 4, the visit without its EVD, runs persistent)
+    const bool persistent = jacobi_mode() == 4 && (!phase_probe() || phase_probe() == 4) && sweep_policy();
     if (persistent) {
       s.d_sweepctl.ensure(sizeof(int) * (1 + (size_t)ng * max_nb));
       launch_jacobi_sweep(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, 4.0 * kEps, 2.0 * kEps,
                           (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p, perm_stride,
                           (double*)s.d_maxoff.p, (int*)s.d_need.p, (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p,
-                          (double*)s.d_offsum.p, (cplx*)s.d_gblk.p, (int*)s.d_sweepctl.p, st);
+                          (double*)s.d_offsum.p, (cplx*)s.d_gblk.p, (int*)s.d_sweepctl.p, phase_probe(), st);
       s.launches += 1;
       ++s.jacobi_launches;
     }

@@ -350,7 +350,13 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
   if (probe == 1) return;  // profiling (MPSIM_PHASE_PROBE): Gram only
   if constexpr (kFuseEvd) {
     cplx* R = reinterpret_cast<cplx*>(S.u.buf);
-    pair_evd_v1(SG, R, S.sc, t, tol_in, floor2, 1, (active[gi] & 2) != 0);
+    if (probe == 4) {  // profiling: the visit without its EVD (R = I)
+      for (int idx = t; idx < kP * kP; idx += 256)
+        R[(idx / kP) * kPad + idx % kP] = make_double2(idx / kP == idx % kP ? 1.0 : 0.0, 0.0);
+      __syncthreads();
+    } else {
+      pair_evd_v1(SG, R, S.sc, t, tol_in, floor2, 1, (active[gi] & 2) != 0);
+    }
     if (probe == 2) return;  // Gram + EVD
     __syncthreads();
     store_inblock();
@@ -557,7 +563,7 @@ void launch_jacobi_round_split(const GateDesc* d_gates, int n_gates, int max_pai
 void launch_jacobi_sweep(const GateDesc* d_gates, int n_gates, int max_pairs, cplx* ws, const int* d_active,
                          int* d_rotated, double tol, double tol_in, const double* frob2, double floor_rel2,
                          const int* perm, long long perm_stride, double* maxoff, int* need, cplx* gbuf, cplx* rbuf,
-                         double* offsum, cplx* gblk, int* ctl, cudaStream_t st) {
+                         double* offsum, cplx* gblk, int* ctl, int probe, cudaStream_t st) {
   static int ctas = 0;
   if (ctas == 0) {
     int dev = 0, sms = 148, per_sm = 1;
@@ -568,7 +574,7 @@ void launch_jacobi_sweep(const GateDesc* d_gates, int n_gates, int max_pairs, cp
   }
   cudaMemsetAsync(ctl, 0, sizeof(int) * (1 + (size_t)n_gates * 2 * max_pairs), st);
   const RoundArgs a = make_args(d_gates, ws, d_active, d_rotated, tol, tol_in, frob2, floor_rel2, perm, perm_stride,
-                                maxoff, need, gbuf, rbuf, offsum, max_pairs, gblk, 0);
+                                maxoff, need, gbuf, rbuf, offsum, max_pairs, gblk, probe);
   jacobi_sweep_kernel<<<ctas, 256, sizeof(PairSmem), st>>>(a, n_gates, 2 * max_pairs - 1, ctl);
 }
 
