@@ -233,50 +233,10 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
   const bool approx = kFuseEvd && (active[gi] & 4) && round > 0;
   cplx* const gblk_a = gblk + ((long long)gi * 2 * max_pairs + c.ba) * (kW * kW);
   cplx* const gblk_b = gblk + ((long long)gi * 2 * max_pairs + c.bb) * (kW * kW);
-  // tiles of G_ext = [[A, B], [B^T, D]]: upper A and D, all of B (Re G = A + D, Im G = B - B^T)
-  int trow[5], tcol[5], nt;
-  if (approx) {
-    // cross block: rows Re_a / Im_a (tiles 0, 1, 4, 5), cols Re_b / Im_b (2, 3, 6, 7)
-    const int r = warp >> 1, c = 2 * (warp & 1);
-    nt = 2;
-    trow[0] = trow[1] = r + (r >= 2 ? 2 : 0);
-    tcol[0] = c + (c >= 2 ? 4 : 2);
-    tcol[1] = tcol[0] + 1;
-    trow[2] = trow[3] = trow[4] = tcol[2] = tcol[3] = tcol[4] = 0;
-  } else if (warp < 4) {
-    nt = 4;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      trow[i] = warp;
-      tcol[i] = 4 + i;
-    }
-    trow[4] = tcol[4] = 0;
-  } else {
-    const int r = warp - 4, na = 4 - r;
-#pragma unroll
-    for (int i = 0; i < 5; ++i) {
-      if (i < na) {
-        trow[i] = r;
-        tcol[i] = r + i;
-      } else {
-        trow[i] = 4 + (3 - r);
-        tcol[i] = 4 + (3 - r) + (i - na);
-      }
-    }
-    nt = 5;
-  }
   // column offsets (plane + index) of this thread's fragments
   auto coff = [&](int col) { return (col < kP ? 0 : kChunkPlane) + (col & (kP - 1)) * kPitchS; };
-  const int oa0 = coff(8 * trow[0] + fr), oa4 = coff(8 * trow[4] + fr);
-  int ob[5];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) ob[i] = coff(8 * tcol[i] + fr);
-  double acc[5][2];
-#pragma unroll
-  for (int i = 0; i < 5; ++i) acc[i][0] = acc[i][1] = 0.0;
   const int nchunks = g.m_pad / kC;
-  ld.issue(S.u.buf[0], 0);
-  for (int k = 0; k < nchunks; ++k) {
+  auto next_chunk = [&](int k) {  // stage k's data ready in shared memory
     if (k + 1 < nchunks) {
       ld.issue(S.u.buf[(k + 1) & 1], (k + 1) * kC);
       cp_async_wait<1>();
@@ -284,23 +244,102 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* B = S.u.buf[k & 1];
+  };
+  ld.issue(S.u.buf[0], 0);
+  if (approx) {
+    // the 16 cross tiles (rows Re_a / Im_a = tiles 0,1 / 4,5; cols Re_b / Im_b =
+    // 2,3 / 6,7) as four 2x2 blocks, warp & 3 picks the block and warp >> 2
+    // the half of each chunk's k-steps: two A and two B loads feed four DMMAs
+    const int q = warp & 3, kh = warp >> 2;
+    const int tr0 = (q >> 1) ? 4 : 0, tc0 = (q & 1) ? 6 : 2;
+    const int oa0 = coff(8 * tr0 + fr), oa1 = coff(8 * (tr0 + 1) + fr);
+    const int ob0 = coff(8 * tc0 + fr), ob1 = coff(8 * (tc0 + 1) + fr);
+    double acc[2][2][2];
 #pragma unroll
-    for (int ks = 0; ks < kC / 4; ++ks) {
-      const int row = 4 * ks + fk;
-      const double a_first = B[row + oa0], a_last = B[row + oa4];
+    for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int i = 0; i < 5; ++i)
-        if (i < nt) dmma_s(acc[i][0], acc[i][1], trow[i] == trow[0] ? a_first : a_last, B[row + ob[i]]);
+      for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int k = 0; k < nchunks; ++k) {
+      next_chunk(k);
+      const double* B = S.u.buf[k & 1];
+#pragma unroll
+      for (int ks = 0; ks < kC / 8; ++ks) {
+        const int row = 4 * (ks + (kC / 8) * kh) + fk;
+        const double a0 = B[row + oa0], a1 = B[row + oa1], b0 = B[row + ob0], b1 = B[row + ob1];
+        dmma_s(acc[0][0][0], acc[0][0][1], a0, b0);
+        dmma_s(acc[0][1][0], acc[0][1][1], a0, b1);
+        dmma_s(acc[1][0][0], acc[1][0][1], a1, b0);
+        dmma_s(acc[1][1][0], acc[1][1][1], a1, b1);
+      }
+      __syncthreads();
     }
+    for (int h = 0; h < 2; ++h) {  // the two k-halves into Gx
+      if (kh == h)
+#pragma unroll
+        for (int a = 0; a < 2; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              double& gx = S.u.Gx[(8 * (tr0 + a) + fr) * 65 + 8 * (tc0 + b) + fk * 2 + v];
+              gx = h == 0 ? acc[a][b][v] : gx + acc[a][b][v];
+            }
+      __syncthreads();
+    }
+  } else {
+    // tiles of G_ext = [[A, B], [B^T, D]]: upper A and D, all of B (Re G = A + D,
+    // Im G = B - B^T); warps 0-3: tile row w of B (4 tiles), warps 4-7: tile row
+    // r of A and 3 - r of D (5 tiles)
+    int trow[5], tcol[5], nt;
+    if (warp < 4) {
+      nt = 4;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        trow[i] = warp;
+        tcol[i] = 4 + i;
+      }
+      trow[4] = tcol[4] = 0;
+    } else {
+      const int r = warp - 4, na = 4 - r;
+#pragma unroll
+      for (int i = 0; i < 5; ++i) {
+        if (i < na) {
+          trow[i] = r;
+          tcol[i] = r + i;
+        } else {
+          trow[i] = 4 + (3 - r);
+          tcol[i] = 4 + (3 - r) + (i - na);
+        }
+      }
+      nt = 5;
+    }
+    const int oa0 = coff(8 * trow[0] + fr), oa4 = coff(8 * trow[4] + fr);
+    int ob[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) ob[i] = coff(8 * tcol[i] + fr);
+    double acc[5][2];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int k = 0; k < nchunks; ++k) {
+      next_chunk(k);
+      const double* B = S.u.buf[k & 1];
+#pragma unroll
+      for (int ks = 0; ks < kC / 4; ++ks) {
+        const int row = 4 * ks + fk;
+        const double a_first = B[row + oa0], a_last = B[row + oa4];
+#pragma unroll
+        for (int i = 0; i < 5; ++i)
+          if (i < nt) dmma_s(acc[i][0], acc[i][1], trow[i] == trow[0] ? a_first : a_last, B[row + ob[i]]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 5; ++i)
+      if (i < nt)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) S.u.Gx[(8 * trow[i] + fr) * 65 + 8 * tcol[i] + fk * 2 + v] = acc[i][v];
     __syncthreads();
   }
-#pragma unroll
-  for (int i = 0; i < 5; ++i)
-    if (i < nt)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) S.u.Gx[(8 * trow[i] + fr) * 65 + 8 * tcol[i] + fk * 2 + v] = acc[i][v];
-  __syncthreads();
   if (approx) {
     const double* Gx = S.u.Gx;
     const int i = t >> 4, j = kW + (t & 15);
