@@ -165,8 +165,9 @@ int mpsim_gpu_sampler_clear_cache(mpsim_gpu_sampler* sp);
 /* Kernel launches and device time accumulated on the state's stream since
  * the last reset (bench.py's gpu_launches / roofline legs). */
 int mpsim_gpu_counters(const mpsim_gpu_state* s, int64_t* launches, double* device_ms, int64_t* svd_sweeps);
-/* The dominant kernel's share: jacobi_round_kernel launches and their
- * CUDA-event time, and the algorithmic flops of the work done (SURVEY 8(d):
+/* The dominant kernel's share: Jacobi sweep launches (one persistent launch
+ * per sweep) and their CUDA-event time, and the algorithmic flops of the work
+ * done (SURVEY 8(d):
  * svd = 32 M N^2 per decomposed theta, gate = full F_2q per applied gate). */
 int mpsim_gpu_kernel_counters(const mpsim_gpu_state* s, int64_t* jacobi_launches, double* jacobi_ms,
                               double* svd_flops, double* gate_flops);

@@ -524,10 +524,10 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       }
       ++s.launches;
       ++s.jacobi_launches;
-      if (sync_debug()) check_launch("jacobi_round_kernel");
+      if (sync_debug()) check_launch("jacobi round");
     }
     CK(cudaEventRecord(s.evj1, st));
-    check_launch("jacobi_round_kernel");
+    check_launch("jacobi sweep");
     ++s.sweeps;
     CK(cudaMemcpyAsync(h_rot, s.d_rot.p, sizeof(int) * ng, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_maxoff, s.d_maxoff.p, sizeof(double) * ng, cudaMemcpyDeviceToHost, st));

@@ -62,7 +62,7 @@ struct State {
   long long launches = 0;
   double device_ms = 0.0;
   long long sweeps = 0;
-  long long jacobi_launches = 0;  // jacobi_round_kernel launches
+  long long jacobi_launches = 0;  // Jacobi sweep (or round) launches
   double jacobi_ms = 0.0;         // CUDA-event time of those launches
   double svd_flops = 0.0;         // algorithmic SVD flops of the decomposed matrices (32 M N^2)
   double gate_flops = 0.0;        // algorithmic F_2q of applied gates
