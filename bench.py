@@ -29,6 +29,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "two-qubit gates/sec (contract+SVD+truncate) at chi=512; circuit wall-time"
+
+
+def metric_name(chi):
+    """BASELINE.json's metric (chi=512); other --chi values name their own chi."""
+    return METRIC if chi == 512 else METRIC.replace("chi=512", f"chi={chi}")
 UNIT = "gates/s"
 
 
@@ -175,7 +180,7 @@ def run_reference(args, rank, world):
     total = sum(per)
     value = args.steps * sample_gates / total
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "impl": "reference", "metric": metric_name(args.chi), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "complex128",
         "data": "synthetic",
@@ -268,7 +273,7 @@ def main():
     jac_ms = c["jacobi_ms"]
     achieved = c["svd_flops"] / (jac_ms / 1e3) / 1e12 if jac_ms > 0 else 0.0
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": metric_name(args.chi), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dev_total / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
         "config": config_block(args),
