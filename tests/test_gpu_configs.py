@@ -75,10 +75,11 @@ def test_c3_brickwork_with_nonadjacent_gates(gpu, oracle):
     assert rg["svd_count"].max() >= 3
     assert (g.bond_dims() == o.bond_dims()).all()
     assert rg["peak_bond"] == ro["peak_bond"] == chi
-    # CX gates leave exactly rank-deficient thetas: weights at the rounding-noise
-    # level (~1e-30 from LAPACK) are exact zeros here (sigma^2 <= (64 eps)^2
-    # ||theta||^2 snaps to 0, P1); compare the weights above that level
-    floor = 1e-20
+    # CX gates leave exactly rank-deficient thetas: discarded weights at the
+    # rounding-noise level (~1e-30 from LAPACK, 0 or ~1e-25 here: sigma^2 <=
+    # (64 eps)^2 ||theta||^2 snaps to 0, P1) carry no information;
+    # compare the weights above 1e-16 (the cutoff is 1e-12)
+    floor = 1e-16
     nz = ro["gate_w"] > floor
     assert nz.sum() > 0  # the cap truncates
     assert np.max(np.abs(rg["gate_w"][nz] - ro["gate_w"][nz]) / ro["gate_w"][nz]) <= 1e-10
