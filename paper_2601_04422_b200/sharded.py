@@ -25,13 +25,28 @@ from . import native as N
 from .mps import MpsState, execute
 
 
-def shard_bounds(n: int, world: int):
-    """Even-aligned contiguous ranges [b_r, b_{r+1})."""
+def shard_bounds(n: int, world: int, chi: int | None = None):
+    """Even-aligned contiguous ranges [b_r, b_{r+1}). With a bond cap `chi`
+    the cut points split the steady-state gate cost (the theta merge and SVD of
+    the gate on (q, q+1) scale as D_q D_{q+1} D_{q+2}, bonds min(chi, 2^q,
+    2^(n-q))) into equal parts, so the cheap edge gates do not leave the edge
+    shards idle; without it the sites are split evenly."""
+    if chi is None or world == 1:
+        cum = [float(q) for q in range(n + 1)]
+    else:
+        bond = [min(chi, 2 ** min(q, n - q, 60)) for q in range(n + 1)]
+        cost = [float(bond[q] * bond[q + 1] * bond[min(q + 2, n)]) for q in range(n)]
+        cum = [0.0]
+        for c in cost:
+            cum.append(cum[-1] + c)
     b = [0]
     for r in range(1, world):
-        x = int(round(r * n / world))
+        target = r * cum[-1] / world
+        x = min(range(n + 1), key=lambda q: abs(cum[q] - target))
         x -= x % 2
-        b.append(max(b[-1] + 2, x))
+        x = max(b[-1] + 2, x)
+        x = min(x, n - 2 * (world - r))  # leave room for the remaining shards
+        b.append(x)
     b.append(n)
     return b
 
@@ -71,7 +86,7 @@ class _CudaArray:
 class ShardedChain:
     def __init__(self, n, chi, rank=0, world=1, device=0, dist=None):
         self.n, self.chi, self.rank, self.world, self.dist = n, chi, rank, world, dist
-        b = shard_bounds(n, world)
+        b = shard_bounds(n, world, chi)
         self.lo, self.hi = b[rank], b[rank + 1]
         self.has_right = rank < world - 1
         self.n_local = self.hi - self.lo + (1 if self.has_right else 0)

@@ -24,9 +24,24 @@ def test_bounds_even_and_covering(n, world):
     assert all(b[i + 1] - b[i] >= 2 for i in range(world))
 
 
+@pytest.mark.parametrize("n,world,chi", [(256, 4, 512), (256, 8, 512), (64, 4, 128), (20, 2, 16)])
+def test_cost_weighted_bounds_balance(n, world, chi):
+    b = shard_bounds(n, world, chi)
+    assert b[0] == 0 and b[-1] == n and all(x % 2 == 0 for x in b[:-1])
+    assert all(b[i + 1] - b[i] >= 2 for i in range(world))
+    bond = [min(chi, 2 ** min(q, n - q)) for q in range(n + 1)]
+    cost = [bond[q] * bond[q + 1] * bond[min(q + 2, n)] for q in range(n)]
+    shard = [sum(cost[b[r]:b[r + 1]]) for r in range(world)]
+    even = shard_bounds(n, world)
+    shard_even = [sum(cost[even[r]:even[r + 1]]) for r in range(world)]
+    # never worse than the even split, within ~12 % of perfect balance
+    assert max(shard) <= max(shard_even) + 1e-9
+    assert max(shard) <= 1.12 * sum(cost) / world
+
+
 @pytest.mark.parametrize("n,world", [(16, 2), (64, 4), (256, 8)])
 def test_every_gate_applied_once(n, world):
-    b = shard_bounds(n, world)
+    b = shard_bounds(n, world, 512 if n >= 64 else None)
     for parity in (0, 1):
         gates = _layer(n, parity)
         seen = []
