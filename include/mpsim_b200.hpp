@@ -3,7 +3,8 @@
 // mpsim/{tensor,mps,gate_apply,executor,sampler,errors}.hpp). A caller of the
 // reference switches the include path and links libmpsim_gpu.so; names,
 // argument meaning and exception types are kept:
-//   std::invalid_argument  <- MPSIM_EINVAL
+//   std::invalid_argument  <- MPSIM_EINVAL (mpsim::ConfigError from the front end)
+//   mpsim::ParseError      <- MPSIM_EPARSE (line / column kept)
 //   mpsim::NumericError    <- MPSIM_ENUMERIC
 //   std::logic_error       <- MPSIM_ELOGIC
 //   std::runtime_error     <- MPSIM_ECUDA
@@ -36,9 +37,29 @@ class NumericError : public std::runtime_error {  // errors.hpp:45-48
   using std::runtime_error::runtime_error;
 };
 
+class ParseError : public std::runtime_error {  // errors.hpp:22-37
+ public:
+  ParseError(int line, int column, const std::string& what) : std::runtime_error(what), line_(line), column_(column) {}
+  int line() const { return line_; }
+  int column() const { return column_; }
+
+ private:
+  int line_, column_;
+};
+
+class ConfigError : public std::runtime_error {  // errors.hpp:39-43
+ public:
+  using std::runtime_error::runtime_error;
+};
+
 namespace detail {
 inline void check(int rc) {
   if (rc == MPSIM_OK) return;
+  if (rc == MPSIM_EPARSE) {
+    int32_t line = 0, col = 0;
+    mpsim_last_parse_location(&line, &col);
+    throw ParseError(line, col, mpsim_gpu_last_error());
+  }
   const std::string msg = mpsim_gpu_last_error();
   switch (rc) {
     case MPSIM_EINVAL: throw std::invalid_argument(msg);
@@ -46,6 +67,11 @@ inline void check(int rc) {
     case MPSIM_ELOGIC: throw std::logic_error(msg);
     default: throw std::runtime_error(msg);
   }
+}
+// The front end's input errors are ConfigError (runner.cpp:42-62, :141-190).
+inline void check_config(int rc) {
+  if (rc == MPSIM_EINVAL) throw ConfigError(mpsim_gpu_last_error());
+  check(rc);
 }
 }  // namespace detail
 
@@ -335,6 +361,144 @@ class Sampler {  // sampler.hpp:50-86
 inline ShotResult sample(const MpsState& s, std::uint64_t shots, std::uint64_t seed, SamplerOptions o = {}) {
   Sampler sp(s, o);
   return sp.sample(shots, seed);
+}
+
+// ---- host front end (circuit.hpp, runner.hpp, generators.hpp) -------------
+// Differences, by design: parse_qasm + fuse_circuit are one call (fuse_qasm)
+// over the library's own parser; run_circuit returns the JSON record text of
+// run_output_to_json (docs/run_output.schema.json) instead of a RunOutput
+// struct plus nlohmann::json.
+
+// parse_qasm + inject_sidecar + fuse_circuit (qasm_parser.cpp, runner.cpp:168-190, fusion.cpp:79-135)
+inline std::vector<FusedGate> fuse_qasm(const std::string& qasm, const std::string& sidecar_json = {},
+                                        int* n_qubits = nullptr) {
+  int32_t n = 0, count = 0;
+  mpsim_gate* g = nullptr;
+  int32_t* fl = nullptr;
+  detail::check_config(mpsim_fuse_qasm(qasm.c_str(), sidecar_json.empty() ? nullptr : sidecar_json.c_str(), &n, &g,
+                                       &fl, &count));
+  std::vector<FusedGate> out(static_cast<size_t>(count));
+  for (int32_t i = 0; i < count; ++i) {
+    FusedGate& f = out[static_cast<size_t>(i)];
+    f.q0 = g[i].q0;
+    f.q1 = g[i].q1;
+    f.flipped = fl[i] != 0;
+    const Index dim = f.q1 >= 0 ? 4 : 2;
+    std::vector<Complex> m(static_cast<size_t>(dim * dim));
+    for (Index e = 0; e < dim * dim; ++e) m[static_cast<size_t>(e)] = Complex(g[i].u[2 * e], g[i].u[2 * e + 1]);
+    f.matrix = CTensor({dim, dim}, std::move(m));
+  }
+  mpsim_free(g);
+  mpsim_free(fl);
+  if (n_qubits) *n_qubits = n;
+  return out;
+}
+
+// layerize(decompose_nonlocal(gates, n)) (fusion.cpp:137-190)
+inline LayerPlan plan_layers(const std::vector<FusedGate>& gates, int n_qubits) {
+  const auto abi = to_abi(gates);
+  mpsim_gate* g = nullptr;
+  int32_t* lo = nullptr;
+  int32_t count = 0, nl = 0;
+  detail::check(mpsim_plan_layers(abi.data(), static_cast<int32_t>(abi.size()), n_qubits, &g, &lo, &count, &nl));
+  LayerPlan plan;
+  plan.layers.resize(static_cast<size_t>(nl));
+  for (int32_t i = 0; i < count; ++i) {
+    FusedGate f;
+    f.q0 = g[i].q0;
+    f.q1 = g[i].q1;
+    const Index dim = f.q1 >= 0 ? 4 : 2;
+    std::vector<Complex> m(static_cast<size_t>(dim * dim));
+    for (Index e = 0; e < dim * dim; ++e) m[static_cast<size_t>(e)] = Complex(g[i].u[2 * e], g[i].u[2 * e + 1]);
+    f.matrix = CTensor({dim, dim}, std::move(m));
+    plan.layers[static_cast<size_t>(lo[i])].push_back(std::move(f));
+  }
+  mpsim_free(g);
+  mpsim_free(lo);
+  return plan;
+}
+
+namespace detail {
+inline std::string take(char* p) {
+  std::string s = p ? p : "";
+  mpsim_free(p);
+  return s;
+}
+}  // namespace detail
+
+inline std::string ghz_qasm(int n_qubits, bool measure = false) {  // generators.cpp:52-71
+  char* q = nullptr;
+  detail::check_config(mpsim_gen_ghz_qasm(n_qubits, measure ? 1 : 0, &q));
+  return detail::take(q);
+}
+
+enum class Entangler { Cx, Haar };  // generators.hpp:40
+struct BrickworkOptions {           // generators.hpp:42-48
+  int n_qubits = 0;
+  int depth = 0;
+  std::uint64_t seed = 1;
+  bool measure = false;
+  Entangler entangler = Entangler::Cx;
+};
+struct GeneratedCircuit {  // generators.hpp:59-62 (sidecar as u4-sidecar-v1 JSON text; empty for cx)
+  std::string qasm;
+  std::string sidecar_json;
+};
+inline GeneratedCircuit brickwork_qasm(const BrickworkOptions& o) {  // generators.cpp:95-145
+  char *q = nullptr, *sc = nullptr;
+  detail::check_config(mpsim_gen_brickwork_qasm(o.n_qubits, o.depth, o.seed, o.measure ? 1 : 0,
+                                                o.entangler == Entangler::Haar ? 1 : 0, &q, &sc));
+  return GeneratedCircuit{detail::take(q), detail::take(sc)};
+}
+
+enum class Backend { MpsSerial, MpsParallel, Statevector };  // runner.hpp:38
+
+struct RunConfig {  // runner.hpp:46-62
+  std::string qasm_path, qasm_text, sidecar_path, sidecar_json, input_label;
+  Backend backend = Backend::MpsSerial;
+  NonlocalMethod nonlocal = NonlocalMethod::Swap;
+  Index max_bond = 0;  // 0 = unbounded
+  double cutoff = 0.0;
+  std::uint64_t shots = 0, seed = 1;
+  int workers = 1;
+  bool memoize = true;
+  std::size_t cache_cap = 0;
+  int statevector_cap = 20;
+  int device = 0;
+};
+
+// run_circuit + run_output_to_json (runner.cpp:219-328): the JSON record text
+inline std::string run_circuit_json(const RunConfig& c) {
+  mpsim_run_config k;
+  mpsim_run_config_defaults(&k);
+  auto cs = [](const std::string& s) { return s.empty() ? nullptr : s.c_str(); };
+  k.qasm_path = cs(c.qasm_path);
+  k.qasm_text = cs(c.qasm_text);
+  k.sidecar_path = cs(c.sidecar_path);
+  k.sidecar_json = cs(c.sidecar_json);
+  k.input_label = cs(c.input_label);
+  k.backend = static_cast<int32_t>(c.backend);
+  k.nonlocal = c.nonlocal == NonlocalMethod::Swap ? MPSIM_NONLOCAL_SWAP : MPSIM_NONLOCAL_BONDPROP;
+  k.max_bond = c.max_bond;
+  k.cutoff = c.cutoff;
+  k.shots = c.shots;
+  k.seed = c.seed;
+  k.workers = c.workers;
+  k.memoize = c.memoize ? 1 : 0;
+  k.cache_cap = c.cache_cap;
+  k.statevector_cap = c.statevector_cap;
+  k.device = c.device;
+  char* json = nullptr;
+  detail::check_config(mpsim_gpu_run_circuit(&k, &json));
+  return detail::take(json);
+}
+
+// exit_code_for_error (runner.cpp:330-341)
+inline int exit_code_for_error(const std::exception& e) {
+  if (dynamic_cast<const ParseError*>(&e)) return 2;
+  if (dynamic_cast<const ConfigError*>(&e)) return 1;
+  if (dynamic_cast<const NumericError*>(&e)) return 3;
+  return 1;
 }
 
 }  // namespace mpsim

@@ -10,7 +10,8 @@
  *
  * Status codes (the reference's C++ exceptions, mapped like
  * exit_code_for_error, runner.cpp:330-341):
- *   MPSIM_OK 0, MPSIM_EINVAL 1 (std::invalid_argument), MPSIM_ENUMERIC 3
+ *   MPSIM_OK 0, MPSIM_EINVAL 1 (std::invalid_argument / ConfigError),
+ *   MPSIM_EPARSE 2 (ParseError, front end only), MPSIM_ENUMERIC 3
  *   (mpsim::NumericError), MPSIM_ELOGIC 4 (std::logic_error), MPSIM_ECUDA 5
  *   (device/runtime failure). mpsim_gpu_last_error() returns the message of
  *   the calling thread's last failure.
@@ -31,6 +32,7 @@ extern "C" {
 
 #define MPSIM_OK 0
 #define MPSIM_EINVAL 1
+#define MPSIM_EPARSE 2 /* mpsim::ParseError, errors.hpp:22-37 */
 #define MPSIM_ENUMERIC 3
 #define MPSIM_ELOGIC 4
 #define MPSIM_ECUDA 5
@@ -176,6 +178,94 @@ int mpsim_gpu_kernel_counters(const mpsim_gpu_state* s, int64_t* jacobi_launches
 int mpsim_gpu_transfer_counters(const mpsim_gpu_state* s, int64_t* h2d_bytes, int64_t* d2h_bytes);
 int mpsim_gpu_reset_counters(mpsim_gpu_state* s);
 int mpsim_gpu_synchronize(mpsim_gpu_state* s);
+
+/* ---- host front end --------------------------------------
+ * OpenQASM 2.0 subset parser (qasm_parser.cpp), u4 sidecar (runner.cpp:
+ * 129-190), fusion / SWAP lowering / layering (fusion.cpp:79-190), circuit
+ * generators (generators.cpp:52-145) and the run pipeline with its JSON
+ * record (runner.cpp:219-328, docs/run_output.schema.json). Parse, fuse,
+ * plan and generate are host-only (no device touched). Errors map like
+ * exit_code_for_error (runner.cpp:330-341): ConfigError -> MPSIM_EINVAL,
+ * ParseError -> MPSIM_EPARSE (location via mpsim_last_parse_location),
+ * NumericError -> MPSIM_ENUMERIC. Library-allocated outputs are released
+ * with mpsim_free. */
+
+/* GateKind, circuit.hpp:33-38 (same order) */
+enum {
+  MPSIM_GATE_H = 0, MPSIM_GATE_X, MPSIM_GATE_Y, MPSIM_GATE_Z, MPSIM_GATE_S, MPSIM_GATE_SDG, MPSIM_GATE_T,
+  MPSIM_GATE_TDG, MPSIM_GATE_RX, MPSIM_GATE_RY, MPSIM_GATE_RZ, MPSIM_GATE_U1, MPSIM_GATE_U2, MPSIM_GATE_U3,
+  MPSIM_GATE_CX, MPSIM_GATE_CZ, MPSIM_GATE_SWAP, MPSIM_GATE_U4
+};
+
+/* PrimOp, circuit.hpp:48-56 (q1 = -1 for one-qubit ops; U4 matrices are not echoed). */
+typedef struct {
+  int32_t kind;
+  int32_t q0;
+  int32_t q1;
+  int32_t nparams;
+  double params[3];
+} mpsim_prim_op;
+
+/* Circuit, circuit.hpp:58-63 */
+typedef struct {
+  int32_t n_qubits;
+  int32_t n_clbits;
+  int32_t has_measure_all;
+  int32_t n_ops;
+} mpsim_circuit_info;
+
+void mpsim_free(void* p);
+/* parse_qasm (circuit.hpp:108-110, qasm_parser.cpp): ops (nullable) receives
+ * the first max_ops ops. */
+int mpsim_parse_qasm(const char* text, mpsim_circuit_info* info, mpsim_prim_op* ops, int32_t max_ops);
+/* ParseError::line() / column() of the calling thread's last MPSIM_EPARSE. */
+int mpsim_last_parse_location(int32_t* line, int32_t* column);
+/* parse_qasm + inject_sidecar (runner.cpp:165-190; sidecar_json nullable,
+ * u4-sidecar-v1 text) + fuse_circuit (fusion.cpp:79-135). Fused two-qubit
+ * gates have q0 < q1 and the matrix in the (q0, q1) basis; flipped[i]
+ * (FusedGate::flipped) records a (high, low) origin. */
+int mpsim_fuse_qasm(const char* qasm, const char* sidecar_json, int32_t* n_qubits, mpsim_gate** gates,
+                    int32_t** flipped, int32_t* count);
+/* decompose_nonlocal + layerize (fusion.cpp:137-190): the lowered local
+ * gates in layer order; layer_of[i] = layer of out[i]. */
+int mpsim_plan_layers(const mpsim_gate* gates, int32_t count, int32_t n_qubits, mpsim_gate** out,
+                      int32_t** layer_of, int32_t* out_count, int32_t* n_layers);
+/* ghz_qasm / brickwork_qasm (generators.cpp:52-145); haar != 0 draws
+ * seeded Haar 4x4 entanglers into *sidecar_json (u4-sidecar-v1), else the
+ * entangler is cx and *sidecar_json is NULL. */
+int mpsim_gen_ghz_qasm(int32_t n, int32_t measure, char** qasm);
+int mpsim_gen_brickwork_qasm(int32_t n, int32_t depth, uint64_t seed, int32_t measure, int32_t haar, char** qasm,
+                             char** sidecar_json);
+
+/* Backend, runner.hpp:38 */
+#define MPSIM_BACKEND_MPS_SERIAL 0
+#define MPSIM_BACKEND_MPS_PARALLEL 1
+#define MPSIM_BACKEND_STATEVECTOR 2
+
+/* RunConfig, runner.hpp:46-62 (+ device / chi_hint for the GPU state). */
+typedef struct {
+  const char* qasm_path;    /* read from file when non-empty */
+  const char* qasm_text;    /* used when qasm_path is empty */
+  const char* sidecar_path; /* explicit sidecar file; else <qasm_path>.u4.json when present */
+  const char* sidecar_json; /* inline sidecar text (instead of a file) */
+  const char* input_label;  /* echoed as config.input */
+  int32_t backend;
+  int32_t nonlocal;         /* MPSIM_NONLOCAL_* */
+  int64_t max_bond;         /* 0 = unbounded */
+  double cutoff;
+  uint64_t shots;
+  uint64_t seed;
+  int32_t workers;
+  int32_t memoize;
+  uint64_t cache_cap;
+  int32_t statevector_cap;
+  int32_t device;
+  int64_t chi_hint;
+} mpsim_run_config;
+void mpsim_run_config_defaults(mpsim_run_config* c);
+/* run_circuit + run_output_to_json (runner.cpp:219-328): *json = the result
+ * record (docs/run_output.schema.json), keys sorted like nlohmann::json. */
+int mpsim_gpu_run_circuit(const mpsim_run_config* c, char** json);
 
 #ifdef __cplusplus
 }

@@ -6,3 +6,5 @@ reference simulator API used by the tests and the benchmark.
 """
 from .native import NumericError, LogicError, DeviceError, UNBOUNDED  # noqa: F401
 from .mps import MpsState, Sampler, execute, execute_parallel, make_gates, sample  # noqa: F401
+from .frontend import (ParseError, ConfigError, parse_qasm, fuse_qasm, plan_layers, ghz_qasm,  # noqa: F401
+                       brickwork_qasm, run_circuit, exit_code_for_error)

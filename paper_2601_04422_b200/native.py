@@ -12,7 +12,7 @@ import os
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libmpsim_gpu.so")
 
-MPSIM_OK, MPSIM_EINVAL, MPSIM_ENUMERIC, MPSIM_ELOGIC, MPSIM_ECUDA = 0, 1, 3, 4, 5
+MPSIM_OK, MPSIM_EINVAL, MPSIM_EPARSE, MPSIM_ENUMERIC, MPSIM_ELOGIC, MPSIM_ECUDA = 0, 1, 2, 3, 4, 5
 UNBOUNDED = (1 << 63) - 1
 NONLOCAL_SWAP, NONLOCAL_BONDPROP = 0, 1
 
@@ -39,6 +39,34 @@ class Gate(C.Structure):
 class ExecStats(C.Structure):
     _fields_ = [("peak_bond", I64), ("total_discarded_weight", DBL), ("layers", I32), ("gates", I32),
                 ("kernel_launches", I64), ("device_ms", DBL)]
+
+
+class PrimOp(C.Structure):
+    _fields_ = [("kind", I32), ("q0", I32), ("q1", I32), ("nparams", I32), ("params", DBL * 3)]
+
+
+class CircuitInfo(C.Structure):
+    _fields_ = [("n_qubits", I32), ("n_clbits", I32), ("has_measure_all", I32), ("n_ops", I32)]
+
+
+class RunConfig(C.Structure):
+    _fields_ = [("qasm_path", C.c_char_p), ("qasm_text", C.c_char_p), ("sidecar_path", C.c_char_p),
+                ("sidecar_json", C.c_char_p), ("input_label", C.c_char_p), ("backend", I32), ("nonlocal_", I32),
+                ("max_bond", I64), ("cutoff", DBL), ("shots", U64), ("seed", U64), ("workers", I32),
+                ("memoize", I32), ("cache_cap", U64), ("statevector_cap", I32), ("device", I32),
+                ("chi_hint", I64)]
+
+
+class ParseError(ValueError):
+    """mpsim::ParseError (errors.hpp:22-37): carries the 1-based line and column."""
+
+    def __init__(self, msg, line=0, column=0):
+        super().__init__(msg)
+        self.line, self.column = line, column
+
+
+class ConfigError(ValueError):
+    """mpsim::ConfigError (errors.hpp:39-43)."""
 
 
 class NumericError(RuntimeError):
@@ -104,6 +132,17 @@ def lib():
         "mpsim_gpu_transfer_counters": (C.c_int, [VP, C.POINTER(I64), C.POINTER(I64)]),
         "mpsim_gpu_reset_counters": (C.c_int, [VP]),
         "mpsim_gpu_synchronize": (C.c_int, [VP]),
+        "mpsim_free": (None, [VP]),
+        "mpsim_parse_qasm": (C.c_int, [C.c_char_p, C.POINTER(CircuitInfo), C.POINTER(PrimOp), I32]),
+        "mpsim_last_parse_location": (C.c_int, [C.POINTER(I32), C.POINTER(I32)]),
+        "mpsim_fuse_qasm": (C.c_int, [C.c_char_p, C.c_char_p, C.POINTER(I32), C.POINTER(C.POINTER(Gate)),
+                                      C.POINTER(C.POINTER(I32)), C.POINTER(I32)]),
+        "mpsim_plan_layers": (C.c_int, [C.POINTER(Gate), I32, I32, C.POINTER(C.POINTER(Gate)),
+                                        C.POINTER(C.POINTER(I32)), C.POINTER(I32), C.POINTER(I32)]),
+        "mpsim_gen_ghz_qasm": (C.c_int, [I32, I32, C.POINTER(VP)]),
+        "mpsim_gen_brickwork_qasm": (C.c_int, [I32, I32, U64, I32, I32, C.POINTER(VP), C.POINTER(VP)]),
+        "mpsim_run_config_defaults": (None, [C.POINTER(RunConfig)]),
+        "mpsim_gpu_run_circuit": (C.c_int, [C.POINTER(RunConfig), C.POINTER(VP)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -119,7 +158,7 @@ def exported_symbols():
     hdr = os.path.join(os.path.dirname(_HERE), "include", "mpsim_gpu.h")
     with open(hdr) as f:
         text = f.read()
-    return sorted(set(re.findall(r"\b(mpsim_gpu_[a-z0-9_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(mpsim_[a-z0-9_]+)\s*\(", text)))
 
 
 def check(rc: int):
@@ -128,6 +167,10 @@ def check(rc: int):
     msg = lib().mpsim_gpu_last_error().decode()
     if rc == MPSIM_EINVAL:
         raise ValueError(msg)
+    if rc == MPSIM_EPARSE:
+        line, col = I32(), I32()
+        lib().mpsim_last_parse_location(C.byref(line), C.byref(col))
+        raise ParseError(msg, line.value, col.value)
     if rc == MPSIM_ENUMERIC:
         raise NumericError(msg)
     if rc == MPSIM_ELOGIC:

@@ -16,7 +16,48 @@ using namespace mpsim;
     }                                                                \
   } while (0)
 
-int main() {
+// Host-only front end: parse/fuse/plan/generate (no device touched).
+static void host_checks() {
+  int n = 0;
+  const auto g = fuse_qasm("OPENQASM 2.0;\nqreg q[3];\nh q[0];\ncx q[2],q[0];\n", {}, &n);
+  CHECK(n == 3 && g.size() == 1 && g[0].q0 == 0 && g[0].q1 == 2 && g[0].flipped);
+  const LayerPlan plan = plan_layers(g, 3);
+  CHECK(plan.layers.size() == 3 && plan.layers[1][0].q0 == 1);
+  bool threw = false;
+  try {
+    fuse_qasm("OPENQASM 2.0; qreg q[2];\nccx q[0],q[1];");
+  } catch (const ParseError& e) {
+    threw = e.line() == 2 && exit_code_for_error(e) == 2;
+  }
+  CHECK(threw);
+  BrickworkOptions o;
+  o.n_qubits = 6;
+  o.depth = 3;
+  o.seed = 5;
+  o.entangler = Entangler::Haar;
+  const GeneratedCircuit gc = brickwork_qasm(o);
+  CHECK(!gc.sidecar_json.empty());
+  const auto fused = fuse_qasm(gc.qasm, gc.sidecar_json);
+  CHECK(fused.size() == 8);  // 3 + 2 + 3 entanglers; every u3 is absorbed
+  threw = false;
+  try {
+    RunConfig bad;
+    bad.qasm_text = ghz_qasm(4);
+    bad.backend = Backend::MpsParallel;
+    bad.nonlocal = NonlocalMethod::BondProp;
+    run_circuit_json(bad);
+  } catch (const ConfigError& e) {
+    threw = exit_code_for_error(e) == 1;
+  }
+  CHECK(threw);
+}
+
+int main(int argc, char** argv) {
+  host_checks();
+  if (argc > 1 && std::string(argv[1]) == "--host-only") {
+    std::printf("facade host ok\n");
+    return 0;
+  }
   const double hs = 1.0 / std::sqrt(2.0);
   const CTensor h({2, 2}, {hs, hs, hs, -hs});
   const CTensor cx({4, 4}, {1, 0, 0, 0, 0, 1, 0, 0, 0, 0, 0, 1, 0, 0, 1, 0});
@@ -77,6 +118,16 @@ int main() {
     const ExecStats st = execute_serial(s, gates, p);
     CHECK(st.peak_bond <= 4 && st.layers == 6);
     CHECK(std::abs(norm(s) - 1.0) < 1e-6 || st.total_discarded_weight > 0.0);
+  }
+  // run_circuit: GHZ counts on the corner strings (test_runner.cpp:37-51)
+  {
+    RunConfig c;
+    c.qasm_text = ghz_qasm(4);
+    c.shots = 1000;
+    c.seed = 5;
+    const std::string j = run_circuit_json(c);
+    CHECK(j.find("\"peak_bond\":2") != std::string::npos);
+    CHECK(j.find("\"0000\":") != std::string::npos && j.find("\"1111\":") != std::string::npos);
   }
   std::printf("facade ok\n");
   return 0;

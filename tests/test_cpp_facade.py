@@ -1,5 +1,6 @@
 """The header-only C++ facade (include/mpsim_b200.hpp) compiles against the C
-ABI here, and runs its reference-style known answers on the GPU."""
+ABI here and runs its host-only front-end checks (parse / fuse / plan /
+generate), and runs its reference-style known answers on the GPU."""
 import os
 import subprocess
 
@@ -21,6 +22,9 @@ def test_facade_compiles():
         subprocess.run(["make", "-s", "-C", os.path.join(LIBDIR, "csrc"), "-j8"], check=True)
     _compile()
     assert os.path.exists(OUT)
+    out = subprocess.run([OUT, "--host-only"], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stderr
+    assert "facade host ok" in out.stdout
 
 
 @pytest.mark.gpu
