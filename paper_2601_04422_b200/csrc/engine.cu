@@ -156,6 +156,24 @@ static int phase_probe() {
   return v;
 }
 
+// MPSIM_FIRST_INBLOCK=0 computes every Gram tile in the first sweep (A/B).
+static bool first_sweep_inblock() {
+  static const bool on = [] {
+    const char* v = std::getenv("MPSIM_FIRST_INBLOCK");
+    return !(v != nullptr && v[0] == '0');
+  }();
+  return on;
+}
+
+// MPSIM_EXACT_CACHE=0 recomputes all 36 Gram tiles in closing sweeps (A/B).
+static bool exact_cache_policy() {
+  static const bool on = [] {
+    const char* v = std::getenv("MPSIM_EXACT_CACHE");
+    return !(v != nullptr && v[0] == '0');
+  }();
+  return on;
+}
+
 // MPSIM_SWEEP_DEBUG=1 prints per-sweep Jacobi convergence to stderr.
 static bool sweep_debug() {
   static const bool on = [] {
@@ -472,7 +490,13 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   }
 
   int* h_rot = (int*)s.h_rot.p;
-  for (int i = 0; i < ng; ++i) h_rot[i] = 1;
+  // The first sweep of a fresh theta is pre-asymptotic: it reuses the pair
+  // EVDs' in-block Grams from round 1 on (bit 4) like the sweeps the maxoff
+  // policy below flags. It cannot end the iteration through kQuadFinish (its
+  // maxoff saw in-block values that may be stale); only a sweep without any
+  // rotation — whose Grams were then all computed exactly — ends it.
+  const int first = (jacobi_mode() >= 3 && inblock_policy() && first_sweep_inblock()) ? (1 | 4) : 1;
+  for (int i = 0; i < ng; ++i) h_rot[i] = first;
   CK(cudaMemcpyAsync(s.d_active.p, h_rot, sizeof(int) * ng, cudaMemcpyHostToDevice, st));
   bool converged = false;
   std::vector<int> still(ng, 1);
@@ -504,7 +528,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     // (phase probes 1-2 run per round; probe 4, the visit without its EVD, runs persistent)
     const bool persistent = jacobi_mode() == 4 && (!phase_probe() || phase_probe() == 4) && sweep_policy();
     if (persistent) {
-      s.d_sweepctl.ensure(sizeof(int) * (1 + (size_t)ng * max_nb));
+      s.d_sweepctl.ensure(sizeof(int) * (1 + 2 * (size_t)ng * max_nb));
       launch_jacobi_sweep(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, 4.0 * kEps, 2.0 * kEps,
                           (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p, perm_stride,
                           (double*)s.d_maxoff.p, (int*)s.d_need.p, (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p,
@@ -564,7 +588,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     }
     bool any = false;
     for (int i = 0; i < ng; ++i) {
-      const bool quad_done = h_maxoff[i] <= kQuadFinish;
+      const bool quad_done = h_maxoff[i] <= kQuadFinish && !(sweep == 0 && (first & 4));
       h_rot[i] = h_rot[i] && !quad_done;
       still[i] = h_rot[i];
       any = any || h_rot[i];
@@ -581,6 +605,9 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // pre-asymptotic and early asymptotic sweeps reuse the in-block Grams the
       // pair EVDs leave behind (jacobi_split.cu); the closing sweeps recompute all
       if (h_rot[i] && jacobi_mode() >= 3 && inblock_policy() && h_maxoff[i] > kInblockMaxoff) h_rot[i] |= 4;
+      // closing sweeps: reuse in-block Grams only while they are exact (flags
+      // kept by the persistent sweep kernel; bit-for-bit the recomputed values)
+      else if (h_rot[i] && exact_cache_policy()) h_rot[i] |= 8;
     }
     if (!any) {
       converged = true;

@@ -195,6 +195,7 @@ struct RoundArgs {
   cplx* gblk;
   int* rotated;
   int probe;
+  int* blkok;  // per block: gblk holds its exact in-block Gram (persistent sweeps; nullable)
 };
 
 // One pair visit (block pair k of gate gi in tournament round `round`).
@@ -231,6 +232,15 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
   // rounding: the blocks have not changed since), so only the cross block
   // X_a^H X_b is computed: 16 of the 36 DMMA tiles.
   const bool approx = kFuseEvd && (active[gi] & 4) && round > 0;
+  // Exact cache (active bit 8, closing sweeps): a visit that computed all 36
+  // tiles and did not rotate leaves the blocks' in-block Grams in gblk and
+  // flags them; a later visit of two flagged (hence unchanged) blocks this
+  // sweep needs only the cross tiles — the in-block values are exactly what
+  // recomputing them would give. A rotation clears the flags.
+  int* const ok_a = A.blkok ? A.blkok + (long long)gi * 2 * max_pairs + c.ba : nullptr;
+  int* const ok_b = A.blkok ? A.blkok + (long long)gi * 2 * max_pairs + c.bb : nullptr;
+  const bool cached = kFuseEvd && !approx && ok_a && (active[gi] & 8) && round > 0 && *ok_a && *ok_b;
+  const bool cross_only = approx || cached;
   cplx* const gblk_a = gblk + ((long long)gi * 2 * max_pairs + c.ba) * (kW * kW);
   cplx* const gblk_b = gblk + ((long long)gi * 2 * max_pairs + c.bb) * (kW * kW);
   // column offsets (plane + index) of this thread's fragments
@@ -246,7 +256,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
     __syncthreads();
   };
   ld.issue(S.u.buf[0], 0);
-  if (approx) {
+  if (cross_only) {
     // the 16 cross tiles (rows Re_a / Im_a = tiles 0,1 / 4,5; cols Re_b / Im_b =
     // 2,3 / 6,7) as four 2x2 blocks, warp & 3 picks the block and warp >> 2
     // the half of each chunk's k-steps: two A and two B loads feed four DMMAs
@@ -340,7 +350,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
         for (int v = 0; v < 2; ++v) S.u.Gx[(8 * trow[i] + fr) * 65 + 8 * tcol[i] + fk * 2 + v] = acc[i][v];
     __syncthreads();
   }
-  if (approx) {
+  if (cross_only) {
     const double* Gx = S.u.Gx;
     const int i = t >> 4, j = kW + (t & 15);
     const double re = Gx[i * 65 + j] + Gx[(kP + i) * 65 + kP + j];
@@ -383,9 +393,13 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
     gblk_b[t] = SG[(kW + r) * kPad + kW + q];
   };
   if (!nd) {
-    if (kFuseEvd && !approx) store_inblock();
+    if (kFuseEvd && !cross_only) {
+      store_inblock();
+      if (ok_a && t == 0) *ok_a = *ok_b = 1;
+    }
     return;
   }
+  if (ok_a && t == 0) *ok_a = *ok_b = 0;
   if (probe == 1) return;  // profiling (MPSIM_PHASE_PROBE): Gram only
   if constexpr (kFuseEvd) {
     cplx* R = reinterpret_cast<cplx*>(S.u.buf);
@@ -549,7 +563,7 @@ void jacobi_split_init() {
 static RoundArgs make_args(const GateDesc* d_gates, cplx* ws, const int* d_active, int* d_rotated, double tol,
                            double tol_in, const double* frob2, double floor_rel2, const int* perm,
                            long long perm_stride, double* maxoff, int* need, cplx* gbuf, cplx* rbuf, double* offsum,
-                           int max_pairs, cplx* gblk, int probe) {
+                           int max_pairs, cplx* gblk, int probe, int* blkok = nullptr) {
   RoundArgs a;
   a.gates = d_gates;
   a.ws = ws;
@@ -569,6 +583,7 @@ static RoundArgs make_args(const GateDesc* d_gates, cplx* ws, const int* d_activ
   a.gblk = gblk;
   a.rotated = d_rotated;
   a.probe = probe;
+  a.blkok = blkok;
   return a;
 }
 
@@ -611,9 +626,11 @@ void launch_jacobi_sweep(const GateDesc* d_gates, int n_gates, int max_pairs, cp
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jacobi_sweep_kernel, 256, sizeof(PairSmem));
     ctas = sms * (per_sm > 0 ? per_sm : 1);
   }
-  cudaMemsetAsync(ctl, 0, sizeof(int) * (1 + (size_t)n_gates * 2 * max_pairs), st);
+  // ctl: [item counter | per-block round counters | per-block exact-Gram flags]
+  const size_t nblk = (size_t)n_gates * 2 * max_pairs;
+  cudaMemsetAsync(ctl, 0, sizeof(int) * (1 + 2 * nblk), st);
   const RoundArgs a = make_args(d_gates, ws, d_active, d_rotated, tol, tol_in, frob2, floor_rel2, perm, perm_stride,
-                                maxoff, need, gbuf, rbuf, offsum, max_pairs, gblk, probe);
+                                maxoff, need, gbuf, rbuf, offsum, max_pairs, gblk, probe, ctl + 1 + nblk);
   jacobi_sweep_kernel<<<ctas, 256, sizeof(PairSmem), st>>>(a, n_gates, 2 * max_pairs - 1, ctl);
 }
 
