@@ -72,25 +72,35 @@ class ClockSampler:
         self.rows = []
         self._stop = threading.Event()
         self._t = None
+        self._nv, self._handles = None, []
+        if self.devices:  # NVML handles resolved before the timed region starts
+            try:
+                import pynvml as nv
+                nv.nvmlInit()
+                self._nv = nv
+            except Exception:
+                return
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+            for d in self.devices:  # CUDA ordinal -> NVML handle (by UUID when torch is loaded)
+                try:
+                    if "torch" in sys.modules:
+                        import torch
+                        self._handles.append(
+                            nv.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(d).uuid)))
+                        continue
+                    ids = [x for x in vis.split(",") if x.strip()]
+                    idx = int(ids[d]) if ids and ids[d].strip().isdigit() else d
+                    self._handles.append(nv.nvmlDeviceGetHandleByIndex(idx))
+                except Exception:
+                    try:
+                        self._handles.append(nv.nvmlDeviceGetHandleByIndex(d))
+                    except Exception:
+                        pass
 
     def _run(self):
-        try:
-            import pynvml as nv
-            nv.nvmlInit()
-        except Exception:
-            return
-        handles = []
-        for d in self.devices:  # CUDA ordinal -> NVML handle by UUID (CUDA_VISIBLE_DEVICES-safe)
-            try:
-                import torch
-                handles.append(nv.nvmlDeviceGetHandleByUUID("GPU-" + str(torch.cuda.get_device_properties(d).uuid)))
-            except Exception:
-                try:
-                    handles.append(nv.nvmlDeviceGetHandleByIndex(d))
-                except Exception:
-                    pass
-        while not self._stop.is_set():
-            for h in handles:
+        nv = self._nv
+        while True:
+            for h in self._handles:
                 try:
                     sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
                     mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
@@ -98,10 +108,11 @@ class ClockSampler:
                     self.rows.append((float(sm), float(mx), int(rs)))
                 except Exception:
                     pass
-            self._stop.wait(self.interval)
+            if self._stop.wait(self.interval):
+                break
 
     def __enter__(self):
-        if self.devices:
+        if self._handles:
             self._t = threading.Thread(target=self._run, daemon=True)
             self._t.start()
         return self
@@ -182,7 +193,7 @@ def run_reference(args, rank, world):
     line = {
         "impl": "reference", "metric": metric_name(args.chi), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "complex128",
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "complex128",
         "data": "synthetic",
         "config": config_block(args),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
@@ -194,10 +205,14 @@ def run_reference(args, rank, world):
 
 
 def config_block(args):
-    return {"workload": f"{args.qubits}-qubit random brickwork (Haar 4x4) at chi={args.chi} steady state, "
+    n = args.qubits
+    return {"workload": f"{n}-qubit random brickwork (Haar 4x4) at chi={args.chi} steady state, "
                         f"one brick layer per step, max_bond={args.chi}, cutoff=1e-12",
-            "n_qubits": args.qubits, "chi": args.chi, "cutoff": 1e-12,
-            "gates_per_step": "128/127 alternating", "l2": "inputs larger than L2 (2 GiB site store)",
+            "n_qubits": n, "chi": args.chi, "cutoff": 1e-12,
+            "gates_per_step": f"{n // 2}/{n // 2 - 1} alternating",
+            "sharding": (f"{args.scaling} scaling: contiguous site shards ({args.per_gpu} qubits per GPU)"
+                         if args.scaling == "weak" else f"strong scaling: one {n}-qubit chain over the GPUs"),
+            "l2": "inputs larger than L2 (2 GiB site store per GPU)",
             "state": "synthetic random MPS saturated at chi (bonds min(chi,2^i,2^(n-i)))"}
 
 
@@ -209,13 +224,19 @@ def main():
     ap.add_argument("--steps", type=int, default=4)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--qubits", type=int, default=256)
+    ap.add_argument("--qubits", type=int, default=256,
+                    help="chain length per GPU (weak scaling) or in total (--scaling strong)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: a qubits*N chain, 128 gates per GPU per layer; strong: one qubits chain split N ways")
     ap.add_argument("--chi", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    args.per_gpu = args.qubits
+    if args.scaling == "weak":
+        args.qubits *= world
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -275,7 +296,7 @@ def main():
     line = {
         "metric": metric_name(args.chi), "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * dev_total / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "complex128", "data": "synthetic",
         "config": config_block(args),
         "circuit_wall_s": wall_total,
         "roofline": {
