@@ -25,7 +25,7 @@ for i, x in enumerate(h):
             pass
 tot = sum(a for a, _ in st) or 1
 m["stall_sample_share"] = {x: round(a / tot, 4) for a, x in sorted(st, reverse=True)[:9]}
-out = {"jacobi_gram_kernel": {"capture": capture,
+out = {"jacobi_sweep_kernel": {"capture": capture,
                               "dram_bytes_per_launch": nbytes("dram__bytes_read.sum") + nbytes("dram__bytes_write.sum"),
                               "metrics": m}}
 print(json.dumps(out, indent=1))
