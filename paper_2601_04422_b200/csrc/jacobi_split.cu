@@ -101,7 +101,8 @@ struct PairSmem {
   } u;
   union {
     cplx G[kP * kPad];
-    cplx Rs[kP * kPitchR];  // R for the rotation
+    cplx Rs[kP * kPitchR];           // R for the rotation
+    double buf3[2 * kChunkPlane];    // third Gram-pass stage (G / Rs are dead then)
   } v;
   EvdScratch sc;
 };
@@ -246,16 +247,26 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
   // column offsets (plane + index) of this thread's fragments
   auto coff = [&](int col) { return (col < kP ? 0 : kChunkPlane) + (col & (kP - 1)) * kPitchS; };
   const int nchunks = g.m_pad / kC;
-  auto next_chunk = [&](int k) {  // stage k's data ready in shared memory
-    if (k + 1 < nchunks) {
-      ld.issue(S.u.buf[(k + 1) & 1], (k + 1) * kC);
+  // Gram pass: a three-stage cp.async ring (two chunk buffers + the G / R
+  // union, free until the Gram is assembled): the pass does only 16-36 tiles
+  // of DMMA per 32-row chunk, too little to hide a load issued one chunk ahead
+  auto stage = [&](int k) -> double* {
+    const int s3 = k % 3;
+    return s3 == 2 ? S.v.buf3 : S.u.buf[s3];
+  };
+  auto next_chunk = [&](int k) {  // chunk k's data ready in shared memory
+    if (k + 2 < nchunks) {
+      ld.issue(stage(k + 2), (k + 2) * kC);
+      cp_async_wait<2>();
+    } else if (k + 1 < nchunks) {
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
     }
     __syncthreads();
   };
-  ld.issue(S.u.buf[0], 0);
+  ld.issue(stage(0), 0);
+  if (nchunks > 1) ld.issue(stage(1), kC);
   if (cross_only) {
     // the 16 cross tiles (rows Re_a / Im_a = tiles 0,1 / 4,5; cols Re_b / Im_b =
     // 2,3 / 6,7) as four 2x2 blocks, warp & 3 picks the block and warp >> 2
@@ -271,7 +282,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
       for (int b = 0; b < 2; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
     for (int k = 0; k < nchunks; ++k) {
       next_chunk(k);
-      const double* B = S.u.buf[k & 1];
+      const double* B = stage(k);
 #pragma unroll
       for (int ks = 0; ks < kC / 8; ++ks) {
         const int row = 4 * (ks + (kC / 8) * kh) + fk;
@@ -332,7 +343,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
     for (int i = 0; i < 5; ++i) acc[i][0] = acc[i][1] = 0.0;
     for (int k = 0; k < nchunks; ++k) {
       next_chunk(k);
-      const double* B = S.u.buf[k & 1];
+      const double* B = stage(k);
 #pragma unroll
       for (int ks = 0; ks < kC / 4; ++ks) {
         const int row = 4 * ks + fk;
