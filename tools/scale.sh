@@ -7,7 +7,7 @@ SC=${SCALING:-weak}
 for n in 1 2 4 8; do
   [ $n -gt $NG ] && break
   if [ $n -eq 1 ]; then
-    python bench.py --steps 4 --warmup 3 --no-cpu-baseline --scaling $SC 2>/dev/null | tail -1 > gpurun_out/scale_${SC}_$n.json
+    python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-pipeline --scaling $SC 2>/dev/null | tail -1 > gpurun_out/scale_${SC}_$n.json
   else
     python -m torch.distributed.run --nnodes=1 --nproc-per-node $n --master-addr 127.0.0.1 --master-port $((29600 + n)) \
       bench.py --gpus $n --steps 4 --warmup 3 --scaling $SC 2>/dev/null | tail -1 > gpurun_out/scale_${SC}_$n.json
