@@ -108,13 +108,12 @@ struct PairSmem {
 };
 static_assert(sizeof(cplx) * kP * kPad <= sizeof(PairSmem::u), "R must fit in the chunk buffers");
 
-// X_P <- X_P R over all chunks, on DMMA in real-extended form
-// X_ext R_ext with R_ext = [[Re R, Im R], [-Im R, Re R]] formed on the fly:
-// one 16-byte load of R[c][j] gives both B fragments (Re and Im output tiles)
-// of a k-step. Warp w computes row tiles {2(w&1), +1} of a chunk and complex
-// column tile w/2 (real column tiles w/2 and 4 + w/2): per k-step two A loads
-// and one B load feed four DMMAs, and each thread ends up with Re and Im of the
-// same complex outputs.
+// X_P <- X_P R over all chunks, on DMMA with the three-real-product complex
+// multiply: one 16-byte load of R[c][j] gives the B fragments of Re R, Im R
+// and Re R + Im R for a k-step. Warp w computes row tiles {2(w&1), +1} of a
+// chunk and complex column tile w/2: per k-step four A loads (Re and Im planes)
+// and one B load feed six DMMAs, and each thread ends up with Re and Im of
+// the same complex outputs.
 __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader& ld, double (*buf)[2 * kChunkPlane],
                                             const cplx* Rs, int nchunks, int t) {
   const int lane = t % 32, warp = t / 32;
@@ -132,24 +131,37 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
     }
     __syncthreads();
     const double* B = buf[k & 1];
+    // complex product in three real products (Gauss): T1 = Xr Rr, T2 = Xi Ri,
+    // T3 = (Xr + Xi)(Rr + Ri); Re = T1 - T2, Im = T3 - T1 - T2. 48 DMMAs per
+    // warp and chunk instead of 64; each output column's error stays bounded
+    // by eps * sum_q |x_q| |R_qp| (columnwise, as the Jacobi needs)
+    double t1[2][2], t2[2][2], t3[2][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a) t1[a][0] = t1[a][1] = t2[a][0] = t2[a][1] = t3[a][0] = t3[a][1] = 0.0;
+#pragma unroll
+    for (int s = 0; s < 8; ++s) {
+      const int cc = 4 * s + fk;
+      const double* pr = B + cc * kPitchS;
+      const double* pim = pr + kChunkPlane;
+      const double ar0 = pr[8 * rbase + fr], ar1 = pr[8 * (rbase + 1) + fr];
+      const double ai0 = pim[8 * rbase + fr], ai1 = pim[8 * (rbase + 1) + fr];
+      const cplx r = Rs[cc * kPitchR + jb];
+      const double rs = r.x + r.y;
+      dmma_s(t1[0][0], t1[0][1], ar0, r.x);
+      dmma_s(t1[1][0], t1[1][1], ar1, r.x);
+      dmma_s(t2[0][0], t2[0][1], ai0, r.y);
+      dmma_s(t2[1][0], t2[1][1], ai1, r.y);
+      dmma_s(t3[0][0], t3[0][1], ar0 + ai0, rs);
+      dmma_s(t3[1][0], t3[1][1], ar1 + ai1, rs);
+    }
     double o[2][2][2];
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int q = 0; q < 2; ++q) o[a][q][0] = o[a][q][1] = 0.0;
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {
-      const int cext = 4 * s + fk, cc = cext & (kP - 1);
-      const double* plane = B + (s < 8 ? 0 : kChunkPlane) + cc * kPitchS;
-      const double a0 = plane[8 * rbase + fr], a1 = plane[8 * (rbase + 1) + fr];
-      const cplx r = Rs[cc * kPitchR + jb];
-      const double b0 = s < 8 ? r.x : -r.y;  // [[Re R, Im R],
-      const double b1 = s < 8 ? r.y : r.x;   //  [-Im R, Re R]]
-      dmma_s(o[0][0][0], o[0][0][1], a0, b0);
-      dmma_s(o[0][1][0], o[0][1][1], a0, b1);
-      dmma_s(o[1][0][0], o[1][0][1], a1, b0);
-      dmma_s(o[1][1][0], o[1][1][1], a1, b1);
-    }
+      for (int v = 0; v < 2; ++v) {
+        o[a][0][v] = t1[a][v] - t2[a][v];
+        o[a][1][v] = t3[a][v] - t1[a][v] - t2[a][v];
+      }
     const int e0 = (nchunks - 1 - k) * kC;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
