@@ -18,7 +18,7 @@ from paper_2601_04422_b200.mps import execute  # noqa: E402
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
 dist.init_process_group("nccl")
-n, chi = 256, 512
+n, chi = int(os.environ.get("NQ", "256")), 512
 rng = np.random.default_rng(1234)
 bonds = B.chain_bonds(n, chi)
 ch = sharded.ShardedChain(n, chi, rank, world, device=local, dist=dist)
