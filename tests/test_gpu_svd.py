@@ -103,3 +103,31 @@ def test_rank_deficient_preconditioned(gpu, shape):
     assert len(s) == 3
     assert np.abs(s - ref[:3]).max() <= 1e-13 * ref[0]
     assert np.linalg.norm(u @ np.diag(s) @ vd - m) / np.linalg.norm(m) <= 1e-12
+
+
+def test_random_shapes_fuzz(gpu):
+    """Seeded fuzz over shapes 1..300 x 1..300 (both sides of the QR
+    preconditioning threshold, odd and ragged sizes, tall and wide): singular
+    values against numpy's LAPACK to 1e-12 relative to s_max, reconstruction
+    to 1e-12, and the kept rank / discarded weight of a cap + cutoff policy
+    against the reference rule applied to numpy's values."""
+    rng = np.random.default_rng(2601)
+    for _ in range(24):
+        r, c = (int(x) for x in rng.integers(1, 301, size=2))
+        # graded spectra exercise the relative-accuracy path
+        a = _rand(rng, r, c) * np.logspace(0, -int(rng.integers(0, 9)), c)[None, :]
+        u, s, vd, w = gpu.mps.svd(a)
+        ref = np.linalg.svd(a, compute_uv=False)
+        assert len(s) == min(r, c)
+        assert np.abs(s - ref).max() <= 1e-12 * ref[0], (r, c)
+        assert np.linalg.norm(u @ np.diag(s) @ vd - a) <= 1e-12 * np.linalg.norm(a), (r, c)
+        cap = int(rng.integers(1, min(r, c) + 1))
+        _, s2, _, w2 = gpu.mps.svd(a, max_rank=cap, cutoff=1e-6)
+        tot = float((ref ** 2).sum())
+        keep, tail = len(ref), 0.0
+        while keep > 1 and tail + ref[keep - 1] ** 2 <= 1e-6 * tot:  # svd.hpp:48-74
+            tail += ref[keep - 1] ** 2
+            keep -= 1
+        keep = min(keep, cap)
+        assert len(s2) == keep, (r, c, cap)
+        assert abs(w2 - float((ref[keep:] ** 2).sum()) / tot) <= 1e-10 * max(w2, 1e-300) + 1e-15, (r, c)
