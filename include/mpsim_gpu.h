@@ -144,6 +144,19 @@ int mpsim_gpu_amplitudes(const mpsim_gpu_state* s, const char* bits, int32_t cou
 int mpsim_gpu_overlap(const mpsim_gpu_state* a, const mpsim_gpu_state* b, double* out); /* mps.cpp:223-239 */
 int mpsim_gpu_to_statevector(const mpsim_gpu_state* s, int32_t max_qubits, double* out); /* mps.cpp:241-256 */
 int mpsim_gpu_move_center(mpsim_gpu_state* s, int32_t center);                    /* mps.cpp:177-187 */
+/* Environment forms for site-sharded chains (SURVEY 8(e) queries): a shard
+ * continues its left neighbour's environment over its local sites [i0, i1)
+ * and hands its own to the right. amplitudes_env: row environments of count
+ * bit strings (n_local chars each, only [i0, i1) read; mps.cpp:204-221);
+ * env_in host count x D_left complex (NULL = chain start), env_out host
+ * count x D_right. transfer_env: E' = sum_p A_p^H E B_p (mps.cpp:189-202,
+ * :223-239), op2x2 (nullable) applied to y at local site q (the P9
+ * expectation form); env_in host D_left(x) x D_left(y) row-major (NULL =
+ * [[1]]), env_out D_right(x) x D_right(y). */
+int mpsim_gpu_amplitudes_env(const mpsim_gpu_state* s, int32_t i0, int32_t i1, const char* bits, int32_t count,
+                             const double* env_in, double* env_out);
+int mpsim_gpu_transfer_env(const mpsim_gpu_state* x, const mpsim_gpu_state* y, int32_t i0, int32_t i1,
+                           const double* op2x2, int32_t q, const double* env_in, double* env_out);
 /* <psi| O_q |psi> for a 2x2 operator (the P9 definition: overlap(psi,
  * apply_1q(copy psi, O, q))); out = complex. */
 int mpsim_gpu_expect_1q(const mpsim_gpu_state* s, const double* op2x2, int32_t q, double* out);

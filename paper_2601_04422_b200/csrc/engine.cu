@@ -928,9 +928,18 @@ void transfer_step(State& a, int i, const State& b, const cplx* E, long long ldE
   if (first) launch_fill(E2, (long long)dra * ldE2, make_double2(0.0, 0.0), st);
 }
 
-cd chain_contract(State& a, const State& b, const std::map<int, const cd*>& ops) {
+// E' = sum_p A_p^H E B_p over every site (mps.cpp:223-239), optional 2x2
+// operators on B's physical index. env_in (host, sdl_a[0] x sdl_b[0],
+// row-major; nullptr = [[1]]) / env_out (host, sdr_a[n-1] x sdr_b[n-1]):
+// a shard of a longer chain contracts from its left neighbour's environment
+// (SURVEY 8(e) queries).
+void chain_env(State& a, const State& b, const std::map<int, const cd*>& ops, const cplx* env_in, cplx* env_out,
+               int i0 = 0, int i1 = -1) {
   if (a.n != b.n) fail(MPSIM_EINVAL, "overlap requires equal qubit counts");
   if (a.device != b.device) fail(MPSIM_EINVAL, "overlap requires both states on one device");
+  if (i1 < 0) i1 = a.n;
+  if (i0 < 0 || i1 > a.n || i0 >= i1) fail(MPSIM_EINVAL, "site range out of bounds");
+  if (!env_in && (a.sdl[i0] != 1 || b.sdl[i0] != 1)) fail(MPSIM_EINVAL, "open left bond needs an input environment");
   DeviceGuard g(a.device);
   cudaStream_t st = a.st;
   if (&a != &b) CK(cudaStreamSynchronize(b.st));
@@ -942,16 +951,28 @@ cd chain_contract(State& a, const State& b, const std::map<int, const cd*>& ops)
   cplx* E = (cplx*)a.q1.p;
   cplx* E2 = (cplx*)a.q2.p;
   const cplx one = make_double2(1.0, 0.0);
-  CK(cudaMemcpyAsync(E, &one, sizeof(cplx), cudaMemcpyHostToDevice, st));
-  for (int i = 0; i < a.n; ++i) {
+  if (env_in)
+    CK(cudaMemcpy2DAsync(E, sizeof(cplx) * c, env_in, sizeof(cplx) * b.sdl[i0], sizeof(cplx) * b.sdl[i0], a.sdl[i0],
+                         cudaMemcpyHostToDevice, st));
+  else
+    CK(cudaMemcpyAsync(E, &one, sizeof(cplx), cudaMemcpyHostToDevice, st));
+  for (int i = i0; i < i1; ++i) {
     auto it = ops.find(i);
     transfer_step(a, i, b, E, c, E2, c, (cplx*)a.q3.p, (cplx*)a.q4.p, c, it == ops.end() ? nullptr : it->second, st);
     std::swap(E, E2);
   }
   check_launch();
-  cplx r;
-  CK(cudaMemcpyAsync(&r, E, sizeof(cplx), cudaMemcpyDeviceToHost, st));
+  const long long ra = a.sdr[i1 - 1], rb = b.sdr[i1 - 1];
+  CK(cudaMemcpy2DAsync(env_out, sizeof(cplx) * rb, E, sizeof(cplx) * c, sizeof(cplx) * rb, ra, cudaMemcpyDeviceToHost,
+                       st));
   CK(cudaStreamSynchronize(st));
+}
+
+cd chain_contract(State& a, const State& b, const std::map<int, const cd*>& ops) {
+  if (a.n != b.n) fail(MPSIM_EINVAL, "overlap requires equal qubit counts");
+  if (a.sdr[a.n - 1] != 1 || b.sdr[b.n - 1] != 1) fail(MPSIM_EINVAL, "open right bond: use the environment form");
+  cplx r;
+  chain_env(a, b, ops, nullptr, &r);
   return cd(r.x, r.y);
 }
 
@@ -1372,42 +1393,78 @@ int mpsim_gpu_expect_2q(const mpsim_gpu_state* s, const double* op_a, int32_t qa
   });
 }
 
+// Row environments of `count` bit strings through every site (mps.cpp:204-221):
+// env_in (host, count x sdl[0]; nullptr = ones at a chain start), env_out
+// (host, count x sdr[n-1]); amplitudes are the 1 x 1 case.
+static void amplitude_env(State& a, const char* bits, int32_t count, const cplx* env_in, cplx* env_out, int i0 = 0,
+                          int i1 = -1) {
+  if (count < 0) fail(MPSIM_EINVAL, "negative count");
+  if (i1 < 0) i1 = a.n;
+  if (i0 < 0 || i1 > a.n || i0 >= i1) fail(MPSIM_EINVAL, "site range out of bounds");
+  for (long long i = 0; i < (long long)count * a.n; ++i)
+    if (bits[i] != '0' && bits[i] != '1') fail(MPSIM_EINVAL, "bit string must contain only 0 and 1");
+  if (!env_in && a.sdl[i0] != 1) fail(MPSIM_EINVAL, "open left bond needs an input environment");
+  if (count == 0) return;
+  DeviceGuard g(a.device);
+  cudaStream_t st = a.st;
+  const int chunk = 4096;
+  const long long l0 = a.sdl[i0], rn = a.sdr[i1 - 1];
+  a.qbits.ensure((size_t)std::min(count, chunk) * a.n);
+  a.q1.ensure(sizeof(cplx) * (size_t)std::min(count, chunk) * a.chi);
+  a.q2.ensure(sizeof(cplx) * (size_t)std::min(count, chunk) * a.chi);
+  for (int c0 = 0; c0 < count; c0 += chunk) {
+    const int c = std::min(chunk, count - c0);
+    CK(cudaMemcpyAsync(a.qbits.p, bits + (long long)c0 * a.n, (size_t)c * a.n, cudaMemcpyHostToDevice, st));
+    cplx* E = (cplx*)a.q1.p;
+    cplx* E2 = (cplx*)a.q2.p;
+    long long ld = l0;
+    if (env_in)
+      CK(cudaMemcpyAsync(E, env_in + (long long)c0 * l0, sizeof(cplx) * c * l0, cudaMemcpyHostToDevice, st));
+    else
+      launch_fill(E, c, make_double2(1.0, 0.0), st);  // env = ones(1) per string, ld = 1 at site 0
+    for (int i = i0; i < i1; ++i) {
+      launch_amp_step(E, ld, E2, a.sdr[i], (const char*)a.qbits.p, a.n, i, c, a.sites + (long long)i * a.stride,
+                      a.chi, (int)a.sdl[i], (int)a.sdr[i], st);
+      ++a.launches;
+      ld = a.sdr[i];
+      std::swap(E, E2);
+    }
+    check_launch();
+    CK(cudaMemcpyAsync(env_out + (long long)c0 * rn, E, sizeof(cplx) * c * rn, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+}
+
+int mpsim_gpu_amplitudes_env(const mpsim_gpu_state* s, int32_t i0, int32_t i1, const char* bits, int32_t count,
+                             const double* env_in, double* env_out) {
+  return guarded([&] {
+    State& a = const_cast<State&>(S(s));
+    if (!env_out) fail(MPSIM_EINVAL, "null output");
+    amplitude_env(a, bits, count, reinterpret_cast<const cplx*>(env_in), reinterpret_cast<cplx*>(env_out), i0, i1);
+  });
+}
+
+int mpsim_gpu_transfer_env(const mpsim_gpu_state* x, const mpsim_gpu_state* y, int32_t i0, int32_t i1,
+                           const double* op2x2, int32_t q, const double* env_in, double* env_out) {
+  return guarded([&] {
+    State& a = const_cast<State&>(S(x));
+    if (!env_out) fail(MPSIM_EINVAL, "null output");
+    cd o[4];
+    std::map<int, const cd*> ops;
+    if (op2x2) {
+      if (q < 0 || q >= a.n) fail(MPSIM_EINVAL, "qubit out of range");
+      for (int i = 0; i < 4; ++i) o[i] = cd(op2x2[2 * i], op2x2[2 * i + 1]);
+      ops[q] = o;
+    }
+    chain_env(a, S(y), ops, reinterpret_cast<const cplx*>(env_in), reinterpret_cast<cplx*>(env_out), i0, i1);
+  });
+}
+
 int mpsim_gpu_amplitudes(const mpsim_gpu_state* s, const char* bits, int32_t count, double* out) {
   return guarded([&] {
     State& a = const_cast<State&>(S(s));
-    if (count < 0) fail(MPSIM_EINVAL, "negative count");
-    for (long long i = 0; i < (long long)count * a.n; ++i)
-      if (bits[i] != '0' && bits[i] != '1') fail(MPSIM_EINVAL, "bit string must contain only 0 and 1");
-    if (count == 0) return;
-    DeviceGuard g(a.device);
-    cudaStream_t st = a.st;
-    const int chunk = 4096;
-    a.qbits.ensure((size_t)std::min(count, chunk) * a.n);
-    a.q1.ensure(sizeof(cplx) * (size_t)std::min(count, chunk) * a.chi);
-    a.q2.ensure(sizeof(cplx) * (size_t)std::min(count, chunk) * a.chi);
-    for (int c0 = 0; c0 < count; c0 += chunk) {
-      const int c = std::min(chunk, count - c0);
-      CK(cudaMemcpyAsync(a.qbits.p, bits + (long long)c0 * a.n, (size_t)c * a.n, cudaMemcpyHostToDevice, st));
-      cplx* E = (cplx*)a.q1.p;
-      cplx* E2 = (cplx*)a.q2.p;
-      launch_fill(E, c, make_double2(1.0, 0.0), st);  // env = ones(1) per string, ld = 1 at site 0
-      long long ld = 1;
-      for (int i = 0; i < a.n; ++i) {
-        launch_amp_step(E, ld, E2, a.sdr[i], (const char*)a.qbits.p, a.n, i, c, a.sites + (long long)i * a.stride,
-                        a.chi, (int)a.sdl[i], (int)a.sdr[i], st);
-        ++a.launches;
-        ld = a.sdr[i];
-        std::swap(E, E2);
-      }
-      check_launch();
-      std::vector<cplx> h((size_t)c);
-      CK(cudaMemcpyAsync(h.data(), E, sizeof(cplx) * c, cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      for (int i = 0; i < c; ++i) {
-        out[2 * (c0 + i)] = h[(size_t)i].x;
-        out[2 * (c0 + i) + 1] = h[(size_t)i].y;
-      }
-    }
+    if (a.sdr[a.n - 1] != 1) fail(MPSIM_EINVAL, "open right bond: use mpsim_gpu_amplitudes_env");
+    amplitude_env(a, bits, count, nullptr, reinterpret_cast<cplx*>(out));
   });
 }
 

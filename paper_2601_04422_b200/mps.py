@@ -213,6 +213,42 @@ class MpsState:
         check(N.lib().mpsim_gpu_overlap(self._h, other._h, out.ctypes.data_as(_DP)))
         return complex(out[0], out[1])
 
+    # ---- environment forms (site-sharded chains, SURVEY 8(e) queries)
+    def amplitudes_env(self, bitstrings, env_in=None, i0=0, i1=None) -> np.ndarray:
+        """Row environments of bit strings (length n, sites [i0, i1) read)
+        continued from env_in (count x D_left) -> count x D_right."""
+        n = self.n
+        i1 = n if i1 is None else int(i1)
+        for b in bitstrings:
+            if len(b) != n:
+                raise ValueError(f"bit string length {len(b)} does not match qubit count {n}")
+        dims = self.bond_dims()
+        count = len(bitstrings)
+        ein = None
+        if env_in is not None:
+            ein = np.ascontiguousarray(env_in, dtype=np.complex128).reshape(count, int(dims[i0]))
+        out = np.zeros((count, int(dims[i1])), dtype=np.complex128)
+        check(N.lib().mpsim_gpu_amplitudes_env(self._h, int(i0), i1, "".join(bitstrings).encode(), count,
+                                               None if ein is None else ein.ctypes.data_as(_DP),
+                                               out.ctypes.data_as(_DP)))
+        return out
+
+    def transfer_env(self, other: "MpsState", env_in=None, op=None, q=-1, i0=0, i1=None) -> np.ndarray:
+        """E' = sum_p A_p^H E B_p over sites [i0, i1) of self (A) and other (B),
+        op (2x2) applied to B at site q: D_left(A) x D_left(B) -> D_right(A) x D_right(B)."""
+        i1 = self.n if i1 is None else int(i1)
+        da, db = self.bond_dims(), other.bond_dims()
+        ein = None
+        if env_in is not None:
+            ein = np.ascontiguousarray(env_in, dtype=np.complex128).reshape(int(da[i0]), int(db[i0]))
+        o = None if op is None else _cm(op, 2)
+        out = np.zeros((int(da[i1]), int(db[i1])), dtype=np.complex128)
+        check(N.lib().mpsim_gpu_transfer_env(self._h, other._h, int(i0), i1,
+                                             None if o is None else o.ctypes.data_as(_DP), int(q),
+                                             None if ein is None else ein.ctypes.data_as(_DP),
+                                             out.ctypes.data_as(_DP)))
+        return out
+
     def to_statevector(self, max_qubits=20) -> np.ndarray:
         n = self.n
         if n > max_qubits:

@@ -180,6 +180,61 @@ class ShardedChain:
             self._exchange_out(straddle_left, straddle_right)
         return st
 
+    # ---- queries over the shards: the chain is sequential, so
+    # each rank continues its left neighbour's environment over its owned
+    # sites [lo, hi) and sends its own to the right; the last rank holds the
+    # result and broadcasts it. NCCL moves the environments (count x chi or
+    # chi x chi complex128) as device tensors.
+    def _env_chain(self, compute, shape_in, result_len):
+        """compute(env_in) on every rank in chain order (rank r receives the
+        environment of rank r - 1); the last rank's result, flattened to
+        result_len values, is returned on every rank."""
+        torch, dist = self._torch, self.dist
+        dev = f"cuda:{self.device}"
+        env = None
+        if self.rank > 0:
+            t = torch.empty(shape_in, dtype=torch.complex128, device=dev)
+            dist.recv(t, self.rank - 1)
+            env = t.cpu().numpy()
+        out = compute(env)
+        if self.rank < self.world - 1:
+            dist.send(torch.from_numpy(np.ascontiguousarray(out)).to(dev), self.rank + 1)
+            res = torch.empty((result_len,), dtype=torch.complex128, device=dev)
+        else:
+            res = torch.from_numpy(np.ascontiguousarray(out.reshape(-1))).to(dev)
+        dist.broadcast(res, self.world - 1)
+        return res.cpu().numpy()
+
+    def amplitudes(self, bitstrings):
+        """amplitude (mps.cpp:204-221) of full-length bit strings of the chain."""
+        k = self.hi - self.lo
+        local = [b[self.lo:self.hi] + "0" * (self.state.n - k) for b in bitstrings]
+        if self.world == 1:
+            return self.state.amplitudes_env(local, None, 0, k)[:, 0]
+        d0 = int(self.state.bond_dims()[0])
+        return self._env_chain(lambda e: self.state.amplitudes_env(local, e, 0, k), (len(bitstrings), d0),
+                               len(bitstrings))
+
+    def _transfer(self, other, op=None, q=-1):
+        k = self.hi - self.lo
+        if self.world == 1:
+            return complex(self.state.transfer_env(other.state, None, op, q, 0, k)[0, 0])
+        da, db = int(self.state.bond_dims()[0]), int(other.state.bond_dims()[0])
+        return complex(self._env_chain(lambda e: self.state.transfer_env(other.state, e, op, q, 0, k), (da, db), 1)[0])
+
+    def overlap(self, other: "ShardedChain") -> complex:
+        """<self|other> (mps.cpp:223-239) of two chains sharded alike."""
+        return self._transfer(other)
+
+    def norm(self) -> float:
+        """mps.cpp:189-202."""
+        return float(np.sqrt(max(self._transfer(self).real, 0.0)))
+
+    def expect_1q(self, op, q) -> complex:
+        """<psi|O_q|psi>, the P9 definition, with O applied on the owning shard."""
+        own = self.lo <= q < self.hi
+        return self._transfer(self, op if own else None, q - self.lo if own else -1)
+
     def bond_dims(self):
         """Bonds of the owned range [lo, hi]."""
         return self.state.bond_dims()[: self.hi - self.lo + 1]

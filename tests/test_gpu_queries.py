@@ -124,3 +124,36 @@ def test_sampler_rejects_bad_inputs(gpu):
         gpu.Sampler(s)
     with pytest.raises(ValueError):
         gpu.sample(gpu.MpsState(2), 0, 1)
+
+
+def test_environment_forms_chain_across_shards(gpu, oracle):
+    """SURVEY 8(e) queries: a chain split into two open-boundary shard states
+    gives the full chain's amplitudes, norm, overlap and <O_q> when each shard
+    continues the other's environment (amplitudes_env / transfer_env) — the
+    same kernels in the same order, so bit-for-bit equal."""
+    n, k = 14, 6
+    o = oracle.MpsState.random(n, 16, 4)
+    full = gpu.MpsState(n, chi_hint=16)
+    left, right = gpu.MpsState(k, chi_hint=16), gpu.MpsState(n - k, chi_hint=16)
+    for s in (left, right):
+        s.set_open_boundaries(True)
+    for i in range(n):
+        t = o.site(i)
+        full.set_site(i, t)
+        (left.set_site(i, t) if i < k else right.set_site(i - k, t))
+    rng = np.random.default_rng(5)
+    bits = ["".join(rng.choice(["0", "1"], n)) for _ in range(40)]
+    e = left.amplitudes_env([b[:k] for b in bits])
+    amp = right.amplitudes_env([b[k:] for b in bits], e)[:, 0]
+    assert np.array_equal(amp, full.amplitudes(bits))
+    e = left.transfer_env(left)
+    assert right.transfer_env(right, e)[0, 0] == full.overlap(full)
+    pz = np.diag([1.0, -1.0]).astype(np.complex128)
+    for q in (2, 9):
+        if q < k:
+            v = right.transfer_env(right, left.transfer_env(left, None, pz, q))[0, 0]
+        else:
+            v = right.transfer_env(right, left.transfer_env(left), pz, q - k)[0, 0]
+        assert abs(v - full.expect_1q(pz, q)) <= 1e-14
+    with pytest.raises(ValueError, match="input environment"):
+        right.amplitudes_env([b[k:] for b in bits])

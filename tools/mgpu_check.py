@@ -41,6 +41,13 @@ def main():
     chain.finalize_setup()
     for layer in plan:
         chain.apply_layer(layer, chi, 1e-12)
+    # sharded queries (environments passed rank to rank over NCCL)
+    qbits = ["".join(np.random.default_rng(9).choice(["0", "1"], n)) for _ in range(64)]
+    s_amp = chain.amplitudes(qbits)
+    s_norm = chain.norm()
+    pz = np.diag([1.0, -1.0]).astype(np.complex128)
+    qs = [0, n // 3, n // 2, n - 1]
+    s_exp = [chain.expect_1q(pz, q) for q in qs]
     mine = {i: chain.state.site(i - chain.lo) for i in range(chain.lo, chain.hi)}
     allsites = [None] * world
     dist.all_gather_object(allsites, mine)
@@ -61,9 +68,13 @@ def main():
         bits = ["".join(np.random.default_rng(9).choice(["0", "1"], n)) for _ in range(64)]
         a, b = got.amplitudes(bits), ref.amplitudes(bits)
         err = float(np.max(np.abs(a - b) / np.abs(b)))
-        ok = bool((gb == rb).all()) and err <= 1e-10
+        q_amp = float(np.max(np.abs(s_amp - b) / np.abs(b)))
+        q_norm = abs(s_norm - ref.norm()) / ref.norm()
+        q_exp = max(abs(e - ref.expect_1q(pz, q)) for e, q in zip(s_exp, qs))
+        ok = bool((gb == rb).all()) and err <= 1e-10 and q_amp <= 1e-10 and q_norm <= 1e-12 and q_exp <= 1e-10
         print(f"MGPU world={world} n={n} chi={chi} bonds_equal={bool((gb == rb).all())} "
-              f"max_rel_amp_err={err:.2e} {'OK' if ok else 'FAIL'}", flush=True)
+              f"max_rel_amp_err={err:.2e} sharded_queries: amp {q_amp:.2e} norm {q_norm:.2e} "
+              f"<Z> {q_exp:.2e} {'OK' if ok else 'FAIL'}", flush=True)
         if not ok:
             sys.exit(1)
     dist.barrier()
