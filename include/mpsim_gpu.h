@@ -153,6 +153,14 @@ int mpsim_gpu_move_center(mpsim_gpu_state* s, int32_t center);                  
  * :223-239), op2x2 (nullable) applied to y at local site q (the P9
  * expectation form); env_in host D_left(x) x D_left(y) row-major (NULL =
  * [[1]]), env_out D_right(x) x D_right(y). */
+/* move_center pieces for sharded chains (mps.cpp:57-95): left steps over
+ * sites [i0, i1) (site i -> Q, R into site i+1), right steps over sites i1
+ * down to i0 >= 1 (site i -> Q^H, R^H into site i-1); the ortho centre
+ * becomes unknown. site_norm2: squared Frobenius norm of one site (the
+ * zero-norm centre check, mps.cpp:183-185). */
+int mpsim_gpu_sweep_left(mpsim_gpu_state* s, int32_t i0, int32_t i1);
+int mpsim_gpu_sweep_right(mpsim_gpu_state* s, int32_t i0, int32_t i1);
+int mpsim_gpu_site_norm2(const mpsim_gpu_state* s, int32_t i, double* out);
 int mpsim_gpu_amplitudes_env(const mpsim_gpu_state* s, int32_t i0, int32_t i1, const char* bits, int32_t count,
                              const double* env_in, double* env_out);
 int mpsim_gpu_transfer_env(const mpsim_gpu_state* x, const mpsim_gpu_state* y, int32_t i0, int32_t i1,

@@ -144,6 +144,46 @@ thread_local std::string g_err_canon;
 
 }  // namespace
 
+// Pieces of move_center for site-sharded chains: left steps
+// i = i0 .. i1 - 1 (site i -> Q, R absorbed into i + 1) or right steps
+// i = i1 .. i0 (site i -> Q^H, R^H absorbed into i - 1, i0 >= 1) over the
+// local slots, the boundary step run by the left shard on its ghost slot.
+void sweep_left_impl(State& s, int i0, int i1) {
+  if (i0 < 0 || i1 > s.n - 1 || i0 > i1) fail(MPSIM_EINVAL, "left sweep range out of bounds");
+  DeviceGuard g(s.device);
+  QrWork w;
+  for (int i = i0; i < i1; ++i) left_step(s, w, i);
+  CKC(cudaStreamSynchronize(s.st));
+  CKC(cudaGetLastError());
+  for (DeviceBuf* b : {&w.W, &w.P, &w.Vall, &w.Tall, &w.tau, &w.W1, &w.W2, &w.Q, &w.R, &w.tmp, &w.nrm}) b->release();
+  s.center = -1;
+}
+
+void sweep_right_impl(State& s, int i0, int i1) {
+  if (i0 < 1 || i1 > s.n - 1 || i0 > i1 + 1) fail(MPSIM_EINVAL, "right sweep range out of bounds");
+  DeviceGuard g(s.device);
+  QrWork w;
+  for (int i = i1; i >= i0; --i) right_step(s, w, i);
+  CKC(cudaStreamSynchronize(s.st));
+  CKC(cudaGetLastError());
+  for (DeviceBuf* b : {&w.W, &w.P, &w.Vall, &w.Tall, &w.tau, &w.W1, &w.W2, &w.Q, &w.R, &w.tmp, &w.nrm}) b->release();
+  s.center = -1;
+}
+
+double site_norm2_impl(State& s, int i) {
+  if (i < 0 || i >= s.n) fail(MPSIM_EINVAL, "site index out of range");
+  DeviceGuard g(s.device);
+  DeviceBuf nrm;
+  nrm.ensure(sizeof(double));
+  launch_sum_abs2(s.sites + (long long)i * s.stride, s.chi, (int)(2 * s.sdl[i]), (int)s.sdr[i], (double*)nrm.p, s.st);
+  ++s.launches;
+  double n2 = 0.0;
+  CKC(cudaMemcpyAsync(&n2, nrm.p, sizeof(double), cudaMemcpyDeviceToHost, s.st));
+  CKC(cudaStreamSynchronize(s.st));
+  nrm.release();
+  return n2;
+}
+
 void move_center_impl(State& s, int c) {
   if (c < 0 || c >= s.n) fail(MPSIM_EINVAL, "center out of range");
   DeviceGuard g(s.device);

@@ -1348,6 +1348,21 @@ int mpsim_gpu_move_center(mpsim_gpu_state* s, int32_t center) {  // mps.cpp:177-
   return guarded([&] { move_center_impl(S(s), center); });
 }
 
+int mpsim_gpu_sweep_left(mpsim_gpu_state* s, int32_t i0, int32_t i1) {  // mps.cpp:69-80, sites [i0, i1)
+  return guarded([&] { sweep_left_impl(S(s), i0, i1); });
+}
+
+int mpsim_gpu_sweep_right(mpsim_gpu_state* s, int32_t i0, int32_t i1) {  // mps.cpp:84-95, sites i1 .. i0
+  return guarded([&] { sweep_right_impl(S(s), i0, i1); });
+}
+
+int mpsim_gpu_site_norm2(const mpsim_gpu_state* s, int32_t i, double* out) {
+  return guarded([&] {
+    if (!out) fail(MPSIM_EINVAL, "null output");
+    *out = site_norm2_impl(const_cast<State&>(S(s)), i);
+  });
+}
+
 int mpsim_gpu_norm(const mpsim_gpu_state* s, double* out) {
   return guarded([&] {
     State& a = const_cast<State&>(S(s));

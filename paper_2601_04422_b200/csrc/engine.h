@@ -79,6 +79,9 @@ struct State {
 
 // QR sweeps of move_center (canon.cu).
 void move_center_impl(State& s, int center);
+void sweep_left_impl(State& s, int i0, int i1);
+void sweep_right_impl(State& s, int i0, int i1);
+double site_norm2_impl(State& s, int i);
 
 // Batched Jacobi SVD + truncation + split of the descriptors (engine.cu). The
 // operand comes from the theta kernel (src == nullptr) or, for a single

@@ -213,6 +213,20 @@ class MpsState:
         check(N.lib().mpsim_gpu_overlap(self._h, other._h, out.ctypes.data_as(_DP)))
         return complex(out[0], out[1])
 
+    # ---- move_center pieces (site-sharded chains)
+    def sweep_left(self, i0, i1):
+        """Left steps on sites [i0, i1) (mps.cpp:69-80)."""
+        check(N.lib().mpsim_gpu_sweep_left(self._h, int(i0), int(i1)))
+
+    def sweep_right(self, i0, i1):
+        """Right steps on sites i1 down to i0 >= 1 (mps.cpp:84-95)."""
+        check(N.lib().mpsim_gpu_sweep_right(self._h, int(i0), int(i1)))
+
+    def site_norm2(self, i) -> float:
+        v = C.c_double()
+        check(N.lib().mpsim_gpu_site_norm2(self._h, int(i), C.byref(v)))
+        return v.value
+
     # ---- environment forms (site-sharded chains, SURVEY 8(e) queries)
     def amplitudes_env(self, bitstrings, env_in=None, i0=0, i1=None) -> np.ndarray:
         """Row environments of bit strings (length n, sites [i0, i1) read)

@@ -119,6 +119,9 @@ def lib():
         "mpsim_gpu_overlap": (C.c_int, [VP, VP, DP]),
         "mpsim_gpu_to_statevector": (C.c_int, [VP, I32, DP]),
         "mpsim_gpu_move_center": (C.c_int, [VP, I32]),
+        "mpsim_gpu_sweep_left": (C.c_int, [VP, I32, I32]),
+        "mpsim_gpu_sweep_right": (C.c_int, [VP, I32, I32]),
+        "mpsim_gpu_site_norm2": (C.c_int, [VP, I32, DP]),
         "mpsim_gpu_amplitudes_env": (C.c_int, [VP, I32, I32, C.c_char_p, I32, DP, DP]),
         "mpsim_gpu_transfer_env": (C.c_int, [VP, VP, I32, I32, DP, I32, DP, DP]),
         "mpsim_gpu_expect_1q": (C.c_int, [VP, DP, I32, DP]),

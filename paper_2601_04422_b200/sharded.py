@@ -222,6 +222,71 @@ class ShardedChain:
         da, db = int(self.state.bond_dims()[0]), int(other.state.bond_dims()[0])
         return complex(self._env_chain(lambda e: self.state.transfer_env(other.state, e, op, q, 0, k), (da, db), 1)[0])
 
+    # ---- centre moves across the shards (move_center, mps.cpp:177-187): the
+    # left sweep runs rank by rank towards the centre, each rank absorbing its
+    # last R into its ghost copy of the right neighbour's first site and
+    # handing it back; the right sweep mirrors it from the chain's end, the
+    # left rank running the boundary step on its ghost slot. Same QRs in the
+    # same order as MpsState.move_center.
+    def _p2p(self, send=None, recv=None):
+        torch, dist = self._torch, self.dist
+        dev = f"cuda:{self.device}"
+        ops = []
+        if send is not None:
+            li, dst = send
+            b = self.state.bond_dims()
+            dims = torch.tensor([b[li], b[li + 1]], dtype=torch.int64, device=dev)
+            ops += [dist.P2POp(dist.isend, dims, dst), dist.P2POp(dist.isend, self._slot_tensor(li), dst)]
+        if recv is not None:
+            li, src = recv
+            dims_in = torch.zeros(2, dtype=torch.int64, device=dev)
+            ops += [dist.P2POp(dist.irecv, dims_in, src), dist.P2POp(dist.irecv, self._slot_tensor(li), src)]
+        for r in dist.batch_isend_irecv(ops):
+            r.wait()
+        torch.cuda.synchronize()
+        if recv is not None:
+            dl, dr = (int(x) for x in dims_in.tolist())
+            self.state.set_site_dims(recv[0], dl, dr)
+
+    def move_center(self, c):
+        if not 0 <= c < self.n:
+            raise ValueError("center out of range")
+        if self.world == 1:
+            self.state.move_center(c)
+            return
+        self.state.synchronize()
+        bounds = shard_bounds(self.n, self.world, self.chi)
+        rc = max(r for r in range(self.world) if bounds[r] <= c)
+        k, ghost, r = self.hi - self.lo, self.hi - self.lo, self.rank
+        if r <= rc:  # left sweep, ranks 0 .. rc in order
+            if r > 0:
+                self._p2p(send=(0, r - 1))   # my first site becomes r-1's ghost ...
+                self._p2p(recv=(0, r - 1))   # ... and comes back with its R absorbed
+            if r < rc:
+                self._p2p(recv=(ghost, r + 1))
+                self.state.sweep_left(0, k)
+                self._p2p(send=(ghost, r + 1))
+            else:
+                self.state.sweep_left(0, c - self.lo)
+        if r >= rc:  # right sweep, ranks world-1 .. rc in order
+            if r < self.world - 1:
+                self._p2p(recv=(ghost, r + 1))
+                self.state.sweep_right(ghost, ghost)
+                self._p2p(send=(ghost, r + 1))
+            lo_step = 1 if r > rc else c - self.lo + 1
+            if k - 1 >= lo_step:
+                self.state.sweep_right(lo_step, k - 1)
+            if r > rc:
+                self._p2p(send=(0, r - 1))
+                self._p2p(recv=(0, r - 1))
+        bad = self._torch.zeros(1, dtype=self._torch.float64, device=f"cuda:{self.device}")
+        if r == rc and np.sqrt(self.state.site_norm2(c - self.lo)) < 1e-14:
+            bad += 1.0
+        self.dist.all_reduce(bad)
+        if bad.item() > 0:
+            raise N.NumericError("cannot canonicalize a zero-norm state")
+        self.center = c
+
     def overlap(self, other: "ShardedChain") -> complex:
         """<self|other> (mps.cpp:223-239) of two chains sharded alike."""
         return self._transfer(other)

@@ -51,6 +51,12 @@ def main():
     mine = {i: chain.state.site(i - chain.lo) for i in range(chain.lo, chain.hi)}
     allsites = [None] * world
     dist.all_gather_object(allsites, mine)
+    # centre move across the shards (QR sweeps handed rank to rank)
+    cc = (2 * n) // 3
+    chain.move_center(cc)
+    mine2 = {i: chain.state.site(i - chain.lo) for i in range(chain.lo, chain.hi)}
+    allsites2 = [None] * world
+    dist.all_gather_object(allsites2, mine2)
     if rank == 0:
         full = {}
         for d in allsites:
@@ -75,7 +81,20 @@ def main():
         print(f"MGPU world={world} n={n} chi={chi} bonds_equal={bool((gb == rb).all())} "
               f"max_rel_amp_err={err:.2e} sharded_queries: amp {q_amp:.2e} norm {q_norm:.2e} "
               f"<Z> {q_exp:.2e} {'OK' if ok else 'FAIL'}", flush=True)
-        if not ok:
+        full2 = {}
+        for d in allsites2:
+            full2.update(d)
+        got2 = P.MpsState(n, chi_hint=chi, device=local)
+        for i in range(n):
+            got2.set_site(i, full2[i])
+        ref.move_center(cc)
+        mb_ok = bool((got2.bond_dims() == ref.bond_dims()).all())
+        m_err = float(np.max(np.abs(got2.amplitudes(bits) - ref.amplitudes(bits)) / np.abs(ref.amplitudes(bits))))
+        site_eq = all(np.array_equal(full2[i], ref.site(i)) for i in range(n))
+        ok2 = mb_ok and m_err <= 1e-10
+        print(f"MGPU world={world} n={n} chi={chi} move_center({cc}): bonds_equal={mb_ok} "
+              f"max_rel_amp_err={m_err:.2e} sites_bit_identical={site_eq} {'OK' if ok2 else 'FAIL'}", flush=True)
+        if not (ok and ok2):
             sys.exit(1)
     dist.barrier()
     dist.destroy_process_group()
