@@ -183,6 +183,21 @@ int mpsim_gpu_sample(mpsim_gpu_sampler* sp, uint64_t shots, uint64_t seed, int32
 int mpsim_gpu_sampler_result(const mpsim_gpu_sampler* sp, int32_t i, char* bits /* n chars */, uint64_t* count);
 int mpsim_gpu_sampler_stats(const mpsim_gpu_sampler* sp, uint64_t* cache_hits, uint64_t* cache_size);
 int mpsim_gpu_sampler_clear_cache(mpsim_gpu_sampler* sp);
+/* The sampler's site walk over sites [i0, i1) of an already canonicalised
+ * state (a shard of a right-canonical chain): u holds shots x
+ * (i1 - i0) variates (the reference's shot-major stream restricted to these
+ * sites); env_in (host, u_in x D_left complex, NULL = chain start with one
+ * node) and node_in (shots, NULL = all 0) carry the distinct prefixes of the
+ * sites to the left. Outputs: *u_out distinct prefixes at i1, env_out (host,
+ * capacity shots x D_right complex, nullable) their normalised
+ * environments, node_out (shots) each shot's prefix, bits_out (shots x
+ * (i1 - i0) chars) each shot's bits on these sites. */
+int mpsim_gpu_sample_segment(const mpsim_gpu_state* s, int32_t i0, int32_t i1, uint64_t shots, const double* u,
+                             int32_t u_in, const double* env_in, const int32_t* node_in, int32_t* u_out,
+                             double* env_out, int32_t* node_out, char* bits_out);
+/* count variates of std::mt19937_64(seed) after skipping skip draws, as
+ * (x >> 11) * 2^-53 (generators.cpp:31-33, sampler.cpp:115). Host only. */
+int mpsim_uniform_variates(uint64_t seed, uint64_t skip, uint64_t count, double* out);
 
 /* ---- instrumentation ----------------------------------------------------- */
 /* Kernel launches and device time accumulated on the state's stream since

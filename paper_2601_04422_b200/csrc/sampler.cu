@@ -123,25 +123,17 @@ struct mpsim_gpu_sampler {
 
 namespace {
 
-void run_sample(mpsim_gpu_sampler& sp, uint64_t shots, uint64_t seed) {
-  State& s = *sp.st;
-  const int n = sp.n;
-  DeviceGuard g(s.device);
-  // Variates in the reference order: shot-major, one per site.
-  std::mt19937_64 eng(seed);
-  std::vector<double> u((size_t)shots * n);
-  for (size_t i = 0; i < u.size(); ++i) u[i] = static_cast<double>(eng() >> 11) * 0x1.0p-53;
-
-  std::vector<int> node_of(shots, 0);  // shot -> node at the current depth
-  std::vector<std::string> prefix(1, std::string());  // node -> prefix
-  int U = 1;
-  DeviceBuf dE, dE2, dT, dRaw, dSrc, dBit, dScale;
-  const long long c = s.chi;
-  dE.ensure(sizeof(cplx) * c);
+// The walk over sites [i0, i1): U distinct prefixes (nodes) with their left
+// environments dE (U x sdl[i0], device, ld = sdl[i0]); node_of[shot] the
+// shot's node; prefix[node] its bits so far; u(shot, site) the variate.
+// On return dE holds the U' x sdr[i1 - 1] environments of the new nodes.
+template <class Var>
+void sample_walk(State& s, int i0, int i1, uint64_t shots, Var u, int& U, DeviceBuf& dE,
+                 std::vector<int>& node_of, std::vector<std::string>& prefix) {
+  DeviceBuf dE2, dT, dRaw, dSrc, dBit, dScale;
   const cplx one = make_double2(1.0, 0.0);
-  CKS(cudaMemcpyAsync(dE.p, &one, sizeof(cplx), cudaMemcpyHostToDevice, s.st));
   std::vector<double> raw;
-  for (int site = 0; site < n; ++site) {
+  for (int site = i0; site < i1; ++site) {
     const int dl = (int)s.sdl[site], dr = (int)s.sdr[site];
     const cplx* A = s.sites + (long long)site * s.stride;
     dT.ensure(sizeof(cplx) * (size_t)U * 2 * dr);
@@ -172,7 +164,7 @@ void run_sample(mpsim_gpu_sampler& sp, uint64_t shots, uint64_t seed) {
     std::vector<std::string> nprefix;
     for (uint64_t sh = 0; sh < shots; ++sh) {
       const int k = node_of[sh];
-      const int b = u[sh * n + site] < p0[(size_t)k] ? 0 : 1;  // sampler.cpp:116-117
+      const int b = u(sh, site) < p0[(size_t)k] ? 0 : 1;  // sampler.cpp:116-117
       int& cid = child_id[2 * (size_t)k + b];
       if (cid < 0) {
         const double r = raw[2 * (size_t)k + b];
@@ -205,6 +197,25 @@ void run_sample(mpsim_gpu_sampler& sp, uint64_t shots, uint64_t seed) {
     prefix.swap(nprefix);
     U = U2;
   }
+}
+
+void run_sample(mpsim_gpu_sampler& sp, uint64_t shots, uint64_t seed) {
+  State& s = *sp.st;
+  const int n = sp.n;
+  DeviceGuard g(s.device);
+  // Variates in the reference order: shot-major, one per site.
+  std::mt19937_64 eng(seed);
+  std::vector<double> u((size_t)shots * n);
+  for (size_t i = 0; i < u.size(); ++i) u[i] = static_cast<double>(eng() >> 11) * 0x1.0p-53;
+
+  std::vector<int> node_of(shots, 0);  // shot -> node at the current depth
+  std::vector<std::string> prefix(1, std::string());  // node -> prefix
+  int U = 1;
+  DeviceBuf dE;
+  dE.ensure(sizeof(cplx) * s.chi);
+  const cplx one = make_double2(1.0, 0.0);
+  CKS(cudaMemcpyAsync(dE.p, &one, sizeof(cplx), cudaMemcpyHostToDevice, s.st));
+  sample_walk(s, 0, n, shots, [&](uint64_t sh, int site) { return u[sh * n + site]; }, U, dE, node_of, prefix);
   // counts, lexicographic (std::map order, sampler.cpp:140)
   std::vector<uint64_t> cnt((size_t)U, 0);
   for (uint64_t sh = 0; sh < shots; ++sh) ++cnt[(size_t)node_of[sh]];
@@ -265,6 +276,58 @@ int mpsim_gpu_sampler_create(const mpsim_gpu_state* s, int32_t memoize, uint64_t
       throw;
     }
     *out = sp;
+  });
+}
+
+int mpsim_gpu_sample_segment(const mpsim_gpu_state* s, int32_t i0, int32_t i1, uint64_t shots, const double* u,
+                             int32_t u_in, const double* env_in, const int32_t* node_in, int32_t* u_out,
+                             double* env_out, int32_t* node_out, char* bits_out) {
+  return sguard([&] {
+    if (!s || !u || !u_out || !node_out || !bits_out) fail(MPSIM_EINVAL, "null argument");
+    State& st = const_cast<State&>(*reinterpret_cast<const State*>(s));
+    if (i0 < 0 || i1 > st.n || i0 >= i1) fail(MPSIM_EINVAL, "site range out of bounds");
+    if (shots == 0) fail(MPSIM_EINVAL, "shots must be positive");
+    DeviceGuard g(st.device);
+    const int w = i1 - i0;
+    int U = env_in ? u_in : 1;
+    if (U < 1) fail(MPSIM_EINVAL, "need at least one input environment");
+    if (!env_in && st.sdl[i0] != 1) fail(MPSIM_EINVAL, "open left bond needs input environments");
+    DeviceBuf dE;
+    const long long dl0 = st.sdl[i0];
+    dE.ensure(sizeof(cplx) * (size_t)U * dl0);
+    if (env_in) {
+      CKS(cudaMemcpyAsync(dE.p, env_in, sizeof(cplx) * (size_t)U * dl0, cudaMemcpyHostToDevice, st.st));
+    } else {
+      const cplx one = make_double2(1.0, 0.0);
+      CKS(cudaMemcpyAsync(dE.p, &one, sizeof(cplx), cudaMemcpyHostToDevice, st.st));
+    }
+    std::vector<int> node_of(shots, 0);
+    if (env_in && node_in)
+      for (uint64_t sh = 0; sh < shots; ++sh) {
+        if (node_in[sh] < 0 || node_in[sh] >= U) fail(MPSIM_EINVAL, "node index out of range");
+        node_of[sh] = node_in[sh];
+      }
+    std::vector<std::string> prefix((size_t)U, std::string());
+    sample_walk(st, i0, i1, shots, [&](uint64_t sh, int site) { return u[sh * w + (site - i0)]; }, U, dE, node_of,
+                prefix);
+    const long long dr = st.sdr[i1 - 1];
+    if (env_out)
+      CKS(cudaMemcpyAsync(env_out, dE.p, sizeof(cplx) * (size_t)U * dr, cudaMemcpyDeviceToHost, st.st));
+    CKS(cudaStreamSynchronize(st.st));
+    *u_out = U;
+    for (uint64_t sh = 0; sh < shots; ++sh) {
+      node_out[sh] = node_of[sh];
+      std::memcpy(bits_out + sh * w, prefix[(size_t)node_of[sh]].data(), (size_t)w);
+    }
+  });
+}
+
+int mpsim_uniform_variates(uint64_t seed, uint64_t skip, uint64_t count, double* out) {
+  return sguard([&] {
+    if (!out && count) fail(MPSIM_EINVAL, "null output");
+    std::mt19937_64 eng(seed);
+    eng.discard(skip);
+    for (uint64_t i = 0; i < count; ++i) out[i] = static_cast<double>(eng() >> 11) * 0x1.0p-53;
   });
 }
 

@@ -227,6 +227,33 @@ class MpsState:
         check(N.lib().mpsim_gpu_site_norm2(self._h, int(i), C.byref(v)))
         return v.value
 
+    def sample_segment(self, i0, i1, u, env_in=None, node_in=None):
+        """The sampler's site walk over sites [i0, i1) of a canonicalised
+        state: u (shots x (i1 - i0)) variates; env_in (U x D_left) / node_in
+        (shots) the prefixes from the left. Returns (env_out U' x D_right,
+        node_out, bits) with bits a list of per-shot strings."""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        shots, w = u.shape
+        dims = self.bond_dims()
+        ein = nin = None
+        uin = 1
+        if env_in is not None:
+            ein = np.ascontiguousarray(env_in, dtype=np.complex128)
+            uin = ein.shape[0]
+            nin = np.ascontiguousarray(node_in, dtype=np.int32)
+        dr = int(dims[i1])
+        eout = np.zeros((shots, dr), dtype=np.complex128)
+        nout = np.zeros(shots, dtype=np.int32)
+        bits = C.create_string_buffer(shots * w)
+        uo = N.I32()
+        check(N.lib().mpsim_gpu_sample_segment(
+            self._h, int(i0), int(i1), shots, u.ctypes.data_as(_DP), uin,
+            None if ein is None else ein.ctypes.data_as(_DP),
+            None if nin is None else nin.ctypes.data_as(C.POINTER(N.I32)), C.byref(uo), eout.ctypes.data_as(_DP),
+            nout.ctypes.data_as(C.POINTER(N.I32)), bits))
+        raw = bits.raw.decode()
+        return eout[: uo.value], nout, [raw[i * w:(i + 1) * w] for i in range(shots)]
+
     # ---- environment forms (site-sharded chains, SURVEY 8(e) queries)
     def amplitudes_env(self, bitstrings, env_in=None, i0=0, i1=None) -> np.ndarray:
         """Row environments of bit strings (length n, sites [i0, i1) read)
@@ -384,6 +411,13 @@ class Sampler:
 
     def clear_cache(self):
         check(N.lib().mpsim_gpu_sampler_clear_cache(self._h))
+
+
+def uniform_variates(seed, skip, count) -> np.ndarray:
+    """std::mt19937_64(seed) draws skip .. skip + count as (x >> 11) 2^-53."""
+    out = np.zeros(int(count))
+    check(N.lib().mpsim_uniform_variates(int(seed), int(skip), int(count), out.ctypes.data_as(_DP)))
+    return out
 
 
 def sample(state: MpsState, shots, seed, memoize=True, cache_cap=0):

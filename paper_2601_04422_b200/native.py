@@ -132,6 +132,9 @@ def lib():
         "mpsim_gpu_sampler_result": (C.c_int, [VP, I32, C.c_char_p, C.POINTER(U64)]),
         "mpsim_gpu_sampler_stats": (C.c_int, [VP, C.POINTER(U64), C.POINTER(U64)]),
         "mpsim_gpu_sampler_clear_cache": (C.c_int, [VP]),
+        "mpsim_gpu_sample_segment": (C.c_int, [VP, I32, I32, U64, DP, I32, DP, C.POINTER(I32), C.POINTER(I32), DP,
+                                               C.POINTER(I32), C.c_char_p]),
+        "mpsim_uniform_variates": (C.c_int, [U64, U64, U64, DP]),
         "mpsim_gpu_counters": (C.c_int, [VP, C.POINTER(I64), DP, C.POINTER(I64)]),
         "mpsim_gpu_kernel_counters": (C.c_int, [VP, C.POINTER(I64), DP, DP, DP]),
         "mpsim_gpu_transfer_counters": (C.c_int, [VP, C.POINTER(I64), C.POINTER(I64)]),

@@ -287,6 +287,61 @@ class ShardedChain:
             raise N.NumericError("cannot canonicalize a zero-norm state")
         self.center = c
 
+    # ---- perfect sampling across the shards (Sampler, sampler.cpp:35-143)
+    def _clone(self):
+        c = object.__new__(ShardedChain)
+        c.__dict__.update(self.__dict__)
+        c.state = self.state.copy()
+        if self.world > 1:
+            c.state.set_open_boundaries(True)
+        return c
+
+    def sample(self, shots, seed, chunk=4096):
+        """Counts of `shots` perfect samples, identical to Sampler(state).sample
+        on the whole chain: a left + right canonicalised copy, then each rank
+        walks its sites for every shot from the distinct-prefix environments
+        its left neighbour hands over; variates are the reference's
+        shot-major mt19937_64 stream restricted to the rank's sites."""
+        from .mps import uniform_variates
+        if shots <= 0:
+            raise ValueError("shots must be positive")
+        nrm = self.norm()
+        if abs(nrm - 1.0) > 1e-8:  # sampler.cpp:36-40
+            raise N.NumericError(f"sampling requires a normalized state, norm is {nrm:.6f}")
+        prep = self._clone()
+        prep.move_center(self.n - 1)  # left_canonicalize (sampler.cpp:46)
+        prep.move_center(0)           # right_canonicalize (sampler.cpp:47)
+        k, n = self.hi - self.lo, self.n
+        counts = {}
+        torch, dist = self._torch, self.dist
+        dev = f"cuda:{self.device}"
+        for c0 in range(0, shots, chunk):
+            cs = min(chunk, shots - c0)
+            u = uniform_variates(seed, c0 * n, cs * n).reshape(cs, n)[:, self.lo:self.hi]
+            env_in = node_in = None
+            if self.rank > 0:
+                meta = torch.zeros(1, dtype=torch.int64, device=dev)
+                dist.recv(meta, self.rank - 1)
+                U = int(meta.item())
+                d0 = int(prep.state.bond_dims()[0])
+                t_env = torch.empty((U, d0), dtype=torch.complex128, device=dev)
+                t_node = torch.empty((cs,), dtype=torch.int32, device=dev)
+                dist.recv(t_env, self.rank - 1)
+                dist.recv(t_node, self.rank - 1)
+                env_in, node_in = t_env.cpu().numpy(), t_node.cpu().numpy()
+            env_out, node_out, bits = prep.state.sample_segment(0, k, u, env_in, node_in)
+            if self.rank < self.world - 1:
+                dist.send(torch.tensor([env_out.shape[0]], dtype=torch.int64, device=dev), self.rank + 1)
+                dist.send(torch.from_numpy(np.ascontiguousarray(env_out)).to(dev), self.rank + 1)
+                dist.send(torch.from_numpy(node_out).to(dev), self.rank + 1)
+            parts = [None] * self.world if self.world > 1 else [bits]
+            if self.world > 1:
+                dist.all_gather_object(parts, bits)
+            for sh in range(cs):
+                key = "".join(p[sh] for p in parts)
+                counts[key] = counts.get(key, 0) + 1
+        return dict(sorted(counts.items()))
+
     def overlap(self, other: "ShardedChain") -> complex:
         """<self|other> (mps.cpp:223-239) of two chains sharded alike."""
         return self._transfer(other)

@@ -177,3 +177,34 @@ def test_sweep_pieces_compose_to_move_center(gpu, oracle):
     for i in range(n):
         assert np.array_equal(a.site(i), b.site(i)), i
     assert b.site_norm2(c) > 0
+
+
+def test_sample_segments_compose_to_the_sampler(gpu, oracle):
+    """The sharded sampler's pieces: the site walk split at k over a
+    canonicalised copy, fed the reference's variate stream restricted to each
+    part, gives exactly the counts of sample() on the whole chain; and a
+    one-rank ShardedChain.sample agrees too."""
+    from paper_2601_04422_b200 import sharded
+    from paper_2601_04422_b200.mps import uniform_variates
+    n, k, shots, seed = 12, 5, 2000, 77
+    o = oracle.MpsState.random(n, 8, 21)
+    g = gpu.MpsState(n, chi_hint=16)
+    for i in range(n):
+        g.set_site(i, o.site(i))
+    g.move_center(0)
+    g.set_site(0, g.site(0) / g.norm())
+    want = gpu.sample(g, shots, seed)
+    prep = g.copy()
+    prep.move_center(n - 1)
+    prep.move_center(0)
+    u = uniform_variates(seed, 0, shots * n).reshape(shots, n)
+    env, node, b1 = prep.sample_segment(0, k, u[:, :k])
+    _, _, b2 = prep.sample_segment(k, n, u[:, k:], env, node)
+    got = {}
+    for x, y in zip(b1, b2):
+        got[x + y] = got.get(x + y, 0) + 1
+    assert got == want
+    ch = sharded.ShardedChain(n, 16, 0, 1)
+    for i in range(n):
+        ch.set_site(i, g.site(i))
+    assert ch.sample(shots, seed, chunk=512) == want

@@ -55,6 +55,11 @@ def main():
     cc = (2 * n) // 3
     chain.move_center(cc)
     mine2 = {i: chain.state.site(i - chain.lo) for i in range(chain.lo, chain.hi)}
+    # normalise at the centre, then sample across the shards
+    nrm = chain.norm()
+    if chain.lo <= cc < chain.hi:
+        chain.state.set_site(cc - chain.lo, chain.state.site(cc - chain.lo) / nrm)
+    s_counts = chain.sample(3000, 5, chunk=1024)
     allsites2 = [None] * world
     dist.all_gather_object(allsites2, mine2)
     if rank == 0:
@@ -91,7 +96,12 @@ def main():
         mb_ok = bool((got2.bond_dims() == ref.bond_dims()).all())
         m_err = float(np.max(np.abs(got2.amplitudes(bits) - ref.amplitudes(bits)) / np.abs(ref.amplitudes(bits))))
         site_eq = all(np.array_equal(full2[i], ref.site(i)) for i in range(n))
-        ok2 = mb_ok and m_err <= 1e-10
+        ref.set_site(cc, ref.site(cc) / ref.norm())
+        r_counts = P.sample(ref, 3000, 5)
+        ok3 = s_counts == r_counts
+        print(f"MGPU world={world} n={n} chi={chi} sharded sample(3000, seed 5): {len(s_counts)} outcomes, "
+              f"counts_equal={ok3} {'OK' if ok3 else 'FAIL'}", flush=True)
+        ok2 = mb_ok and m_err <= 1e-10 and ok3
         print(f"MGPU world={world} n={n} chi={chi} move_center({cc}): bonds_equal={mb_ok} "
               f"max_rel_amp_err={m_err:.2e} sites_bit_identical={site_eq} {'OK' if ok2 else 'FAIL'}", flush=True)
         if not (ok and ok2):
