@@ -156,6 +156,18 @@ static int phase_probe() {
   return v;
 }
 
+// Cross-block-only pair EVDs outside a period of rounds in the asymptotic
+// sweeps: MPSIM_ALT_CROSS=2 (odd rounds, default), 3 (two rounds in three)
+// or 0 (full EVDs every round, A/B). Returns the active bits to add.
+static int alt_cross_bits() {
+  static const int bits = [] {
+    const char* v = std::getenv("MPSIM_ALT_CROSS");
+    const int p = v ? std::atoi(v) : 2;
+    return p == 2 ? 16 : p == 3 ? (16 | 32) : 0;
+  }();
+  return bits;
+}
+
 // MPSIM_FIRST_INBLOCK=0 computes every Gram tile in the first sweep (A/B).
 static bool first_sweep_inblock() {
   static const bool on = [] {
@@ -495,7 +507,8 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   // policy below flags. It cannot end the iteration through kQuadFinish (its
   // maxoff saw in-block values that may be stale); only a sweep without any
   // rotation — whose Grams were then all computed exactly — ends it.
-  const int first = (jacobi_mode() >= 3 && inblock_policy() && first_sweep_inblock()) ? (1 | 4) : 1;
+  const int first = ((jacobi_mode() >= 3 && inblock_policy() && first_sweep_inblock()) ? (1 | 4) : 1) |
+                    alt_cross_bits();
   for (int i = 0; i < ng; ++i) h_rot[i] = first;
   CK(cudaMemcpyAsync(s.d_active.p, h_rot, sizeof(int) * ng, cudaMemcpyHostToDevice, st));
   bool converged = false;
@@ -602,6 +615,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       if (h_rot[i] && cross_policy() && rms > cross_rms() && h_maxoff[i] > 1e-3 && sweep < cross_sweeps() &&
           descs[i].nb >= 8)
         h_rot[i] |= 2;
+      if (h_rot[i]) h_rot[i] |= alt_cross_bits();
       // pre-asymptotic and early asymptotic sweeps reuse the in-block Grams the
       // pair EVDs leave behind (jacobi_split.cu); the closing sweeps recompute all
       if (h_rot[i] && jacobi_mode() >= 3 && inblock_policy() && h_maxoff[i] > kInblockMaxoff) h_rot[i] |= 4;

@@ -187,6 +187,16 @@ __device__ __forceinline__ void copy_rotation(const cplx* R, long long rpitch, c
 
 }  // namespace
 
+// Cross-block-only pair EVD: every round of a pre-asymptotic sweep (active
+// bit 2), else the rounds off a period of 2 (bit 16) or 3 (bits 16 | 32):
+// the remaining rounds still rotate the in-block pairs, which keeps the
+// outer sweep count (tools/emu_jacobi.py).
+__device__ __forceinline__ bool cross_only_evd(int active, int round) {
+  if (active & 2) return true;
+  if (!(active & 16)) return false;
+  return round % ((active & 32) ? 3 : 2) != 0;
+}
+
 // kMode 0: Gram only (G -> gbuf); 1: Gram + pair EVD (R -> rbuf); 2: the whole
 // pair visit, Gram + EVD + rotation, in one CTA.
 struct RoundArgs {
@@ -431,7 +441,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
         R[(idx / kP) * kPad + idx % kP] = make_double2(idx / kP == idx % kP ? 1.0 : 0.0, 0.0);
       __syncthreads();
     } else {
-      pair_evd_v1(SG, R, S.sc, t, tol_in, floor2, 1, (active[gi] & 2) != 0);
+      pair_evd_v1(SG, R, S.sc, t, tol_in, floor2, 1, cross_only_evd(active[gi], round));
     }
     if (probe == 2) return;  // Gram + EVD
     __syncthreads();
@@ -539,7 +549,7 @@ __global__ void __launch_bounds__(256, 6) jacobi_evd_kernel(const GateDesc* __re
   const cplx* gin = gbuf + slot * (kP * kP);
   for (int idx = t; idx < kP * kP; idx += 256) S.G[(idx / kP) * kPad + idx % kP] = gin[idx];
   __syncthreads();
-  pair_evd_v1(S.G, S.R, S.sc, t, tol_in, floor_rel2 * frob2[gi], 1, (active[gi] & 2) != 0);
+  pair_evd_v1(S.G, S.R, S.sc, t, tol_in, floor_rel2 * frob2[gi], 1, cross_only_evd(active[gi], round));
   __syncthreads();
   cplx* rout = rbuf + slot * (kP * kP);
   for (int idx = t; idx < kP * kP; idx += 256) rout[idx] = S.R[(idx / kP) * kPad + idx % kP];
