@@ -312,7 +312,7 @@ class ShardedChain:
         prep.move_center(self.n - 1)  # left_canonicalize (sampler.cpp:46)
         prep.move_center(0)           # right_canonicalize (sampler.cpp:47)
         k, n = self.hi - self.lo, self.n
-        counts = {}
+        counts, mine = {}, []
         torch, dist = self._torch, self.dist
         dev = f"cuda:{self.device}"
         for c0 in range(0, shots, chunk):
@@ -334,12 +334,16 @@ class ShardedChain:
                 dist.send(torch.tensor([env_out.shape[0]], dtype=torch.int64, device=dev), self.rank + 1)
                 dist.send(torch.from_numpy(np.ascontiguousarray(env_out)).to(dev), self.rank + 1)
                 dist.send(torch.from_numpy(node_out).to(dev), self.rank + 1)
-            parts = [None] * self.world if self.world > 1 else [bits]
-            if self.world > 1:
-                dist.all_gather_object(parts, bits)
-            for sh in range(cs):
-                key = "".join(p[sh] for p in parts)
-                counts[key] = counts.get(key, 0) + 1
+            mine.extend(bits)
+        # one gather after the chunk loop: no per-chunk collective, so rank r
+        # runs chunk j while rank r + 1 is still on chunk j - 1 (the handed
+        # environments are the only coupling between ranks)
+        parts = [None] * self.world if self.world > 1 else [mine]
+        if self.world > 1:
+            dist.all_gather_object(parts, mine)
+        for sh in range(shots):
+            key = "".join(p[sh] for p in parts)
+            counts[key] = counts.get(key, 0) + 1
         return dict(sorted(counts.items()))
 
     def overlap(self, other: "ShardedChain") -> complex:

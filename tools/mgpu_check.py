@@ -59,7 +59,12 @@ def main():
     nrm = chain.norm()
     if chain.lo <= cc < chain.hi:
         chain.state.set_site(cc - chain.lo, chain.state.site(cc - chain.lo) / nrm)
+    import time
+    chain.sample(3000, 5, chunk=1024)  # warm-up (communicators, allocations)
+    dist.barrier()
+    t0 = time.perf_counter()
     s_counts = chain.sample(3000, 5, chunk=1024)
+    t_sample = chain.max_over_ranks(time.perf_counter() - t0)
     allsites2 = [None] * world
     dist.all_gather_object(allsites2, mine2)
     if rank == 0:
@@ -100,7 +105,7 @@ def main():
         r_counts = P.sample(ref, 3000, 5)
         ok3 = s_counts == r_counts
         print(f"MGPU world={world} n={n} chi={chi} sharded sample(3000, seed 5): {len(s_counts)} outcomes, "
-              f"counts_equal={ok3} {'OK' if ok3 else 'FAIL'}", flush=True)
+              f"{t_sample * 1e3:.1f} ms (max over ranks), counts_equal={ok3} {'OK' if ok3 else 'FAIL'}", flush=True)
         ok2 = mb_ok and m_err <= 1e-10 and ok3
         print(f"MGPU world={world} n={n} chi={chi} move_center({cc}): bonds_equal={mb_ok} "
               f"max_rel_amp_err={m_err:.2e} sites_bit_identical={site_eq} {'OK' if ok2 else 'FAIL'}", flush=True)
