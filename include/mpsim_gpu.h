@@ -195,6 +195,13 @@ int mpsim_gpu_sampler_clear_cache(mpsim_gpu_sampler* sp);
 int mpsim_gpu_sample_segment(const mpsim_gpu_state* s, int32_t i0, int32_t i1, uint64_t shots, const double* u,
                              int32_t u_in, const double* env_in, const int32_t* node_in, int32_t* u_out,
                              double* env_out, int32_t* node_out, char* bits_out);
+/* As mpsim_gpu_sample_segment, but env_in / env_out are device pointers on
+ * the state's device (the rank-to-rank prefix environments stay in HBM and go
+ * straight to NCCL send/recv; SURVEY 8(e) "Queries"). The caller orders any
+ * producer of env_in before the call; env_out is complete on return. */
+int mpsim_gpu_sample_segment_dev(const mpsim_gpu_state* s, int32_t i0, int32_t i1, uint64_t shots, const double* u,
+                                 int32_t u_in, const double* env_in, const int32_t* node_in, int32_t* u_out,
+                                 double* env_out, int32_t* node_out, char* bits_out);
 /* count variates of std::mt19937_64(seed) after skipping skip draws, as
  * (x >> 11) * 2^-53 (generators.cpp:31-33, sampler.cpp:115). Host only. */
 int mpsim_uniform_variates(uint64_t seed, uint64_t skip, uint64_t count, double* out);

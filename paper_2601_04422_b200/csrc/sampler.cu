@@ -279,9 +279,15 @@ int mpsim_gpu_sampler_create(const mpsim_gpu_state* s, int32_t memoize, uint64_t
   });
 }
 
-int mpsim_gpu_sample_segment(const mpsim_gpu_state* s, int32_t i0, int32_t i1, uint64_t shots, const double* u,
-                             int32_t u_in, const double* env_in, const int32_t* node_in, int32_t* u_out,
-                             double* env_out, int32_t* node_out, char* bits_out) {
+}  // extern "C"
+
+namespace {
+
+// env_dev: env_in / env_out live on the state's device (the sharded sampler's
+// hand-off buffers, NCCL send/recv'd without a host round trip), else host.
+int sample_segment_impl(const mpsim_gpu_state* s, int32_t i0, int32_t i1, uint64_t shots, const double* u,
+                        int32_t u_in, const double* env_in, const int32_t* node_in, int32_t* u_out, double* env_out,
+                        int32_t* node_out, char* bits_out, bool env_dev) {
   return sguard([&] {
     if (!s || !u || !u_out || !node_out || !bits_out) fail(MPSIM_EINVAL, "null argument");
     State& st = const_cast<State&>(*reinterpret_cast<const State*>(s));
@@ -296,7 +302,8 @@ int mpsim_gpu_sample_segment(const mpsim_gpu_state* s, int32_t i0, int32_t i1, u
     const long long dl0 = st.sdl[i0];
     dE.ensure(sizeof(cplx) * (size_t)U * dl0);
     if (env_in) {
-      CKS(cudaMemcpyAsync(dE.p, env_in, sizeof(cplx) * (size_t)U * dl0, cudaMemcpyHostToDevice, st.st));
+      CKS(cudaMemcpyAsync(dE.p, env_in, sizeof(cplx) * (size_t)U * dl0,
+                          env_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st.st));
     } else {
       const cplx one = make_double2(1.0, 0.0);
       CKS(cudaMemcpyAsync(dE.p, &one, sizeof(cplx), cudaMemcpyHostToDevice, st.st));
@@ -312,7 +319,8 @@ int mpsim_gpu_sample_segment(const mpsim_gpu_state* s, int32_t i0, int32_t i1, u
                 prefix);
     const long long dr = st.sdr[i1 - 1];
     if (env_out)
-      CKS(cudaMemcpyAsync(env_out, dE.p, sizeof(cplx) * (size_t)U * dr, cudaMemcpyDeviceToHost, st.st));
+      CKS(cudaMemcpyAsync(env_out, dE.p, sizeof(cplx) * (size_t)U * dr,
+                          env_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, st.st));
     CKS(cudaStreamSynchronize(st.st));
     *u_out = U;
     for (uint64_t sh = 0; sh < shots; ++sh) {
@@ -320,6 +328,22 @@ int mpsim_gpu_sample_segment(const mpsim_gpu_state* s, int32_t i0, int32_t i1, u
       std::memcpy(bits_out + sh * w, prefix[(size_t)node_of[sh]].data(), (size_t)w);
     }
   });
+}
+
+}  // namespace
+
+extern "C" {
+
+int mpsim_gpu_sample_segment(const mpsim_gpu_state* s, int32_t i0, int32_t i1, uint64_t shots, const double* u,
+                             int32_t u_in, const double* env_in, const int32_t* node_in, int32_t* u_out,
+                             double* env_out, int32_t* node_out, char* bits_out) {
+  return sample_segment_impl(s, i0, i1, shots, u, u_in, env_in, node_in, u_out, env_out, node_out, bits_out, false);
+}
+
+int mpsim_gpu_sample_segment_dev(const mpsim_gpu_state* s, int32_t i0, int32_t i1, uint64_t shots, const double* u,
+                                 int32_t u_in, const double* env_in, const int32_t* node_in, int32_t* u_out,
+                                 double* env_out, int32_t* node_out, char* bits_out) {
+  return sample_segment_impl(s, i0, i1, shots, u, u_in, env_in, node_in, u_out, env_out, node_out, bits_out, true);
 }
 
 int mpsim_uniform_variates(uint64_t seed, uint64_t skip, uint64_t count, double* out) {

@@ -254,6 +254,33 @@ class MpsState:
         raw = bits.raw.decode()
         return eout[: uo.value], nout, [raw[i * w:(i + 1) * w] for i in range(shots)]
 
+    def sample_segment_dev(self, i0, i1, u, env_out, env_in=None, node_in=None):
+        """sample_segment with the prefix environments in HBM: env_in
+        (U x D_left) and env_out (capacity shots x D_right) are contiguous
+        complex128 CUDA tensors on the state's device (the sharded sampler's
+        NCCL hand-off buffers). Returns (U', node_out, bits); env_out[:U']
+        holds the distinct prefixes' environments."""
+        u = np.ascontiguousarray(u, dtype=np.float64)
+        shots, w = u.shape
+        if env_out.shape[0] < shots or env_out.shape[1] != int(self.bond_dims()[i1]) or not env_out.is_contiguous():
+            raise ValueError("env_out must be a contiguous (shots x D_right) tensor")
+        uin, nin = 1, None
+        if env_in is not None:
+            if not env_in.is_contiguous():
+                raise ValueError("env_in must be contiguous")
+            uin = int(env_in.shape[0])
+            nin = np.ascontiguousarray(node_in, dtype=np.int32)
+        nout = np.zeros(shots, dtype=np.int32)
+        bits = C.create_string_buffer(shots * w)
+        uo = N.I32()
+        check(N.lib().mpsim_gpu_sample_segment_dev(
+            self._h, int(i0), int(i1), shots, u.ctypes.data_as(_DP), uin,
+            None if env_in is None else C.c_void_p(env_in.data_ptr()),
+            None if nin is None else nin.ctypes.data_as(C.POINTER(N.I32)), C.byref(uo),
+            C.c_void_p(env_out.data_ptr()), nout.ctypes.data_as(C.POINTER(N.I32)), bits))
+        raw = bits.raw.decode()
+        return uo.value, nout, [raw[i * w:(i + 1) * w] for i in range(shots)]
+
     # ---- environment forms (site-sharded chains, SURVEY 8(e) queries)
     def amplitudes_env(self, bitstrings, env_in=None, i0=0, i1=None) -> np.ndarray:
         """Row environments of bit strings (length n, sites [i0, i1) read)

@@ -134,6 +134,8 @@ def lib():
         "mpsim_gpu_sampler_clear_cache": (C.c_int, [VP]),
         "mpsim_gpu_sample_segment": (C.c_int, [VP, I32, I32, U64, DP, I32, DP, C.POINTER(I32), C.POINTER(I32), DP,
                                                C.POINTER(I32), C.c_char_p]),
+        "mpsim_gpu_sample_segment_dev": (C.c_int, [VP, I32, I32, U64, DP, I32, VP, C.POINTER(I32),
+                                                   C.POINTER(I32), VP, C.POINTER(I32), C.c_char_p]),
         "mpsim_uniform_variates": (C.c_int, [U64, U64, U64, DP]),
         "mpsim_gpu_counters": (C.c_int, [VP, C.POINTER(I64), DP, C.POINTER(I64)]),
         "mpsim_gpu_kernel_counters": (C.c_int, [VP, C.POINTER(I64), DP, DP, DP]),

@@ -315,6 +315,8 @@ class ShardedChain:
         counts, mine = {}, []
         torch, dist = self._torch, self.dist
         dev = f"cuda:{self.device}"
+        dims = prep.state.bond_dims()
+        d0, dk = int(dims[0]), int(dims[k])
         for c0 in range(0, shots, chunk):
             cs = min(chunk, shots - c0)
             u = uniform_variates(seed, c0 * n, cs * n).reshape(cs, n)[:, self.lo:self.hi]
@@ -323,16 +325,21 @@ class ShardedChain:
                 meta = torch.zeros(1, dtype=torch.int64, device=dev)
                 dist.recv(meta, self.rank - 1)
                 U = int(meta.item())
-                d0 = int(prep.state.bond_dims()[0])
-                t_env = torch.empty((U, d0), dtype=torch.complex128, device=dev)
+                env_in = torch.empty((U, d0), dtype=torch.complex128, device=dev)
                 t_node = torch.empty((cs,), dtype=torch.int32, device=dev)
-                dist.recv(t_env, self.rank - 1)
+                dist.recv(env_in, self.rank - 1)
                 dist.recv(t_node, self.rank - 1)
-                env_in, node_in = t_env.cpu().numpy(), t_node.cpu().numpy()
-            env_out, node_out, bits = prep.state.sample_segment(0, k, u, env_in, node_in)
+                node_in = t_node.cpu().numpy()   # synchronises: env_in is in place
+            if self.world == 1:
+                _, _, bits = prep.state.sample_segment(0, k, u)
+                mine.extend(bits)
+                continue
+            env_out = torch.empty((cs, dk), dtype=torch.complex128, device=dev)
+            U_out, node_out, bits = prep.state.sample_segment_dev(0, k, u, env_out, env_in, node_in)
             if self.rank < self.world - 1:
-                dist.send(torch.tensor([env_out.shape[0]], dtype=torch.int64, device=dev), self.rank + 1)
-                dist.send(torch.from_numpy(np.ascontiguousarray(env_out)).to(dev), self.rank + 1)
+                # the prefix environments go from HBM to HBM, no host staging
+                dist.send(torch.tensor([U_out], dtype=torch.int64, device=dev), self.rank + 1)
+                dist.send(env_out[:U_out], self.rank + 1)
                 dist.send(torch.from_numpy(node_out).to(dev), self.rank + 1)
             mine.extend(bits)
         # one gather after the chunk loop: no per-chunk collective, so rank r

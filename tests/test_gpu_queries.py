@@ -204,6 +204,16 @@ def test_sample_segments_compose_to_the_sampler(gpu, oracle):
     for x, y in zip(b1, b2):
         got[x + y] = got.get(x + y, 0) + 1
     assert got == want
+    # the device-resident hand-off (ShardedChain at N > 1) gives the same walk
+    import torch
+    dims = prep.bond_dims()
+    e_out = torch.empty((shots, int(dims[k])), dtype=torch.complex128, device="cuda:0")
+    U, node_d, b1d = prep.sample_segment_dev(0, k, u[:, :k], e_out)
+    assert U == env.shape[0] and b1d == b1 and (node_d == node).all()
+    assert np.array_equal(e_out[:U].cpu().numpy(), env)
+    e_fin = torch.empty((shots, 1), dtype=torch.complex128, device="cuda:0")
+    _, _, b2d = prep.sample_segment_dev(k, n, u[:, k:], e_fin, e_out[:U], node_d)
+    assert b2d == b2
     ch = sharded.ShardedChain(n, 16, 0, 1)
     for i in range(n):
         ch.set_site(i, g.site(i))
