@@ -13,6 +13,24 @@ namespace mpsim_gpu {
 
 constexpr int kQB = 32;  // panel width
 
+// acc += sum over rows r0, r0 + 32, ... < L of conj(a[r]) b[r] (cfmac), in
+// that order, with four rows' loads in flight per lane (the panel lives in
+// L2, so a one-load-at-a-time loop is latency bound).
+__device__ __forceinline__ void dot_rows(cplx& acc, const cplx* a, const cplx* b, int r0, int L) {
+  int r = r0;
+  for (; r + 96 < L; r += 128) {
+    cplx aa[4], bb[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      aa[q] = a[r + 32 * q];
+      bb[q] = b[r + 32 * q];
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cfmac(acc, aa[q], bb[q]);
+  }
+  for (; r < L; r += 32) cfmac(acc, a[r], b[r]);
+}
+
 // Factor panel columns [c0, c0 + jb) of A (row-major, ld), rows [c0, m).
 // Writes: A (R part + Householder vectors below the diagonal), V (explicit,
 // row-major (m - c0) x kQB, unit diagonal, zeros above), T (kQB x kQB,
@@ -75,7 +93,7 @@ __global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, lo
       for (int c = j + 1 + warp; c < jb; c += nw) {
         cplx* y = P + (long long)c * L;
         cplx w = lane == 0 ? y[j] : make_double2(0.0, 0.0);
-        for (int r = j + 1 + lane; r < L; r += 32) cfmac(w, x[r], y[r]);
+        dot_rows(w, x, y, j + 1 + lane, L);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           w.x += __shfl_xor_sync(0xffffffffu, w.x, o);
@@ -83,7 +101,21 @@ __global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, lo
         }
         const cplx f = cmul(conjc(tv), w);  // conj(tau) * (v^H y)
         if (lane == 0) y[j] = make_double2(y[j].x - f.x, y[j].y - f.y);
-        for (int r = j + 1 + lane; r < L; r += 32) {
+        int r = j + 1 + lane;
+        for (; r + 96 < L; r += 128) {  // four rows in flight per lane (x, y distinct columns)
+          cplx xa[4], ya[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            xa[q] = x[r + 32 * q];
+            ya[q] = y[r + 32 * q];
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const cplx u = cmul(xa[q], f);
+            y[r + 32 * q] = make_double2(ya[q].x - u.x, ya[q].y - u.y);
+          }
+        }
+        for (; r < L; r += 32) {
           const cplx u = cmul(x[r], f);
           y[r] = make_double2(y[r].x - u.x, y[r].y - u.y);
         }
@@ -95,7 +127,7 @@ __global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, lo
       cplx acc = make_double2(0.0, 0.0);
       // v_j has an implicit 1 at row j and zeros above; v_l has its stored entries below l.
       if (lane == 0) acc = conjc(vl[j]);
-      for (int r = j + 1 + lane; r < L; r += 32) cfmac(acc, vl[r], x[r]);
+      dot_rows(acc, vl, x, j + 1 + lane, L);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);

@@ -3,6 +3,8 @@
 // (mps.cpp:189-202, :223-239) and the statevector export (mps.cpp:241-256),
 // plus a row-gathered GEMM step that advances the left environments of many
 // bit strings at once (amplitude, mps.cpp:204-221, batched over strings).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace mpsim_gpu {
@@ -12,7 +14,11 @@ namespace mpsim_gpu {
 constexpr int kGT = 64;  // tile
 constexpr int kGK = 16;  // k chunk
 
-__global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs a) {
+// kSplit: blockIdx.z takes K range [z * kchunk, (z + 1) * kchunk) and writes
+// its raw partial product to ws[z] (M x N, ld N); cgemm_splitk_reduce then
+// sums the slices in z order (deterministic) and applies alpha / accumulate.
+template <bool kSplit>
+__global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs a, cplx* __restrict__ ws, int kchunk) {
   __shared__ cplx As[kGK][kGT + 1];
   __shared__ cplx Bs[kGK][kGT + 1];
   const int t = threadIdx.x, tx = t % 16, ty = t / 16;
@@ -22,7 +28,9 @@ __global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs a) {
   for (int x = 0; x < 4; ++x)
 #pragma unroll
     for (int y = 0; y < 4; ++y) acc[x][y] = make_double2(0.0, 0.0);
-  for (int k0 = 0; k0 < a.K; k0 += kGK) {
+  const int kb = kSplit ? blockIdx.z * kchunk : 0;
+  const int ke = kSplit ? min(a.K, kb + kchunk) : a.K;
+  for (int k0 = kb; k0 < ke; k0 += kGK) {
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       const int idx = t + 256 * s;
@@ -36,7 +44,7 @@ __global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs a) {
       }
       const int gi = i0 + i, gk = k0 + k;
       cplx v = make_double2(0.0, 0.0);
-      if (gi < a.M && gk < a.K) {
+      if (gi < a.M && gk < ke) {
         if (a.opA == 0) {
           v = a.A[(long long)gi * a.lda + gk];
         } else {
@@ -59,7 +67,7 @@ __global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs a) {
       }
       const int gj = j0 + j, gk = k0 + k;
       cplx v = make_double2(0.0, 0.0);
-      if (gj < a.N && gk < a.K) {
+      if (gj < a.N && gk < ke) {
         if (a.opB == 0) {
           v = a.B[(long long)gk * a.ldb + gj];
         } else {
@@ -89,7 +97,9 @@ __global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs a) {
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
       const int gi = i0 + ty + 16 * x, gj = j0 + tx + 16 * y;
-      if (gi < a.M && gj < a.N) {
+      if (kSplit) {
+        if (gi < a.M && gj < a.N) ws[((long long)blockIdx.z * a.M + gi) * a.N + gj] = acc[x][y];
+      } else if (gi < a.M && gj < a.N) {
         cplx v = cmul(a.alpha, acc[x][y]);
         cplx* c = a.C + (long long)gi * a.ldc + gj;
         if (a.accumulate) v = cadd(v, *c);
@@ -98,9 +108,45 @@ __global__ void __launch_bounds__(256) cgemm_kernel(GemmArgs a) {
     }
 }
 
+__global__ void cgemm_splitk_reduce(GemmArgs a, const cplx* __restrict__ ws, int slices) {
+  const long long mn = (long long)a.M * a.N;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < mn; e += (long long)gridDim.x * blockDim.x) {
+    cplx sum = ws[e];
+    for (int z = 1; z < slices; ++z) sum = cadd(sum, ws[z * mn + e]);
+    const long long gi = e / a.N, gj = e % a.N;
+    cplx v = cmul(a.alpha, sum);
+    cplx* c = a.C + gi * a.ldc + gj;
+    if (a.accumulate) v = cadd(v, *c);
+    *c = v;
+  }
+}
+
 void launch_cgemm(const GemmArgs& a, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0) return;
-  cgemm_kernel<<<dim3((a.N + kGT - 1) / kGT, (a.M + kGT - 1) / kGT), 256, 0, st>>>(a);
+  const dim3 g((a.N + kGT - 1) / kGT, (a.M + kGT - 1) / kGT);
+  const int tiles = (int)(g.x * g.y);
+  // Skinny products with a long K (the QR sweeps' V^H A2 / V^H Y panels,
+  // 32 x n x m) fill a handful of SMs: split K so ~2 CTAs per SM run.
+  int slices = 1;
+  if (tiles < 74 && a.K >= 256) slices = std::min({a.K / 128, (2 * 148 + tiles - 1) / tiles, 16});
+  if (slices <= 1) {
+    cgemm_kernel<false><<<g, 256, 0, st>>>(a, nullptr, 0);
+    return;
+  }
+  const int kchunk = ((a.K + slices - 1) / slices + kGK - 1) / kGK * kGK;
+  slices = (a.K + kchunk - 1) / kchunk;
+  cplx* ws = nullptr;
+  const size_t bytes = sizeof(cplx) * (size_t)slices * a.M * a.N;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), bytes, st);
+  if (e != cudaSuccess) {  // no workspace: the unsplit kernel
+    (void)cudaGetLastError();
+    cgemm_kernel<false><<<g, 256, 0, st>>>(a, nullptr, 0);
+    return;
+  }
+  cgemm_kernel<true><<<dim3(g.x, g.y, slices), 256, 0, st>>>(a, ws, kchunk);
+  const long long mn = (long long)a.M * a.N;
+  cgemm_splitk_reduce<<<(unsigned)std::min<long long>((mn + 255) / 256, 4 * 148), 256, 0, st>>>(a, ws, slices);
+  cudaFreeAsync(ws, st);
 }
 
 // env'[b][r] = sum_l env[b][l] * site[(l*2 + bit_b)*chi + r] for every string b.
