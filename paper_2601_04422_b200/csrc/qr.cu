@@ -7,6 +7,8 @@
 // Q_panel = I - V T V^H); the trailing matrix is updated with three complex
 // GEMMs, A2 <- (I - V T^H V^H) A2. The thin Q (m x k, k = min(m, n)) is then
 // formed by applying the block reflectors to [I; 0] in reverse order.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace mpsim_gpu {
@@ -37,7 +39,8 @@ __device__ __forceinline__ void dot_rows(cplx& acc, const cplx* a, const cplx* b
 // row-major, upper triangular), tau[c0 + j].
 __global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, long long lda, int m, int c0, int jb,
                                                         cplx* __restrict__ P, cplx* __restrict__ V,
-                                                        cplx* __restrict__ T, cplx* __restrict__ tau) {
+                                                        cplx* __restrict__ T, cplx* __restrict__ tau,
+                                                        int chunked) {
   const int L = m - c0;  // rows in the panel
   const int t = threadIdx.x, warp = t / 32, lane = t % 32, nw = blockDim.x / 32;
   // P: column-major panel copy, column j at P + j * L.
@@ -48,6 +51,7 @@ __global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, lo
   __shared__ double red[32];
   __shared__ cplx s_tau, s_beta;
   __shared__ cplx z[kQB];
+  __shared__ cplx part[kQB][kQB];  // partial column dots per (column, row chunk)
   __shared__ cplx Ts[kQB][kQB + 1];
   for (int i = t; i < kQB * (kQB + 1); i += blockDim.x) Ts[i / (kQB + 1)][i % (kQB + 1)] = make_double2(0.0, 0.0);
   __syncthreads();
@@ -88,21 +92,40 @@ __global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, lo
       tau[c0 + j] = tv;
     }
     __syncthreads();
-    // apply H^H = I - conj(tau) v v^H to panel columns j+1..jb-1 (one warp per column)
-    if (tv.x != 0.0 || tv.y != 0.0) {
-      for (int c = j + 1 + warp; c < jb; c += nw) {
-        cplx* y = P + (long long)c * L;
-        cplx w = lane == 0 ? y[j] : make_double2(0.0, 0.0);
-        dot_rows(w, x, y, j + 1 + lane, L);
+    // apply H^H = I - conj(tau) v v^H to panel columns j+1..jb-1: every warp
+    // takes one (column, row chunk) item, so late columns (few left) still
+    // use the whole CTA; partial dots meet in shared memory and are summed
+    // in chunk order (deterministic).
+    const int ncols = jb - j - 1;
+    if (ncols > 0 && (tv.x != 0.0 || tv.y != 0.0)) {
+      const int G = chunked ? max(1, nw / ncols) : 1;
+      const int R = L - j - 1;
+      const int CH = ((R + G - 1) / G + 31) / 32 * 32;
+      const int items = ncols * G;
+      for (int it = warp; it < items; it += nw) {
+        const int ci = it / G, g = it % G;
+        const cplx* y = P + (long long)(j + 1 + ci) * L;
+        const int rb = j + 1 + g * CH, re = min(L, rb + CH);
+        cplx w = (g == 0 && lane == 0) ? y[j] : make_double2(0.0, 0.0);
+        dot_rows(w, x, y, rb + lane, re);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           w.x += __shfl_xor_sync(0xffffffffu, w.x, o);
           w.y += __shfl_xor_sync(0xffffffffu, w.y, o);
         }
+        if (lane == 0) part[ci][g] = w;
+      }
+      __syncthreads();
+      for (int it = warp; it < items; it += nw) {
+        const int ci = it / G, g = it % G;
+        cplx* y = P + (long long)(j + 1 + ci) * L;
+        const int rb = j + 1 + g * CH, re = min(L, rb + CH);
+        cplx w = part[ci][0];
+        for (int q = 1; q < G; ++q) w = cadd(w, part[ci][q]);
         const cplx f = cmul(conjc(tv), w);  // conj(tau) * (v^H y)
-        if (lane == 0) y[j] = make_double2(y[j].x - f.x, y[j].y - f.y);
-        int r = j + 1 + lane;
-        for (; r + 96 < L; r += 128) {  // four rows in flight per lane (x, y distinct columns)
+        if (g == 0 && lane == 0) y[j] = make_double2(y[j].x - f.x, y[j].y - f.y);
+        int r = rb + lane;
+        for (; r + 96 < re; r += 128) {  // four rows in flight per lane (x, y distinct columns)
           cplx xa[4], ya[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -115,7 +138,7 @@ __global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, lo
             y[r + 32 * q] = make_double2(ya[q].x - u.x, ya[q].y - u.y);
           }
         }
-        for (; r < L; r += 32) {
+        for (; r < re; r += 32) {
           const cplx u = cmul(x[r], f);
           y[r] = make_double2(y[r].x - u.x, y[r].y - u.y);
         }
@@ -241,7 +264,11 @@ static unsigned blocks_for(long long n) {
 
 void launch_qr_panel(cplx* A, long long lda, int m, int c0, int jb, cplx* P, cplx* V, cplx* T, cplx* tau,
                      cudaStream_t st) {
-  qr_panel_kernel<<<1, 1024, 0, st>>>(A, lda, m, c0, jb, P, V, T, tau);
+  static const int chunked = [] {  // MPSIM_QR_PANEL_CHUNKED=0: one warp per column (A/B)
+    const char* v = std::getenv("MPSIM_QR_PANEL_CHUNKED");
+    return v != nullptr && v[0] == '0' ? 0 : 1;
+  }();
+  qr_panel_kernel<<<1, 1024, 0, st>>>(A, lda, m, c0, jb, P, V, T, tau, chunked);
 }
 void launch_set_identity(cplx* Y, long long ld, int m, int k, cudaStream_t st) {
   set_identity_kernel<<<blocks_for((long long)m * k), 256, 0, st>>>(Y, ld, m, k);
