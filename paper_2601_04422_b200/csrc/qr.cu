@@ -92,36 +92,59 @@ __global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, lo
       tau[c0 + j] = tv;
     }
     __syncthreads();
-    // apply H^H = I - conj(tau) v v^H to panel columns j+1..jb-1: every warp
-    // takes one (column, row chunk) item, so late columns (few left) still
-    // use the whole CTA; partial dots meet in shared memory and are summed
-    // in chunk order (deterministic).
+    // Phase A, one round of warp items: the dots v^H y of the columns the
+    // reflector updates (column, row chunk) and the zlarft dots V[:, l]^H v
+    // of T's column j (l < j, forward); ncols + j < 32 warps, so the chunks
+    // are sized to keep all items in one round. Partial dots meet in shared
+    // memory and are summed in chunk order (deterministic).
     const int ncols = jb - j - 1;
-    if (ncols > 0 && (tv.x != 0.0 || tv.y != 0.0)) {
-      const int G = chunked ? max(1, nw / ncols) : 1;
-      const int R = L - j - 1;
-      const int CH = ((R + G - 1) / G + 31) / 32 * 32;
-      const int items = ncols * G;
-      for (int it = warp; it < items; it += nw) {
-        const int ci = it / G, g = it % G;
+    const bool refl = tv.x != 0.0 || tv.y != 0.0;
+    const int GA = chunked ? max(1, (nw - j) / max(ncols, 1)) : 1;
+    const int CHA = ((L - j - 1 + GA - 1) / GA + 31) / 32 * 32;
+    const int itemsU = (refl && ncols > 0) ? ncols * GA : 0;
+    for (int it = warp; it < itemsU + j; it += nw) {
+      cplx w = make_double2(0.0, 0.0);
+      if (it < itemsU) {
+        const int ci = it / GA, g = it % GA;
         const cplx* y = P + (long long)(j + 1 + ci) * L;
-        const int rb = j + 1 + g * CH, re = min(L, rb + CH);
-        cplx w = (g == 0 && lane == 0) ? y[j] : make_double2(0.0, 0.0);
+        const int rb = j + 1 + g * CHA, re = min(L, rb + CHA);
+        if (g == 0 && lane == 0) w = y[j];
         dot_rows(w, x, y, rb + lane, re);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          w.x += __shfl_xor_sync(0xffffffffu, w.x, o);
-          w.y += __shfl_xor_sync(0xffffffffu, w.y, o);
-        }
-        if (lane == 0) part[ci][g] = w;
+      } else {
+        // v_j has an implicit 1 at row j and zeros above; v_l has its stored entries below l.
+        const cplx* vl = P + (long long)(it - itemsU) * L;
+        if (lane == 0) w = conjc(vl[j]);
+        dot_rows(w, vl, x, j + 1 + lane, L);
       }
-      __syncthreads();
-      for (int it = warp; it < items; it += nw) {
-        const int ci = it / G, g = it % G;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        w.x += __shfl_xor_sync(0xffffffffu, w.x, o);
+        w.y += __shfl_xor_sync(0xffffffffu, w.y, o);
+      }
+      if (lane == 0) {
+        if (it < itemsU) part[it / GA][it % GA] = w;
+        else z[it - itemsU] = w;
+      }
+    }
+    __syncthreads();
+    // T column j: T[0:j, j] = -tau_j T[0:j, 0:j] (V[:, 0:j]^H v_j)  (zlarft, forward)
+    if (t < j) {
+      cplx acc = make_double2(0.0, 0.0);
+      for (int l = t; l < j; ++l) cfma(acc, Ts[t][l], z[l]);
+      const cplx v = cmul(acc, tv);
+      Ts[t][j] = make_double2(-v.x, -v.y);
+    }
+    // Phase B: apply H^H = I - conj(tau) v v^H to columns j+1..jb-1, every
+    // warp one (column, row chunk) item so late columns use the whole CTA.
+    if (itemsU > 0) {
+      const int GB = chunked ? max(1, nw / ncols) : 1;
+      const int CHB = ((L - j - 1 + GB - 1) / GB + 31) / 32 * 32;
+      for (int it = warp; it < ncols * GB; it += nw) {
+        const int ci = it / GB, g = it % GB;
         cplx* y = P + (long long)(j + 1 + ci) * L;
-        const int rb = j + 1 + g * CH, re = min(L, rb + CH);
+        const int rb = j + 1 + g * CHB, re = min(L, rb + CHB);
         cplx w = part[ci][0];
-        for (int q = 1; q < G; ++q) w = cadd(w, part[ci][q]);
+        for (int q = 1; q < GA; ++q) w = cadd(w, part[ci][q]);
         const cplx f = cmul(conjc(tv), w);  // conj(tau) * (v^H y)
         if (g == 0 && lane == 0) y[j] = make_double2(y[j].x - f.x, y[j].y - f.y);
         int r = rb + lane;
@@ -143,27 +166,6 @@ __global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, lo
           y[r] = make_double2(y[r].x - u.x, y[r].y - u.y);
         }
       }
-    }
-    // T column j: T[0:j, j] = -tau_j T[0:j, 0:j] (V[:, 0:j]^H v_j)  (zlarft, forward)
-    for (int l = warp; l < j; l += nw) {
-      const cplx* vl = P + (long long)l * L;
-      cplx acc = make_double2(0.0, 0.0);
-      // v_j has an implicit 1 at row j and zeros above; v_l has its stored entries below l.
-      if (lane == 0) acc = conjc(vl[j]);
-      dot_rows(acc, vl, x, j + 1 + lane, L);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-      }
-      if (lane == 0) z[l] = acc;
-    }
-    __syncthreads();
-    if (t < j) {
-      cplx acc = make_double2(0.0, 0.0);
-      for (int l = t; l < j; ++l) cfma(acc, Ts[t][l], z[l]);
-      const cplx v = cmul(acc, tv);
-      Ts[t][j] = make_double2(-v.x, -v.y);
     }
     if (t == 0) Ts[j][j] = tv;
     __syncthreads();
@@ -264,7 +266,7 @@ static unsigned blocks_for(long long n) {
 
 void launch_qr_panel(cplx* A, long long lda, int m, int c0, int jb, cplx* P, cplx* V, cplx* T, cplx* tau,
                      cudaStream_t st) {
-  static const int chunked = [] {  // MPSIM_QR_PANEL_CHUNKED=0: one warp per column (A/B)
+  static const int chunked = [] {  // MPSIM_QR_PANEL_CHUNKED=0: one warp per column, no row chunks (A/B)
     const char* v = std::getenv("MPSIM_QR_PANEL_CHUNKED");
     return v != nullptr && v[0] == '0' ? 0 : 1;
   }();
