@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, lo
     P[(long long)j * L + r] = A[(long long)(c0 + r) * lda + c0 + j];
   }
   __shared__ double red[32];
-  __shared__ cplx s_tau, s_beta;
+  __shared__ cplx s_tau, s_beta, s_alpha;
   __shared__ cplx z[kQB];
   __shared__ cplx part[kQB][kQB];  // partial column dots per (column, row chunk)
   __shared__ cplx Ts[kQB][kQB + 1];
@@ -76,9 +76,10 @@ __global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, lo
       }
       s_tau = tv;
       s_beta = beta;
+      s_alpha = alpha;
     }
     __syncthreads();
-    const cplx tv = s_tau, beta = s_beta, alpha = x[j];
+    const cplx tv = s_tau, beta = s_beta, alpha = s_alpha;
     if (tv.x != 0.0 || tv.y != 0.0) {
       // v = x / (alpha - beta) below the diagonal
       const cplx d = make_double2(alpha.x - beta.x, alpha.y - beta.y);
@@ -86,8 +87,7 @@ __global__ void __launch_bounds__(1024) qr_panel_kernel(cplx* __restrict__ A, lo
       const cplx inv = make_double2(d.x / dd, -d.y / dd);
       for (int r = j + 1 + t; r < L; r += blockDim.x) x[r] = cmul(x[r], inv);
     }
-    __syncthreads();
-    if (t == 0) {
+    if (t == 0) {  // row j is not touched by the scaling (alpha was staged)
       x[j] = beta;
       tau[c0 + j] = tv;
     }
