@@ -154,51 +154,63 @@ def ncu_traffic():
 
 # ---------------------------------------------------------------- CPU reference path
 
-def cpu_sample(workers, chi=512, gates=16, seed=7, repeats=1):
-    """Times the CPU oracle (execute_parallel restatement, LAPACK zgesdd) on one
-    layer of `gates` two-qubit gates at full bond chi. Returns gates/s."""
+def cpu_layer_sample(workers, chi=512, per_gpu=256, parity=0, seed=7):
+    """Times the CPU oracle (execute_parallel restatement, LAPACK zgesdd) on a
+    bounded, stratified sample of one bench step: a short chain with the same
+    capped bond profile, min(chi, 2^i, 2^(n-i)), whose edges are exactly the
+    256-qubit chain's edges. Its brick layer holds every edge (unsaturated) gate
+    of the real layer plus 16 or 17 saturated gates; both groups are timed
+    separately and the step time is t_edges + t_saturated * (saturated gates
+    of the real layer / saturated gates sampled). Returns (layer gates, est.
+    layer seconds, description)."""
     from oracle import oracle as O
     O.build()
-    rng = np.random.default_rng(seed)
+    rng = np.random.default_rng(seed + parity)
     lg = int(np.log2(chi))
-    n = 2 * (lg + 1) + 2 * gates
+    n = 2 * (lg + 1) + 32
     bonds = chain_bonds(n, chi)
-    base = O.MpsState(n)
+    s = O.MpsState(n)
     for i in range(n):
-        base.set_site(i, random_site(rng, bonds[i], bonds[i + 1]))
-    start = lg + 1 + ((lg + 1) % 2)
-    times = []
-    for _ in range(repeats):
-        s = base.copy()
-        gl = O.GateList([(q, q + 1, haar4(rng)) for q in range(start, start + 2 * gates, 2)])
-        t0 = time.perf_counter()
-        O.execute_parallel(s, gl, chi, 1e-12, workers=workers)
-        times.append(time.perf_counter() - t0)
-    return gates, times
+        s.set_site(i, random_site(rng, bonds[i], bonds[i + 1]))
+    gates = layer_gates(n, parity, rng)
+    is_sat = [bonds[q] == bonds[q + 1] == bonds[q + 2] == chi for q, _, _ in gates]
+    sat = [g for g, f in zip(gates, is_sat) if f]
+    edge = [g for g, f in zip(gates, is_sat) if not f]
+    t0 = time.perf_counter()
+    O.execute_parallel(s, O.GateList(edge), chi, 1e-12, workers=workers)
+    t1 = time.perf_counter()
+    O.execute_parallel(s, O.GateList(sat), chi, 1e-12, workers=workers)
+    t2 = time.perf_counter()
+    big = chain_bonds(per_gpu, chi)
+    real = list(range(parity, per_gpu - 1, 2))
+    real_sat = sum(1 for q in real if big[q] == big[q + 1] == big[q + 2] == chi)
+    est = (t1 - t0) + (t2 - t1) * real_sat / len(sat)
+    desc = (f"stratified sample of the {per_gpu}-qubit step: all {len(edge)} edge gates timed + {len(sat)} of "
+            f"{real_sat} saturated gates timed and scaled; execute_parallel restatement with {workers} workers, "
+            f"LAPACK zgesdd")
+    return len(real), est, desc
 
 
 def run_reference(args, rank, world):
     if rank != 0:
         return
     workers = os.cpu_count() or 1
-    sample_gates = 16
-    for _ in range(args.warmup):
-        cpu_sample(workers, chi=args.chi, gates=sample_gates)
-    per = []
-    for _ in range(args.steps):
-        g, t = cpu_sample(workers, chi=args.chi, gates=sample_gates)
-        per.append(t[0])
+    for s in range(args.warmup):
+        cpu_layer_sample(workers, chi=args.chi, per_gpu=args.per_gpu, parity=s % 2)
+    per, ngates, desc = [], 0, ""
+    for s in range(args.warmup, args.warmup + args.steps):
+        g, t, desc = cpu_layer_sample(workers, chi=args.chi, per_gpu=args.per_gpu, parity=s % 2)
+        per.append(t)
+        ngates += g
     total = sum(per)
-    value = args.steps * sample_gates / total
+    value = ngates / total
     line = {
         "impl": "reference", "metric": metric_name(args.chi), "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
         "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "complex128",
         "data": "synthetic",
         "config": config_block(args),
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port",
-                         "sample": f"{sample_gates} gates/step at Dl=Dm=Dr={args.chi} (one disjoint layer), "
-                                   f"execute_parallel restatement with {workers} workers, LAPACK zgesdd"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": workers, "kind": "port", "sample": desc},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -265,23 +277,16 @@ def main():
         run_reference(args, rank, world)
         return
 
-    dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-
+    # one process per GPU; the library's NCCL layer moves the boundary sites
+    # (the NCCL id is bootstrapped over a TCP socket: no torch on any path)
     from paper_2601_04422_b200 import sharded
-    import paper_2601_04422_b200 as P
 
     n, chi = args.qubits, args.chi
     rng = np.random.default_rng(1234)
     bonds = chain_bonds(n, chi)
-    chain = sharded.ShardedChain(n, chi, rank, world, device=local, dist=dist)
+    chain = sharded.ShardedChain(n, chi, rank, world, device=local)
     for i in range(chain.lo, chain.hi):
         chain.set_site(i, random_site(np.random.default_rng(10_000 + i), bonds[i], bonds[i + 1]))
-    chain.finalize_setup()
     steps = [layer_gates(n, s % 2, rng) for s in range(args.warmup + args.steps)]
 
     for s in range(args.warmup):
@@ -289,21 +294,13 @@ def main():
     chain.barrier()
     chain.reset_counters()
     dev_ms, wall, ngates = [], [], 0
-    torch = chain._torch
     with ClockSampler(range(world) if rank == 0 else []) as clk:
         chain.barrier()
         for s in range(args.warmup, args.warmup + args.steps):
-            if torch is not None:
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
             t0 = time.perf_counter()
             st = chain.apply_layer(steps[s], chi, 1e-12)
-            if torch is not None:
-                e1.record()
-                torch.cuda.synchronize()
-                dev_ms.append(e0.elapsed_time(e1))  # step incl. boundary exchange (all syncs inside)
-            else:
-                dev_ms.append(st["device_ms"])  # CUDA events on the library stream
+            # CUDA events on the shard stream around exchange in + layer + exchange out
+            dev_ms.append(st["device_ms"])
             wall.append(time.perf_counter() - t0)
             ngates += len(steps[s])
         chain.barrier()
@@ -339,20 +336,31 @@ def main():
         },
         "e2e": {"value": e2e, "unit": UNIT, "h2d_bytes_per_step": c["h2d_bytes"] // args.steps,
                 "d2h_bytes_per_step": c["d2h_bytes"] // args.steps,
-                "note": "host wall clock around mpsim_gpu_execute per layer: gate list in from host, "
-                        "per-gate reports out; the MPS stays resident in HBM as the simulator state"},
+                "note": "host wall clock around mpsim_gpu_shard_apply_layer per layer (max over ranks): gate "
+                        "list in from host, per-gate reports out, boundary exchange over NCCL; the MPS stays "
+                        "resident in HBM as the simulator state"},
         "gpu_launches": c["launches"],
         "svd_sweeps": c["sweeps"],
         "clocks": clk.summary(),
     }
+    if world == 1:
+        # saturated gates only (Dl = Dm = Dr = chi), outside the timed region:
+        # the same steps without the ~7 % cheap edge gates of the chain's ends
+        sat_ms, sat_n = 0.0, 0
+        for s in range(args.warmup, args.warmup + min(args.steps, 2)):
+            sat = [g for g in steps[s] if bonds[g[0]] == bonds[g[0] + 1] == bonds[g[0] + 2] == chi]
+            st = chain.apply_layer(sat, chi, 1e-12)
+            sat_ms += st["device_ms"]
+            sat_n += len(sat)
+        line["saturated_only"] = {"value": sat_n / (sat_ms / 1e3), "unit": UNIT, "gates": sat_n,
+                                  "note": "device time of layers holding only the saturated gates of two bench "
+                                          "steps (applied after the timed region)"}
     if world == 1 and not args.no_pipeline:
         line["e2e_pipeline"] = pipeline_run()
     if world == 1 and not args.no_cpu_baseline:
         workers = os.cpu_count() or 1
-        g, t = cpu_sample(workers, chi=chi, gates=16)
-        line["cpu_baseline"] = {"value": g / t[0], "unit": UNIT, "cores": workers, "kind": "port",
-                                "sample": f"{g} gates at Dl=Dm=Dr={chi}, one layer, execute_parallel "
-                                          f"restatement with {workers} workers (LAPACK zgesdd)"}
+        g, t, desc = cpu_layer_sample(workers, chi=chi, per_gpu=args.per_gpu, parity=0)
+        line["cpu_baseline"] = {"value": g / t, "unit": UNIT, "cores": workers, "kind": "port", "sample": desc}
     print(json.dumps(line), flush=True)
 
 

@@ -110,6 +110,68 @@ int mpsim_gpu_set_open_boundaries(mpsim_gpu_state* s, int32_t open);
 int mpsim_gpu_site_slot(const mpsim_gpu_state* s, int32_t i, void** device_ptr, int64_t* chi);
 int mpsim_gpu_set_site_dims(mpsim_gpu_state* s, int32_t i, int64_t dl, int64_t dr);
 
+/* ---- multi-GPU chains: one process per GPU, NCCL over NVLink ---------------
+ * Replaces execute_parallel's worker pool (executor.cpp:99-232) for a chain
+ * that spans GPUs, and the paper's TAMM/GlobalArrays layer distribution
+ * (SURVEY 8(e)). Rank r owns global sites [lo, hi) (even,
+ * cost-weighted cut points) plus a ghost slot for the straddling gate of odd
+ * layers; boundary sites and query environments move by NCCL send/recv on the
+ * shard's stream (NCCL is loaded at run time, libnccl.so.2). Results are bit
+ * for bit those of one GPU. The unique id comes from rank 0
+ * (mpsim_gpu_nccl_unique_id) and reaches the other ranks out of band (MPI,
+ * a TCP store, a file: the caller's choice, as with ncclCommInitRank). */
+typedef struct mpsim_gpu_shard mpsim_gpu_shard;
+#define MPSIM_REDUCE_SUM 0
+#define MPSIM_REDUCE_MAX 1
+#define MPSIM_REDUCE_MIN 2
+/* host planning, no device: world + 1 bounds; chi <= 0 = even split */
+int mpsim_shard_bounds(int32_t n_qubits, int32_t world, int64_t chi, int32_t* out);
+/* one layer of local gates (global indices) -> the gates shard [lo, hi) runs
+ * (local indices; the straddling gate on (hi-1, hi) uses the ghost slot hi-lo)
+ * and whether it lends its first site left / borrows its right neighbour's */
+int mpsim_shard_partition_layer(const mpsim_gate* gates, int32_t count, int32_t lo, int32_t hi, int32_t rank,
+                                int32_t world, mpsim_gate* local, int32_t* n_local, int32_t* straddle_left,
+                                int32_t* straddle_right);
+int mpsim_gpu_nccl_unique_id(void* id_out /* 128 bytes */);
+/* |0...0> shard of an n-qubit chain; nccl_id may be NULL when world == 1 */
+int mpsim_gpu_shard_create(int32_t n_qubits, int64_t chi, int32_t rank, int32_t world, const void* nccl_id,
+                           int32_t device, mpsim_gpu_shard** out);
+int mpsim_gpu_shard_destroy(mpsim_gpu_shard* s);
+/* owned range and the local state (borrowed: sites [0, hi-lo) + ghost) */
+int mpsim_gpu_shard_info(const mpsim_gpu_shard* s, int32_t* lo, int32_t* hi, mpsim_gpu_state** local_state);
+/* global site index i in [lo, hi) (MpsState::site(i) import / export) */
+int mpsim_gpu_shard_set_site(mpsim_gpu_shard* s, int32_t i, int64_t dl, int64_t dr, const double* data);
+int mpsim_gpu_shard_get_site(mpsim_gpu_shard* s, int32_t i, int64_t* dl, int64_t* dr, double* out);
+int mpsim_gpu_shard_bond_dims(mpsim_gpu_shard* s, int64_t* out /* hi - lo + 1: bonds lo .. hi */);
+/* one layer of disjoint local gates in global indices (every rank passes the
+ * same layer): exchange in, one batched launch sequence, exchange out;
+ * stats->device_ms spans all three (CUDA events on the shard stream) */
+int mpsim_gpu_shard_apply_layer(mpsim_gpu_shard* s, const mpsim_gate* gates, int32_t count,
+                                const mpsim_policy* policy, mpsim_exec_stats* stats);
+/* execute_parallel over the whole chain: decompose_nonlocal + layerize
+ * (fusion.cpp:137-190) on every rank, then the layers in order; stats are
+ * reduced over the ranks (peak bond max, discarded weight sum) */
+int mpsim_gpu_shard_execute(mpsim_gpu_shard* s, const mpsim_gate* gates, int32_t count, const mpsim_policy* policy,
+                            mpsim_exec_stats* stats);
+/* queries over the whole chain (every rank calls; every rank gets the result):
+ * amplitudes of count full-length bit strings (mps.cpp:204-221), overlap of two
+ * chains sharded alike (mps.cpp:223-239), norm (mps.cpp:189-202), <O_q> (P9) */
+int mpsim_gpu_shard_amplitudes(mpsim_gpu_shard* s, const char* bits, int32_t count, double* out);
+int mpsim_gpu_shard_overlap(mpsim_gpu_shard* a, mpsim_gpu_shard* b, double* out);
+int mpsim_gpu_shard_norm(mpsim_gpu_shard* s, double* out);
+int mpsim_gpu_shard_expect_1q(mpsim_gpu_shard* s, const double* op2x2, int32_t q, double* out);
+/* move_center (mps.cpp:177-187) with the same QR steps in the same order */
+int mpsim_gpu_shard_move_center(mpsim_gpu_shard* s, int32_t center);
+int mpsim_gpu_shard_ortho_center(const mpsim_gpu_shard* s, int32_t* out);
+/* perfect sampling (Sampler::sample, sampler.cpp:35-143) of the whole chain:
+ * shot chunks (chunk, 0 = 4096) walk rank to rank; ordered counts afterwards
+ * through mpsim_gpu_shard_sample_result (same on every rank) */
+int mpsim_gpu_shard_sample(mpsim_gpu_shard* s, uint64_t shots, uint64_t seed, uint64_t chunk, int32_t* unique);
+int mpsim_gpu_shard_sample_result(const mpsim_gpu_shard* s, int32_t i, char* bits /* n chars */, uint64_t* count);
+/* plumbing for harnesses: element-wise all-reduce of host doubles, barrier */
+int mpsim_gpu_shard_allreduce(mpsim_gpu_shard* s, double* values, int32_t count, int32_t op);
+int mpsim_gpu_shard_barrier(mpsim_gpu_shard* s);
+
 /* ---- gate application (gate_apply.hpp:48-78) --------------------------- */
 int mpsim_gpu_apply_1q(mpsim_gpu_state* s, const double* u2x2, int32_t q, mpsim_report* rep);
 /* apply_2q_local (q1 == q0+1), apply_2q_swap / apply_2q_bondprop otherwise. */

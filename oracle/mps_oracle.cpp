@@ -29,6 +29,10 @@ void scipy_cblas_zgemm(int order, int ta, int tb, int m, int n, int k, const voi
                        const void* a, int lda, const void* b, int ldb, const void* beta, void* c,
                        int ldc);
 void scipy_openblas_set_num_threads(int);
+void scipy_zgesvj_(const char* joba, const char* jobu, const char* jobv, const int* m, const int* n,
+                   oracle::cplx* a, const int* lda, double* sva, const int* mv, oracle::cplx* v, const int* ldv,
+                   oracle::cplx* cwork, const int* lwork, double* rwork, const int* lrwork, int* info, size_t,
+                   size_t, size_t);
 }
 
 namespace oracle {
@@ -193,10 +197,59 @@ Index truncation_rank(const std::vector<double>& s, Index max_rank, double cutof
   return keep;
 }
 
+// Second, independent SVD for pinning the oracle (tests/golden/make_golden.py):
+// LAPACK zgesvj, one-sided Jacobi (de Rijk pivoting, Drmac-Veselic) — an
+// algorithm family unrelated to zgesdd's bidiagonal divide and conquer.
+// zgesvj needs rows >= cols; wider matrices go through their adjoint.
+std::atomic<int> g_svd_backend{0};
+
+namespace {
+SvdResult svd_jacobi(const Mat& m, Index max_rank, double cutoff) {
+  const bool tr = m.rows < m.cols;
+  const int rows = static_cast<int>(tr ? m.cols : m.rows), cols = static_cast<int>(tr ? m.rows : m.cols);
+  std::vector<cplx> a(static_cast<size_t>(rows) * cols);  // column-major rows x cols
+  for (Index i = 0; i < m.rows; ++i)
+    for (Index j = 0; j < m.cols; ++j) {
+      if (tr) a[static_cast<size_t>(i * rows + j)] = std::conj(m(i, j));
+      else a[static_cast<size_t>(j * rows + i)] = m(i, j);
+    }
+  std::vector<double> sva(static_cast<size_t>(cols));
+  std::vector<cplx> v(static_cast<size_t>(cols) * cols);
+  const int lwork = rows + cols, lrwork = std::max(6, cols);
+  std::vector<cplx> cwork(static_cast<size_t>(lwork));
+  std::vector<double> rwork(static_cast<size_t>(lrwork));
+  int info = 0, mv = 0;
+  const char ja = 'G', ju = 'U', jv = 'V';
+  scipy_zgesvj_(&ja, &ju, &jv, &rows, &cols, a.data(), &rows, sva.data(), &mv, v.data(), &cols, cwork.data(),
+                &lwork, rwork.data(), &lrwork, &info, 1, 1, 1);
+  if (info != 0)
+    throw NumericError("zgesvj did not converge for (" + std::to_string(rows) + "," + std::to_string(cols) +
+                       ") matrix");
+  const double scale = rwork[0];
+  std::vector<double> s(static_cast<size_t>(cols));
+  for (int i = 0; i < cols; ++i) s[static_cast<size_t>(i)] = sva[static_cast<size_t>(i)] * scale;
+  SvdResult r;
+  const Index keep = truncation_rank(s, max_rank, cutoff, &r.discarded_weight);
+  // A = Ua S V^H (column-major Ua in a); for the adjoint case m = V S Ua^H.
+  r.u = Mat(m.rows, keep);
+  r.vdag = Mat(keep, m.cols);
+  for (Index j = 0; j < keep; ++j) {
+    for (Index i = 0; i < m.rows; ++i)
+      r.u(i, j) = tr ? v[static_cast<size_t>(j * cols + i)] : a[static_cast<size_t>(j * rows + i)];
+    for (Index i = 0; i < m.cols; ++i)
+      r.vdag(j, i) = tr ? std::conj(a[static_cast<size_t>(j * rows + i)])
+                        : std::conj(v[static_cast<size_t>(j * cols + i)]);
+  }
+  r.s.assign(s.begin(), s.begin() + keep);
+  return r;
+}
+}  // namespace
+
 // svd.hpp:79-110, with Eigen::BDCSVD replaced by LAPACK zgesdd (thin U, V).
 SvdResult svd(const Mat& m, Index max_rank, double cutoff) {
   if (max_rank < 1) throw std::invalid_argument("svd max_rank must be >= 1");
   if (cutoff < 0.0 || cutoff >= 1.0) throw std::invalid_argument("svd cutoff must lie in [0, 1)");
+  if (g_svd_backend.load(std::memory_order_relaxed) == 1) return svd_jacobi(m, max_rank, cutoff);
   const int rows = static_cast<int>(m.rows), cols = static_cast<int>(m.cols);
   const int mn = std::min(rows, cols), mx = std::max(rows, cols);
   std::vector<cplx> a = to_colmajor(m);

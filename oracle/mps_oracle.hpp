@@ -18,6 +18,7 @@
 // restatement below.
 #pragma once
 
+#include <atomic>
 #include <array>
 #include <complex>
 #include <cstdint>
@@ -67,6 +68,7 @@ Index truncation_rank(const std::vector<double>& s, Index max_rank, double cutof
 
 // svd.hpp:79-110
 SvdResult svd(const Mat& m, Index max_rank = kUnbounded, double cutoff = 0.0);
+extern std::atomic<int> g_svd_backend;  // 0 zgesdd, 1 zgesvj (oracle pinning)
 
 // One MPS site (Dl, 2, Dr), flat index (l*2+p)*Dr + r (tensor.hpp:139-148).
 struct Site {

@@ -106,6 +106,7 @@ def lib():
         L.orc_sampler_cache_size.argtypes = [vp]
         L.orc_sampler_cache_size.restype = U64
         L.orc_sampler_clear.argtypes = [vp]
+        L.orc_set_svd_backend.argtypes = [C.c_int]
         _lib = L
     return _lib
 
@@ -275,6 +276,12 @@ def svd(m, max_rank=None, cutoff=0.0):
     _check(lib().orc_svd(r, c, _dp(m), mr, float(cutoff), C.byref(k), _dp(s), _dp(u), _dp(v), C.byref(w)))
     kk = k.value
     return u.reshape(-1)[: r * kk].reshape(r, kk), s[:kk], v.reshape(-1)[: kk * c].reshape(kk, c), w.value
+
+
+def set_svd_backend(name: str):
+    """'zgesdd' (default; divide and conquer, Eigen BDCSVD's family) or 'zgesvj'
+    (one-sided Jacobi): the second is an independent check of the first."""
+    lib().orc_set_svd_backend({"zgesdd": 0, "zgesvj": 1}[name])
 
 
 def truncation_rank(s, max_rank=None, cutoff=0.0):

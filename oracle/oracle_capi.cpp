@@ -168,6 +168,12 @@ int orc_svd(int rows, int cols, const double* data, Index max_rank, double cutof
     *w = r.discarded_weight;
   });
 }
+// 0: zgesdd (default, BDCSVD's family), 1: zgesvj (independent cross-check)
+int orc_set_svd_backend(int b) {
+  oracle::g_svd_backend.store(b == 1 ? 1 : 0);
+  return 0;
+}
+
 Index orc_truncation_rank(const double* s, Index n, Index max_rank, double cutoff, double* w) {
   std::vector<double> v(s, s + n);
   return truncation_rank(v, max_rank, cutoff, w);

@@ -16,7 +16,22 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 namespace mpsim_gpu {
+
+// A/B switches of sweep policy and kernel variants (MPSIM_QR, MPSIM_JACOBI,
+// MPSIM_CROSS*, ...): read from the environment only in an A/B build
+// (make AB=1 -> -DMPSIM_AB_KNOBS). The product library ignores them, so a stray
+// variable cannot change numerics of the drop-in path.
+inline const char* ab_knob(const char* name) {
+#ifdef MPSIM_AB_KNOBS
+  return std::getenv(name);
+#else
+  (void)name;
+  return nullptr;
+#endif
+}
 
 typedef double2 cplx;
 

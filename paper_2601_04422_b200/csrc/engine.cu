@@ -34,7 +34,7 @@ void launch_jacobi_sweep(const GateDesc*, int, int, cplx*, const int*, int*, dou
 // one launch per tournament round.
 static bool sweep_policy() {
   static const bool on = [] {
-    const char* v = std::getenv("MPSIM_SWEEP");
+    const char* v = ab_knob("MPSIM_SWEEP");
     return !(v != nullptr && std::string(v) == "rounds");
   }();
   return on;
@@ -51,7 +51,7 @@ constexpr int kQrMinN = 128;
 constexpr int kMaxSvdN = 2048;  // derijk_kernel / truncate_kernel: one 1024-thread CTA, 2048 keys
 static int qr_policy() {
   static const int v = [] {
-    const char* e = std::getenv("MPSIM_QR");
+    const char* e = ab_knob("MPSIM_QR");
     if (e == nullptr) return 2;
     const int x = std::atoi(e);
     return x < 0 ? 0 : (x > 2 ? 2 : x);
@@ -68,14 +68,14 @@ constexpr int kCrossSweepsDefault = 4;  // cross-only EVDs in sweeps 1 .. kCross
 // (MPSIM_CROSS_RMS / MPSIM_CROSS_SWEEPS override both, A/B only)
 static double cross_rms() {
   static const double v = [] {
-    const char* e = std::getenv("MPSIM_CROSS_RMS");
+    const char* e = ab_knob("MPSIM_CROSS_RMS");
     return e ? std::atof(e) : kCrossRmsDefault;
   }();
   return v;
 }
 static int cross_sweeps() {
   static const int v = [] {
-    const char* e = std::getenv("MPSIM_CROSS_SWEEPS");
+    const char* e = ab_knob("MPSIM_CROSS_SWEEPS");
     return e ? std::atoi(e) : kCrossSweepsDefault;
   }();
   return v;
@@ -85,14 +85,14 @@ static int cross_sweeps() {
 constexpr double kInblockMaxoff = 1e-4;
 static bool inblock_policy() {
   static const bool on = [] {
-    const char* v = std::getenv("MPSIM_INBLOCK");
+    const char* v = ab_knob("MPSIM_INBLOCK");
     return !(v != nullptr && v[0] == '0');
   }();
   return on;
 }
 static bool cross_policy() {
   static const bool on = [] {
-    const char* v = std::getenv("MPSIM_CROSS");
+    const char* v = ab_knob("MPSIM_CROSS");
     return !(v != nullptr && v[0] == '0');
   }();
   return on;
@@ -102,7 +102,7 @@ static bool cross_policy() {
 // EVD / rotation) and "split3" (Gram / EVD / rotation) launch per round (A/B).
 static int jacobi_mode() {
   static const int m = [] {
-    const char* v = std::getenv("MPSIM_JACOBI");
+    const char* v = ab_knob("MPSIM_JACOBI");
     if (v != nullptr && std::string(v) == "split3") return 2;
     if (v != nullptr && std::string(v) == "split2") return 3;
     return 4;
@@ -150,7 +150,7 @@ static bool sync_debug() {
 // (1) or after the pair EVD (2), with a single sweep, to time the phases.
 static int phase_probe() {
   static const int v = [] {
-    const char* e = std::getenv("MPSIM_PHASE_PROBE");
+    const char* e = ab_knob("MPSIM_PHASE_PROBE");
     return e ? std::atoi(e) : 0;
   }();
   return v;
@@ -161,7 +161,7 @@ static int phase_probe() {
 // or 0 (full EVDs every round, A/B). Returns the active bits to add.
 static int alt_cross_bits() {
   static const int bits = [] {
-    const char* v = std::getenv("MPSIM_ALT_CROSS");
+    const char* v = ab_knob("MPSIM_ALT_CROSS");
     const int p = v ? std::atoi(v) : 2;
     return p == 2 ? 16 : p == 3 ? (16 | 32) : 0;
   }();
@@ -171,7 +171,7 @@ static int alt_cross_bits() {
 // MPSIM_FIRST_INBLOCK=0 computes every Gram tile in the first sweep (A/B).
 static bool first_sweep_inblock() {
   static const bool on = [] {
-    const char* v = std::getenv("MPSIM_FIRST_INBLOCK");
+    const char* v = ab_knob("MPSIM_FIRST_INBLOCK");
     return !(v != nullptr && v[0] == '0');
   }();
   return on;
@@ -180,7 +180,7 @@ static bool first_sweep_inblock() {
 // MPSIM_EXACT_CACHE=0 recomputes all 36 Gram tiles in closing sweeps (A/B).
 static bool exact_cache_policy() {
   static const bool on = [] {
-    const char* v = std::getenv("MPSIM_EXACT_CACHE");
+    const char* v = ab_knob("MPSIM_EXACT_CACHE");
     return !(v != nullptr && v[0] == '0');
   }();
   return on;
@@ -203,10 +203,10 @@ static void check_launch(const char* what = "kernel") {
 
 void DeviceBuf::ensure(size_t b) {
   if (b <= bytes) return;
+  size_t nb = std::max(b, bytes + bytes / 2);
   if (p) cudaFree(p);
   p = nullptr;
   bytes = 0;
-  size_t nb = std::max(b, bytes + bytes / 2);
   if (cudaMalloc(&p, nb) != cudaSuccess) {
     cudaGetLastError();
     if (cudaMalloc(&p, b) != cudaSuccess) {
@@ -218,7 +218,17 @@ void DeviceBuf::ensure(size_t b) {
   bytes = nb;
 }
 void DeviceBuf::release() {
-  if (p) cudaFree(p);
+  if (p) {
+    int dev = -1;  // the owning device may not be current (multi-GPU hosts)
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) == cudaSuccess) dev = a.device;
+    cudaGetLastError();
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (dev >= 0 && dev != cur) cudaSetDevice(dev);
+    cudaFree(p);
+    if (dev >= 0 && dev != cur) cudaSetDevice(cur);
+  }
   p = nullptr;
   bytes = 0;
 }
@@ -267,6 +277,16 @@ State::State(int n_, long long chi_hint, int dev) : n(n_), device(dev) {
   CK(cudaEventCreate(&ev1));
   CK(cudaEventCreate(&evj0));
   CK(cudaEventCreate(&evj1));
+  {
+    // split-K GEMM workspaces (queries.cu) come from the stream-ordered pool:
+    // keep up to 1 GiB cached across stream syncs instead of trimming it
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = 1ull << 30;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  }
   static bool inited = false;
   if (!inited) {
     jacobi_split_init();
@@ -300,11 +320,7 @@ void State::launch_fill_sites_zero_state() {
 State::~State() {
   DeviceGuard g(device);
   cudaStreamSynchronize(st);
-  sites_buf.release();
-  for (DeviceBuf* b : {&ws, &d_gates, &d_out, &d_sigma, &d_order, &d_active, &d_rot, &d_frob, &d_perm, &d_maxoff,
-                       &d_g1, &q1, &q2, &q3, &q4, &qbits, &d_need, &d_gbuf, &d_rbuf})
-    b->release();
-  for (PinnedBuf* b : {&h_gates, &h_out, &h_rot, &h_g1, &h_small, &h_maxoff}) b->release();
+  // every DeviceBuf / PinnedBuf member frees itself (RAII)
   cudaEventDestroy(ev0);
   cudaEventDestroy(ev1);
   cudaEventDestroy(evj0);
@@ -331,11 +347,7 @@ void State::grow(int new_chi) {
   check_launch();
   ++launches;
   CK(cudaStreamSynchronize(st));
-  dd.release();
-  sites_buf.release();
-  sites_buf = nb;
-  nb.p = nullptr;
-  nb.bytes = 0;
+  sites_buf = std::move(nb);
   sites = (cplx*)sites_buf.p;
   chi = new_chi;
   stride = nstride;
@@ -967,7 +979,7 @@ void chain_env(State& a, const State& b, const std::map<int, const cd*>& ops, co
   const cplx one = make_double2(1.0, 0.0);
   if (env_in)
     CK(cudaMemcpy2DAsync(E, sizeof(cplx) * c, env_in, sizeof(cplx) * b.sdl[i0], sizeof(cplx) * b.sdl[i0], a.sdl[i0],
-                         cudaMemcpyHostToDevice, st));
+                         cudaMemcpyDefault, st));  // host or device (UVA): sharded chains pass HBM
   else
     CK(cudaMemcpyAsync(E, &one, sizeof(cplx), cudaMemcpyHostToDevice, st));
   for (int i = i0; i < i1; ++i) {
@@ -977,7 +989,7 @@ void chain_env(State& a, const State& b, const std::map<int, const cd*>& ops, co
   }
   check_launch();
   const long long ra = a.sdr[i1 - 1], rb = b.sdr[i1 - 1];
-  CK(cudaMemcpy2DAsync(env_out, sizeof(cplx) * rb, E, sizeof(cplx) * c, sizeof(cplx) * rb, ra, cudaMemcpyDeviceToHost,
+  CK(cudaMemcpy2DAsync(env_out, sizeof(cplx) * rb, E, sizeof(cplx) * c, sizeof(cplx) * rb, ra, cudaMemcpyDefault,
                        st));
   CK(cudaStreamSynchronize(st));
 }
@@ -1448,7 +1460,7 @@ static void amplitude_env(State& a, const char* bits, int32_t count, const cplx*
     cplx* E2 = (cplx*)a.q2.p;
     long long ld = l0;
     if (env_in)
-      CK(cudaMemcpyAsync(E, env_in + (long long)c0 * l0, sizeof(cplx) * c * l0, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(E, env_in + (long long)c0 * l0, sizeof(cplx) * c * l0, cudaMemcpyDefault, st));
     else
       launch_fill(E, c, make_double2(1.0, 0.0), st);  // env = ones(1) per string, ld = 1 at site 0
     for (int i = i0; i < i1; ++i) {
@@ -1459,7 +1471,7 @@ static void amplitude_env(State& a, const char* bits, int32_t count, const cplx*
       std::swap(E, E2);
     }
     check_launch();
-    CK(cudaMemcpyAsync(env_out + (long long)c0 * rn, E, sizeof(cplx) * c * rn, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(env_out + (long long)c0 * rn, E, sizeof(cplx) * c * rn, cudaMemcpyDefault, st));
     CK(cudaStreamSynchronize(st));
   }
 }

@@ -18,9 +18,31 @@ struct Error : std::runtime_error {
 [[noreturn]] void fail(int code, const std::string& msg);
 std::string& last_error_slot();  // mpsim_gpu_last_error() of the calling thread
 
+// Owning device / pinned-host buffers: move-only, freed by the destructor, so
+// a workspace added later (or a local left on an error path) cannot leak.
+// ensure() grows by at least 1.5x so buffers that grow step by step (the
+// sampler's prefix environments) reallocate O(log) times.
 struct DeviceBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  DeviceBuf() = default;
+  DeviceBuf(const DeviceBuf&) = delete;
+  DeviceBuf& operator=(const DeviceBuf&) = delete;
+  DeviceBuf(DeviceBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  DeviceBuf& operator=(DeviceBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      bytes = o.bytes;
+      o.p = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DeviceBuf() { release(); }
   void ensure(size_t b);
   void release();
 };
@@ -28,6 +50,24 @@ struct DeviceBuf {
 struct PinnedBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  PinnedBuf() = default;
+  PinnedBuf(const PinnedBuf&) = delete;
+  PinnedBuf& operator=(const PinnedBuf&) = delete;
+  PinnedBuf(PinnedBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  PinnedBuf& operator=(PinnedBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p;
+      bytes = o.bytes;
+      o.p = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~PinnedBuf() { release(); }
   void ensure(size_t b);
   void release();
 };

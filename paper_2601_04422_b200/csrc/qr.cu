@@ -267,7 +267,7 @@ static unsigned blocks_for(long long n) {
 void launch_qr_panel(cplx* A, long long lda, int m, int c0, int jb, cplx* P, cplx* V, cplx* T, cplx* tau,
                      cudaStream_t st) {
   static const int chunked = [] {  // MPSIM_QR_PANEL_CHUNKED=0: one warp per column, no row chunks (A/B)
-    const char* v = std::getenv("MPSIM_QR_PANEL_CHUNKED");
+    const char* v = ab_knob("MPSIM_QR_PANEL_CHUNKED");
     return v != nullptr && v[0] == '0' ? 0 : 1;
   }();
   qr_panel_kernel<<<1, 1024, 0, st>>>(A, lda, m, c0, jb, P, V, T, tau, chunked);

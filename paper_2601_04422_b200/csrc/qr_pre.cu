@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(256) qrp_zinit_kernel(const GateDesc* __restri
 // MPSIM_PANEL=legacy selects the L2-streaming panel kernel (A/B only).
 static bool panel_legacy() {
   static const bool v = [] {
-    const char* e = std::getenv("MPSIM_PANEL");
+    const char* e = ab_knob("MPSIM_PANEL");
     return e != nullptr && std::string(e) == "legacy";
   }();
   return v;

@@ -199,55 +199,68 @@ void sample_walk(State& s, int i0, int i1, uint64_t shots, Var u, int& U, Device
   }
 }
 
+// Statistics replay (sampler.cpp:91-138) of one chunk of shots: shot-major,
+// site-minor, on the host trie that persists across chunks and calls.
+void replay_stats(mpsim_gpu_sampler& sp, uint64_t shots, const std::vector<int>& node_of,
+                  const std::vector<std::string>& prefix) {
+  const int n = sp.n;
+  // map (depth, node) -> trie node, built lazily per shot
+  for (uint64_t sh = 0; sh < shots; ++sh) {
+    int tnode = 0;
+    for (int site = 0; site < n; ++site) {
+      if (site == 0) {
+        if (sp.root_known) ++sp.hits;
+        else sp.root_known = true;
+      } else if (sp.trie.entry[(size_t)tnode]) {
+        if (sp.trie.known[(size_t)tnode]) ++sp.hits;
+        else sp.trie.known[(size_t)tnode] = 1;
+      }
+      // bit of this shot at this site: the node at depth site+1 tells it
+      const std::string& pre = prefix[(size_t)node_of[sh]];
+      const int b = pre[(size_t)site] - '0';
+      tnode = sp.trie.step(tnode, b);
+      if (sp.trie.entry[(size_t)tnode]) continue;  // env reused from the cache
+      if (sp.cap == 0 || sp.cache_size < sp.cap) {
+        sp.trie.entry[(size_t)tnode] = 1;
+        ++sp.cache_size;
+      }
+    }
+  }
+}
+
 void run_sample(mpsim_gpu_sampler& sp, uint64_t shots, uint64_t seed) {
   State& s = *sp.st;
   const int n = sp.n;
   DeviceGuard g(s.device);
-  // Variates in the reference order: shot-major, one per site.
+  // Shots go in chunks so host variates (chunk x n doubles) and device
+  // environments (distinct prefixes x 2 chi) stay bounded for any shot count;
+  // the variates come from one engine that carries over between chunks, in the
+  // reference order (shot-major, one per site, sampler.cpp:84/115).
+  const uint64_t chunk = std::max<uint64_t>(1024, (256ull << 20) / (32ull * (uint64_t)s.chi));
   std::mt19937_64 eng(seed);
-  std::vector<double> u((size_t)shots * n);
-  for (size_t i = 0; i < u.size(); ++i) u[i] = static_cast<double>(eng() >> 11) * 0x1.0p-53;
-
-  std::vector<int> node_of(shots, 0);  // shot -> node at the current depth
-  std::vector<std::string> prefix(1, std::string());  // node -> prefix
-  int U = 1;
-  DeviceBuf dE;
-  dE.ensure(sizeof(cplx) * s.chi);
-  const cplx one = make_double2(1.0, 0.0);
-  CKS(cudaMemcpyAsync(dE.p, &one, sizeof(cplx), cudaMemcpyHostToDevice, s.st));
-  sample_walk(s, 0, n, shots, [&](uint64_t sh, int site) { return u[sh * n + site]; }, U, dE, node_of, prefix);
-  // counts, lexicographic (std::map order, sampler.cpp:140)
-  std::vector<uint64_t> cnt((size_t)U, 0);
-  for (uint64_t sh = 0; sh < shots; ++sh) ++cnt[(size_t)node_of[sh]];
   std::map<std::string, uint64_t> counts;
-  for (int k = 0; k < U; ++k) counts[prefix[(size_t)k]] += cnt[(size_t)k];
-  sp.result.assign(counts.begin(), counts.end());
-
-  // Statistics replay (sampler.cpp:91-138): shot-major, site-minor.
-  if (sp.memoize) {
-    // map (depth, node) -> trie node, built lazily per shot
-    for (uint64_t sh = 0; sh < shots; ++sh) {
-      int tnode = 0;
-      for (int site = 0; site < n; ++site) {
-        if (site == 0) {
-          if (sp.root_known) ++sp.hits;
-          else sp.root_known = true;
-        } else if (sp.trie.entry[(size_t)tnode]) {
-          if (sp.trie.known[(size_t)tnode]) ++sp.hits;
-          else sp.trie.known[(size_t)tnode] = 1;
-        }
-        // bit of this shot at this site: the node at depth site+1 tells it
-        const std::string& pre = prefix[(size_t)node_of[sh]];
-        const int b = pre[(size_t)site] - '0';
-        tnode = sp.trie.step(tnode, b);
-        if (sp.trie.entry[(size_t)tnode]) continue;  // env reused from the cache
-        if (sp.cap == 0 || sp.cache_size < sp.cap) {
-          sp.trie.entry[(size_t)tnode] = 1;
-          ++sp.cache_size;
-        }
-      }
-    }
+  std::vector<double> u;
+  std::vector<int> node_of;
+  std::vector<std::string> prefix;
+  DeviceBuf dE;
+  const cplx one = make_double2(1.0, 0.0);
+  for (uint64_t c0 = 0; c0 < shots; c0 += chunk) {
+    const uint64_t cs = std::min(chunk, shots - c0);
+    u.resize((size_t)cs * n);
+    for (size_t i = 0; i < u.size(); ++i) u[i] = static_cast<double>(eng() >> 11) * 0x1.0p-53;
+    node_of.assign(cs, 0);  // shot -> node at the current depth
+    prefix.assign(1, std::string());  // node -> prefix
+    int U = 1;
+    dE.ensure(sizeof(cplx) * s.chi);
+    CKS(cudaMemcpyAsync(dE.p, &one, sizeof(cplx), cudaMemcpyHostToDevice, s.st));
+    sample_walk(s, 0, n, cs, [&](uint64_t sh, int site) { return u[sh * n + site]; }, U, dE, node_of, prefix);
+    // counts, lexicographic (std::map order, sampler.cpp:140)
+    std::vector<uint64_t> cnt((size_t)U, 0);
+    for (uint64_t sh = 0; sh < cs; ++sh) ++cnt[(size_t)node_of[sh]];
+    for (int k = 0; k < U; ++k) counts[prefix[(size_t)k]] += cnt[(size_t)k];
+    if (sp.memoize) replay_stats(sp, cs, node_of, prefix);
   }
+  sp.result.assign(counts.begin(), counts.end());
 }
 
 }  // namespace

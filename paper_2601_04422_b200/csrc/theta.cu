@@ -313,7 +313,7 @@ void theta_init() {
 // MPSIM_THETA=simt selects the DFMA kernel (A/B only).
 static bool theta_simt() {
   static const bool v = [] {
-    const char* e = std::getenv("MPSIM_THETA");
+    const char* e = ab_knob("MPSIM_THETA");
     return e != nullptr && std::string(e) == "simt";
   }();
   return v;

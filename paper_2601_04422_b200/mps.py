@@ -75,7 +75,7 @@ class MpsState:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and N._lib is not None:
+        if h is not None and N._lib is not None and not getattr(self, "_borrowed", False):
             N._lib.mpsim_gpu_state_destroy(h)
             self._h = None
 

@@ -153,6 +153,30 @@ def lib():
         "mpsim_gen_brickwork_qasm": (C.c_int, [I32, I32, U64, I32, I32, C.POINTER(VP), C.POINTER(VP)]),
         "mpsim_run_config_defaults": (None, [C.POINTER(RunConfig)]),
         "mpsim_gpu_run_circuit": (C.c_int, [C.POINTER(RunConfig), C.POINTER(VP)]),
+        # multi-GPU shards (csrc/shard.cu)
+        "mpsim_shard_bounds": (C.c_int, [I32, I32, I64, C.POINTER(I32)]),
+        "mpsim_shard_partition_layer": (C.c_int, [C.POINTER(Gate), I32, I32, I32, I32, I32, C.POINTER(Gate),
+                                                  C.POINTER(I32), C.POINTER(I32), C.POINTER(I32)]),
+        "mpsim_gpu_nccl_unique_id": (C.c_int, [VP]),
+        "mpsim_gpu_shard_create": (C.c_int, [I32, I64, I32, I32, VP, I32, C.POINTER(VP)]),
+        "mpsim_gpu_shard_destroy": (C.c_int, [VP]),
+        "mpsim_gpu_shard_info": (C.c_int, [VP, C.POINTER(I32), C.POINTER(I32), C.POINTER(VP)]),
+        "mpsim_gpu_shard_set_site": (C.c_int, [VP, I32, I64, I64, DP]),
+        "mpsim_gpu_shard_get_site": (C.c_int, [VP, I32, C.POINTER(I64), C.POINTER(I64), DP]),
+        "mpsim_gpu_shard_bond_dims": (C.c_int, [VP, C.POINTER(I64)]),
+        "mpsim_gpu_shard_apply_layer": (C.c_int, [VP, C.POINTER(Gate), I32, C.POINTER(Policy),
+                                                  C.POINTER(ExecStats)]),
+        "mpsim_gpu_shard_execute": (C.c_int, [VP, C.POINTER(Gate), I32, C.POINTER(Policy), C.POINTER(ExecStats)]),
+        "mpsim_gpu_shard_amplitudes": (C.c_int, [VP, C.c_char_p, I32, DP]),
+        "mpsim_gpu_shard_overlap": (C.c_int, [VP, VP, DP]),
+        "mpsim_gpu_shard_norm": (C.c_int, [VP, DP]),
+        "mpsim_gpu_shard_expect_1q": (C.c_int, [VP, DP, I32, DP]),
+        "mpsim_gpu_shard_move_center": (C.c_int, [VP, I32]),
+        "mpsim_gpu_shard_ortho_center": (C.c_int, [VP, C.POINTER(I32)]),
+        "mpsim_gpu_shard_sample": (C.c_int, [VP, U64, U64, U64, C.POINTER(I32)]),
+        "mpsim_gpu_shard_sample_result": (C.c_int, [VP, I32, C.c_char_p, C.POINTER(U64)]),
+        "mpsim_gpu_shard_allreduce": (C.c_int, [VP, DP, I32, I32]),
+        "mpsim_gpu_shard_barrier": (C.c_int, [VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -218,3 +218,30 @@ def test_sample_segments_compose_to_the_sampler(gpu, oracle):
     for i in range(n):
         ch.set_site(i, g.site(i))
     assert ch.sample(shots, seed, chunk=512) == want
+
+
+def test_no_device_memory_growth_across_calls(gpu, oracle):
+    """Workspaces are owned (RAII) by the state / call that made them: sampling
+    and creating + destroying states in a loop leaves free device memory flat."""
+    import gc
+
+    import torch
+    o = oracle.MpsState.random(12, 32, 5)
+    g = copy_state_to_gpu(gpu, o, chi_hint=32)
+
+    def cycle():
+        for _ in range(3):
+            gpu.sample(g, 20000, 9)
+            t = g.copy()
+            t.apply_2q_local(CX, 5, max_bond=16, cutoff=1e-12)
+            t.move_center(0)
+            del t
+            gc.collect()
+        g.synchronize()
+
+    cycle()  # first-use allocations (pool, module load)
+    free0, _ = torch.cuda.mem_get_info(0)
+    for _ in range(3):
+        cycle()
+    free1, _ = torch.cuda.mem_get_info(0)
+    assert free0 - free1 <= 64 << 20, (free0, free1)
