@@ -14,6 +14,7 @@
 // batched launch path (every layer is one launch sequence).
 #pragma once
 
+#include <array>
 #include <complex>
 #include <cstdint>
 #include <limits>
@@ -361,6 +362,114 @@ class Sampler {  // sampler.hpp:50-86
 inline ShotResult sample(const MpsState& s, std::uint64_t shots, std::uint64_t seed, SamplerOptions o = {}) {
   Sampler sp(s, o);
   return sp.sample(shots, seed);
+}
+
+// ---- multi-GPU chains (no reference counterpart: the reference is one
+// process; this replaces execute_parallel's worker pool across GPUs). One
+// process per GPU; rank 0 draws the NCCL id (nccl_unique_id) and the caller
+// hands it to the other ranks out of band, as with ncclCommInitRank. Every
+// rank issues the same calls in the same order; results are those of one GPU
+// bit for bit.
+using NcclId = std::array<unsigned char, 128>;
+inline NcclId nccl_unique_id() {
+  NcclId id{};
+  detail::check(mpsim_gpu_nccl_unique_id(id.data()));
+  return id;
+}
+
+class ShardedChain {
+ public:
+  ShardedChain(int n_qubits, Index chi, int rank, int world, const NcclId* id = nullptr, int device = 0)
+      : n_(n_qubits) {
+    detail::check(mpsim_gpu_shard_create(n_qubits, chi, rank, world, id ? id->data() : nullptr, device, &h_));
+    detail::check(mpsim_gpu_shard_info(h_, &lo_, &hi_, nullptr));
+  }
+  ShardedChain(const ShardedChain&) = delete;
+  ShardedChain& operator=(const ShardedChain&) = delete;
+  ~ShardedChain() {
+    if (h_) mpsim_gpu_shard_destroy(h_);
+  }
+  int lo() const { return lo_; }  // owned sites [lo, hi)
+  int hi() const { return hi_; }
+  int num_qubits() const { return n_; }
+  void set_site(int i, const CTensor& t) {
+    if (t.rank() != 3 || t.extent(1) != 2) throw std::invalid_argument("site must be (left, 2, right)");
+    detail::check(mpsim_gpu_shard_set_site(h_, i, t.extent(0), t.extent(2), reinterpret_cast<const double*>(t.data())));
+  }
+  CTensor site(int i) const {
+    int64_t dl = 0, dr = 0;
+    detail::check(mpsim_gpu_shard_get_site(h_, i, &dl, &dr, nullptr));
+    CTensor t({dl, 2, dr});
+    detail::check(mpsim_gpu_shard_get_site(h_, i, &dl, &dr, reinterpret_cast<double*>(t.data())));
+    return t;
+  }
+  std::vector<Index> owned_bond_dims() const {  // bonds lo .. hi
+    std::vector<Index> b(static_cast<size_t>(hi_ - lo_) + 1);
+    detail::check(mpsim_gpu_shard_bond_dims(h_, b.data()));
+    return b;
+  }
+  // one layer of disjoint local gates (global indices), every rank the same layer
+  ExecStats apply_layer(const std::vector<FusedGate>& layer, const TruncationPolicy& p) {
+    const auto g = detail_gates(layer);
+    const mpsim_policy pol{p.max_bond, p.cutoff};
+    mpsim_exec_stats st{};
+    detail::check(mpsim_gpu_shard_apply_layer(h_, g.data(), static_cast<int32_t>(g.size()), &pol, &st));
+    return ExecStats{st.peak_bond, st.total_discarded_weight, st.layers, st.device_ms};
+  }
+  // execute_parallel over the chain (non-local gates SWAP-lowered, fusion.cpp:137-190)
+  ExecStats execute(const std::vector<FusedGate>& gates, const TruncationPolicy& p) {
+    const auto g = detail_gates(gates);
+    const mpsim_policy pol{p.max_bond, p.cutoff};
+    mpsim_exec_stats st{};
+    detail::check(mpsim_gpu_shard_execute(h_, g.data(), static_cast<int32_t>(g.size()), &pol, &st));
+    return ExecStats{st.peak_bond, st.total_discarded_weight, st.layers, st.device_ms};
+  }
+  Complex amplitude(std::string_view bits) {
+    if (bits.size() != static_cast<size_t>(n_)) throw std::invalid_argument("bit string length must equal qubit count");
+    double out[2];
+    detail::check(mpsim_gpu_shard_amplitudes(h_, bits.data(), 1, out));
+    return {out[0], out[1]};
+  }
+  double norm() {
+    double v = 0.0;
+    detail::check(mpsim_gpu_shard_norm(h_, &v));
+    return v;
+  }
+  Complex expect_1q(const CTensor& op, int q) {
+    double out[2];
+    detail::check(mpsim_gpu_shard_expect_1q(h_, reinterpret_cast<const double*>(op.data()), q, out));
+    return {out[0], out[1]};
+  }
+  void move_center(int c) { detail::check(mpsim_gpu_shard_move_center(h_, c)); }
+  ShotResult sample(std::uint64_t shots, std::uint64_t seed, std::uint64_t chunk = 4096) {
+    int32_t unique = 0;
+    detail::check(mpsim_gpu_shard_sample(h_, shots, seed, chunk, &unique));
+    ShotResult r;
+    r.shots = shots;
+    r.seed = seed;
+    std::string bits(static_cast<size_t>(n_), '0');
+    for (int i = 0; i < unique; ++i) {
+      std::uint64_t c = 0;
+      detail::check(mpsim_gpu_shard_sample_result(h_, i, bits.data(), &c));
+      r.counts[bits] = c;
+    }
+    return r;
+  }
+  double max_over_ranks(double x) {
+    detail::check(mpsim_gpu_shard_allreduce(h_, &x, 1, MPSIM_REDUCE_MAX));
+    return x;
+  }
+  void barrier() { detail::check(mpsim_gpu_shard_barrier(h_)); }
+  mpsim_gpu_shard* handle() const { return h_; }
+
+ private:
+  static std::vector<mpsim_gate> detail_gates(const std::vector<FusedGate>& gates);
+  int n_;
+  int32_t lo_ = 0, hi_ = 0;
+  mpsim_gpu_shard* h_ = nullptr;
+};
+inline std::vector<mpsim_gate> ShardedChain::detail_gates(const std::vector<FusedGate>& gates) {
+  return to_abi(gates);
 }
 
 // ---- host front end (circuit.hpp, runner.hpp, generators.hpp) -------------

@@ -9,6 +9,13 @@
 
 namespace mpsim_gpu {
 
+#define CKC(x)                                                                          \
+  do {                                                                                  \
+    cudaError_t e_ = (x);                                                               \
+    if (e_ != cudaSuccess) fail(MPSIM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+#define CK_CANON CKC
+
 void launch_qr_panel(cplx* A, long long lda, int m, int c0, int jb, cplx* P, cplx* V, cplx* T, cplx* tau,
                      cudaStream_t st);
 void launch_set_identity(cplx* Y, long long ld, int m, int k, cudaStream_t st);
@@ -18,6 +25,85 @@ void launch_site_adjoint(const cplx* site, int chi, int dl, int dr, cplx* A, lon
 void launch_site_from_adjoint(const cplx* Q, long long ldq, int k, int dr, cplx* site, int chi, cudaStream_t st);
 void launch_sum_abs2(const cplx* A, long long lda, int rows, int cols, double* out, cudaStream_t st);
 void launch_cgemm(const GemmArgs&, cudaStream_t);
+void launch_qr_factor(const GateDesc*, int, int, int, cplx*, cplx*, long long, cplx*, int, int, cudaStream_t);
+void launch_qr_apply(const GateDesc*, int, int, int, cplx*, const cplx*, long long, const cplx*, int, const int*,
+                     long long, const GateOut*, cudaStream_t);
+
+// ---- tensor-core QR of one site (the gate path's QR machinery, qr_pre.cu:
+// 4-CTA cluster panels with the panel held on chip, DMMA trailing updates and
+// DMMA Q formation) for the large sites of a centre move. Operand layout:
+// columns of the site matrix as split-plane vectors (common.cuh).
+
+// left (right = 0): A_c[r] = site[r chi + c], r < 2 dl, c < dr (the (2Dl x Dr)
+// matricisation); right: A_l[e] = conj(site[(l 2 + p) chi + r]), e = p dr + r
+// (the (Dl x 2Dr)^H one). Rows m .. ld are zeroed.
+__global__ void site_to_qr_kernel(const cplx* __restrict__ site, int chi, int dl, int dr, int right,
+                                  cplx* __restrict__ A, long long ld, int n) {
+  const int m = right ? 2 * dr : 2 * dl;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n * ld;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i / ld), r = (int)(i % ld);
+    cplx v = make_double2(0.0, 0.0);
+    if (r < m) {
+      if (!right) {
+        v = site[(long long)r * chi + c];
+      } else {
+        const int p = r / dr, rr = r % dr;
+        v = site[(long long)(c * 2 + p) * chi + rr];
+        v.y = -v.y;
+      }
+    }
+    xs_set(A + (long long)c * ld, ld, r, v);
+  }
+}
+
+// R (k x n, row-major) = the upper triangle of the factored operand
+__global__ void qr_extract_r_kernel(const cplx* __restrict__ A, long long ld, int k, int n, cplx* __restrict__ R) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)k * n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i / n), c = (int)(i % n);
+    R[i] = j <= c ? xs_get(A + (long long)c * ld, ld, j) : make_double2(0.0, 0.0);
+  }
+}
+
+// X (n vectors of length m_pad) = I, order = identity, out.k = k: the inputs
+// of launch_qr_apply that make it form Q = Q1 [I_k; 0] in the QR area.
+__global__ void qr_identity_kernel(cplx* __restrict__ X, long long m_pad, int n, int n_pad, int* __restrict__ order,
+                                   GateOut* __restrict__ out, int k) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)n_pad * m_pad;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i / m_pad), r = (int)(i % m_pad);
+    xs_set(X + (long long)j * m_pad, m_pad, r, make_double2(j == r && j < n ? 1.0 : 0.0, 0.0));
+    if (r == 0) order[j] = j;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    GateOut o;
+    o.k = k;
+    o.status = 0;
+    o.w = 0.0;
+    o.scale = 1.0;
+    *out = o;
+  }
+}
+
+// site <- Q (left: rows r < 2 dl, columns j < k) or Q^H (right: site[(j 2 + p)
+// chi + r] = conj(Q_j[p dr + r]))
+__global__ void q_to_site_kernel(const cplx* __restrict__ Z, long long ld, int k, int dl, int dr, int right,
+                                 cplx* __restrict__ site, int chi) {
+  const int m = right ? 2 * dr : 2 * dl;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)k * m;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int j = (int)(i / m), r = (int)(i % m);
+    cplx v = xs_get(Z + (long long)j * ld, ld, r);
+    if (!right) {
+      site[(long long)r * chi + j] = v;
+    } else {
+      const int p = r / dr, rr = r % dr;
+      v.y = -v.y;
+      site[(long long)(j * 2 + p) * chi + rr] = v;
+    }
+  }
+}
 
 namespace {
 
@@ -25,7 +111,61 @@ constexpr int kQB = 32;
 
 struct QrWork {
   DeviceBuf W, P, Vall, Tall, tau, W1, W2, Q, R, tmp, nrm;
+  DeviceBuf ws, vbuf, tbuf, desc, order, out;  // tensor-core path
 };
+
+unsigned grid_of(long long n) { return (unsigned)std::max(1LL, std::min((n + 255) / 256, 8LL * 148)); }
+
+// The tensor-core path covers tall operands whose panels the cluster kernel
+// holds on chip (m <= 2048); small or wide sites keep the streaming panel.
+bool tc_qr(int m, int n) { return n >= 64 && m >= n && m <= 2048; }
+
+// Factor the site's matricisation with the qr_pre.cu machinery: R (k x n,
+// row-major) into w.R, Q written back into the site (Q or Q^H per side).
+int tc_site_qr(State& s, QrWork& w, cplx* site, int dl, int dr, int right) {
+  const int m = right ? 2 * dr : 2 * dl, n = right ? dl : dr, k = std::min(m, n);
+  GateDesc d{};
+  d.q = 0;
+  d.n = n;
+  d.n_pad = (n + kP - 1) / kP * kP;
+  d.nb = d.n_pad / kW;
+  d.qr_m = m;
+  d.qr_m_pad = (m + kE - 1) / kE * kE;
+  d.m = n;
+  d.m_pad = (n + kE - 1) / kE * kE;
+  d.pre = 1;
+  d.ws_off = 0;                                          // X (form_rh / identity)
+  d.qr_off = (long long)d.n_pad * d.m_pad;                 // the QR operand
+  const long long elems = d.qr_off + (long long)d.n_pad * d.qr_m_pad;
+  const int npan = d.n_pad / kQB;
+  w.ws.ensure(sizeof(cplx) * (size_t)elems);
+  w.vbuf.ensure(sizeof(cplx) * (size_t)npan * kQB * d.qr_m_pad);
+  w.tbuf.ensure(sizeof(cplx) * (size_t)npan * kQB * kQB);
+  w.desc.ensure(sizeof(GateDesc));
+  w.order.ensure(sizeof(int) * (size_t)d.n_pad);
+  w.out.ensure(sizeof(GateOut));
+  w.R.ensure(sizeof(cplx) * (size_t)k * n);
+  cplx* ws = (cplx*)w.ws.p;
+  cudaStream_t st = s.st;
+  CK_CANON(cudaMemcpyAsync(w.desc.p, &d, sizeof(GateDesc), cudaMemcpyHostToDevice, st));
+  const GateDesc* dd = (const GateDesc*)w.desc.p;
+  site_to_qr_kernel<<<grid_of((long long)n * d.qr_m_pad), 256, 0, st>>>(site, s.chi, dl, dr, right, ws + d.qr_off,
+                                                                         d.qr_m_pad, n);
+  // zero padding vectors n .. n_pad of the operand
+  if (d.n_pad > n)
+    CK_CANON(cudaMemsetAsync(ws + d.qr_off + (long long)n * d.qr_m_pad, 0,
+                             sizeof(cplx) * (size_t)(d.n_pad - n) * d.qr_m_pad, st));
+  launch_qr_factor(dd, 1, d.n_pad, d.m_pad, ws, (cplx*)w.vbuf.p, d.qr_m_pad, (cplx*)w.tbuf.p, npan, 0, st);
+  qr_extract_r_kernel<<<grid_of((long long)k * n), 256, 0, st>>>(ws + d.qr_off, d.qr_m_pad, k, n, (cplx*)w.R.p);
+  qr_identity_kernel<<<grid_of((long long)d.n_pad * d.m_pad), 256, 0, st>>>(ws, d.m_pad, n, d.n_pad,
+                                                                             (int*)w.order.p, (GateOut*)w.out.p, k);
+  launch_qr_apply(dd, 1, d.n_pad, (int)d.qr_m_pad, ws, (const cplx*)w.vbuf.p, d.qr_m_pad, (const cplx*)w.tbuf.p, npan,
+                  (const int*)w.order.p, d.n_pad, (const GateOut*)w.out.p, st);
+  q_to_site_kernel<<<grid_of((long long)k * m), 256, 0, st>>>(ws + d.qr_off, d.qr_m_pad, k, dl, dr, right, site,
+                                                              s.chi);
+  s.launches += 4 + 2 * npan + 1 + npan + 1;
+  return k;
+}
 
 void gemm(State& s, int M, int N, int K, const cplx* A, long long lda, int opA, const cplx* B, long long ldb,
           int opB, cplx* C, long long ldc, double alpha, int acc) {
@@ -82,11 +222,6 @@ int thin_qr(State& s, QrWork& w, cplx* W, int m, int n, cplx* Q, long long ldq, 
   return k;
 }
 
-#define CKC(x)                                                                          \
-  do {                                                                                  \
-    cudaError_t e_ = (x);                                                               \
-    if (e_ != cudaSuccess) fail(MPSIM_ECUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
-  } while (0)
 
 // sweep_left_of (mps.cpp:69-80): site i = Q (Dl,2,k), site i+1 = R * site i+1.
 void left_step(State& s, QrWork& w, int i) {
@@ -97,10 +232,15 @@ void left_step(State& s, QrWork& w, int i) {
   w.W.ensure(sizeof(cplx) * (size_t)m * n);
   w.R.ensure(sizeof(cplx) * (size_t)std::min(m, n) * n);
   w.tmp.ensure(sizeof(cplx) * (size_t)s.stride);
-  cplx* W = (cplx*)w.W.p;
-  launch_copy_matrix(site, s.chi, W, n, m, n, 0, s.st);
-  ++s.launches;
-  const int k = thin_qr(s, w, W, m, n, site, s.chi, (cplx*)w.R.p, n);
+  int k;
+  if (tc_qr(m, n)) {
+    k = tc_site_qr(s, w, site, dl, dr, 0);
+  } else {
+    cplx* W = (cplx*)w.W.p;
+    launch_copy_matrix(site, s.chi, W, n, m, n, 0, s.st);
+    ++s.launches;
+    k = thin_qr(s, w, W, m, n, site, s.chi, (cplx*)w.R.p, n);
+  }
   const int dr2 = (int)s.sdr[i + 1];
   cplx* tmp = (cplx*)w.tmp.p;
   for (int p = 0; p < 2; ++p)
@@ -124,12 +264,16 @@ void right_step(State& s, QrWork& w, int i) {
   w.R.ensure(sizeof(cplx) * (size_t)k * n);
   w.Q.ensure(sizeof(cplx) * (size_t)m * k);
   w.tmp.ensure(sizeof(cplx) * (size_t)s.stride);
-  cplx* W = (cplx*)w.W.p;
-  launch_site_adjoint(site, s.chi, dl, dr, W, n, s.st);
-  ++s.launches;
-  thin_qr(s, w, W, m, n, (cplx*)w.Q.p, k, (cplx*)w.R.p, n);
-  launch_site_from_adjoint((cplx*)w.Q.p, k, k, dr, site, s.chi, s.st);
-  ++s.launches;
+  if (tc_qr(m, n)) {
+    tc_site_qr(s, w, site, dl, dr, 1);
+  } else {
+    cplx* W = (cplx*)w.W.p;
+    launch_site_adjoint(site, s.chi, dl, dr, W, n, s.st);
+    ++s.launches;
+    thin_qr(s, w, W, m, n, (cplx*)w.Q.p, k, (cplx*)w.R.p, n);
+    launch_site_from_adjoint((cplx*)w.Q.p, k, k, dr, site, s.chi, s.st);
+    ++s.launches;
+  }
   const int dl2 = (int)s.sdl[i - 1];
   cplx* tmp = (cplx*)w.tmp.p;
   gemm(s, 2 * dl2, k, n, prev, s.chi, 0, (cplx*)w.R.p, n, 1, tmp, s.chi, 1.0, 0);
@@ -155,7 +299,6 @@ void sweep_left_impl(State& s, int i0, int i1) {
   for (int i = i0; i < i1; ++i) left_step(s, w, i);
   CKC(cudaStreamSynchronize(s.st));
   CKC(cudaGetLastError());
-  for (DeviceBuf* b : {&w.W, &w.P, &w.Vall, &w.Tall, &w.tau, &w.W1, &w.W2, &w.Q, &w.R, &w.tmp, &w.nrm}) b->release();
   s.center = -1;
 }
 
@@ -166,7 +309,6 @@ void sweep_right_impl(State& s, int i0, int i1) {
   for (int i = i1; i >= i0; --i) right_step(s, w, i);
   CKC(cudaStreamSynchronize(s.st));
   CKC(cudaGetLastError());
-  for (DeviceBuf* b : {&w.W, &w.P, &w.Vall, &w.Tall, &w.tau, &w.W1, &w.W2, &w.Q, &w.R, &w.tmp, &w.nrm}) b->release();
   s.center = -1;
 }
 
@@ -197,7 +339,6 @@ void move_center_impl(State& s, int c) {
   CKC(cudaMemcpyAsync(&n2, w.nrm.p, sizeof(double), cudaMemcpyDeviceToHost, s.st));
   CKC(cudaStreamSynchronize(s.st));
   CKC(cudaGetLastError());
-  for (DeviceBuf* b : {&w.W, &w.P, &w.Vall, &w.Tall, &w.tau, &w.W1, &w.W2, &w.Q, &w.R, &w.tmp, &w.nrm}) b->release();
   if (std::sqrt(n2) < 1e-14) fail(MPSIM_ENUMERIC, "cannot canonicalize a zero-norm state");
   s.center = c;
 }

@@ -41,6 +41,10 @@ constexpr int kW = 16;
 constexpr int kP = 2 * kW;  // vectors per block pair
 constexpr int kE = 64;      // element chunk
 constexpr int kPad = 33;    // padded smem row (complex) for [e][vector] tiles
+// Per-gate singular-value sorts (de Rijk order, truncation) run in one CTA
+// with the keys in shared memory: 12 bytes per vector -> 16384 vectors
+// (bond dimensions up to 8192).
+constexpr int kMaxSortN = 16384;
 
 // One two-qubit gate of a batched layer launch.
 struct GateDesc {

@@ -18,6 +18,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+
 #include "common.cuh"
 #include "engine.h"
 #include "mpsim_gpu.h"
@@ -25,7 +27,8 @@
 namespace mpsim_gpu {
 
 // ---- launchers implemented in the kernel translation units
-void launch_theta(const GateDesc*, int, int, const cplx*, long long, int, cplx*, double*, cudaStream_t);
+int launch_theta(const GateDesc*, const GateDesc*, int, int, const cplx*, long long, int, cplx*, double*, CUtensorMap*,
+                 CUtensorMap*, cudaStream_t);
 int theta_tiles(int dl, int dr);
 void jacobi_split_init();
 void launch_jacobi_sweep(const GateDesc*, int, int, cplx*, const int*, int*, double, double, const double*, double,
@@ -48,7 +51,7 @@ void launch_qr_apply(const GateDesc*, int, int, int, cplx*, const cplx*, long lo
 // QR preconditioning (qr_pre.cu) of gates whose SVD operand has at least
 // kQrMinN vectors: MPSIM_QR=2 (default) two QR steps, 1 one, 0 none.
 constexpr int kQrMinN = 128;
-constexpr int kMaxSvdN = 2048;  // derijk_kernel / truncate_kernel: one 1024-thread CTA, 2048 keys
+constexpr int kMaxSvdN = kMaxSortN;  // derijk_kernel / truncate_kernel: one CTA, keys in shared memory
 static int qr_policy() {
   static const int v = [] {
     const char* e = ab_knob("MPSIM_QR");
@@ -109,9 +112,10 @@ static int jacobi_mode() {
   }();
   return m;
 }
-void launch_derijk(const GateDesc*, int, const cplx*, const int*, int*, long long, cudaStream_t);
+void launch_derijk(const GateDesc*, int, const cplx*, const int*, int*, long long, int, cudaStream_t);
 void launch_norms(const GateDesc*, int, int, const cplx*, double*, long long, cudaStream_t);
-void launch_truncate(const GateDesc*, int, double*, int*, long long, GateOut*, const double*, double, cudaStream_t);
+void launch_truncate(const GateDesc*, int, double*, int*, long long, GateOut*, const double*, double, int,
+                     cudaStream_t);
 void launch_write_factors(const GateDesc*, int, int, int, int, const cplx*, const double*, const int*, long long,
                           const GateOut*, const double*, double, cudaStream_t);
 void launch_apply1q(const Gate1Desc*, int, long long, cplx*, long long, int, cudaStream_t);
@@ -429,7 +433,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   for (const GateDesc& d : descs)
     if (d.n_pad > kMaxSvdN)  // de Rijk / truncation sort one gate's vectors in one CTA
       fail(MPSIM_EINVAL, "SVD operand with " + std::to_string(d.n) + " vectors (min dimension) exceeds the " +
-                             std::to_string(kMaxSvdN) + " this build supports (bond dimension <= 1024)");
+                             std::to_string(kMaxSvdN) + " this build supports (bond dimension <= 8192)");
   long long ws_elems = 0;
   int max_tiles = 1, max_nb = 2, max_m = 1, max_n = 1;
   int max_n0 = 1, qr_n_pad = 0, qr_m_pad = 0, qr_jm_pad = 0, max_out_m = 1;
@@ -481,7 +485,11 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   cplx* ws = (cplx*)s.ws.p;
   CK(cudaMemsetAsync(s.d_frob.p, 0, sizeof(double) * ng, st));
   if (src == nullptr) {
-    launch_theta(dph, ng, max_tiles, s.sites, s.stride, s.chi, ws, (double*)s.d_frob.p, st);
+    s.h_maps.ensure(sizeof(CUtensorMap) * 2 * ng);
+    s.d_maps.ensure(sizeof(CUtensorMap) * 2 * ng);
+    const int tv = launch_theta(dph, (const GateDesc*)s.h_gates.p, ng, max_tiles, s.sites, s.stride, s.chi, ws,
+                                (double*)s.d_frob.p, (CUtensorMap*)s.h_maps.p, (CUtensorMap*)s.d_maps.p, st);
+    if (tv == 0) s.h2d_bytes += (long long)sizeof(CUtensorMap) * 2 * ng;
     check_launch("theta_kernel");
     ++s.launches;
   } else {
@@ -543,7 +551,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     CK(cudaMemsetAsync(s.d_rot.p, 0, sizeof(int) * ng, st));
     CK(cudaMemsetAsync(s.d_maxoff.p, 0, sizeof(double) * ng, st));
     CK(cudaMemsetAsync(s.d_offsum.p, 0, sizeof(double) * ng, st));
-    launch_derijk(dg, ng, ws, (const int*)s.d_active.p, (int*)s.d_perm.p, perm_stride, st);
+    launch_derijk(dg, ng, ws, (const int*)s.d_active.p, (int*)s.d_perm.p, perm_stride, (int)perm_stride, st);
     ++s.launches;
     CK(cudaEventRecord(s.evj0, st));
     // One cyclic sweep of the inner 2W x 2W eigensolver per pair visit: the
@@ -644,7 +652,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   launch_norms(dg, ng, max_n, ws, (double*)s.d_sigma.p, sig_stride, st);
   check_launch("norms_kernel");
   launch_truncate(dg, ng, (double*)s.d_sigma.p, (int*)s.d_order.p, sig_stride, (GateOut*)s.d_out.p,
-                  (const double*)s.d_frob.p, kFloorRel2, st);
+                  (const double*)s.d_frob.p, kFloorRel2, max_n, st);
   check_launch("truncate_kernel");
   if (any_pre2) {
     launch_qr_apply(dph + 3 * ng, ng, qr_n_pad, qr_m_pad, ws, (const cplx*)s.d_qrv.p, qr_m_pad,

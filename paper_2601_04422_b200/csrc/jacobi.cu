@@ -18,11 +18,12 @@ __global__ void __launch_bounds__(1024) derijk_kernel(const GateDesc* __restrict
   const int gi = blockIdx.x;
   const GateDesc& g = gates[gi];
   if (!active[gi]) return;
-  __shared__ double key[2048];
-  __shared__ int idx[2048];
   const int n2 = g.n_pad;  // multiple of 32; pad to a power of two below
   int p2 = 1;
   while (p2 < n2) p2 <<= 1;
+  extern __shared__ double sort_smem[];  // p2 keys then p2 indices (launch: the batch's largest p2)
+  double* key = sort_smem;
+  int* idx = reinterpret_cast<int*>(sort_smem + p2);
   const cplx* X = ws + g.ws_off;
   // norms: one warp per vector
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -66,9 +67,18 @@ __global__ void __launch_bounds__(1024) derijk_kernel(const GateDesc* __restrict
   for (int i = threadIdx.x; i < n2; i += blockDim.x) perm[gi * perm_stride + i] = idx[i];
 }
 
+// Sort capacity: one CTA holds a gate's keys in shared memory (12 bytes per
+// vector): up to kMaxSortN = 16384 vectors, i.e. bond dimensions up to 8192.
 void launch_derijk(const GateDesc* d_gates, int n_gates, const cplx* ws, const int* d_active, int* perm,
-                   long long perm_stride, cudaStream_t st) {
-  derijk_kernel<<<n_gates, 1024, 0, st>>>(d_gates, ws, d_active, perm, perm_stride);
+                   long long perm_stride, int max_n_pad, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(derijk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSortN * 12);
+    init = true;
+  }
+  int p2 = 1;
+  while (p2 < max_n_pad) p2 <<= 1;
+  derijk_kernel<<<n_gates, 1024, (size_t)p2 * 12, st>>>(d_gates, ws, d_active, perm, perm_stride);
 }
 
 }  // namespace mpsim_gpu

@@ -123,13 +123,11 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
   // chunks last to first: the rows the Gram pass read last are the likeliest
   // still in L2 (the caller issues chunk nchunks - 1 into buffer 0)
   for (int k = 0; k < nchunks; ++k) {
-    if (k + 1 < nchunks) {
-      ld.issue(buf[(k + 1) & 1], (nchunks - 2 - k) * kC);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    // one barrier per chunk: it publishes chunk k and certifies that every
+    // warp is done with chunk k - 1, whose buffer the next load then reuses
+    cp_async_wait<0>();
     __syncthreads();
+    if (k + 1 < nchunks) ld.issue(buf[(k + 1) & 1], (nchunks - 2 - k) * kC);
     const double* B = buf[k & 1];
     // complex product in three real products (Gauss): T1 = Xr Rr, T2 = Xi Ri,
     // T3 = (Xr + Xi)(Rr + Ri); Re = T1 - T2, Im = T3 - T1 - T2. 48 DMMAs per
@@ -173,7 +171,6 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
         xj[e0 + e] = o[a][0][v];
         xj[c.mp + e0 + e] = o[a][1][v];
       }
-    __syncthreads();
   }
 }
 
@@ -276,16 +273,13 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
     const int s3 = k % 3;
     return s3 == 2 ? S.v.buf3 : S.u.buf[s3];
   };
+  // One barrier per chunk: after it, chunk k is visible to every warp and every
+  // warp is done with chunk k - 1, whose stage the load of chunk k + 2 reuses.
   auto next_chunk = [&](int k) {  // chunk k's data ready in shared memory
-    if (k + 2 < nchunks) {
-      ld.issue(stage(k + 2), (k + 2) * kC);
-      cp_async_wait<2>();
-    } else if (k + 1 < nchunks) {
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
-    }
+    if (k + 1 < nchunks) cp_async_wait<1>();
+    else cp_async_wait<0>();
     __syncthreads();
+    if (k + 2 < nchunks) ld.issue(stage(k + 2), (k + 2) * kC);
   };
   ld.issue(stage(0), 0);
   if (nchunks > 1) ld.issue(stage(1), kC);
@@ -314,8 +308,8 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
         dmma_s(acc[1][0][0], acc[1][0][1], a1, b0);
         dmma_s(acc[1][1][0], acc[1][1][1], a1, b1);
       }
-      __syncthreads();
     }
+    __syncthreads();  // the last stage is read; Gx aliases the chunk buffers
     for (int h = 0; h < 2; ++h) {  // the two k-halves into Gx
       if (kh == h)
 #pragma unroll
@@ -374,8 +368,8 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
         for (int i = 0; i < 5; ++i)
           if (i < nt) dmma_s(acc[i][0], acc[i][1], trow[i] == trow[0] ? a_first : a_last, B[row + ob[i]]);
       }
-      __syncthreads();
     }
+    __syncthreads();  // the last stage is read; Gx aliases the chunk buffers
 #pragma unroll
     for (int i = 0; i < 5; ++i)
       if (i < nt)

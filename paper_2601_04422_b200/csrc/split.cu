@@ -32,15 +32,14 @@ __global__ void __launch_bounds__(256) norms_kernel(const GateDesc* __restrict__
 }
 
 // ---- sort descending + truncation rule (svd.hpp:48-74) + renorm factor.
-// One CTA (1024 threads) per gate; n <= 2048.
+// One CTA (1024 threads) per gate; its keys sit in dynamic shared memory
+// (12 bytes per value, n <= kMaxSortN).
 __global__ void __launch_bounds__(1024) truncate_kernel(const GateDesc* __restrict__ gates,
                                                         double* __restrict__ sigma,
                                                         int* __restrict__ order, long long sig_stride,
                                                         GateOut* __restrict__ out,
                                                         const double* __restrict__ frob2, double floor_rel2) {
   const GateDesc& g = gates[blockIdx.y];
-  __shared__ double key[2048];
-  __shared__ int idx[2048];
   // Singular values at the rounding-noise level of ||theta||_F are exact
   // zeros of a structurally rank-deficient theta (Clifford gates on product
   // states, SWAPs): report them as 0 so svd.hpp:58's cutoff-0 rule trims them
@@ -51,6 +50,9 @@ __global__ void __launch_bounds__(1024) truncate_kernel(const GateDesc* __restri
   const int n = g.n;
   int n2 = 1;
   while (n2 < n) n2 <<= 1;
+  extern __shared__ double sort_smem[];
+  double* key = sort_smem;
+  int* idx = reinterpret_cast<int*>(sort_smem + n2);
   double* sg = sigma + blockIdx.y * sig_stride;
   int* od = order + blockIdx.y * sig_stride;
   if (threadIdx.x == 0) bad = 0;
@@ -252,8 +254,15 @@ void launch_norms(const GateDesc* d_gates, int n_gates, int max_n, const cplx* w
 }
 
 void launch_truncate(const GateDesc* d_gates, int n_gates, double* sigma, int* order, long long sig_stride,
-                     GateOut* d_out, const double* frob2, double floor_rel2, cudaStream_t st) {
-  truncate_kernel<<<dim3(1, n_gates), 1024, 0, st>>>(d_gates, sigma, order, sig_stride, d_out, frob2, floor_rel2);
+                     GateOut* d_out, const double* frob2, double floor_rel2, int max_n, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    cudaFuncSetAttribute(truncate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSortN * 12);
+    init = true;
+  }
+  int p2 = 1;
+  while (p2 < max_n) p2 <<= 1;
+  truncate_kernel<<<dim3(1, n_gates), 1024, (size_t)p2 * 12, st>>>(d_gates, sigma, order, sig_stride, d_out, frob2, floor_rel2);
 }
 
 void launch_write_factors(const GateDesc* d_gates, int n_gates, int max_m, int max_n, int max_n0, const cplx* ws,

@@ -105,6 +105,7 @@ class ShardedChain:
 
     def __init__(self, n, chi, rank=0, world=1, device=0, nccl_id=None):
         self.n, self.chi, self.rank, self.world, self.device = n, chi, rank, world, device
+        os.environ.setdefault("NCCL_DEBUG", "WARN")  # no banner on stdout (bench.py prints one JSON line)
         if world > 1 and nccl_id is None:
             nccl_id = nccl_rendezvous(rank, world)
         h = C.c_void_p()

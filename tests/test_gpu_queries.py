@@ -60,6 +60,27 @@ def test_move_center_mixed_form_large_bonds(gpu, oracle):
     assert np.max(np.abs(g.amplitudes(bits) - ref) / np.abs(ref)) <= 1e-10
 
 
+def test_move_center_tensor_core_qr_chi512(gpu, oracle):
+    """Sites of 1024 x 512 (chi = 512) go through the tensor-core QR (qr_pre.cu
+    cluster panels + DMMA updates + DMMA Q formation): isometries, bonds and
+    amplitudes against the oracle's Householder QR (any exact QR gives the same
+    state; mps.cpp:57-95 fixes only the bond k = min(m, n))."""
+    n = 22
+    o = oracle.MpsState.random(n, 512, 61)
+    g = copy_state_to_gpu(gpu, o, chi_hint=512)
+    bits = ["".join(np.random.default_rng(4).choice(["0", "1"], n)) for _ in range(16)]
+    ref = np.array([o.amplitude(b) for b in bits])
+    g.move_center(11)
+    o.move_center(11)
+    assert g.ortho_center == 11 and (g.bond_dims() == o.bond_dims()).all()
+    for i in range(11):
+        assert _left_defect(g.site(i)) <= 1e-11
+    for i in range(12, n):
+        assert _right_defect(g.site(i)) <= 1e-11
+    assert np.max(np.abs(g.amplitudes(bits) - ref) / np.abs(ref)) <= 1e-10
+    assert abs(g.norm() - o.norm()) <= 1e-12 * o.norm()
+
+
 def test_idempotent_and_zero_norm(gpu, oracle):
     g = copy_state_to_gpu(gpu, oracle.MpsState.random(5, 6, 55))
     g.left_canonicalize()
