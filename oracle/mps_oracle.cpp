@@ -249,7 +249,8 @@ SvdResult svd_jacobi(const Mat& m, Index max_rank, double cutoff) {
 SvdResult svd(const Mat& m, Index max_rank, double cutoff) {
   if (max_rank < 1) throw std::invalid_argument("svd max_rank must be >= 1");
   if (cutoff < 0.0 || cutoff >= 1.0) throw std::invalid_argument("svd cutoff must lie in [0, 1)");
-  if (g_svd_backend.load(std::memory_order_relaxed) == 1) return svd_jacobi(m, max_rank, cutoff);
+  const int backend = g_svd_backend.load(std::memory_order_relaxed);
+  if (backend == 1) return svd_jacobi(m, max_rank, cutoff);
   const int rows = static_cast<int>(m.rows), cols = static_cast<int>(m.cols);
   const int mn = std::min(rows, cols), mx = std::max(rows, cols);
   std::vector<cplx> a = to_colmajor(m);
@@ -263,12 +264,17 @@ SvdResult svd(const Mat& m, Index max_rank, double cutoff) {
   cplx wq;
   const char jobz = 'S';
   std::vector<cplx> a_copy = a;
-  scipy_zgesdd_(&jobz, &rows, &cols, a.data(), &rows, s.data(), u.data(), &rows, vt.data(), &mn, &wq,
-                &lwork, rwork.data(), iwork.data(), &info, 1);
-  lwork = std::max(1, static_cast<int>(wq.real()));
-  std::vector<cplx> work(static_cast<size_t>(lwork));
-  scipy_zgesdd_(&jobz, &rows, &cols, a.data(), &rows, s.data(), u.data(), &rows, vt.data(), &mn,
-                work.data(), &lwork, rwork.data(), iwork.data(), &info, 1);
+  std::vector<cplx> work;
+  if (backend == 2) {
+    info = 1;  // zgesvd (bidiagonal QR iteration) below, the spread check of make_golden.py
+  } else {
+    scipy_zgesdd_(&jobz, &rows, &cols, a.data(), &rows, s.data(), u.data(), &rows, vt.data(), &mn, &wq,
+                  &lwork, rwork.data(), iwork.data(), &info, 1);
+    lwork = std::max(1, static_cast<int>(wq.real()));
+    work.resize(static_cast<size_t>(lwork));
+    scipy_zgesdd_(&jobz, &rows, &cols, a.data(), &rows, s.data(), u.data(), &rows, vt.data(), &mn,
+                  work.data(), &lwork, rwork.data(), iwork.data(), &info, 1);
+  }
   if (info > 0) {
     // Divide-and-conquer did not converge: retry with QR-iteration zgesvd
     // before reporting failure (svd.hpp:96-99 throws NumericError).

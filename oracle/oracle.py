@@ -279,9 +279,10 @@ def svd(m, max_rank=None, cutoff=0.0):
 
 
 def set_svd_backend(name: str):
-    """'zgesdd' (default; divide and conquer, Eigen BDCSVD's family) or 'zgesvj'
-    (one-sided Jacobi): the second is an independent check of the first."""
-    lib().orc_set_svd_backend({"zgesdd": 0, "zgesvj": 1}[name])
+    """'zgesdd' (default; divide and conquer, Eigen BDCSVD's family), 'zgesvj'
+    (one-sided Jacobi: an independent check of the first) or 'zgesvd'
+    (bidiagonal QR iteration)."""
+    lib().orc_set_svd_backend({"zgesdd": 0, "zgesvj": 1, "zgesvd": 2}[name])
 
 
 def truncation_rank(s, max_rank=None, cutoff=0.0):

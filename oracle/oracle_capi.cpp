@@ -168,9 +168,10 @@ int orc_svd(int rows, int cols, const double* data, Index max_rank, double cutof
     *w = r.discarded_weight;
   });
 }
-// 0: zgesdd (default, BDCSVD's family), 1: zgesvj (independent cross-check)
+// 0: zgesdd (default, BDCSVD's family), 1: zgesvj (independent cross-check),
+// 2: zgesvd (bidiagonal QR iteration)
 int orc_set_svd_backend(int b) {
-  oracle::g_svd_backend.store(b == 1 ? 1 : 0);
+  oracle::g_svd_backend.store(b == 1 || b == 2 ? b : 0);
   return 0;
 }
 

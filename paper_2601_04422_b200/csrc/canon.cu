@@ -28,6 +28,9 @@ void launch_cgemm(const GemmArgs&, cudaStream_t);
 void launch_qr_factor(const GateDesc*, int, int, int, cplx*, cplx*, long long, cplx*, int, int, cudaStream_t);
 void launch_qr_apply(const GateDesc*, int, int, int, cplx*, const cplx*, long long, const cplx*, int, const int*,
                      long long, const GateOut*, cudaStream_t);
+bool site_qr_supported(int m, int n);
+int site_qr(State& s, cplx* site, int dl, int dr, int right, DeviceBuf& Abuf, DeviceBuf& Vbuf, DeviceBuf& Tbuf,
+            DeviceBuf& Qbuf, cplx* R, cudaStream_t aux, cudaEvent_t* evs);
 
 // ---- tensor-core QR of one site (the gate path's QR machinery, qr_pre.cu:
 // 4-CTA cluster panels with the panel held on chip, DMMA trailing updates and
@@ -116,9 +119,22 @@ struct QrWork {
 
 unsigned grid_of(long long n) { return (unsigned)std::max(1LL, std::min((n + 255) / 256, 8LL * 148)); }
 
-// The tensor-core path covers tall operands whose panels the cluster kernel
-// holds on chip (m <= 2048); small or wide sites keep the streaming panel.
+// Site QRs: up to 1024 rows, the latency-shaped kernels of qr_site.cu
+// (register-resident 8-column panels, look-ahead updates on a second
+// stream); up to 2048 rows, the gate path's cluster panels + DMMA updates
+// (qr_pre.cu); small or wide sites keep the streaming panel of qr.cu.
 bool tc_qr(int m, int n) { return n >= 64 && m >= n && m <= 2048; }
+
+int fast_site_qr(State& s, QrWork& w, cplx* site, int dl, int dr, int right) {
+  if (!s.aux) {
+    CK_CANON(cudaStreamCreateWithFlags(&s.aux, cudaStreamNonBlocking));
+    CK_CANON(cudaEventCreateWithFlags(&s.evq[0], cudaEventDisableTiming));
+    CK_CANON(cudaEventCreateWithFlags(&s.evq[1], cudaEventDisableTiming));
+  }
+  const int m = right ? 2 * dr : 2 * dl, n = right ? dl : dr, k = std::min(m, n);
+  w.R.ensure(sizeof(cplx) * (size_t)k * n);
+  return site_qr(s, site, dl, dr, right, w.W, w.Vall, w.Tall, w.Q, (cplx*)w.R.p, s.aux, s.evq);
+}
 
 // Factor the site's matricisation with the qr_pre.cu machinery: R (k x n,
 // row-major) into w.R, Q written back into the site (Q or Q^H per side).
@@ -233,7 +249,9 @@ void left_step(State& s, QrWork& w, int i) {
   w.R.ensure(sizeof(cplx) * (size_t)std::min(m, n) * n);
   w.tmp.ensure(sizeof(cplx) * (size_t)s.stride);
   int k;
-  if (tc_qr(m, n)) {
+  if (site_qr_supported(m, n)) {
+    k = fast_site_qr(s, w, site, dl, dr, 0);
+  } else if (tc_qr(m, n)) {
     k = tc_site_qr(s, w, site, dl, dr, 0);
   } else {
     cplx* W = (cplx*)w.W.p;
@@ -264,7 +282,9 @@ void right_step(State& s, QrWork& w, int i) {
   w.R.ensure(sizeof(cplx) * (size_t)k * n);
   w.Q.ensure(sizeof(cplx) * (size_t)m * k);
   w.tmp.ensure(sizeof(cplx) * (size_t)s.stride);
-  if (tc_qr(m, n)) {
+  if (site_qr_supported(m, n)) {
+    fast_site_qr(s, w, site, dl, dr, 1);
+  } else if (tc_qr(m, n)) {
     tc_site_qr(s, w, site, dl, dr, 1);
   } else {
     cplx* W = (cplx*)w.W.p;

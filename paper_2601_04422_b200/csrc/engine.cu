@@ -329,6 +329,12 @@ State::~State() {
   cudaEventDestroy(ev1);
   cudaEventDestroy(evj0);
   cudaEventDestroy(evj1);
+  if (aux) {
+    cudaStreamSynchronize(aux);
+    cudaStreamDestroy(aux);
+  }
+  for (cudaEvent_t e : evq)
+    if (e) cudaEventDestroy(e);
   cudaStreamDestroy(st);
 }
 

@@ -108,6 +108,9 @@ struct State {
   double svd_flops = 0.0;         // algorithmic SVD flops of the decomposed matrices (32 M N^2)
   double gate_flops = 0.0;        // algorithmic F_2q of applied gates
   cudaEvent_t evj0 = nullptr, evj1 = nullptr;
+  // centre moves (qr_site.cu): a second stream for trailing updates, two join events
+  cudaStream_t aux = nullptr;
+  cudaEvent_t evq[2] = {nullptr, nullptr};
   long long h2d_bytes = 0, d2h_bytes = 0;  // gate-path host<->device traffic
 
   State(int n, long long chi_hint, int device);

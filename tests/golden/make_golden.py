@@ -18,10 +18,13 @@ execute path as is), the oracle's per-gate kept rank and discarded weight in
 gate order (SWAPs included), the final bond dims, 64 amplitudes of seeded
 random bit strings, and <Z_q>, <X_q> (P9 definition, overlap(psi, O_q psi)).
 The oracle run uses LAPACK zgesdd (Eigen BDCSVD's divide-and-conquer family);
-the same circuit is re-run with LAPACK zgesvj (one-sided Jacobi), and the
-fixture records that the two independent SVDs give identical kept ranks and
-discarded weights within 1e-10 — the oracle's own pin, since the reference
-cannot be built here (Eigen3 absent).
+the same circuit is re-run with a second SVD (c4: LAPACK zgesvj, one-sided
+Jacobi; c3: zgesvd, bidiagonal QR iteration, zgesvj being too slow for ~2000
+1024 x 1024 thetas on 8 cores) and the fixture records that both give the
+same kept ranks and discarded weights within 1e-10, plus the amplitude spread
+between the two runs. For c3, sampled saturated thetas of the run itself also
+go through zgesvj (kept rank, weight). This is the oracle's own pin, since the
+reference cannot be built here (Eigen3 absent).
 """
 import json
 import os
@@ -74,17 +77,60 @@ def tfim_step(n, u, jdt=0.8):
     return c.fuse()
 
 
-def run_oracle(n, gate_list, chi, cutoff, workers):
-    """execute_parallel over the (local) list; reports back in gate order."""
+def run_oracle(n, gate_list, chi, cutoff, workers, pin=None):
+    """execute_parallel layer by layer over the (local) list (the same layer
+    plan the one-call run uses); reports back in gate order. pin(o, layer,
+    gates) runs before each layer (the SVD pin samples its thetas)."""
     o = O.MpsState(n)
-    r = O.execute_parallel(o, gate_list, chi, cutoff, workers=workers)
-    layer_of, _ = gate_list.layer_of()
-    plan = np.argsort(layer_of, kind="stable")  # execute_parallel reports in layer-plan order
-    k = np.empty(len(gate_list), dtype=np.int64)
-    w = np.empty(len(gate_list))
-    k[plan] = r["gate_k"]
-    w[plan] = r["gate_w"]
+    layer_of, nl = gate_list.layer_of()
+    gates = gate_list.gates()
+    k = np.empty(len(gates), dtype=np.int64)
+    w = np.empty(len(gates))
+    for L in range(nl):
+        idx = np.nonzero(layer_of == L)[0]
+        lg = [(gates[i][0], gates[i][1], gates[i][3]) for i in idx]
+        if pin is not None:
+            pin(o, L, lg)
+        r = O.execute_parallel(o, O.GateList(lg), chi, cutoff, workers=workers)
+        k[idx] = r["gate_k"]
+        w[idx] = r["gate_w"]
     return o, k, w
+
+
+def theta_of(o, q, u):
+    """apply_2q_local's theta (gate_apply.cpp:121-131): (2 Dl) x (2 Dr)."""
+    a, b = o.site(q), o.site(q + 1)
+    m = np.einsum("lam,mbr->labr", a, b)
+    dl, dr = a.shape[0], b.shape[2]
+    t = np.einsum("xy,lyr->lxr", u, m.reshape(dl, 4, dr)).reshape(dl, 2, 2, dr)
+    return t.reshape(2 * dl, 2 * dr)
+
+
+def make_pin(chi, cutoff, every, per_layer, start, workers, log):
+    """Pin the oracle's SVD decisions on the fixture's own matrices: sampled
+    saturated thetas go through zgesdd and zgesvj (one-sided Jacobi, an
+    unrelated algorithm); kept ranks must agree and discarded weights to 1e-10."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def pin(o, L, lg):
+        if L < start or (L - start) % every:
+            return
+        bonds = o.bond_dims()
+        cand = [(q0, u) for q0, q1, u in lg if q1 >= 0 and bonds[q0] == bonds[q0 + 1] == bonds[q0 + 2] == chi]
+        for q0, u in cand[:per_layer]:
+            th = theta_of(o, q0, u)
+            res = {}
+            for name in ("zgesdd", "zgesvj"):
+                O.set_svd_backend(name)
+                _, s_, _, w_ = O.svd(th, chi, cutoff)
+                res[name] = (len(s_), w_)
+            O.set_svd_backend("zgesdd")
+            (k1, w1), (k2, w2) = res["zgesdd"], res["zgesvj"]
+            log.append({"layer": int(L), "q": int(q0), "k_zgesdd": k1, "k_zgesvj": k2, "w_zgesdd": w1,
+                        "w_zgesvj": w2, "w_rel_diff": abs(w1 - w2) / max(w1, 1e-300)})
+            print(f"  pin layer {L} gate {q0}: k {k1} / {k2}, w {w1:.3e} / {w2:.3e}, rel diff "
+                  f"{log[-1]['w_rel_diff']:.2e}", flush=True)
+    return pin
 
 
 def observables(o, n, qs, workers, seed=7, count=64):
@@ -149,16 +195,21 @@ def make(which, workers):
                           f"u_i from mt19937_64(256)), {steps} Trotter steps (centre bond reaches 1024, then 2 "
                           f"more), chi=1024, cutoff 1e-12", "steps": steps}
     gates = gl.gates()
+    second = "zgesvj" if which == "c4" else "zgesvd"
     print(f"{which}: {len(gates)} local gates, running the oracle (zgesdd) on {workers} workers", flush=True)
     O.set_svd_backend("zgesdd")
-    o, k, w = run_oracle(n, gl, chi, cutoff, workers)
+    pins = []
+    pin = make_pin(chi, cutoff, every=4, per_layer=2, start=16, workers=workers, log=pins) if which == "c3" else None
+    o, k, w = run_oracle(n, gl, chi, cutoff, workers, pin)
     t1 = time.time()
     print(f"{which}: zgesdd run {t1 - t0:.0f} s, peak bond {k.max()}", flush=True)
     bonds = o.bond_dims()
     bits, amps, z, x = observables(o, n, qs, workers)
     print(f"{which}: observables {time.time() - t1:.0f} s", flush=True)
     del o
-    O.set_svd_backend("zgesvj")
+    # the same circuit through a second SVD: kept ranks, weights, and the
+    # amplitude spread two correct SVDs leave after many truncations (P10)
+    O.set_svd_backend(second)
     t2 = time.time()
     o2, k2, w2 = run_oracle(n, gl, chi, cutoff, workers)
     O.set_svd_backend("zgesdd")
@@ -170,12 +221,22 @@ def make(which, workers):
         "n": n, "chi": chi, "cutoff": cutoff, "local_gates": len(gates),
         "saturated_gates": int((k == chi).sum()), "peak_bond": int(k.max()),
         "total_discarded_weight": float(w.sum()),
-        "zgesvj_check": {"kept_ranks_equal": bool((k2 == k).all()), "rank_mismatches": int((k2 != k).sum()),
+        "second_svd": second,
+        "zgesvj_check": {"second_svd": second, "kept_ranks_equal": bool((k2 == k).all()),
+                         "rank_mismatches": int((k2 != k).sum()),
                          "max_rel_w_diff": w_rel, "max_rel_amp_diff": a_rel,
                          "bonds_equal": bool((o2.bond_dims() == bonds).all()), "seconds": time.time() - t2},
+        "svd_pins": pins,
         "oracle_seconds": t1 - t0, "workers": workers,
         "generator": "tests/golden/make_golden.py " + which,
     })
+    if pins:
+        # weights at the rounding level (a SWAP undoing an earlier SWAP leaves a
+        # theta of rank <= chi: w ~ 1e-30, two SVDs' noise) carry no information
+        real = [p for p in pins if p["w_zgesdd"] > 1e-10]
+        meta["svd_pin_summary"] = {"samples": len(pins), "samples_with_w_above_1e-10": len(real),
+                                   "kept_ranks_equal": all(p["k_zgesdd"] == p["k_zgesvj"] for p in pins),
+                                   "max_w_rel_diff_w_above_1e-10": max((p["w_rel_diff"] for p in real), default=0.0)}
     print(json.dumps(meta, indent=1), flush=True)
     save({"c3": "c3_full", "c4": "c4_window"}[which], n, chi, cutoff, gates, k, w, bonds, bits, amps, qs, z, x,
          meta)

@@ -25,7 +25,7 @@ def test_svd_of_a_4096_vector_operand(gpu, oracle):
         return q * (np.diag(r) / np.abs(np.diag(r)))
     s_true = np.logspace(0, -10, n)
     a = (haar(n) * s_true) @ haar(n).conj().T
-    u, s, vd, w = gpu.svd(a)
+    u, s, vd, w = gpu.mps.svd(a)
     ref = np.linalg.svd(a, compute_uv=False)
     assert len(s) == n
     assert np.max(np.abs(s - ref)) <= 1e-12 * ref[0]
@@ -33,7 +33,7 @@ def test_svd_of_a_4096_vector_operand(gpu, oracle):
     assert np.max(np.abs(rec - a)) <= 1e-12 * ref[0]
     assert np.max(np.abs(u.conj().T @ u - np.eye(n))) <= 1e-12
     for cap, cutoff in ((1500, 0.0), (None, 1e-12)):
-        _, s2, _, w2 = gpu.svd(a, max_rank=cap, cutoff=cutoff)
+        _, s2, _, w2 = gpu.mps.svd(a, max_rank=cap, cutoff=cutoff)
         k_ref, w_ref = oracle.truncation_rank(ref, cap, cutoff)
         assert len(s2) == k_ref
         assert abs(w2 - w_ref) <= 1e-10 * w_ref

@@ -58,7 +58,8 @@ def main():
         chain.set_site(i, sites[i])
     for layer in plan:
         chain.apply_layer(layer, chi, 1e-12)
-    qbits = ["".join(np.random.default_rng(9).choice(["0", "1"], n)) for _ in range(64)]
+    brng = np.random.default_rng(9)
+    qbits = ["".join(brng.choice(["0", "1"], n)) for _ in range(64)]
     s_amp = chain.amplitudes(qbits)
     s_norm = chain.norm()
     pz = np.diag([1.0, -1.0]).astype(np.complex128)
