@@ -287,6 +287,266 @@ __global__ void site_from_q_kernel(const cplx* __restrict__ Q, int ldq, int k, i
   }
 }
 
+// ---- one persistent launch per site QR (factor) and one for Q formation.
+// CTA c owns columns [8c, 8c + 8) for the whole factorisation, in registers
+// (warp w holds column 8c + w, rows lane + 32 s): it applies the block
+// reflectors of panels 0 .. c-1 as each one is published (flag[p],
+// release / acquire at gpu scope; V_p staged once in shared memory, then
+// both products run from shared memory and registers), factors its own
+// panel in place, publishes V_c / T_c, and releases flag[c]. The serial
+// chain is panel p -> apply to panel p+1's columns -> factor panel p+1.
+// Q = H_0 ... H_{np-1} [I; 0]: CTA c owns Q columns [8c, 8c + 8) and applies
+// Q_c, ..., Q_0 to its identity columns (no cross-CTA dependencies).
+namespace {
+struct SiteQrSmem {
+  cplx vs[kSW][kSL * 32];  // a staged V_p (rows relative to 8p) or this CTA's own V_c
+  cplx w[kSW][kSW];
+  cplx w2[kSW][kSW];
+  cplx taus[kSW];
+  cplx gv[kSW][kSW];
+  cplx ts[kSW][kSW];
+};
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// a (this warp's column, rows lane + 32 s) <- ((I - V op(T) V^H) A)[:, warp]
+// for rows >= r0. V (global, column i at V + i * ldv, rows relative to r0)
+// and T are read with ld.global.cg: during the factorisation other CTAs of
+// the same launch wrote them (published by flags).
+__device__ __forceinline__ void apply_block(SiteQrSmem& S, cplx (&a)[kSL], const cplx* V, int ldv, const cplx* T,
+                                            int r0, int m, bool adjoint) {
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, L = m - r0;
+#pragma unroll 8
+  for (int idx = t; idx < kSW * L; idx += 256) {
+    const int i = idx / L, rr = idx - i * L;
+    S.vs[i][rr] = __ldcg(V + (long long)i * ldv + rr);
+  }
+  __syncthreads();
+  cplx acc[kSW];
+#pragma unroll
+  for (int i = 0; i < kSW; ++i) acc[i] = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int s = 0; s < kSL; ++s) {
+    const int r = lane + 32 * s;
+    if (r >= r0 && r < m) {
+#pragma unroll
+      for (int i = 0; i < kSW; ++i) cfmac(acc[i], S.vs[i][r - r0], a[s]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kSW; ++i) {
+    const cplx d = warp_sum(acc[i]);
+    if (lane == 0) S.w[i][warp] = d;
+  }
+  __syncthreads();
+  if (t < 64) {
+    const int i = t >> 3, c = t & 7;
+    cplx x = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int k = 0; k < kSW; ++k) {
+      const cplx tk = adjoint ? conjc(__ldcg(T + k * kSW + i)) : __ldcg(T + i * kSW + k);
+      cfma(x, tk, S.w[k][c]);
+    }
+    S.w2[i][c] = x;
+  }
+  __syncthreads();
+  cplx w2[kSW];
+#pragma unroll
+  for (int i = 0; i < kSW; ++i) w2[i] = S.w2[i][warp];
+#pragma unroll
+  for (int s = 0; s < kSL; ++s) {
+    const int r = lane + 32 * s;
+    if (r >= r0 && r < m) {
+#pragma unroll
+      for (int i = 0; i < kSW; ++i) {
+        const cplx u = cmul(S.vs[i][r - r0], w2[i]);
+        a[s].x -= u.x;
+        a[s].y -= u.y;
+      }
+    }
+  }
+  __syncthreads();  // vs is restaged by the next block
+}
+}  // namespace
+
+// A (column-major, lda, m x n, m >= n, m <= 1024): R (n x n row-major,
+// upper) written; V (np panels x 8 columns x ldv, rows relative to the
+// panel) and T (np x 64) published; flags (np ints, zeroed by the caller).
+__global__ void __launch_bounds__(256, 1) site_qr_factor_kernel(const cplx* __restrict__ A, int lda, int m, int n,
+                                                                cplx* __restrict__ Vall, int ldv,
+                                                                cplx* __restrict__ Tall, int* __restrict__ flags,
+                                                                cplx* __restrict__ R) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SiteQrSmem& S = *reinterpret_cast<SiteQrSmem*>(smem_raw);
+  const int cta = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int c0 = kSW * cta, jb = min(kSW, n - c0);
+  cplx a[kSL];
+#pragma unroll
+  for (int s = 0; s < kSL; ++s) {
+    const int r = lane + 32 * s;
+    a[s] = (warp < jb && r < m) ? A[(long long)(c0 + warp) * lda + r] : make_double2(0.0, 0.0);
+  }
+  for (int p = 0; p < cta; ++p) {
+    if (t == 0)
+      while (ld_acquire(flags + p) == 0) __nanosleep(20);
+    __syncthreads();
+    apply_block(S, a, Vall + (long long)p * kSW * ldv, ldv, Tall + (long long)p * kSW * kSW, kSW * p, m, true);
+  }
+  // factor the panel (rows >= c0; relative row j of column j is its diagonal)
+  for (int j = 0; j < jb; ++j) {
+    const int dg = c0 + j;  // absolute diagonal row
+    if (warp == j) {
+      double sn = 0.0;
+#pragma unroll
+      for (int s = 0; s < kSL; ++s) {
+        const int r = lane + 32 * s;
+        if (r > dg && r < m) sn += cabs2(a[s]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sn += __shfl_xor_sync(0xffffffffu, sn, o);
+      // alpha = a(dg): lane dg % 32, slot dg / 32
+      cplx al = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int s = 0; s < kSL; ++s)
+        if (s == dg / 32) al = a[s];
+      al = make_double2(__shfl_sync(0xffffffffu, al.x, dg & 31), __shfl_sync(0xffffffffu, al.y, dg & 31));
+      cplx tau = make_double2(0.0, 0.0), inv = make_double2(0.0, 0.0);
+      double beta = al.x;
+      if (!(sn == 0.0 && al.y == 0.0)) {  // zlarfg
+        beta = -copysign(sqrt(cabs2(al) + sn), al.x);
+        tau = make_double2((beta - al.x) / beta, -al.y / beta);
+        const cplx d = make_double2(al.x - beta, al.y);
+        const double dd = cabs2(d);
+        inv = make_double2(d.x / dd, -d.y / dd);
+      }
+      const bool refl = tau.x != 0.0 || tau.y != 0.0;
+#pragma unroll
+      for (int s = 0; s < kSL; ++s) {
+        const int r = lane + 32 * s;
+        cplx v = make_double2(0.0, 0.0);
+        if (r == dg) {
+          v = make_double2(1.0, 0.0);
+          if (refl) a[s] = make_double2(beta, 0.0);
+        } else if (r > dg && r < m && refl) {
+          v = cmul(a[s], inv);
+        }
+        if (r >= c0 && r < m) S.vs[j][r - c0] = v;
+      }
+      if (lane == 0) S.taus[j] = tau;
+    }
+    __syncthreads();  // v_j and tau_j published
+    const cplx tau = S.taus[j];
+    if (warp > j && warp < jb && (tau.x != 0.0 || tau.y != 0.0)) {
+      cplx d = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int s = 0; s < kSL; ++s) {
+        const int r = lane + 32 * s;
+        if (r >= dg && r < m) cfmac(d, S.vs[j][r - c0], a[s]);
+      }
+      d = warp_sum(d);
+      const cplx coef = cmul(make_double2(tau.x, -tau.y), d);  // H^H x = x - conj(tau) v (v^H x)
+#pragma unroll
+      for (int s = 0; s < kSL; ++s) {
+        const int r = lane + 32 * s;
+        if (r >= dg && r < m) {
+          const cplx u = cmul(S.vs[j][r - c0], coef);
+          a[s].x -= u.x;
+          a[s].y -= u.y;
+        }
+      }
+    } else if (warp < j) {
+      cplx d = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int s = 0; s < kSL; ++s) {
+        const int r = lane + 32 * s;
+        if (r >= dg && r < m) cfmac(d, S.vs[warp][r - c0], S.vs[j][r - c0]);
+      }
+      d = warp_sum(d);
+      if (lane == 0) S.gv[warp][j] = d;
+    }
+  }
+  // columns >= jb of a short last panel: zero reflectors
+  for (int idx = t; idx < (kSW - jb) * (m - c0); idx += 256) {
+    const int jj = jb + idx / (m - c0), rr = idx % (m - c0);
+    S.vs[jj][rr] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  // publish V_c and T_c, then the flag
+  const int L = m - c0;
+  cplx* V = Vall + (long long)cta * kSW * ldv;
+  for (int idx = t; idx < kSW * L; idx += 256) {
+    const int jj = idx / L, rr = idx - jj * L;
+    V[(long long)jj * ldv + rr] = S.vs[jj][rr];
+  }
+  if (warp == 0) {  // zlarft (forward, columnwise)
+    for (int j = 0; j < kSW; ++j) {
+      cplx v = make_double2(0.0, 0.0);
+      if (lane < j && j < jb) {
+        for (int q = lane; q < j; ++q) cfma(v, S.ts[lane][q], S.gv[q][j]);
+        const cplx tj = S.taus[j];
+        v = make_double2(-(tj.x * v.x - tj.y * v.y), -(tj.x * v.y + tj.y * v.x));
+      } else if (lane == j && j < jb) {
+        v = S.taus[j];
+      }
+      if (lane < kSW) S.ts[lane][j] = (lane <= j && j < jb) ? v : make_double2(0.0, 0.0);
+      __syncwarp();
+    }
+    if (lane < kSW)
+      for (int j = 0; j < kSW; ++j) Tall[(long long)cta * kSW * kSW + lane * kSW + j] = S.ts[lane][j];
+  }
+  __syncthreads();
+  if (t == 0) {
+    __threadfence();
+    st_release(flags + cta, 1);
+  }
+  // R[j][c0 + warp] for j <= c0 + warp (R is n x n row-major)
+  if (warp < jb) {
+#pragma unroll
+    for (int s = 0; s < kSL; ++s) {
+      const int r = lane + 32 * s;
+      if (r < n) R[(long long)r * n + c0 + warp] = r <= c0 + warp ? a[s] : make_double2(0.0, 0.0);
+    }
+  }
+}
+
+// Q = H_0 ... H_{np-1} [I; 0] (m x n): CTA c forms columns [8c, 8c + 8) and
+// writes them into the site (left: Q; right: Q^H, see site_from_q_kernel).
+__global__ void __launch_bounds__(256, 1) site_qr_q_kernel(int m, int n, const cplx* __restrict__ Vall, int ldv,
+                                                           const cplx* __restrict__ Tall, int dl, int dr, int right,
+                                                           cplx* __restrict__ site, int chi) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SiteQrSmem& S = *reinterpret_cast<SiteQrSmem*>(smem_raw);
+  const int cta = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int c0 = kSW * cta, jb = min(kSW, n - c0);
+  const int j = c0 + warp;
+  cplx a[kSL];
+#pragma unroll
+  for (int s = 0; s < kSL; ++s) a[s] = make_double2(lane + 32 * s == j ? 1.0 : 0.0, 0.0);
+  for (int p = cta; p >= 0; --p)
+    apply_block(S, a, Vall + (long long)p * kSW * ldv, ldv, Tall + (long long)p * kSW * kSW, kSW * p, m, false);
+  if (warp >= jb) return;
+#pragma unroll
+  for (int s = 0; s < kSL; ++s) {
+    const int r = lane + 32 * s;
+    if (r >= m) continue;
+    cplx v = a[s];
+    if (!right) {
+      site[(long long)r * chi + j] = v;
+    } else {
+      const int pp = r / dr, rr = r % dr;
+      v.y = -v.y;
+      site[(long long)(j * 2 + pp) * chi + rr] = v;
+    }
+  }
+}
+
 namespace {
 unsigned grid_of(long long n) { return (unsigned)std::max(1LL, std::min((n + 255) / 256, 8LL * 148)); }
 #define CKQ(x)                                                                             \
@@ -296,7 +556,8 @@ unsigned grid_of(long long n) { return (unsigned)std::max(1LL, std::min((n + 255
   } while (0)
 }  // namespace
 
-bool site_qr_supported(int m, int n) { return m >= n && m <= kSL * 32 && n >= 16; }
+// persistent kernels: one CTA per 8-column panel, all resident (one per SM)
+bool site_qr_supported(int m, int n) { return m >= n && m <= kSL * 32 && n >= 16 && (n + kSW - 1) / kSW <= 148; }
 
 // QR of the site's matricisation (left: (2 Dl x Dr); right: (Dl x 2 Dr)^H):
 // R (k x n, row-major) into R, Q (or Q^H) written into the site. Work
@@ -305,65 +566,32 @@ bool site_qr_supported(int m, int n) { return m >= n && m <= kSL * 32 && n >= 16
 // into s.st.
 int site_qr(State& s, cplx* site, int dl, int dr, int right, DeviceBuf& Abuf, DeviceBuf& Vbuf, DeviceBuf& Tbuf,
             DeviceBuf& Qbuf, cplx* R, cudaStream_t aux, cudaEvent_t* evs) {
+  (void)aux;
+  (void)evs;
   static bool init = false;
   if (!init) {
-    CKQ(cudaFuncSetAttribute(site_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)sizeof(PanelSmemS)));
+    CKQ(cudaFuncSetAttribute(site_qr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(SiteQrSmem)));
+    CKQ(cudaFuncSetAttribute(site_qr_q_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)sizeof(SiteQrSmem)));
     init = true;
   }
   const int m = right ? 2 * dr : 2 * dl, n = right ? dl : dr, k = std::min(m, n);
   const int lda = (m + 31) / 32 * 32;
-  const int np = (k + kSW - 1) / kSW;
+  const int np = (n + kSW - 1) / kSW;
   Abuf.ensure(sizeof(cplx) * (size_t)lda * n);
   Vbuf.ensure(sizeof(cplx) * (size_t)np * kSW * lda);
   Tbuf.ensure(sizeof(cplx) * (size_t)np * kSW * kSW);
-  Qbuf.ensure(sizeof(cplx) * (size_t)lda * k);
+  Qbuf.ensure(sizeof(int) * (size_t)np);
   cplx* A = (cplx*)Abuf.p;
-  cplx* Vall = (cplx*)Vbuf.p;
-  cplx* Tall = (cplx*)Tbuf.p;
-  cplx* Q = (cplx*)Qbuf.p;
   cudaStream_t st = s.st;
   site_matrix_kernel<<<grid_of((long long)n * m), 256, 0, st>>>(site, s.chi, dl, dr, right, A, lda);
-  ++s.launches;
-  // Panel p runs on st concurrently with the trailing update of panel p - 1
-  // beyond panel p's columns (aux). Panel p's own columns were updated on st
-  // (look-ahead) after st waited for aux: Householder updates of a column
-  // apply in panel order.
-  auto join = [&](cudaStream_t from, cudaStream_t to, cudaEvent_t e) {
-    CKQ(cudaEventRecord(e, from));
-    CKQ(cudaStreamWaitEvent(to, e, 0));
-  };
-  for (int p = 0; p < np; ++p) {
-    const int c0 = p * kSW, jb = std::min(kSW, k - c0);
-    cplx* V = Vall + (long long)p * kSW * lda;
-    cplx* T = Tall + (long long)p * kSW * kSW;
-    site_panel_kernel<<<1, 256, sizeof(PanelSmemS), st>>>(A, lda, m, c0, jb, V, lda, T);
-    ++s.launches;
-    const int c1 = c0 + kSW;
-    if (c1 >= n) continue;
-    const int la = std::min(n, c1 + kSW);
-    if (la < n) join(st, aux, evs[0]);  // aux: the rest of panel p's update needs V_p, T_p
-    join(aux, st, evs[1]);              // st: panel p - 1's aux update reached these columns first
-    site_update_kernel<<<1, 256, 0, st>>>(A, lda, m, c0, c1, la, V, lda, T, 1);
-    ++s.launches;
-    if (la < n) {
-      site_update_kernel<<<(n - la + kSW - 1) / kSW, 256, 0, aux>>>(A, lda, m, c0, la, n, V, lda, T, 1);
-      ++s.launches;
-    }
-  }
-  join(aux, st, evs[1]);  // the factorisation is complete on st
-  site_r_and_identity_kernel<<<grid_of((long long)k * std::max(n, m)), 256, 0, st>>>(A, lda, m, n, k, R, Q, lda);
-  ++s.launches;
-  // Q = H_0 ... H_{np-1} [I; 0], last reflector block first (columns >= c0)
-  for (int p = np - 1; p >= 0; --p) {
-    const int c0 = p * kSW;
-    site_update_kernel<<<(k - c0 + kSW - 1) / kSW, 256, 0, st>>>(Q, lda, m, c0, c0, k,
-                                                                 Vall + (long long)p * kSW * lda, lda,
-                                                                 Tall + (long long)p * kSW * kSW, 0);
-    ++s.launches;
-  }
-  site_from_q_kernel<<<grid_of((long long)k * m), 256, 0, st>>>(Q, lda, k, dl, dr, right, site, s.chi);
-  ++s.launches;
+  CKQ(cudaMemsetAsync(Qbuf.p, 0, sizeof(int) * (size_t)np, st));
+  site_qr_factor_kernel<<<np, 256, sizeof(SiteQrSmem), st>>>(A, lda, m, n, (cplx*)Vbuf.p, lda, (cplx*)Tbuf.p,
+                                                             (int*)Qbuf.p, R);
+  site_qr_q_kernel<<<np, 256, sizeof(SiteQrSmem), st>>>(m, n, (const cplx*)Vbuf.p, lda, (const cplx*)Tbuf.p, dl, dr,
+                                                        right, site, s.chi);
+  s.launches += 3;
   return k;
 }
 
