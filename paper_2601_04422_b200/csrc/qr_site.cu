@@ -19,6 +19,8 @@
 // site). Any exact QR gives the same state; only k = min(m, n) is fixed by
 // the reference (mps.cpp:57-65), and the reflector convention is zlarfg's.
 #include <algorithm>
+#include <cstdio>
+#include <vector>
 #include <cmath>
 #include <string>
 
@@ -382,7 +384,8 @@ __device__ __forceinline__ void apply_block(SiteQrSmem& S, cplx (&a)[kSL], const
 __global__ void __launch_bounds__(256, 1) site_qr_factor_kernel(const cplx* __restrict__ A, int lda, int m, int n,
                                                                 cplx* __restrict__ Vall, int ldv,
                                                                 cplx* __restrict__ Tall, int* __restrict__ flags,
-                                                                cplx* __restrict__ R) {
+                                                                cplx* __restrict__ R,
+                                                                unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SiteQrSmem& S = *reinterpret_cast<SiteQrSmem*>(smem_raw);
   const int cta = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -393,12 +396,22 @@ __global__ void __launch_bounds__(256, 1) site_qr_factor_kernel(const cplx* __re
     const int r = lane + 32 * s;
     a[s] = (warp < jb && r < m) ? A[(long long)(c0 + warp) * lda + r] : make_double2(0.0, 0.0);
   }
+  auto stamp = [&](int k) {  // A/B timeline (tools/qr_case.py with MPSIM_QR_TRACE): %globaltimer ns
+    if (trace && t == 0) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      trace[cta * 4 + k] = g;
+    }
+  };
+  stamp(0);
   for (int p = 0; p < cta; ++p) {
     if (t == 0)
       while (ld_acquire(flags + p) == 0) __nanosleep(20);
     __syncthreads();
+    if (p == cta - 1) stamp(1);
     apply_block(S, a, Vall + (long long)p * kSW * ldv, ldv, Tall + (long long)p * kSW * kSW, kSW * p, m, true);
   }
+  stamp(2);
   // factor the panel (rows >= c0; relative row j of column j is its diagonal)
   for (int j = 0; j < jb; ++j) {
     const int dg = c0 + j;  // absolute diagonal row
@@ -506,6 +519,7 @@ __global__ void __launch_bounds__(256, 1) site_qr_factor_kernel(const cplx* __re
     __threadfence();
     st_release(flags + cta, 1);
   }
+  stamp(3);
   // R[j][c0 + warp] for j <= c0 + warp (R is n x n row-major)
   if (warp < jb) {
 #pragma unroll
@@ -587,8 +601,24 @@ int site_qr(State& s, cplx* site, int dl, int dr, int right, DeviceBuf& Abuf, De
   cudaStream_t st = s.st;
   site_matrix_kernel<<<grid_of((long long)n * m), 256, 0, st>>>(site, s.chi, dl, dr, right, A, lda);
   CKQ(cudaMemsetAsync(Qbuf.p, 0, sizeof(int) * (size_t)np, st));
+  static const bool trace_on = ab_knob("MPSIM_QR_TRACE") != nullptr;
+  static DeviceBuf tbuf;
+  if (trace_on) tbuf.ensure(sizeof(unsigned long long) * 4 * 160);
   site_qr_factor_kernel<<<np, 256, sizeof(SiteQrSmem), st>>>(A, lda, m, n, (cplx*)Vbuf.p, lda, (cplx*)Tbuf.p,
-                                                             (int*)Qbuf.p, R);
+                                                             (int*)Qbuf.p, R,
+                                                             trace_on ? (unsigned long long*)tbuf.p : nullptr);
+  if (trace_on) {  // per panel: start, last flag seen, applies done, published (us from launch start)
+    std::vector<unsigned long long> h(4 * (size_t)np);
+    CKQ(cudaMemcpyAsync(h.data(), tbuf.p, sizeof(unsigned long long) * 4 * np, cudaMemcpyDeviceToHost, st));
+    CKQ(cudaStreamSynchronize(st));
+    unsigned long long t0 = h[0];
+    for (int c = 0; c < np; ++c) t0 = std::min(t0, h[4 * c]);
+    std::fprintf(stderr, "[qr trace m=%d n=%d]", m, n);
+    for (int c = 0; c < np; c += std::max(1, np / 16))
+      std::fprintf(stderr, " %d:%.1f/%.1f/%.1f/%.1f", c, (h[4 * c] - t0) * 1e-3, c ? (h[4 * c + 1] - t0) * 1e-3 : 0.0,
+                   (h[4 * c + 2] - t0) * 1e-3, (h[4 * c + 3] - t0) * 1e-3);
+    std::fprintf(stderr, "\n");
+  }
   site_qr_q_kernel<<<np, 256, sizeof(SiteQrSmem), st>>>(m, n, (const cplx*)Vbuf.p, lda, (const cplx*)Tbuf.p, dl, dr,
                                                         right, site, s.chi);
   s.launches += 3;

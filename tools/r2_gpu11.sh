@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+rm -rf /tmp/abrepo && cp -r . /tmp/abrepo && (cd /tmp/abrepo/paper_2601_04422_b200/csrc && make -s clean && make -s AB=1 -j16 > /dev/null 2>&1)
+(cd /tmp/abrepo && REPS=1 MPSIM_QR_TRACE=1 timeout 300 python tools/qr_case.py > $GRAFT_REPO_ROOT/gpurun_out/r2_qr_trace.txt 2>&1)
