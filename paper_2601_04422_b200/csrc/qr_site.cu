@@ -290,23 +290,31 @@ __global__ void site_from_q_kernel(const cplx* __restrict__ Q, int ldq, int k, i
 }
 
 // ---- one persistent launch per site QR (factor) and one for Q formation.
-// CTA c owns columns [8c, 8c + 8) for the whole factorisation, in registers
-// (warp w holds column 8c + w, rows lane + 32 s): it applies the block
-// reflectors of panels 0 .. c-1 as each one is published (flag[p],
-// release / acquire at gpu scope; V_p staged once in shared memory, then
-// both products run from shared memory and registers), factors its own
-// panel in place, publishes V_c / T_c, and releases flag[c]. The serial
-// chain is panel p -> apply to panel p+1's columns -> factor panel p+1.
-// Q = H_0 ... H_{np-1} [I; 0]: CTA c owns Q columns [8c, 8c + 8) and applies
-// Q_c, ..., Q_0 to its identity columns (no cross-CTA dependencies).
+// CTA c (1024 threads) owns columns [8c, 8c + 8) for the whole
+// factorisation, in registers: warp w holds column 8c + (w & 7), rows
+// 256 (w >> 3) + lane + 32 s (s < 8), i.e. four warps per column. It applies
+// the block reflectors of panels 0 .. c-1 as each one is published (flag[p],
+// release / acquire at gpu scope; V_p staged once in shared memory), factors
+// its own panel in place (three block barriers per reflector, reductions
+// over a column's four warps through shared memory), publishes V_c / T_c and
+// releases flag[c]. The serial chain is panel p -> apply to panel p+1's
+// columns -> factor panel p+1. Q = H_0 ... H_{np-1} [I; 0]: CTA c forms Q
+// columns [8c, 8c + 8) by applying Q_c, ..., Q_0 (no cross-CTA dependencies).
 namespace {
+constexpr int kG = 4;   // warps (row groups of 256) per column
+constexpr int kRL = 8;  // rows per lane
+
 struct SiteQrSmem {
-  cplx vs[kSW][kSL * 32];  // a staged V_p (rows relative to 8p) or this CTA's own V_c
-  cplx w[kSW][kSW];
+  cplx vs[kSW][kG * 256];  // a staged V_p (rows relative to 8p) or this CTA's own V_c
+  cplx part[kSW][kSW][kG]; // per-group partials: V^H A (apply), v_j^H a_c and v_w^H v_j (factor)
+  double pn[kG];
   cplx w2[kSW][kSW];
   cplx taus[kSW];
   cplx gv[kSW][kSW];
   cplx ts[kSW][kSW];
+  cplx xr[2][kG * 256];    // raw column j below its diagonal (rows relative to c0), by reflector parity
+  cplx adg[2][kSW];        // a_col(dg) of the reflector being formed, by reflector parity
+  cplx inv;                // 1 / (alpha - beta) of the reflector being formed
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -318,34 +326,57 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// a (this warp's column, rows lane + 32 s) <- ((I - V op(T) V^H) A)[:, warp]
-// for rows >= r0. V (global, column i at V + i * ldv, rows relative to r0)
-// and T are read with ld.global.cg: during the factorisation other CTAs of
-// the same launch wrote them (published by flags).
-__device__ __forceinline__ void apply_block(SiteQrSmem& S, cplx (&a)[kSL], const cplx* V, int ldv, const cplx* T,
+// Warp sum of 4 complex values at once (reduce-scatter butterfly: 5 complex
+// shuffles instead of 20): lane l ends with the total of value
+// 2 ((l >> 4) & 1) + ((l >> 3) & 1).
+__device__ __forceinline__ cplx warp_sum4(cplx (&v)[4], int lane) {
+  auto sx = [](cplx x, int o) {
+    return make_double2(__shfl_xor_sync(0xffffffffu, x.x, o), __shfl_xor_sync(0xffffffffu, x.y, o));
+  };
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const bool up = lane & 16;
+    const cplx r = sx(up ? v[k] : v[k + 2], 16);
+    v[k] = cadd(up ? v[k + 2] : v[k], r);
+  }
+  {
+    const bool up = lane & 8;
+    const cplx r = sx(up ? v[0] : v[1], 8);
+    v[0] = cadd(up ? v[1] : v[0], r);
+  }
+  v[0] = cadd(v[0], sx(v[0], 4));
+  v[0] = cadd(v[0], sx(v[0], 2));
+  v[0] = cadd(v[0], sx(v[0], 1));
+  return v[0];
+}
+
+// a (this thread's rows of column `col`) <- ((I - V op(T) V^H) A) for rows >=
+// r0. V (global, column i at V + i * ldv, rows relative to r0) and T are read
+// with ld.global.cg: during the factorisation other CTAs of this launch wrote
+// them (published by flags).
+__device__ __forceinline__ void apply_block(SiteQrSmem& S, cplx (&a)[kRL], const cplx* V, int ldv, const cplx* T,
                                             int r0, int m, bool adjoint) {
-  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, L = m - r0;
-#pragma unroll 8
-  for (int idx = t; idx < kSW * L; idx += 256) {
-    const int i = idx / L, rr = idx - i * L;
-    S.vs[i][rr] = __ldcg(V + (long long)i * ldv + rr);
-  }
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, col = warp & 7, grp = warp >> 3;
+  const int L = m - r0;
+#pragma unroll
+  for (int i = 0; i < kSW; ++i)
+    for (int rr = t; rr < L; rr += 1024) S.vs[i][rr] = __ldcg(V + (long long)i * ldv + rr);
   __syncthreads();
-  cplx acc[kSW];
 #pragma unroll
-  for (int i = 0; i < kSW; ++i) acc[i] = make_double2(0.0, 0.0);
+  for (int h = 0; h < 2; ++h) {  // V^H a in two halves of four reflectors (register budget of 1024 threads)
+    cplx acc[4];
 #pragma unroll
-  for (int s = 0; s < kSL; ++s) {
-    const int r = lane + 32 * s;
-    if (r >= r0 && r < m) {
+    for (int i = 0; i < 4; ++i) acc[i] = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int i = 0; i < kSW; ++i) cfmac(acc[i], S.vs[i][r - r0], a[s]);
+    for (int s = 0; s < kRL; ++s) {
+      const int r = 256 * grp + lane + 32 * s;
+      if (r >= r0 && r < m) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) cfmac(acc[i], S.vs[4 * h + i][r - r0], a[s]);
+      }
     }
-  }
-#pragma unroll
-  for (int i = 0; i < kSW; ++i) {
-    const cplx d = warp_sum(acc[i]);
-    if (lane == 0) S.w[i][warp] = d;
+    const cplx tot = warp_sum4(acc, lane);
+    if ((lane & 7) == 0) S.part[4 * h + ((lane >> 4) & 1) * 2 + ((lane >> 3) & 1)][col][grp] = tot;
   }
   __syncthreads();
   if (t < 64) {
@@ -353,22 +384,20 @@ __device__ __forceinline__ void apply_block(SiteQrSmem& S, cplx (&a)[kSL], const
     cplx x = make_double2(0.0, 0.0);
 #pragma unroll
     for (int k = 0; k < kSW; ++k) {
+      const cplx wk = cadd(cadd(S.part[k][c][0], S.part[k][c][1]), cadd(S.part[k][c][2], S.part[k][c][3]));
       const cplx tk = adjoint ? conjc(__ldcg(T + k * kSW + i)) : __ldcg(T + i * kSW + k);
-      cfma(x, tk, S.w[k][c]);
+      cfma(x, tk, wk);
     }
     S.w2[i][c] = x;
   }
   __syncthreads();
-  cplx w2[kSW];
 #pragma unroll
-  for (int i = 0; i < kSW; ++i) w2[i] = S.w2[i][warp];
-#pragma unroll
-  for (int s = 0; s < kSL; ++s) {
-    const int r = lane + 32 * s;
+  for (int s = 0; s < kRL; ++s) {
+    const int r = 256 * grp + lane + 32 * s;
     if (r >= r0 && r < m) {
 #pragma unroll
       for (int i = 0; i < kSW; ++i) {
-        const cplx u = cmul(S.vs[i][r - r0], w2[i]);
+        const cplx u = cmul(S.vs[i][r - r0], S.w2[i][col]);  // w2: a shared-memory broadcast
         a[s].x -= u.x;
         a[s].y -= u.y;
       }
@@ -381,29 +410,29 @@ __device__ __forceinline__ void apply_block(SiteQrSmem& S, cplx (&a)[kSL], const
 // A (column-major, lda, m x n, m >= n, m <= 1024): R (n x n row-major,
 // upper) written; V (np panels x 8 columns x ldv, rows relative to the
 // panel) and T (np x 64) published; flags (np ints, zeroed by the caller).
-__global__ void __launch_bounds__(256, 1) site_qr_factor_kernel(const cplx* __restrict__ A, int lda, int m, int n,
-                                                                cplx* __restrict__ Vall, int ldv,
-                                                                cplx* __restrict__ Tall, int* __restrict__ flags,
-                                                                cplx* __restrict__ R,
-                                                                unsigned long long* __restrict__ trace) {
+__global__ void __launch_bounds__(1024, 1) site_qr_factor_kernel(const cplx* __restrict__ A, int lda, int m, int n,
+                                                                 cplx* __restrict__ Vall, int ldv,
+                                                                 cplx* __restrict__ Tall, int* __restrict__ flags,
+                                                                 cplx* __restrict__ R,
+                                                                 unsigned long long* __restrict__ trace) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SiteQrSmem& S = *reinterpret_cast<SiteQrSmem*>(smem_raw);
-  const int cta = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int cta = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5, col = warp & 7, grp = warp >> 3;
   const int c0 = kSW * cta, jb = min(kSW, n - c0);
-  cplx a[kSL];
-#pragma unroll
-  for (int s = 0; s < kSL; ++s) {
-    const int r = lane + 32 * s;
-    a[s] = (warp < jb && r < m) ? A[(long long)(c0 + warp) * lda + r] : make_double2(0.0, 0.0);
-  }
   auto stamp = [&](int k) {  // A/B timeline (tools/qr_case.py with MPSIM_QR_TRACE): %globaltimer ns
     if (trace && t == 0) {
       unsigned long long g;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
-      trace[cta * 4 + k] = g;
+      trace[cta * 6 + k] = g;
     }
   };
   stamp(0);
+  cplx a[kRL];
+#pragma unroll
+  for (int s = 0; s < kRL; ++s) {
+    const int r = 256 * grp + lane + 32 * s;
+    a[s] = (col < jb && r < m) ? A[(long long)(c0 + col) * lda + r] : make_double2(0.0, 0.0);
+  }
   for (int p = 0; p < cta; ++p) {
     if (t == 0)
       while (ld_acquire(flags + p) == 0) __nanosleep(20);
@@ -412,37 +441,56 @@ __global__ void __launch_bounds__(256, 1) site_qr_factor_kernel(const cplx* __re
     apply_block(S, a, Vall + (long long)p * kSW * ldv, ldv, Tall + (long long)p * kSW * kSW, kSW * p, m, true);
   }
   stamp(2);
-  // factor the panel (rows >= c0; relative row j of column j is its diagonal)
+  // Two block barriers per reflector: (1) column j's warps publish the raw
+  // column (rows >= its diagonal) and partial norms, and the warp owning row
+  // dg of every column publishes a_col(dg); (2) every warp forms zlarfg
+  // redundantly and its partial x_j^H a_col (v = [1; x / (alpha - beta)], so
+  // v^H a = a(dg) + conj(inv) x^H a below the diagonal); after the second
+  // barrier the partials are summed and a_col is updated.
   for (int j = 0; j < jb; ++j) {
-    const int dg = c0 + j;  // absolute diagonal row
-    if (warp == j) {
+    const int dg = c0 + j;  // absolute diagonal row of reflector j
+    const int pb = j & 1;   // xr / adg buffer: the previous reflector's update may still read the other
+    const bool own_dg = dg >= 256 * grp && dg < 256 * grp + 256;
+    if (own_dg) {
+      cplx x = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int s = 0; s < kRL; ++s)
+        if (256 * grp + 32 * s + (dg & 31) == dg) x = a[s];
+      x = make_double2(__shfl_sync(0xffffffffu, x.x, dg & 31), __shfl_sync(0xffffffffu, x.y, dg & 31));
+      if (lane == 0) S.adg[pb][col] = x;
+    }
+    if (col == j) {
       double sn = 0.0;
 #pragma unroll
-      for (int s = 0; s < kSL; ++s) {
-        const int r = lane + 32 * s;
-        if (r > dg && r < m) sn += cabs2(a[s]);
+      for (int s = 0; s < kRL; ++s) {
+        const int r = 256 * grp + lane + 32 * s;
+        if (r > dg && r < m) {
+          sn += cabs2(a[s]);
+          S.xr[pb][r - c0] = a[s];
+        }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sn += __shfl_xor_sync(0xffffffffu, sn, o);
-      // alpha = a(dg): lane dg % 32, slot dg / 32
-      cplx al = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int s = 0; s < kSL; ++s)
-        if (s == dg / 32) al = a[s];
-      al = make_double2(__shfl_sync(0xffffffffu, al.x, dg & 31), __shfl_sync(0xffffffffu, al.y, dg & 31));
+      if (lane == 0) S.pn[grp] = sn;
+    }
+    __syncthreads();
+    if (col == j) {  // zlarfg on column j's warps; tau / inv / beta published with v
+      const double sn = (S.pn[0] + S.pn[1]) + (S.pn[2] + S.pn[3]);
+      const cplx al = S.adg[pb][j];
       cplx tau = make_double2(0.0, 0.0), inv = make_double2(0.0, 0.0);
       double beta = al.x;
-      if (!(sn == 0.0 && al.y == 0.0)) {  // zlarfg
+      if (!(sn == 0.0 && al.y == 0.0)) {
         beta = -copysign(sqrt(cabs2(al) + sn), al.x);
-        tau = make_double2((beta - al.x) / beta, -al.y / beta);
+        const double rb = 1.0 / beta;
+        tau = make_double2((beta - al.x) * rb, -al.y * rb);
         const cplx d = make_double2(al.x - beta, al.y);
-        const double dd = cabs2(d);
-        inv = make_double2(d.x / dd, -d.y / dd);
+        const double rdd = 1.0 / cabs2(d);
+        inv = make_double2(d.x * rdd, -d.y * rdd);
       }
       const bool refl = tau.x != 0.0 || tau.y != 0.0;
 #pragma unroll
-      for (int s = 0; s < kSL; ++s) {
-        const int r = lane + 32 * s;
+      for (int s = 0; s < kRL; ++s) {  // v_j into the reflector store; R diagonal
+        const int r = 256 * grp + lane + 32 * s;
         cplx v = make_double2(0.0, 0.0);
         if (r == dg) {
           v = make_double2(1.0, 0.0);
@@ -452,52 +500,67 @@ __global__ void __launch_bounds__(256, 1) site_qr_factor_kernel(const cplx* __re
         }
         if (r >= c0 && r < m) S.vs[j][r - c0] = v;
       }
-      if (lane == 0) S.taus[j] = tau;
-    }
-    __syncthreads();  // v_j and tau_j published
-    const cplx tau = S.taus[j];
-    if (warp > j && warp < jb && (tau.x != 0.0 || tau.y != 0.0)) {
-      cplx d = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int s = 0; s < kSL; ++s) {
-        const int r = lane + 32 * s;
-        if (r >= dg && r < m) cfmac(d, S.vs[j][r - c0], a[s]);
+      if (t == 32 * j) {
+        S.taus[j] = tau;
+        S.inv = inv;
       }
-      d = warp_sum(d);
-      const cplx coef = cmul(make_double2(tau.x, -tau.y), d);  // H^H x = x - conj(tau) v (v^H x)
+    }
+    cplx d = make_double2(0.0, 0.0);  // partial x_j^H a_col (col > j) or v_col^H x_j (col < j), rows > dg
+    if (col > j && col < jb) {
 #pragma unroll
-      for (int s = 0; s < kSL; ++s) {
-        const int r = lane + 32 * s;
-        if (r >= dg && r < m) {
-          const cplx u = cmul(S.vs[j][r - c0], coef);
-          a[s].x -= u.x;
-          a[s].y -= u.y;
+      for (int s = 0; s < kRL; ++s) {
+        const int r = 256 * grp + lane + 32 * s;
+        if (r > dg && r < m) cfmac(d, S.xr[pb][r - c0], a[s]);
+      }
+    } else if (col < j) {
+#pragma unroll
+      for (int s = 0; s < kRL; ++s) {
+        const int r = 256 * grp + lane + 32 * s;
+        if (r > dg && r < m) cfmac(d, S.vs[col][r - c0], S.xr[pb][r - c0]);
+      }
+    }
+    if (col != j && col < jb) {
+      d = warp_sum(d);
+      if (lane == 0) S.part[0][col][grp] = d;
+    }
+    __syncthreads();
+    if (col != j && col < jb) {
+      const cplx tau = S.taus[j], inv = S.inv;
+      const cplx tot = cadd(cadd(S.part[0][col][0], S.part[0][col][1]), cadd(S.part[0][col][2], S.part[0][col][3]));
+      if (col > j) {
+        if (tau.x != 0.0 || tau.y != 0.0) {
+          // H^H a = a - conj(tau) v (v^H a), v^H a = a(dg) + conj(inv) tot, v = x inv below dg
+          const cplx vha = cadd(S.adg[pb][col], cmul(conjc(inv), tot));
+          const cplx coef = cmul(make_double2(tau.x, -tau.y), vha);
+          const cplx cc = cmul(inv, coef);
+#pragma unroll
+          for (int s = 0; s < kRL; ++s) {
+            const int r = 256 * grp + lane + 32 * s;
+            if (r > dg && r < m) {
+              const cplx x = S.xr[pb][r - c0];
+              a[s].x = fma(-x.x, cc.x, fma(x.y, cc.y, a[s].x));
+              a[s].y = fma(-x.x, cc.y, fma(-x.y, cc.x, a[s].y));
+            } else if (r == dg) {
+              a[s].x -= coef.x;
+              a[s].y -= coef.y;
+            }
+          }
         }
+      } else if (grp == 0 && lane == 0) {  // zlarft's v_col^H v_j
+        S.gv[col][j] = cadd(conjc(S.vs[col][dg - c0]), cmul(tot, inv));
       }
-    } else if (warp < j) {
-      cplx d = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int s = 0; s < kSL; ++s) {
-        const int r = lane + 32 * s;
-        if (r >= dg && r < m) cfmac(d, S.vs[warp][r - c0], S.vs[j][r - c0]);
-      }
-      d = warp_sum(d);
-      if (lane == 0) S.gv[warp][j] = d;
     }
   }
+  stamp(3);
   // columns >= jb of a short last panel: zero reflectors
-  for (int idx = t; idx < (kSW - jb) * (m - c0); idx += 256) {
-    const int jj = jb + idx / (m - c0), rr = idx % (m - c0);
-    S.vs[jj][rr] = make_double2(0.0, 0.0);
-  }
+  for (int jj = jb; jj < kSW; ++jj)
+    for (int rr = t; rr < m - c0; rr += 1024) S.vs[jj][rr] = make_double2(0.0, 0.0);
   __syncthreads();
-  // publish V_c and T_c, then the flag
   const int L = m - c0;
   cplx* V = Vall + (long long)cta * kSW * ldv;
-  for (int idx = t; idx < kSW * L; idx += 256) {
-    const int jj = idx / L, rr = idx - jj * L;
-    V[(long long)jj * ldv + rr] = S.vs[jj][rr];
-  }
+#pragma unroll
+  for (int jj = 0; jj < kSW; ++jj)
+    for (int rr = t; rr < L; rr += 1024) V[(long long)jj * ldv + rr] = S.vs[jj][rr];
   if (warp == 0) {  // zlarft (forward, columnwise)
     for (int j = 0; j < kSW; ++j) {
       cplx v = make_double2(0.0, 0.0);
@@ -515,40 +578,41 @@ __global__ void __launch_bounds__(256, 1) site_qr_factor_kernel(const cplx* __re
       for (int j = 0; j < kSW; ++j) Tall[(long long)cta * kSW * kSW + lane * kSW + j] = S.ts[lane][j];
   }
   __syncthreads();
+  stamp(4);
   if (t == 0) {
     __threadfence();
     st_release(flags + cta, 1);
   }
-  stamp(3);
-  // R[j][c0 + warp] for j <= c0 + warp (R is n x n row-major)
-  if (warp < jb) {
+  stamp(5);
+  // R[r][c0 + col] for r <= c0 + col (R is n x n row-major)
+  if (col < jb) {
 #pragma unroll
-    for (int s = 0; s < kSL; ++s) {
-      const int r = lane + 32 * s;
-      if (r < n) R[(long long)r * n + c0 + warp] = r <= c0 + warp ? a[s] : make_double2(0.0, 0.0);
+    for (int s = 0; s < kRL; ++s) {
+      const int r = 256 * grp + lane + 32 * s;
+      if (r < n) R[(long long)r * n + c0 + col] = r <= c0 + col ? a[s] : make_double2(0.0, 0.0);
     }
   }
 }
 
 // Q = H_0 ... H_{np-1} [I; 0] (m x n): CTA c forms columns [8c, 8c + 8) and
 // writes them into the site (left: Q; right: Q^H, see site_from_q_kernel).
-__global__ void __launch_bounds__(256, 1) site_qr_q_kernel(int m, int n, const cplx* __restrict__ Vall, int ldv,
-                                                           const cplx* __restrict__ Tall, int dl, int dr, int right,
-                                                           cplx* __restrict__ site, int chi) {
+__global__ void __launch_bounds__(1024, 1) site_qr_q_kernel(int m, int n, const cplx* __restrict__ Vall, int ldv,
+                                                            const cplx* __restrict__ Tall, int dl, int dr, int right,
+                                                            cplx* __restrict__ site, int chi) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SiteQrSmem& S = *reinterpret_cast<SiteQrSmem*>(smem_raw);
-  const int cta = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int cta = blockIdx.x, t = threadIdx.x, lane = t & 31, warp = t >> 5, col = warp & 7, grp = warp >> 3;
   const int c0 = kSW * cta, jb = min(kSW, n - c0);
-  const int j = c0 + warp;
-  cplx a[kSL];
+  const int j = c0 + col;
+  cplx a[kRL];
 #pragma unroll
-  for (int s = 0; s < kSL; ++s) a[s] = make_double2(lane + 32 * s == j ? 1.0 : 0.0, 0.0);
+  for (int s = 0; s < kRL; ++s) a[s] = make_double2(256 * grp + lane + 32 * s == j ? 1.0 : 0.0, 0.0);
   for (int p = cta; p >= 0; --p)
     apply_block(S, a, Vall + (long long)p * kSW * ldv, ldv, Tall + (long long)p * kSW * kSW, kSW * p, m, false);
-  if (warp >= jb) return;
+  if (col >= jb) return;
 #pragma unroll
-  for (int s = 0; s < kSL; ++s) {
-    const int r = lane + 32 * s;
+  for (int s = 0; s < kRL; ++s) {
+    const int r = 256 * grp + lane + 32 * s;
     if (r >= m) continue;
     cplx v = a[s];
     if (!right) {
@@ -603,23 +667,25 @@ int site_qr(State& s, cplx* site, int dl, int dr, int right, DeviceBuf& Abuf, De
   CKQ(cudaMemsetAsync(Qbuf.p, 0, sizeof(int) * (size_t)np, st));
   static const bool trace_on = ab_knob("MPSIM_QR_TRACE") != nullptr;
   static DeviceBuf tbuf;
-  if (trace_on) tbuf.ensure(sizeof(unsigned long long) * 4 * 160);
-  site_qr_factor_kernel<<<np, 256, sizeof(SiteQrSmem), st>>>(A, lda, m, n, (cplx*)Vbuf.p, lda, (cplx*)Tbuf.p,
+  if (trace_on) tbuf.ensure(sizeof(unsigned long long) * 6 * 160);
+  site_qr_factor_kernel<<<np, 1024, sizeof(SiteQrSmem), st>>>(A, lda, m, n, (cplx*)Vbuf.p, lda, (cplx*)Tbuf.p,
                                                              (int*)Qbuf.p, R,
                                                              trace_on ? (unsigned long long*)tbuf.p : nullptr);
   if (trace_on) {  // per panel: start, last flag seen, applies done, published (us from launch start)
-    std::vector<unsigned long long> h(4 * (size_t)np);
-    CKQ(cudaMemcpyAsync(h.data(), tbuf.p, sizeof(unsigned long long) * 4 * np, cudaMemcpyDeviceToHost, st));
+    std::vector<unsigned long long> h(6 * (size_t)np);
+    CKQ(cudaMemcpyAsync(h.data(), tbuf.p, sizeof(unsigned long long) * 6 * np, cudaMemcpyDeviceToHost, st));
     CKQ(cudaStreamSynchronize(st));
     unsigned long long t0 = h[0];
-    for (int c = 0; c < np; ++c) t0 = std::min(t0, h[4 * c]);
+    for (int c = 0; c < np; ++c) t0 = std::min(t0, h[6 * c]);
     std::fprintf(stderr, "[qr trace m=%d n=%d]", m, n);
-    for (int c = 0; c < np; c += std::max(1, np / 16))
-      std::fprintf(stderr, " %d:%.1f/%.1f/%.1f/%.1f", c, (h[4 * c] - t0) * 1e-3, c ? (h[4 * c + 1] - t0) * 1e-3 : 0.0,
-                   (h[4 * c + 2] - t0) * 1e-3, (h[4 * c + 3] - t0) * 1e-3);
+    for (int c = 0; c < np; c += std::max(1, np / 16)) {
+      std::fprintf(stderr, " %d:", c);
+      for (int k = 0; k < 6; ++k)
+        std::fprintf(stderr, "%s%.1f", k ? "/" : "", (k == 1 && c == 0) ? 0.0 : (h[6 * c + k] - t0) * 1e-3);
+    }
     std::fprintf(stderr, "\n");
   }
-  site_qr_q_kernel<<<np, 256, sizeof(SiteQrSmem), st>>>(m, n, (const cplx*)Vbuf.p, lda, (const cplx*)Tbuf.p, dl, dr,
+  site_qr_q_kernel<<<np, 1024, sizeof(SiteQrSmem), st>>>(m, n, (const cplx*)Vbuf.p, lda, (const cplx*)Tbuf.p, dl, dr,
                                                         right, site, s.chi);
   s.launches += 3;
   return k;
