@@ -30,7 +30,7 @@ void launch_qr_apply(const GateDesc*, int, int, int, cplx*, const cplx*, long lo
                      long long, const GateOut*, cudaStream_t);
 bool site_qr_supported(int m, int n);
 int site_qr(State& s, cplx* site, int dl, int dr, int right, DeviceBuf& Abuf, DeviceBuf& Vbuf, DeviceBuf& Tbuf,
-            DeviceBuf& Qbuf, cplx* R, cudaStream_t aux, cudaEvent_t* evs);
+            DeviceBuf& Qbuf, cplx* R, cudaStream_t aux, cudaEvent_t* evs, int set);
 
 // ---- tensor-core QR of one site (the gate path's QR machinery, qr_pre.cu:
 // 4-CTA cluster panels with the panel held on chip, DMMA trailing updates and
@@ -114,8 +114,18 @@ constexpr int kQB = 32;
 
 struct QrWork {
   DeviceBuf W, P, Vall, Tall, tau, W1, W2, Q, R, tmp, nrm;
-  DeviceBuf ws, vbuf, tbuf, desc, order, out;  // tensor-core path
+  DeviceBuf ws, vbuf, tbuf, desc, order, out;  // cluster-panel path (qr_pre.cu)
+  DeviceBuf V2[2], T2[2];                      // site QR (qr_site.cu): alternate reflector sets
+  int set = 0;
 };
+
+// The site QRs' Q formations run on s.aux: the sweep's last step joins them
+// back into s.st (every public entry point ends with this before its sync).
+void join_aux(State& s) {
+  if (!s.aux) return;
+  CK_CANON(cudaEventRecord(s.evq[0], s.aux));
+  CK_CANON(cudaStreamWaitEvent(s.st, s.evq[0], 0));
+}
 
 unsigned grid_of(long long n) { return (unsigned)std::max(1LL, std::min((n + 255) / 256, 8LL * 148)); }
 
@@ -128,12 +138,13 @@ bool tc_qr(int m, int n) { return n >= 64 && m >= n && m <= 2048; }
 int fast_site_qr(State& s, QrWork& w, cplx* site, int dl, int dr, int right) {
   if (!s.aux) {
     CK_CANON(cudaStreamCreateWithFlags(&s.aux, cudaStreamNonBlocking));
-    CK_CANON(cudaEventCreateWithFlags(&s.evq[0], cudaEventDisableTiming));
-    CK_CANON(cudaEventCreateWithFlags(&s.evq[1], cudaEventDisableTiming));
+    for (cudaEvent_t& e : s.evq) CK_CANON(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   const int m = right ? 2 * dr : 2 * dl, n = right ? dl : dr, k = std::min(m, n);
   w.R.ensure(sizeof(cplx) * (size_t)k * n);
-  return site_qr(s, site, dl, dr, right, w.W, w.Vall, w.Tall, w.Q, (cplx*)w.R.p, s.aux, s.evq);
+  const int set = w.set;
+  w.set ^= 1;
+  return site_qr(s, site, dl, dr, right, w.W, w.V2[set], w.T2[set], w.Q, (cplx*)w.R.p, s.aux, s.evq, set);
 }
 
 // Factor the site's matricisation with the qr_pre.cu machinery: R (k x n,
@@ -317,6 +328,7 @@ void sweep_left_impl(State& s, int i0, int i1) {
   DeviceGuard g(s.device);
   QrWork w;
   for (int i = i0; i < i1; ++i) left_step(s, w, i);
+  join_aux(s);
   CKC(cudaStreamSynchronize(s.st));
   CKC(cudaGetLastError());
   s.center = -1;
@@ -327,6 +339,7 @@ void sweep_right_impl(State& s, int i0, int i1) {
   DeviceGuard g(s.device);
   QrWork w;
   for (int i = i1; i >= i0; --i) right_step(s, w, i);
+  join_aux(s);
   CKC(cudaStreamSynchronize(s.st));
   CKC(cudaGetLastError());
   s.center = -1;
@@ -341,6 +354,7 @@ double site_norm2_impl(State& s, int i) {
   ++s.launches;
   double n2 = 0.0;
   CKC(cudaMemcpyAsync(&n2, nrm.p, sizeof(double), cudaMemcpyDeviceToHost, s.st));
+  join_aux(s);
   CKC(cudaStreamSynchronize(s.st));
   nrm.release();
   return n2;
@@ -357,6 +371,7 @@ void move_center_impl(State& s, int c) {
   ++s.launches;
   double n2 = 0.0;
   CKC(cudaMemcpyAsync(&n2, w.nrm.p, sizeof(double), cudaMemcpyDeviceToHost, s.st));
+  join_aux(s);
   CKC(cudaStreamSynchronize(s.st));
   CKC(cudaGetLastError());
   if (std::sqrt(n2) < 1e-14) fail(MPSIM_ENUMERIC, "cannot canonicalize a zero-norm state");

@@ -110,7 +110,7 @@ struct State {
   cudaEvent_t evj0 = nullptr, evj1 = nullptr;
   // centre moves (qr_site.cu): a second stream for trailing updates, two join events
   cudaStream_t aux = nullptr;
-  cudaEvent_t evq[2] = {nullptr, nullptr};
+  cudaEvent_t evq[3] = {nullptr, nullptr, nullptr};
   long long h2d_bytes = 0, d2h_bytes = 0;  // gate-path host<->device traffic
 
   State(int n, long long chi_hint, int device);

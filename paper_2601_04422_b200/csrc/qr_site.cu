@@ -642,10 +642,13 @@ bool site_qr_supported(int m, int n) { return m >= n && m <= kSL * 32 && n >= 16
 // buffers grow as needed. Launched on s.st (panels, look-ahead updates) and
 // aux (trailing updates, Q formation); on return aux has been joined back
 // into s.st.
+// V / T come in two sets used by alternate sites: the Q formation of site i
+// runs on `aux` concurrently with the factorisation of site i + 1 (only R
+// gates the next site); evs[0] orders Q after the factorisation, evs[1 + set]
+// keeps a set from being refactored while its Q formation still reads it.
+// The caller joins aux back into s.st at the end of the sweep.
 int site_qr(State& s, cplx* site, int dl, int dr, int right, DeviceBuf& Abuf, DeviceBuf& Vbuf, DeviceBuf& Tbuf,
-            DeviceBuf& Qbuf, cplx* R, cudaStream_t aux, cudaEvent_t* evs) {
-  (void)aux;
-  (void)evs;
+            DeviceBuf& Qbuf, cplx* R, cudaStream_t aux, cudaEvent_t* evs, int set) {
   static bool init = false;
   if (!init) {
     CKQ(cudaFuncSetAttribute(site_qr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -663,6 +666,7 @@ int site_qr(State& s, cplx* site, int dl, int dr, int right, DeviceBuf& Abuf, De
   Qbuf.ensure(sizeof(int) * (size_t)np);
   cplx* A = (cplx*)Abuf.p;
   cudaStream_t st = s.st;
+  CKQ(cudaStreamWaitEvent(st, evs[1 + set], 0));  // this V / T set's previous Q formation is done
   site_matrix_kernel<<<grid_of((long long)n * m), 256, 0, st>>>(site, s.chi, dl, dr, right, A, lda);
   CKQ(cudaMemsetAsync(Qbuf.p, 0, sizeof(int) * (size_t)np, st));
   static const bool trace_on = ab_knob("MPSIM_QR_TRACE") != nullptr;
@@ -685,8 +689,11 @@ int site_qr(State& s, cplx* site, int dl, int dr, int right, DeviceBuf& Abuf, De
     }
     std::fprintf(stderr, "\n");
   }
-  site_qr_q_kernel<<<np, 1024, sizeof(SiteQrSmem), st>>>(m, n, (const cplx*)Vbuf.p, lda, (const cplx*)Tbuf.p, dl, dr,
-                                                        right, site, s.chi);
+  CKQ(cudaEventRecord(evs[0], st));
+  CKQ(cudaStreamWaitEvent(aux, evs[0], 0));
+  site_qr_q_kernel<<<np, 1024, sizeof(SiteQrSmem), aux>>>(m, n, (const cplx*)Vbuf.p, lda, (const cplx*)Tbuf.p, dl,
+                                                         dr, right, site, s.chi);
+  CKQ(cudaEventRecord(evs[1 + set], aux));
   s.launches += 3;
   return k;
 }
