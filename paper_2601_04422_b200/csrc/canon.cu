@@ -361,6 +361,7 @@ double site_norm2_impl(State& s, int i) {
 }
 
 void move_center_impl(State& s, int c) {
+  NvtxRange nv("mpsim: move_center (QR sweeps)");
   if (c < 0 || c >= s.n) fail(MPSIM_EINVAL, "center out of range");
   DeviceGuard g(s.device);
   QrWork w;

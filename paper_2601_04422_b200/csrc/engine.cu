@@ -435,6 +435,7 @@ static GateDesc phase_desc(const GateDesc& d, int phase) {
 
 void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs,
                               const cplx* src, long long src_ld) {
+  NvtxRange nv("mpsim: theta + svd + truncate (apply_2q_local batch)");
   const int ng = (int)descs.size();
   for (const GateDesc& d : descs)
     if (d.n_pad > kMaxSvdN)  // de Rijk / truncation sort one gate's vectors in one CTA
@@ -554,6 +555,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   double* h_offsum = (double*)s.h_offsum.p;
   const int max_sweeps = phase_probe() ? 1 : kMaxSweeps;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
+    NvtxRange nvs("mpsim: jacobi sweep");
     CK(cudaMemsetAsync(s.d_rot.p, 0, sizeof(int) * ng, st));
     CK(cudaMemsetAsync(s.d_maxoff.p, 0, sizeof(double) * ng, st));
     CK(cudaMemsetAsync(s.d_offsum.p, 0, sizeof(double) * ng, st));
@@ -692,6 +694,7 @@ namespace {
 // Applies disjoint local gates. reports[idx] is filled for every gate.
 void run_layer(State& s, const std::vector<G2>& two, const std::vector<G1>& one, const mpsim_policy& pol,
                std::vector<Rep>& reports) {
+  NvtxRange nv("mpsim: layer (execute_parallel barrier interval)");
   cudaStream_t st = s.st;
   if (!one.empty()) {
     const int ng = (int)one.size();

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <stdexcept>
 #include <string>
@@ -70,6 +71,15 @@ struct PinnedBuf {
   ~PinnedBuf() { release(); }
   void ensure(size_t b);
   void release();
+};
+
+// NVTX range for Nsight timelines (header-only NVTX v3: a no-op unless a
+// tool is attached). Named after the reference step each range replaces.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 struct DeviceGuard {

@@ -649,6 +649,7 @@ bool site_qr_supported(int m, int n) { return m >= n && m <= kSL * 32 && n >= 16
 // The caller joins aux back into s.st at the end of the sweep.
 int site_qr(State& s, cplx* site, int dl, int dr, int right, DeviceBuf& Abuf, DeviceBuf& Vbuf, DeviceBuf& Tbuf,
             DeviceBuf& Qbuf, cplx* R, cudaStream_t aux, cudaEvent_t* evs, int set) {
+  NvtxRange nv("mpsim: site qr");
   static bool init = false;
   if (!init) {
     CKQ(cudaFuncSetAttribute(site_qr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -229,6 +229,7 @@ void replay_stats(mpsim_gpu_sampler& sp, uint64_t shots, const std::vector<int>&
 }
 
 void run_sample(mpsim_gpu_sampler& sp, uint64_t shots, uint64_t seed) {
+  NvtxRange nv("mpsim: sample");
   State& s = *sp.st;
   const int n = sp.n;
   DeviceGuard g(s.device);

@@ -254,6 +254,7 @@ void allreduce(mpsim_gpu_shard& s, double* v, int count, ncclRedOp_t op) {
 // rank `dst` and / or receive a slot into local slot `recv_li` from `src`, in
 // one NCCL group (both directions at once cannot deadlock).
 void p2p(mpsim_gpu_shard& s, int send_li, int dst, int recv_li, int src) {
+  NvtxRange nv("mpsim: shard boundary exchange (NCCL)");
   State& a = s.st();
   const auto& api = nccl();
   const size_t slot = (size_t)a.stride * 2;  // doubles per padded slot
@@ -295,6 +296,7 @@ void agree_capacity(mpsim_gpu_shard& s) {
 
 void apply_layer(mpsim_gpu_shard& s, const mpsim_gate* gates, int count, const mpsim_policy& pol,
                  mpsim_exec_stats* stats) {
+  NvtxRange nv("mpsim: shard layer (exchange, layer, exchange)");
   DeviceGuard g(s.device);
   std::vector<mpsim_gate> local;
   bool sl = false, sr = false;
