@@ -81,6 +81,31 @@ def test_move_center_tensor_core_qr_chi512(gpu, oracle):
     assert abs(g.norm() - o.norm()) <= 1e-12 * o.norm()
 
 
+def test_move_center_ragged_bonds(gpu, oracle):
+    """Bond dimensions that are not multiples of the 8-column panel width (a
+    short last panel in the site QR of qr_site.cu) and wide / tall operands on
+    either side of the centre: isometries, bonds and the state."""
+    bonds = [1, 2, 4, 8, 16, 29, 21, 13, 8, 4, 2, 1]
+    n = len(bonds) - 1
+    rng = np.random.default_rng(29)
+    o = oracle.MpsState(n)
+    g = gpu.MpsState(n, chi_hint=32)
+    for i in range(n):
+        t = rng.standard_normal((bonds[i], 2, bonds[i + 1])) + 1j * rng.standard_normal((bonds[i], 2, bonds[i + 1]))
+        o.set_site(i, t)
+        g.set_site(i, t)
+    ref = o.to_statevector()
+    for c in (n - 1, 0, 5):
+        g.move_center(c)
+        o.move_center(c)
+        assert g.ortho_center == c and (g.bond_dims() == o.bond_dims()).all()
+        for i in range(c):
+            assert _left_defect(g.site(i)) <= 1e-11
+        for i in range(c + 1, n):
+            assert _right_defect(g.site(i)) <= 1e-11
+        assert np.max(np.abs(g.to_statevector() - ref)) <= 1e-11 * np.max(np.abs(ref))
+
+
 def test_idempotent_and_zero_norm(gpu, oracle):
     g = copy_state_to_gpu(gpu, oracle.MpsState.random(5, 6, 55))
     g.left_canonicalize()
