@@ -281,6 +281,8 @@ void p2p(mpsim_gpu_shard& s, int send_li, int dst, int recv_li, int src) {
     CKH(cudaMemcpyAsync(hd + 2, s.dims_recv.p, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s.stream()));
     sync(s);
     ABI(mpsim_gpu_set_site_dims(s.state, recv_li, hd[2], hd[3]));
+  } else {
+    sync(s);  // the pinned extents are reused by the next call
   }
 }
 
