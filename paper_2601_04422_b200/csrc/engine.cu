@@ -32,13 +32,60 @@ int launch_theta(const GateDesc*, const GateDesc*, int, int, const cplx*, long l
 int theta_tiles(int dl, int dr);
 void jacobi_split_init();
 void launch_jacobi_sweep(const GateDesc*, int, int, cplx*, const int*, int*, double, double, const double*, double,
-                         const int*, long long, double*, int*, cplx*, cplx*, double*, cplx*, int*, int, cudaStream_t);
+                         const int*, long long, double*, int*, cplx*, cplx*, double*, cplx*, int*, int, int,
+                         cudaStream_t);
+// L2 eviction priorities in the persistent sweep (jacobi_split.cu RoundArgs::l2hint).
+static int l2hint_policy() {
+  static const int v = [] {
+    const char* e = ab_knob("MPSIM_L2HINT");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
 // One persistent launch per sweep (jacobi_split.cu); MPSIM_SWEEP=rounds selects
 // one launch per tournament round.
 static bool sweep_policy() {
   static const bool on = [] {
     const char* v = ab_knob("MPSIM_SWEEP");
     return !(v != nullptr && std::string(v) == "rounds");
+  }();
+  return on;
+}
+void launch_jacobi_sweep_cl(const GateDesc*, int, int, cplx*, const int*, const int*, int, int, int*, double, double,
+                            const double*, double, const int*, long long, double*, int*, double*, cplx*, int*,
+                            cudaStream_t);
+// Persistent sweeps with one CTA per visit over the whole layer (default), or
+// as 4-CTA cluster visits claimed gate group by gate group (MPSIM_SWEEP_CL=1).
+static bool cluster_policy() {
+  static const bool on = [] {
+    const char* v = ab_knob("MPSIM_SWEEP_CL");
+    return v != nullptr && std::string(v) == "1";
+  }();
+  return on;
+}
+// Gates per claim group of the cluster sweep: the group's operands (16 MB per
+// gate at chi = 512) stay in L2 between rounds.
+static int group_policy() {
+  static const int g = [] {
+    const char* v = ab_knob("MPSIM_GROUP");
+    const int x = v ? std::atoi(v) : 0;
+    return x > 0 ? x : 6;
+  }();
+  return g;
+}
+void launch_jacobi_sweep_w32(const GateDesc*, int, int, cplx*, const int*, int*, double, double, const double*, double,
+                             const int*, long long, double*, double*, cplx*, int*, cudaStream_t);
+// Persistent sweeps with 32-vector blocks (jacobi_w32.cu, A/B: MPSIM_W32=1)
+// when every operand's n_pad is a multiple of 64 and the largest is at least
+// kW32MinN. Measured slower than 16-vector blocks: not default.
+constexpr int kW32MinN = 256;
+// Vector-count padding of gate and plain-SVD operands (a multiple of both
+// block pair widths, so either sweep kernel can run the batch).
+constexpr int kNAlign = 64;
+static bool w32_policy() {
+  static const bool on = [] {
+    const char* v = ab_knob("MPSIM_W32");
+    return v != nullptr && std::string(v) == "1";
   }();
   return on;
 }
@@ -472,12 +519,12 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   s.d_out.ensure(sizeof(GateOut) * ng);
   s.d_sigma.ensure(sizeof(double) * sig_stride * ng);
   s.d_order.ensure(sizeof(int) * sig_stride * ng);
-  s.d_active.ensure(sizeof(int) * ng);
+  s.d_active.ensure(sizeof(int) * 2 * ng);  // active flags, then the active-gate list
   s.d_rot.ensure(sizeof(int) * ng);
   s.d_frob.ensure(sizeof(double) * ng);
   s.h_gates.ensure(sizeof(GateDesc) * 5 * ng);
   s.h_out.ensure(sizeof(GateOut) * ng);
-  s.h_rot.ensure(sizeof(int) * ng);
+  s.h_rot.ensure(sizeof(int) * 2 * ng);
   {
     GateDesc* h = (GateDesc*)s.h_gates.p;
     for (int ph = 0; ph < 5; ++ph)
@@ -537,7 +584,16 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   const int first = ((jacobi_mode() >= 3 && inblock_policy() && first_sweep_inblock()) ? (1 | 4) : 1) |
                     alt_cross_bits();
   for (int i = 0; i < ng; ++i) h_rot[i] = first;
-  CK(cudaMemcpyAsync(s.d_active.p, h_rot, sizeof(int) * ng, cudaMemcpyHostToDevice, st));
+  int n_list = 0;
+  // flags h_rot[0, ng) -> device, with the list of active gates after them
+  // (the cluster sweep claims its visits gate group by gate group over it)
+  auto upload_active = [&]() {
+    n_list = 0;
+    for (int i = 0; i < ng; ++i)
+      if (h_rot[i]) h_rot[ng + n_list++] = i;
+    CK(cudaMemcpyAsync(s.d_active.p, h_rot, sizeof(int) * (ng + n_list), cudaMemcpyHostToDevice, st));
+  };
+  upload_active();
   bool converged = false;
   std::vector<int> still(ng, 1);
   s.d_maxoff.ensure(sizeof(double) * ng);
@@ -546,7 +602,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     s.d_need.ensure(sizeof(int) * slots);
     s.d_gbuf.ensure(sizeof(cplx) * slots * kP * kP);
     s.d_rbuf.ensure(sizeof(cplx) * slots * kP * kP);
-    s.d_gblk.ensure(sizeof(cplx) * slots * 2 * kW * kW);
+    s.d_gblk.ensure(sizeof(cplx) * slots * 2 * kW * kW * 2);  // (twice: 32 x 32 blocks of the W = 32 sweep)
   }
   s.h_maxoff.ensure(sizeof(double) * ng);
   double* h_maxoff = (double*)s.h_maxoff.p;
@@ -554,6 +610,8 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   s.h_offsum.ensure(sizeof(double) * ng);
   double* h_offsum = (double*)s.h_offsum.p;
   const int max_sweeps = phase_probe() ? 1 : kMaxSweeps;
+  bool use_w32 = w32_policy() && max_nb * kW >= kW32MinN;
+  for (const GateDesc& d : descs) use_w32 = use_w32 && d.n_pad % (4 * kW) == 0;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     NvtxRange nvs("mpsim: jacobi sweep");
     CK(cudaMemsetAsync(s.d_rot.p, 0, sizeof(int) * ng, st));
@@ -567,13 +625,29 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     // converged inner EVD (measured in emulation and on the B200), at a
     // fraction of the cost. Final orthogonality is at the tol level.
     // (phase probes 1-2 run per round; probe 4, the visit without its EVD, runs persistent)
-    const bool persistent = jacobi_mode() == 4 && (!phase_probe() || phase_probe() == 4) && sweep_policy();
-    if (persistent) {
+    const bool persistent = jacobi_mode() == 4 && sweep_policy();
+    if (persistent && use_w32 && !phase_probe()) {
+      s.d_sweepctl.ensure(sizeof(int) * (1 + 2 * (size_t)ng * max_nb));
+      launch_jacobi_sweep_w32(dg, ng, max_nb / 4, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, 4.0 * kEps,
+                              2.0 * kEps, (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p, perm_stride,
+                              (double*)s.d_maxoff.p, (double*)s.d_offsum.p, (cplx*)s.d_gblk.p,
+                              (int*)s.d_sweepctl.p, st);
+      s.launches += 1;
+      ++s.jacobi_launches;
+    } else if (persistent && cluster_policy() && !phase_probe()) {
+      s.d_sweepctl.ensure(sizeof(int) * (1 + 2 * (size_t)ng * max_nb));
+      launch_jacobi_sweep_cl(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (const int*)s.d_active.p + ng, n_list,
+                             group_policy(), (int*)s.d_rot.p, 4.0 * kEps, 2.0 * kEps, (const double*)s.d_frob.p,
+                             kFloorRel2, (const int*)s.d_perm.p, perm_stride, (double*)s.d_maxoff.p,
+                             (int*)s.d_need.p, (double*)s.d_offsum.p, (cplx*)s.d_gblk.p, (int*)s.d_sweepctl.p, st);
+      s.launches += 1;
+      ++s.jacobi_launches;
+    } else if (persistent) {
       s.d_sweepctl.ensure(sizeof(int) * (1 + 2 * (size_t)ng * max_nb));
       launch_jacobi_sweep(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, 4.0 * kEps, 2.0 * kEps,
                           (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p, perm_stride,
                           (double*)s.d_maxoff.p, (int*)s.d_need.p, (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p,
-                          (double*)s.d_offsum.p, (cplx*)s.d_gblk.p, (int*)s.d_sweepctl.p, phase_probe(), st);
+                          (double*)s.d_offsum.p, (cplx*)s.d_gblk.p, (int*)s.d_sweepctl.p, phase_probe(), l2hint_policy(), st);
       s.launches += 1;
       ++s.jacobi_launches;
     }
@@ -655,7 +729,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       converged = true;
       break;
     }
-    CK(cudaMemcpyAsync(s.d_active.p, h_rot, sizeof(int) * ng, cudaMemcpyHostToDevice, st));
+    upload_active();
   }
   launch_norms(dg, ng, max_n, ws, (double*)s.d_sigma.p, sig_stride, st);
   check_launch("norms_kernel");
@@ -777,7 +851,7 @@ void run_layer(State& s, const std::vector<G2>& two, const std::vector<G1>& one,
     d.trans = M >= N ? 0 : 1;
     d.m = std::max(M, N);
     d.n = std::min(M, N);
-    d.n_pad = ((d.n + kP - 1) / kP) * kP;
+    d.n_pad = ((d.n + kNAlign - 1) / kNAlign) * kNAlign;
     d.m_pad = ((d.m + kE - 1) / kE) * kE;
     d.nb = d.n_pad / kW;
     d.max_bond = pol.max_bond;
@@ -1585,7 +1659,7 @@ int mpsim_gpu_svd(int32_t rows, int32_t cols, const double* a, int64_t max_rank,
     d.trans = rows >= cols ? 0 : 1;
     d.m = std::max(rows, cols);
     d.n = std::min(rows, cols);
-    d.n_pad = ((d.n + kP - 1) / kP) * kP;
+    d.n_pad = ((d.n + kNAlign - 1) / kNAlign) * kNAlign;
     d.m_pad = ((d.m + kE - 1) / kE) * kE;
     d.nb = d.n_pad / kW;
     d.max_bond = max_rank;

@@ -19,12 +19,14 @@
 
 namespace mpsim_gpu {
 
-struct EvdScratch {
-  double cs[kP / 2], sn[kP / 2];
-  cplx ph[kP / 2];
-  int pp[kP / 2], pq[kP / 2];
+template <int kPP>
+struct EvdScratchT {
+  double cs[kPP / 2], sn[kPP / 2];
+  cplx ph[kPP / 2];
+  int pp[kPP / 2], pq[kPP / 2];
   int any;
 };
+using EvdScratch = EvdScratchT<kP>;
 
 __device__ __forceinline__ void rr_pair(int step, int k, int M, int& a, int& b) {
   // Round-robin tournament over M+1 players (M odd); player M is fixed.
@@ -41,26 +43,32 @@ __device__ __forceinline__ void rr_pair(int step, int k, int M, int& a, int& b) 
 // the noise floor. All 256 threads must call it. If maxoff != nullptr the
 // largest relative off-diagonal of the block is folded into *maxoff
 // (atomicMax on the bit pattern: non-negative doubles order as integers).
-__device__ __forceinline__ bool pair_needs_rotation(const cplx* G, int t, double tolg, double floor2,
-                                                    double* maxoff = nullptr) {
-  const int ip = t / 16, jp = t % 16;
+// (kPP x kPP Gram with row pitch kLd, kT threads; kPP^2 / 4 must be a multiple of kT)
+template <int kPP, int kLd, int kT>
+__device__ __forceinline__ bool pair_needs_rotation_t(const cplx* G, int t, double tolg, double floor2,
+                                                      double* maxoff = nullptr) {
   bool need = false;
   double mx = 0.0;
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int h = 0; h < (kPP * kPP / 4) / kT; ++h) {
+    const int blk = t + h * kT;
+    const int ip = blk / (kPP / 2), jp = blk % (kPP / 2);
 #pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      const int i = 2 * ip + a, j = 2 * jp + b;
-      if (i < j) {
-        const double gij = sqrt(cabs2(G[i * kPad + j]));
-        const double gii = G[i * kPad + i].x, gjj = G[j * kPad + j].x;
-        if (gij > 0.0 && fmin(gii, gjj) > floor2) {
-          const double rel = gij / sqrt(gii * gjj);
-          mx = fmax(mx, rel);
-          if (rel > tolg) need = true;
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int i = 2 * ip + a, j = 2 * jp + b;
+        if (i < j) {
+          const double gij = sqrt(cabs2(G[i * kLd + j]));
+          const double gii = G[i * kLd + i].x, gjj = G[j * kLd + j].x;
+          if (gij > 0.0 && fmin(gii, gjj) > floor2) {
+            const double rel = gij / sqrt(gii * gjj);
+            mx = fmax(mx, rel);
+            if (rel > tolg) need = true;
+          }
         }
       }
-    }
+  }
   if (maxoff != nullptr) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -69,37 +77,46 @@ __device__ __forceinline__ bool pair_needs_rotation(const cplx* G, int t, double
   }
   return __syncthreads_or(need);
 }
+__device__ __forceinline__ bool pair_needs_rotation(const cplx* G, int t, double tolg, double floor2,
+                                                    double* maxoff = nullptr) {
+  return pair_needs_rotation_t<kP, kPad, 256>(G, t, tolg, floor2, maxoff);
+}
 
 // Two barriers per step: 16 threads form the parameters, then all 256 update.
 // cross = true: one pass over the 256 pairs (i < W <= j) that straddle the two
 // blocks only, 16 steps of pairs (i, W + (i + step) % W) instead of 31 steps
 // over all 496 pairs. Used in the pre-asymptotic outer sweeps (engine.cu),
 // where the in-block pairs are near-orthogonal from their previous visits.
-__device__ __forceinline__ void pair_evd_v1(cplx* G, cplx* R, EvdScratch& S, int t, double tol_in, double floor2,
-                                            int max_in, bool cross = false) {
-  for (int idx = t; idx < kP * kP; idx += 256) {
-    const int i = idx / kP, j = idx % kP;
-    R[i * kPad + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+// kPP x kPP Hermitian G and R (row pitch kLd), kT threads; each thread owns
+// (kPP / 2)^2 / kT (row pair, column pair) blocks per step.
+template <int kPP, int kLd, int kT>
+__device__ __forceinline__ void pair_evd_t(cplx* G, cplx* R, EvdScratchT<kPP>& S, int t, double tol_in,
+                                           double floor2, int max_in, bool cross = false) {
+  constexpr int kH = kPP / 2;
+  constexpr int kBlk = kH * kH / kT;
+  static_assert(kH * kH % kT == 0, "blocks per thread");
+  for (int idx = t; idx < kPP * kPP; idx += kT) {
+    const int i = idx / kPP, j = idx % kPP;
+    R[i * kLd + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
   }
-  if (t < kP) G[t * kPad + t].y = 0.0;
+  if (t < kPP) G[t * kLd + t].y = 0.0;
   const double tol2 = tol_in * tol_in;
-  const int ba = t / (kP / 2), bb = t % (kP / 2);  // this thread's (row pair, column pair)
   __syncthreads();
   for (int sweep = 0; sweep < max_in; ++sweep) {
     if (t == 0) S.any = 0;
     __syncthreads();
-    const int nsteps = cross ? kP / 2 : kP - 1;
+    const int nsteps = cross ? kH : kPP - 1;
     for (int step = 0; step < nsteps; ++step) {
-      if (t < kP / 2) {
+      if (t < kH) {
         int p, q;
         if (cross) {
           p = t;
-          q = kP / 2 + (t + step) % (kP / 2);
+          q = kH + (t + step) % kH;
         } else {
-          rr_pair(step, t, kP - 1, p, q);
+          rr_pair(step, t, kPP - 1, p, q);
         }
-        const double a = G[p * kPad + p].x, b = G[q * kPad + q].x;
-        const cplx g = G[p * kPad + q];
+        const double a = G[p * kLd + p].x, b = G[q * kLd + q].x;
+        const cplx g = G[p * kLd + q];
         const double c2 = cabs2(g);
         double cs = 1.0, sn = 0.0;
         cplx ph = make_double2(1.0, 0.0);
@@ -121,6 +138,9 @@ __device__ __forceinline__ void pair_evd_v1(cplx* G, cplx* R, EvdScratch& S, int
         S.pq[t] = q;
       }
       __syncthreads();
+#pragma unroll
+      for (int hb = 0; hb < kBlk; ++hb) {
+      const int ba = (t + hb * kT) / kH, bb = (t + hb * kT) % kH;  // this thread's (row pair, column pair)
       const double csa = S.cs[ba], sna = S.sn[ba], csb = S.cs[bb], snb = S.sn[bb];
       if (sna != 0.0 || snb != 0.0) {
         const int pa = S.pp[ba], qa = S.pq[ba], pb = S.pp[bb], qb = S.pq[bb];
@@ -129,7 +149,7 @@ __device__ __forceinline__ void pair_evd_v1(cplx* G, cplx* R, EvdScratch& S, int
         const cplx jb_qp = make_double2(-phb.x * snb, -phb.y * snb), jb_qq = make_double2(phb.x * csb, phb.y * csb);
         // conj(J_a) entries used on the left: conj(Jpp)=cs, conj(Jqp)=-conj(ph) sn, conj(Jpq)=sn, conj(Jqq)=conj(ph) cs
         const cplx ca_qp = make_double2(-pha.x * sna, pha.y * sna), ca_qq = make_double2(pha.x * csa, -pha.y * csa);
-        const cplx b00 = G[pa * kPad + pb], b01 = G[pa * kPad + qb], b10 = G[qa * kPad + pb], b11 = G[qa * kPad + qb];
+        const cplx b00 = G[pa * kLd + pb], b01 = G[pa * kLd + qb], b10 = G[qa * kLd + pb], b11 = G[qa * kLd + qb];
         // M = J_a^H B
         cplx m00 = make_double2(csa * b00.x, csa * b00.y), m01 = make_double2(csa * b01.x, csa * b01.y);
         cplx m10 = make_double2(sna * b00.x, sna * b00.y), m11 = make_double2(sna * b01.x, sna * b01.y);
@@ -150,22 +170,23 @@ __device__ __forceinline__ void pair_evd_v1(cplx* G, cplx* R, EvdScratch& S, int
           n01 = make_double2(0.0, 0.0);
           n10 = make_double2(0.0, 0.0);
         }
-        G[pa * kPad + pb] = n00;
-        G[pa * kPad + qb] = n01;
-        G[qa * kPad + pb] = n10;
-        G[qa * kPad + qb] = n11;
+        G[pa * kLd + pb] = n00;
+        G[pa * kLd + qb] = n01;
+        G[qa * kLd + pb] = n10;
+        G[qa * kLd + qb] = n11;
         if (snb != 0.0) {  // R <- R J_b on rows (pa, qa), columns (pb, qb)
 #pragma unroll
           for (int r = 0; r < 2; ++r) {
             const int row = r == 0 ? pa : qa;
-            const cplx x0 = R[row * kPad + pb], x1 = R[row * kPad + qb];
+            const cplx x0 = R[row * kLd + pb], x1 = R[row * kLd + qb];
             cplx y0 = make_double2(csb * x0.x, csb * x0.y), y1 = make_double2(snb * x0.x, snb * x0.y);
             cfma(y0, x1, jb_qp);
             cfma(y1, x1, jb_qq);
-            R[row * kPad + pb] = y0;
-            R[row * kPad + qb] = y1;
+            R[row * kLd + pb] = y0;
+            R[row * kLd + qb] = y1;
           }
         }
+      }
       }
       __syncthreads();
     }
@@ -173,6 +194,10 @@ __device__ __forceinline__ void pair_evd_v1(cplx* G, cplx* R, EvdScratch& S, int
     __syncthreads();
     if (!any) break;
   }
+}
+__device__ __forceinline__ void pair_evd_v1(cplx* G, cplx* R, EvdScratch& S, int t, double tol_in, double floor2,
+                                            int max_in, bool cross = false) {
+  pair_evd_t<kP, kPad, 256>(G, R, S, t, tol_in, floor2, max_in, cross);
 }
 
 }  // namespace mpsim_gpu

@@ -14,6 +14,9 @@
 #include "common.cuh"
 #include "evd.cuh"
 
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
+
 namespace mpsim_gpu {
 
 namespace {
@@ -61,6 +64,25 @@ __device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
 }
+// 16-byte copy with an L2 eviction-priority hint (createpolicy below)
+__device__ __forceinline__ void cp_async16_hint(double* smem, const double* gmem, unsigned long long pol) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "l"(pol));
+}
+// L2 policies: 0 normal, 1 evict_first, 2 evict_last
+__device__ __forceinline__ unsigned long long l2_policy(int kind) {
+  unsigned long long p;
+  if (kind == 1)
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else if (kind == 2)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_hint(double* gmem, double v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(gmem), "d"(v), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -81,10 +103,11 @@ struct ChunkLoader {
     for (int s = 0; s < 4; ++s) src[s] = c.vec(warp + 8 * s) + plane * c.mp + 2 * rp;
     soff = plane * kChunkPlane + warp * kPitchS + 2 * rp;
   }
+  unsigned long long pol;  // L2 policy of the copies (set per pass)
   // rows e0 .. e0 + kC of the pair -> buffer (Re plane at buf, Im at buf + kChunkPlane)
   __device__ __forceinline__ void issue(double* buf, int e0) const {
 #pragma unroll
-    for (int s = 0; s < 4; ++s) cp_async16(buf + soff + 8 * s * kPitchS, src[s] + e0);
+    for (int s = 0; s < 4; ++s) cp_async16_hint(buf + soff + 8 * s * kPitchS, src[s] + e0, pol);
     cp_async_commit();
   }
 };
@@ -115,20 +138,22 @@ static_assert(sizeof(cplx) * kP * kPad <= sizeof(PairSmem::u), "R must fit in th
 // and one B load feed six DMMAs, and each thread ends up with Re and Im of
 // the same complex outputs.
 __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader& ld, double (*buf)[2 * kChunkPlane],
-                                            const cplx* Rs, int nchunks, int t) {
+                                            const cplx* Rs, int c0, int nchunks, int t, int b0 = 0,
+                                            unsigned long long spol = 0, bool shint = false) {
   const int lane = t % 32, warp = t / 32;
   const int fr = lane / 4, fk = lane % 4;
   const int rbase = 2 * (warp & 1), cj = warp >> 1;
   const int jb = 8 * cj + fr;
-  // chunks last to first: the rows the Gram pass read last are the likeliest
-  // still in L2 (the caller issues chunk nchunks - 1 into buffer 0)
+  // chunks [c0, c0 + nchunks) last to first: the rows the Gram pass read last
+  // are the likeliest still in L2 (the caller issues chunk c0 + nchunks - 1
+  // into buffer b0)
   for (int k = 0; k < nchunks; ++k) {
     // one barrier per chunk: it publishes chunk k and certifies that every
     // warp is done with chunk k - 1, whose buffer the next load then reuses
     cp_async_wait<0>();
     __syncthreads();
-    if (k + 1 < nchunks) ld.issue(buf[(k + 1) & 1], (nchunks - 2 - k) * kC);
-    const double* B = buf[k & 1];
+    if (k + 1 < nchunks) ld.issue(buf[(k + 1 + b0) & 1], (c0 + nchunks - 2 - k) * kC);
+    const double* B = buf[(k + b0) & 1];
     // complex product in three real products (Gauss): T1 = Xr Rr, T2 = Xi Ri,
     // T3 = (Xr + Xi)(Rr + Ri); Re = T1 - T2, Im = T3 - T1 - T2. 48 DMMAs per
     // warp and chunk instead of 64; each output column's error stays bounded
@@ -160,7 +185,7 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
         o[a][0][v] = t1[a][v] - t2[a][v];
         o[a][1][v] = t3[a][v] - t1[a][v] - t2[a][v];
       }
-    const int e0 = (nchunks - 1 - k) * kC;
+    const int e0 = (c0 + nchunks - 1 - k) * kC;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -168,8 +193,13 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
         const int e = 8 * (rbase + a) + fr;
         const int j = 8 * cj + 2 * fk + v;
         double* xj = c.vec(j);
-        xj[e0 + e] = o[a][0][v];
-        xj[c.mp + e0 + e] = o[a][1][v];
+        if (shint) {
+          st_hint(xj + e0 + e, o[a][0][v], spol);
+          st_hint(xj + c.mp + e0 + e, o[a][1][v], spol);
+        } else {
+          xj[e0 + e] = o[a][0][v];
+          xj[c.mp + e0 + e] = o[a][1][v];
+        }
       }
   }
 }
@@ -184,88 +214,15 @@ __device__ __forceinline__ void copy_rotation(const cplx* R, long long rpitch, c
 
 }  // namespace
 
-// Cross-block-only pair EVD: every round of a pre-asymptotic sweep (active
-// bit 2), else the rounds off a period of 2 (bit 16) or 3 (bits 16 | 32):
-// the remaining rounds still rotate the in-block pairs, which keeps the
-// outer sweep count (tools/emu_jacobi.py).
-__device__ __forceinline__ bool cross_only_evd(int active, int round) {
-  if (active & 2) return true;
-  if (!(active & 16)) return false;
-  return round % ((active & 32) ? 3 : 2) != 0;
-}
-
-// kMode 0: Gram only (G -> gbuf); 1: Gram + pair EVD (R -> rbuf); 2: the whole
-// pair visit, Gram + EVD + rotation, in one CTA.
-struct RoundArgs {
-  const GateDesc* gates;
-  cplx* ws;
-  const int* active;
-  double tol;
-  const double* frob2;
-  double floor_rel2;
-  const int* perm;
-  long long perm_stride;
-  double* maxoff;
-  int* need;
-  cplx* gbuf;
-  int max_pairs;
-  double* offsum;
-  cplx* rbuf;
-  double tol_in;
-  cplx* gblk;
-  int* rotated;
-  int probe;
-  int* blkok;  // per block: gblk holds its exact in-block Gram (persistent sweeps; nullable)
-};
-
-// One pair visit (block pair k of gate gi in tournament round `round`).
-template <int kMode>
-__device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round, int k, PairSmem& S) {
-  constexpr bool kFuseEvd = kMode >= 1;
-  const GateDesc* __restrict__ gates = A.gates;
-  cplx* __restrict__ ws = A.ws;
-  const int* __restrict__ active = A.active;
-  const double tol = A.tol, floor_rel2 = A.floor_rel2, tol_in = A.tol_in;
-  const double* __restrict__ frob2 = A.frob2;
-  const int* __restrict__ perm = A.perm;
-  const long long perm_stride = A.perm_stride;
-  double* __restrict__ maxoff = A.maxoff;
-  int* __restrict__ need = A.need;
-  cplx* __restrict__ gbuf = A.gbuf;
-  const int max_pairs = A.max_pairs;
-  double* __restrict__ offsum = A.offsum;
-  cplx* __restrict__ rbuf = A.rbuf;
-  cplx* __restrict__ gblk = A.gblk;
-  int* __restrict__ rotated = A.rotated;
-  const int probe = A.probe;
-  const GateDesc& g = gates[gi];
-  PairCtx c;
-  if (!pair_ctx(g, gi, round, active, ws, perm, perm_stride, c, k)) return;
-  cplx* const SG = S.v.G;
-  const int t = threadIdx.x, lane = t % 32, warp = t / 32;
-  ChunkLoader ld;
-  ld.init(c, t);
+// Gram pass over chunks [c0, c0 + nchunks) of the pair into S.u.Gx: the 16
+// cross tiles (cross_only) or the 36 tiles of the upper real-extended Gram.
+// nchunks may be 0 (the tiles are then zero). Ends with a block barrier.
+__device__ __forceinline__ void gram_pass(PairSmem& S, const ChunkLoader& ld, int c0, int nchunks, bool cross_only,
+                                          int t) {
+  const int lane = t % 32, warp = t / 32;
   const int fr = lane / 4, fk = lane % 4;
-  // Stored in-block Grams (active bit 4, rounds > 0 of a pre-asymptotic
-  // sweep): the in-block 16 x 16 Grams of both blocks are those the pair EVD
-  // left at the blocks' previous visit this sweep (R^H G R, exact up to
-  // rounding: the blocks have not changed since), so only the cross block
-  // X_a^H X_b is computed: 16 of the 36 DMMA tiles.
-  const bool approx = kFuseEvd && (active[gi] & 4) && round > 0;
-  // Exact cache (active bit 8, closing sweeps): a visit that computed all 36
-  // tiles and did not rotate leaves the blocks' in-block Grams in gblk and
-  // flags them; a later visit of two flagged (hence unchanged) blocks this
-  // sweep needs only the cross tiles — the in-block values are exactly what
-  // recomputing them would give. A rotation clears the flags.
-  int* const ok_a = A.blkok ? A.blkok + (long long)gi * 2 * max_pairs + c.ba : nullptr;
-  int* const ok_b = A.blkok ? A.blkok + (long long)gi * 2 * max_pairs + c.bb : nullptr;
-  const bool cached = kFuseEvd && !approx && ok_a && (active[gi] & 8) && round > 0 && *ok_a && *ok_b;
-  const bool cross_only = approx || cached;
-  cplx* const gblk_a = gblk + ((long long)gi * 2 * max_pairs + c.ba) * (kW * kW);
-  cplx* const gblk_b = gblk + ((long long)gi * 2 * max_pairs + c.bb) * (kW * kW);
   // column offsets (plane + index) of this thread's fragments
   auto coff = [&](int col) { return (col < kP ? 0 : kChunkPlane) + (col & (kP - 1)) * kPitchS; };
-  const int nchunks = g.m_pad / kC;
   // Gram pass: a three-stage cp.async ring (two chunk buffers + the G / R
   // union, free until the Gram is assembled): the pass does only 16-36 tiles
   // of DMMA per 32-row chunk, too little to hide a load issued one chunk ahead
@@ -279,10 +236,10 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
     if (k + 1 < nchunks) cp_async_wait<1>();
     else cp_async_wait<0>();
     __syncthreads();
-    if (k + 2 < nchunks) ld.issue(stage(k + 2), (k + 2) * kC);
+    if (k + 2 < nchunks) ld.issue(stage(k + 2), (c0 + k + 2) * kC);
   };
-  ld.issue(stage(0), 0);
-  if (nchunks > 1) ld.issue(stage(1), kC);
+  if (nchunks > 0) ld.issue(stage(0), c0 * kC);
+  if (nchunks > 1) ld.issue(stage(1), (c0 + 1) * kC);
   if (cross_only) {
     // the 16 cross tiles (rows Re_a / Im_a = tiles 0,1 / 4,5; cols Re_b / Im_b =
     // 2,3 / 6,7) as four 2x2 blocks, warp & 3 picks the block and warp >> 2
@@ -377,6 +334,90 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
         for (int v = 0; v < 2; ++v) S.u.Gx[(8 * trow[i] + fr) * 65 + 8 * tcol[i] + fk * 2 + v] = acc[i][v];
     __syncthreads();
   }
+}
+
+// Cross-block-only pair EVD: every round of a pre-asymptotic sweep (active
+// bit 2), else the rounds off a period of 2 (bit 16) or 3 (bits 16 | 32):
+// the remaining rounds still rotate the in-block pairs, which keeps the
+// outer sweep count (tools/emu_jacobi.py).
+__device__ __forceinline__ bool cross_only_evd(int active, int round) {
+  if (active & 2) return true;
+  if (!(active & 16)) return false;
+  return round % ((active & 32) ? 3 : 2) != 0;
+}
+
+// kMode 0: Gram only (G -> gbuf); 1: Gram + pair EVD (R -> rbuf); 2: the whole
+// pair visit, Gram + EVD + rotation, in one CTA.
+struct RoundArgs {
+  const GateDesc* gates;
+  cplx* ws;
+  const int* active;
+  double tol;
+  const double* frob2;
+  double floor_rel2;
+  const int* perm;
+  long long perm_stride;
+  double* maxoff;
+  int* need;
+  cplx* gbuf;
+  int max_pairs;
+  double* offsum;
+  cplx* rbuf;
+  double tol_in;
+  cplx* gblk;
+  int* rotated;
+  int probe;
+  int* blkok;  // per block: gblk holds its exact in-block Gram (persistent sweeps; nullable)
+  int l2hint;  // L2 priorities: 0 none; 1 rotation loads / stores evict_first; 2 and Gram loads evict_last
+};
+
+// One pair visit (block pair k of gate gi in tournament round `round`).
+template <int kMode>
+__device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round, int k, PairSmem& S) {
+  constexpr bool kFuseEvd = kMode >= 1;
+  const GateDesc* __restrict__ gates = A.gates;
+  cplx* __restrict__ ws = A.ws;
+  const int* __restrict__ active = A.active;
+  const double tol = A.tol, floor_rel2 = A.floor_rel2, tol_in = A.tol_in;
+  const double* __restrict__ frob2 = A.frob2;
+  const int* __restrict__ perm = A.perm;
+  const long long perm_stride = A.perm_stride;
+  double* __restrict__ maxoff = A.maxoff;
+  int* __restrict__ need = A.need;
+  cplx* __restrict__ gbuf = A.gbuf;
+  const int max_pairs = A.max_pairs;
+  double* __restrict__ offsum = A.offsum;
+  cplx* __restrict__ rbuf = A.rbuf;
+  cplx* __restrict__ gblk = A.gblk;
+  int* __restrict__ rotated = A.rotated;
+  const int probe = A.probe;
+  const GateDesc& g = gates[gi];
+  PairCtx c;
+  if (!pair_ctx(g, gi, round, active, ws, perm, perm_stride, c, k)) return;
+  cplx* const SG = S.v.G;
+  const int t = threadIdx.x, lane = t % 32, warp = t / 32;
+  ChunkLoader ld;
+  ld.init(c, t);
+  ld.pol = l2_policy(A.l2hint >= 2 ? 2 : 0);
+  // Stored in-block Grams (active bit 4, rounds > 0 of a pre-asymptotic
+  // sweep): the in-block 16 x 16 Grams of both blocks are those the pair EVD
+  // left at the blocks' previous visit this sweep (R^H G R, exact up to
+  // rounding: the blocks have not changed since), so only the cross block
+  // X_a^H X_b is computed: 16 of the 36 DMMA tiles.
+  const bool approx = kFuseEvd && (active[gi] & 4) && round > 0;
+  // Exact cache (active bit 8, closing sweeps): a visit that computed all 36
+  // tiles and did not rotate leaves the blocks' in-block Grams in gblk and
+  // flags them; a later visit of two flagged (hence unchanged) blocks this
+  // sweep needs only the cross tiles — the in-block values are exactly what
+  // recomputing them would give. A rotation clears the flags.
+  int* const ok_a = A.blkok ? A.blkok + (long long)gi * 2 * max_pairs + c.ba : nullptr;
+  int* const ok_b = A.blkok ? A.blkok + (long long)gi * 2 * max_pairs + c.bb : nullptr;
+  const bool cached = kFuseEvd && !approx && ok_a && (active[gi] & 8) && round > 0 && *ok_a && *ok_b;
+  const bool cross_only = approx || cached;
+  cplx* const gblk_a = gblk + ((long long)gi * 2 * max_pairs + c.ba) * (kW * kW);
+  cplx* const gblk_b = gblk + ((long long)gi * 2 * max_pairs + c.bb) * (kW * kW);
+  const int nchunks = g.m_pad / kC;
+  gram_pass(S, ld, 0, nchunks, cross_only, t);
   if (cross_only) {
     const double* Gx = S.u.Gx;
     const int i = t >> 4, j = kW + (t & 15);
@@ -430,6 +471,9 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
   if (probe == 1) return;  // profiling (MPSIM_PHASE_PROBE): Gram only
   if constexpr (kFuseEvd) {
     cplx* R = reinterpret_cast<cplx*>(S.u.buf);
+    static_assert(sizeof(cplx) * kP * kPad <= sizeof(double) * 2 * kChunkPlane, "R must fit in buffer 0");
+    const unsigned long long rpol = l2_policy(A.l2hint >= 1 ? 1 : 0);
+    ld.pol = rpol;
     if (probe == 4) {  // profiling: the visit without its EVD (R = I)
       for (int idx = t; idx < kP * kP; idx += 256)
         R[(idx / kP) * kPad + idx % kP] = make_double2(idx / kP == idx % kP ? 1.0 : 0.0, 0.0);
@@ -448,7 +492,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
       copy_rotation(R, kPad, S.v.Rs, t);
       __syncthreads();  // R (aliased by the chunk buffers) has been read
       ld.issue(S.u.buf[0], (nchunks - 1) * kC);
-      rotate_pair(c, ld, S.u.buf, S.v.Rs, nchunks, t);
+      rotate_pair(c, ld, S.u.buf, S.v.Rs, 0, nchunks, t, 0, rpol, A.l2hint >= 1);
       if (t == 0) atomicAdd(rotated + gi, 1);
     }
   } else {
@@ -520,6 +564,204 @@ __global__ void __launch_bounds__(256, 4) jacobi_sweep_kernel(RoundArgs A, int n
   }
 }
 
+// ---------------------------------------------------------------------------
+// Cluster pair visits. One visit is split by rows over a cluster of kCl CTAs
+// (CTA r streams chunks [r nch / kCl, (r + 1) nch / kCl)): each computes the
+// partial Gram of its rows; rank 0 sums the kCl partials in rank order through
+// distributed shared memory, runs the convergence test and the pair EVD, and
+// writes R into every CTA's shared memory; each CTA rotates its own rows.
+// A quarter of the CTAs are in visits at any time compared with one CTA per
+// visit, and visits are claimed gate group by gate group (`group` gates of
+// the active list, all rounds, then the next group), so the blocks a round
+// writes are read by the next round while still in L2: the sweep's working
+// set is group x 16 MB (chi = 512) instead of the whole layer.
+namespace {
+constexpr int kCl = 4;
+
+__device__ __forceinline__ bool decode_item(const RoundArgs& A, const int* glist, int n_list, int group,
+                                            int max_rounds, long long item, int& gi, int& round, int& k) {
+  const long long per_round_g = (long long)group * A.max_pairs;
+  const long long per_group = per_round_g * max_rounds;
+  const long long grp = item / per_group;
+  long long rem = item - grp * per_group;
+  round = (int)(rem / per_round_g);
+  rem -= (long long)round * per_round_g;
+  const int j = (int)(rem / A.max_pairs);
+  k = (int)(rem - (long long)j * A.max_pairs);
+  const long long idx = grp * group + j;
+  if (idx >= n_list) return false;
+  gi = glist[idx];
+  const int nb = A.gates[gi].nb;
+  return A.active[gi] && round < nb - 1 && k < nb / 2;
+}
+
+__device__ __forceinline__ void wait_round(const int* p, int round) {
+  int v;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if (v >= round) break;
+    __nanosleep(64);
+  }
+}
+
+// One pair visit by the whole cluster (every CTA calls it with the same item).
+__device__ __forceinline__ void pair_visit_cl(const RoundArgs& A, int gi, int round, int k, PairSmem& S, int* s_nd,
+                                              unsigned rank, cg::cluster_group& cl) {
+  const GateDesc& g = A.gates[gi];
+  PairCtx c;
+  rr_pair(round, k, g.nb - 1, c.ba, c.bb);
+  c.X = A.ws + g.ws_off;
+  c.pm = A.perm + gi * A.perm_stride;
+  c.mp = g.m_pad;
+  const int t = threadIdx.x;
+  ChunkLoader ld;
+  ld.init(c, t);
+  ld.pol = l2_policy(0);
+  const int act = A.active[gi];
+  // (see pair_visit: stored in-block Grams / exact cache)
+  const bool approx = (act & 4) && round > 0;
+  int* const ok_a = A.blkok ? A.blkok + (long long)gi * 2 * A.max_pairs + c.ba : nullptr;
+  int* const ok_b = A.blkok ? A.blkok + (long long)gi * 2 * A.max_pairs + c.bb : nullptr;
+  const bool cached = !approx && ok_a && (act & 8) && round > 0 && __ldcg(ok_a) && __ldcg(ok_b);
+  const bool cross_only = approx || cached;
+  const int nch = g.m_pad / kC;
+  const int c0 = (int)((rank * nch) / kCl), c1 = (int)(((rank + 1) * nch) / kCl);
+  gram_pass(S, ld, c0, c1 - c0, cross_only, t);
+  cl.sync();  // every partial Gram is in its CTA's shared memory
+  if (rank == 0) {
+    cplx* const SG = S.v.G;
+    cplx* const gblk_a = A.gblk + ((long long)gi * 2 * A.max_pairs + c.ba) * (kW * kW);
+    cplx* const gblk_b = A.gblk + ((long long)gi * 2 * A.max_pairs + c.bb) * (kW * kW);
+    const double* gx[kCl];
+#pragma unroll
+    for (int r = 0; r < kCl; ++r) gx[r] = cl.map_shared_rank(S.u.Gx, r);
+    auto sum = [&](int off) {
+      double v = gx[0][off];
+#pragma unroll
+      for (int r = 1; r < kCl; ++r) v += gx[r][off];
+      return v;
+    };
+    if (cross_only) {
+      const int i = t >> 4, j = kW + (t & 15);
+      const double re = sum(i * 65 + j) + sum((kP + i) * 65 + kP + j);
+      const double im = sum(i * 65 + kP + j) - sum((kP + i) * 65 + j);
+      SG[i * kPad + j] = make_double2(re, im);
+      SG[j * kPad + i] = make_double2(re, -im);
+      const int r = t >> 4, q = t & 15;
+      SG[r * kPad + q] = gblk_a[t];
+      SG[(kW + r) * kPad + kW + q] = gblk_b[t];
+    } else {
+      for (int idx = t; idx < kP * kP; idx += 256) {
+        const int i = idx / kP, j = idx % kP;
+        if (i > j) continue;
+        const double re = sum(i * 65 + j) + sum((kP + i) * 65 + kP + j);
+        const double im = sum(i * 65 + kP + j) - sum(j * 65 + kP + i);
+        SG[i * kPad + j] = make_double2(re, i == j ? 0.0 : im);
+        if (i != j) SG[j * kPad + i] = make_double2(re, -im);
+      }
+    }
+    __syncthreads();
+    const double tolg = A.tol * fmax(sqrt((double)g.m), (double)kP);
+    const double floor2 = A.floor_rel2 * A.frob2[gi];
+    {
+      const int i = t >> 4, j = kW + (t & 15), lane = t & 31;
+      const double gii = SG[i * kPad + i].x, gjj = SG[j * kPad + j].x;
+      double r = (fmin(gii, gjj) > floor2) ? cabs2(SG[i * kPad + j]) / (gii * gjj) : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+      if (lane == 0 && r > 0.0) atomicAdd(A.offsum + gi, r);
+    }
+    const bool nd = pair_needs_rotation(SG, t, tolg, floor2, A.maxoff + gi);
+    const long long slot = (long long)gi * A.max_pairs + k;
+    if (t == 0) A.need[slot] = nd ? 1 : 0;
+    auto store_inblock = [&]() {
+      const int r = t >> 4, q = t & 15;
+      gblk_a[t] = SG[r * kPad + q];
+      gblk_b[t] = SG[(kW + r) * kPad + kW + q];
+    };
+    if (!nd) {
+      if (!cross_only) {
+        store_inblock();
+        if (ok_a && t == 0) *ok_a = *ok_b = 1;
+      }
+    } else {
+      if (ok_a && t == 0) *ok_a = *ok_b = 0;
+      cplx* R = reinterpret_cast<cplx*>(S.u.buf);  // this CTA's partial Gram is summed: free
+      pair_evd_v1(SG, R, S.sc, t, A.tol_in, floor2, 1, cross_only_evd(act, round));
+      __syncthreads();
+      store_inblock();
+      __syncthreads();  // G (aliased by Rs) has been stored
+#pragma unroll
+      for (int r = 0; r < kCl; ++r) copy_rotation(R, kPad, cl.map_shared_rank(S.v.Rs, r), t);
+      if (t == 0) atomicAdd(A.rotated + gi, 1);
+    }
+    if (t < kCl) *cl.map_shared_rank(s_nd, t) = nd ? 1 : 0;
+  }
+  cl.sync();  // R and the rotate flag are in every CTA
+  if (!*s_nd) return;
+  if (c1 > c0) {
+    ld.issue(S.u.buf[0], (c1 - 1) * kC);
+    rotate_pair(c, ld, S.u.buf, S.v.Rs, c0, c1 - c0, t);
+  }
+}
+}  // namespace
+
+// A whole sweep as a persistent launch of kCl-CTA clusters (one pair visit per
+// cluster at a time, claimed in gate-group order; dataflow start as in
+// jacobi_sweep_kernel: rank 0 waits until both blocks finished the previous
+// round, and releases them when every CTA's rotated rows are written).
+__global__ void __launch_bounds__(256, 4) jacobi_sweep_cl_kernel(RoundArgs A, const int* __restrict__ glist,
+                                                                 int n_list, int group, int max_rounds,
+                                                                 int* __restrict__ ctl) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
+  __shared__ long long s_item;
+  __shared__ int s_nd;
+  cg::cluster_group cl = cg::this_cluster();
+  const unsigned rank = cl.block_rank();
+  int* counter = ctl;
+  int* ready = ctl + 1;  // [gate][block]: rounds completed this sweep
+  const long long total =
+      (long long)((n_list + group - 1) / group) * group * A.max_pairs * max_rounds;
+  const int t = threadIdx.x;
+  for (;;) {
+    if (rank == 0 && t == 0) {
+      long long item;
+      int gi = 0, round = 0, k = 0;
+      for (;;) {
+        item = atomicAdd(counter, 1);
+        if (item >= total || decode_item(A, glist, n_list, group, max_rounds, item, gi, round, k)) break;
+      }
+      if (item < total) {
+        int ba, bb;
+        rr_pair(round, k, A.gates[gi].nb - 1, ba, bb);
+        wait_round(ready + gi * 2 * A.max_pairs + ba, round);
+        wait_round(ready + gi * 2 * A.max_pairs + bb, round);
+      }
+#pragma unroll
+      for (int r = 0; r < kCl; ++r) *cl.map_shared_rank(&s_item, r) = item;
+    }
+    cl.sync();  // the item (and, through rank 0's acquire, its blocks) for every CTA
+    const long long item = s_item;
+    if (item >= total) break;
+    int gi, round, k;
+    decode_item(A, glist, n_list, group, max_rounds, item, gi, round, k);
+    pair_visit_cl(A, gi, round, k, S, &s_nd, rank, cl);
+    __syncthreads();
+    if (t == 0) __threadfence();
+    cl.sync();  // every CTA's rows are written; shared memory is free
+    if (rank == 0 && t == 0) {
+      int ba, bb;
+      rr_pair(round, k, A.gates[gi].nb - 1, ba, bb);
+      __threadfence();
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ready + gi * 2 * A.max_pairs + ba), "r"(round + 1)
+                   : "memory");
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ready + gi * 2 * A.max_pairs + bb), "r"(round + 1)
+                   : "memory");
+    }
+  }
+}
+
 struct EvdSmem {
   cplx G[kP * kPad];
   cplx R[kP * kPad];
@@ -571,10 +813,11 @@ __global__ void __launch_bounds__(256, 3) jacobi_rot_kernel(const GateDesc* __re
   const int t = threadIdx.x;
   ChunkLoader ld;
   ld.init(c, t);
+  ld.pol = l2_policy(0);
   const int nchunks = g.m_pad / kC;
   ld.issue(S.buf[0], (nchunks - 1) * kC);
   copy_rotation(rbuf + slot * (kP * kP), kP, S.Rs, t);
-  rotate_pair(c, ld, S.buf, S.Rs, nchunks, t);
+  rotate_pair(c, ld, S.buf, S.Rs, 0, nchunks, t);
   if (t == 0) atomicAdd(rotated + gi, 1);
 }
 
@@ -583,6 +826,7 @@ void jacobi_split_init() {
   cudaFuncSetAttribute(jacobi_gram_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem));
   cudaFuncSetAttribute(jacobi_gram_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem));
   cudaFuncSetAttribute(jacobi_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem));
+  cudaFuncSetAttribute(jacobi_sweep_cl_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem));
   cudaFuncSetAttribute(jacobi_evd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(EvdSmem));
   cudaFuncSetAttribute(jacobi_rot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(RotSmem));
 }
@@ -590,7 +834,7 @@ void jacobi_split_init() {
 static RoundArgs make_args(const GateDesc* d_gates, cplx* ws, const int* d_active, int* d_rotated, double tol,
                            double tol_in, const double* frob2, double floor_rel2, const int* perm,
                            long long perm_stride, double* maxoff, int* need, cplx* gbuf, cplx* rbuf, double* offsum,
-                           int max_pairs, cplx* gblk, int probe, int* blkok = nullptr) {
+                           int max_pairs, cplx* gblk, int probe, int* blkok = nullptr, int l2hint = 0) {
   RoundArgs a;
   a.gates = d_gates;
   a.ws = ws;
@@ -611,6 +855,7 @@ static RoundArgs make_args(const GateDesc* d_gates, cplx* ws, const int* d_activ
   a.rotated = d_rotated;
   a.probe = probe;
   a.blkok = blkok;
+  a.l2hint = l2hint;
   return a;
 }
 
@@ -644,7 +889,7 @@ void launch_jacobi_round_split(const GateDesc* d_gates, int n_gates, int max_pai
 void launch_jacobi_sweep(const GateDesc* d_gates, int n_gates, int max_pairs, cplx* ws, const int* d_active,
                          int* d_rotated, double tol, double tol_in, const double* frob2, double floor_rel2,
                          const int* perm, long long perm_stride, double* maxoff, int* need, cplx* gbuf, cplx* rbuf,
-                         double* offsum, cplx* gblk, int* ctl, int probe, cudaStream_t st) {
+                         double* offsum, cplx* gblk, int* ctl, int probe, int l2hint, cudaStream_t st) {
   static int ctas = 0;
   if (ctas == 0) {
     int dev = 0, sms = 148, per_sm = 1;
@@ -657,8 +902,44 @@ void launch_jacobi_sweep(const GateDesc* d_gates, int n_gates, int max_pairs, cp
   const size_t nblk = (size_t)n_gates * 2 * max_pairs;
   cudaMemsetAsync(ctl, 0, sizeof(int) * (1 + 2 * nblk), st);
   const RoundArgs a = make_args(d_gates, ws, d_active, d_rotated, tol, tol_in, frob2, floor_rel2, perm, perm_stride,
-                                maxoff, need, gbuf, rbuf, offsum, max_pairs, gblk, probe, ctl + 1 + nblk);
+                                maxoff, need, gbuf, rbuf, offsum, max_pairs, gblk, probe, ctl + 1 + nblk, l2hint);
   jacobi_sweep_kernel<<<ctas, 256, sizeof(PairSmem), st>>>(a, n_gates, 2 * max_pairs - 1, ctl);
+}
+
+// One whole sweep as a persistent launch of 4-CTA clusters over the gates in
+// d_glist (n_list active gates), claimed `group` gates at a time. ctl as for
+// launch_jacobi_sweep.
+void launch_jacobi_sweep_cl(const GateDesc* d_gates, int n_gates, int max_pairs, cplx* ws, const int* d_active,
+                            const int* d_glist, int n_list, int group, int* d_rotated, double tol, double tol_in,
+                            const double* frob2, double floor_rel2, const int* perm, long long perm_stride,
+                            double* maxoff, int* need, double* offsum, cplx* gblk, int* ctl, cudaStream_t st) {
+  static int clusters = 0;
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kCl;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = sizeof(PairSmem);
+  cfg.stream = st;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  if (clusters == 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cfg.gridDim = dim3(kCl * sms);
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, jacobi_sweep_cl_kernel, &cfg) != cudaSuccess || n < 1) n = sms / kCl;
+    clusters = n;
+  }
+  const size_t nblk = (size_t)n_gates * 2 * max_pairs;
+  cudaMemsetAsync(ctl, 0, sizeof(int) * (1 + 2 * nblk), st);
+  const RoundArgs a = make_args(d_gates, ws, d_active, d_rotated, tol, tol_in, frob2, floor_rel2, perm, perm_stride,
+                                maxoff, need, nullptr, nullptr, offsum, max_pairs, gblk, 0, ctl + 1 + nblk);
+  cfg.gridDim = dim3(kCl * clusters);
+  cudaLaunchKernelEx(&cfg, jacobi_sweep_cl_kernel, a, d_glist, n_list, group, 2 * max_pairs - 1, ctl);
 }
 
 }  // namespace mpsim_gpu

@@ -19,7 +19,7 @@ import sys
 import numpy as np
 import scipy.linalg as sl
 
-W = 16
+W = int(__import__("os").environ.get("EMU_W", "16"))
 EPS = 2.220446049250313e-16
 
 
@@ -110,6 +110,21 @@ def main():
     fro2 = np.linalg.norm(th) ** 2
     if variant in ("plain", "cross"):
         X = th.copy()
+    elif variant in ("mp32", "mpgram", "mpgram32", "mp16"):
+        # mixed-precision preconditioner: an approximate right singular basis V0,
+        # made exactly unitary by an FP64 QR, then Jacobi on theta Q
+        if variant == "mp32":
+            V0 = np.linalg.svd(th.astype(np.complex64))[2].conj().T
+        elif variant == "mp16":
+            t16 = th + 1e-4 * np.linalg.norm(th, 2) * (np.random.default_rng(5).standard_normal(th.shape)) / np.sqrt(th.shape[0])
+            V0 = np.linalg.svd(t16)[2].conj().T
+        elif variant == "mpgram":
+            V0 = np.linalg.eigh(th.conj().T @ th)[1][:, ::-1]
+        else:
+            g = (th.conj().T @ th).astype(np.complex64)
+            V0 = np.linalg.eigh(g)[1][:, ::-1]
+        Q = np.linalg.qr(V0.astype(np.complex128))[0]
+        X = th @ Q
     elif variant == "qrcp":
         X = sl.qr(th, pivoting=True, mode='economic')[1].conj().T.copy()
     else:
