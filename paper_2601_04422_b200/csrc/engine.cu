@@ -89,6 +89,16 @@ static bool w32_policy() {
   }();
   return on;
 }
+// Pair EVDs with FP32 Gram updates (bit 64) in the first sweep and in sweeps
+// whose predecessor's largest relative off-diagonal exceeded this; 0 = off
+// (A/B: MPSIM_EVD32_MAXOFF).
+static double evd32_maxoff() {
+  static const double v = [] {
+    const char* e = ab_knob("MPSIM_EVD32_MAXOFF");
+    return e ? std::atof(e) : 0.0;
+  }();
+  return v;
+}
 void qrp_init();
 void split_init();
 void theta_init();
@@ -582,7 +592,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   // maxoff saw in-block values that may be stale); only a sweep without any
   // rotation — whose Grams were then all computed exactly — ends it.
   const int first = ((jacobi_mode() >= 3 && inblock_policy() && first_sweep_inblock()) ? (1 | 4) : 1) |
-                    alt_cross_bits();
+                    alt_cross_bits() | (evd32_maxoff() > 0.0 ? 64 : 0);
   for (int i = 0; i < ng; ++i) h_rot[i] = first;
   int n_list = 0;
   // flags h_rot[0, ng) -> device, with the list of active gates after them
@@ -724,6 +734,8 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // closing sweeps: reuse in-block Grams only while they are exact (flags
       // kept by the persistent sweep kernel; bit-for-bit the recomputed values)
       else if (h_rot[i] && exact_cache_policy()) h_rot[i] |= 8;
+      // pre-asymptotic sweeps: pair EVDs with FP32 Gram updates (evd.cuh pair_evd_f32)
+      if (h_rot[i] && evd32_maxoff() > 0.0 && h_maxoff[i] > evd32_maxoff()) h_rot[i] |= 64;
     }
     if (!any) {
       converged = true;

@@ -23,6 +23,8 @@ template <int kPP>
 struct EvdScratchT {
   double cs[kPP / 2], sn[kPP / 2];
   cplx ph[kPP / 2];
+  float csf[kPP / 2], snf[kPP / 2];
+  float2 phf[kPP / 2];
   int pp[kPP / 2], pq[kPP / 2];
   int any;
 };
@@ -121,9 +123,12 @@ __device__ __forceinline__ void pair_evd_t(cplx* G, cplx* R, EvdScratchT<kPP>& S
         double cs = 1.0, sn = 0.0;
         cplx ph = make_double2(1.0, 0.0);
         if (c2 > 0.0 && c2 > tol2 * fabs(a * b) && fmin(a, b) > floor2) {
+          // the angle in FP32 (its own rsqrt, off the FP64 rsqrt's latency);
+          // ph and cs, which make J unitary, in FP64
           const double inv_c = rsqrt(c2);
+          const bool f32 = c2 > 1e-30 && c2 < 1e30;  // (float range; else from inv_c)
+          const float zf = f32 ? (float)(b - a) * 0.5f * rsqrtf((float)c2) : (float)((b - a) * 0.5 * inv_c);
           ph = make_double2(g.x * inv_c, -g.y * inv_c);  // e^{-i phi}, |ph| = 1 to rounding
-          const float zf = (float)((b - a) * 0.5 * inv_c);
           const float az = fabsf(zf);
           const float tf = copysignf(1.0f, zf) / (az > 1e18f ? 2.0f * az : az + sqrtf(1.0f + zf * zf));
           const double tt = (double)tf;
@@ -143,7 +148,18 @@ __device__ __forceinline__ void pair_evd_t(cplx* G, cplx* R, EvdScratchT<kPP>& S
       const int ba = (t + hb * kT) / kH, bb = (t + hb * kT) % kH;  // this thread's (row pair, column pair)
       const double csa = S.cs[ba], sna = S.sn[ba], csb = S.cs[bb], snb = S.sn[bb];
       if (sna != 0.0 || snb != 0.0) {
-        const int pa = S.pp[ba], qa = S.pq[ba], pb = S.pp[bb], qb = S.pq[bb];
+        // the step's pairs ba and bb, recomputed (no shared-memory round trip
+        // in front of the Gram loads)
+        int pa, qa, pb, qb;
+        if (cross) {
+          pa = ba;
+          qa = kH + (ba + step) % kH;
+          pb = bb;
+          qb = kH + (bb + step) % kH;
+        } else {
+          rr_pair(step, ba, kPP - 1, pa, qa);
+          rr_pair(step, bb, kPP - 1, pb, qb);
+        }
         const cplx pha = S.ph[ba], phb = S.ph[bb];
         // J entries: Jpp = cs, Jpq = sn, Jqp = -ph sn, Jqq = ph cs
         const cplx jb_qp = make_double2(-phb.x * snb, -phb.y * snb), jb_qq = make_double2(phb.x * csb, phb.y * csb);
@@ -195,6 +211,125 @@ __device__ __forceinline__ void pair_evd_t(cplx* G, cplx* R, EvdScratchT<kPP>& S
     if (!any) break;
   }
 }
+// The same inner sweep with the Gram updates in FP32 (pre-asymptotic outer
+// sweeps, where rotation angles need a few digits only): G is copied to the
+// FP32 scratch G32 (kP x kPad float2), every 2 x 2 update of the Gram runs in
+// FP32, while the parameters the rotation is built from (cs, sn = cs t, the
+// phase ph = conj(g) / |g| normalised in FP64) and the accumulation R <- R J
+// stay FP64 — R is exactly as unitary as with pair_evd_v1; only the angles see
+// FP32 Gram values. Cuts the inner sweep's FP64 work (which shares the FP64
+// units with DMMA) by about two thirds. On exit G holds the rotated Gram (FP32
+// accurate). 256 threads.
+__device__ __forceinline__ void pair_evd_f32(cplx* G, float2* G32, cplx* R, EvdScratch& S, int t, double tol_in,
+                                             double floor2, bool cross) {
+  for (int idx = t; idx < kP * kP; idx += 256) {
+    const int i = idx / kP, j = idx % kP;
+    R[i * kPad + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
+    const cplx g = G[i * kPad + j];
+    G32[i * kPad + j] = make_float2((float)g.x, i == j ? 0.0f : (float)g.y);
+  }
+  const float tol2 = (float)(tol_in * tol_in), floor2f = (float)floor2;
+  const int ba = t / (kP / 2), bb = t % (kP / 2);
+  if (t == 0) S.any = 0;
+  __syncthreads();
+  const int nsteps = cross ? kP / 2 : kP - 1;
+  for (int step = 0; step < nsteps; ++step) {
+    if (t < kP / 2) {
+      int p, q;
+      if (cross) {
+        p = t;
+        q = kP / 2 + (t + step) % (kP / 2);
+      } else {
+        rr_pair(step, t, kP - 1, p, q);
+      }
+      const float a = G32[p * kPad + p].x, b = G32[q * kPad + q].x;
+      const float2 g = G32[p * kPad + q];
+      const double c2 = (double)g.x * g.x + (double)g.y * g.y;  // exact: float products
+      double cs = 1.0, sn = 0.0;
+      cplx ph = make_double2(1.0, 0.0);
+      if (c2 > 0.0 && c2 > (double)tol2 * fabs((double)a * b) && fminf(a, b) > floor2f) {
+        const double inv_c = rsqrt(c2);
+        ph = make_double2(g.x * inv_c, -g.y * inv_c);
+        const float zf = (b - a) * 0.5f * (float)inv_c;
+        const float az = fabsf(zf);
+        const float tf = copysignf(1.0f, zf) / (az > 1e18f ? 2.0f * az : az + sqrtf(1.0f + zf * zf));
+        const double tt = (double)tf;
+        cs = rsqrt(1.0 + tt * tt);
+        sn = cs * tt;
+        S.any = 1;
+      }
+      S.cs[t] = cs;
+      S.sn[t] = sn;
+      S.ph[t] = ph;
+      S.csf[t] = (float)cs;
+      S.snf[t] = (float)sn;
+      S.phf[t] = make_float2((float)ph.x, (float)ph.y);
+      S.pp[t] = p;
+      S.pq[t] = q;
+    }
+    __syncthreads();
+    const double csb = S.cs[bb], snb = S.sn[bb];
+    const float csaf = S.csf[ba], snaf = S.snf[ba], csbf = S.csf[bb], snbf = S.snf[bb];
+    if (snaf != 0.0f || snbf != 0.0f || snb != 0.0) {
+      const int pa = S.pp[ba], qa = S.pq[ba], pb = S.pp[bb], qb = S.pq[bb];
+      const float2 pha = S.phf[ba], phb = S.phf[bb];
+      const float2 jb_qp = make_float2(-phb.x * snbf, -phb.y * snbf), jb_qq = make_float2(phb.x * csbf, phb.y * csbf);
+      const float2 ca_qp = make_float2(-pha.x * snaf, pha.y * snaf), ca_qq = make_float2(pha.x * csaf, -pha.y * csaf);
+      const float2 b00 = G32[pa * kPad + pb], b01 = G32[pa * kPad + qb], b10 = G32[qa * kPad + pb],
+                   b11 = G32[qa * kPad + qb];
+      auto fma2 = [](float2& acc, float2 x, float2 y) {  // acc += x y
+        acc.x = fmaf(x.x, y.x, acc.x);
+        acc.x = fmaf(-x.y, y.y, acc.x);
+        acc.y = fmaf(x.x, y.y, acc.y);
+        acc.y = fmaf(x.y, y.x, acc.y);
+      };
+      float2 m00 = make_float2(csaf * b00.x, csaf * b00.y), m01 = make_float2(csaf * b01.x, csaf * b01.y);
+      float2 m10 = make_float2(snaf * b00.x, snaf * b00.y), m11 = make_float2(snaf * b01.x, snaf * b01.y);
+      fma2(m00, ca_qp, b10);
+      fma2(m01, ca_qp, b11);
+      fma2(m10, ca_qq, b10);
+      fma2(m11, ca_qq, b11);
+      float2 n00 = make_float2(csbf * m00.x, csbf * m00.y), n01 = make_float2(snbf * m00.x, snbf * m00.y);
+      float2 n10 = make_float2(csbf * m10.x, csbf * m10.y), n11 = make_float2(snbf * m10.x, snbf * m10.y);
+      fma2(n00, m01, jb_qp);
+      fma2(n01, m01, jb_qq);
+      fma2(n10, m11, jb_qp);
+      fma2(n11, m11, jb_qq);
+      if (ba == bb) {
+        n00.y = 0.0f;
+        n11.y = 0.0f;
+        n01 = make_float2(0.0f, 0.0f);
+        n10 = make_float2(0.0f, 0.0f);
+      }
+      G32[pa * kPad + pb] = n00;
+      G32[pa * kPad + qb] = n01;
+      G32[qa * kPad + pb] = n10;
+      G32[qa * kPad + qb] = n11;
+      if (snb != 0.0) {  // R <- R J_b in FP64
+        const cplx phd = S.ph[bb];
+        const cplx jqp = make_double2(-phd.x * snb, -phd.y * snb), jqq = make_double2(phd.x * csb, phd.y * csb);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int row = r == 0 ? pa : qa;
+          const cplx x0 = R[row * kPad + pb], x1 = R[row * kPad + qb];
+          cplx y0 = make_double2(csb * x0.x, csb * x0.y), y1 = make_double2(snb * x0.x, snb * x0.y);
+          cfma(y0, x1, jqp);
+          cfma(y1, x1, jqq);
+          R[row * kPad + pb] = y0;
+          R[row * kPad + qb] = y1;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = t; idx < kP * kP; idx += 256) {
+    const int i = idx / kP, j = idx % kP;
+    const float2 g = G32[i * kPad + j];
+    G[i * kPad + j] = make_double2(g.x, g.y);
+  }
+  __syncthreads();
+}
+
 __device__ __forceinline__ void pair_evd_v1(cplx* G, cplx* R, EvdScratch& S, int t, double tol_in, double floor2,
                                             int max_in, bool cross = false) {
   pair_evd_t<kP, kPad, 256>(G, R, S, t, tol_in, floor2, max_in, cross);

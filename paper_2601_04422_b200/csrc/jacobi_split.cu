@@ -144,6 +144,8 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
   const int fr = lane / 4, fk = lane % 4;
   const int rbase = 2 * (warp & 1), cj = warp >> 1;
   const int jb = 8 * cj + fr;
+  // this thread's two output vectors (the permutation lookups stay out of the loop)
+  double* const xo[2] = {c.vec(8 * cj + 2 * fk), c.vec(8 * cj + 2 * fk + 1)};
   // chunks [c0, c0 + nchunks) last to first: the rows the Gram pass read last
   // are the likeliest still in L2 (the caller issues chunk c0 + nchunks - 1
   // into buffer b0)
@@ -191,8 +193,7 @@ __device__ __forceinline__ void rotate_pair(const PairCtx& c, const ChunkLoader&
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int e = 8 * (rbase + a) + fr;
-        const int j = 8 * cj + 2 * fk + v;
-        double* xj = c.vec(j);
+        double* xj = xo[v];
         if (shint) {
           st_hint(xj + e0 + e, o[a][0][v], spol);
           st_hint(xj + c.mp + e0 + e, o[a][1][v], spol);
@@ -478,6 +479,12 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
       for (int idx = t; idx < kP * kP; idx += 256)
         R[(idx / kP) * kPad + idx % kP] = make_double2(idx / kP == idx % kP ? 1.0 : 0.0, 0.0);
       __syncthreads();
+    } else if ((active[gi] & 64) && floor2 > 1e-36 && floor2 < 1e36) {
+      // pre-asymptotic sweep: FP32 Gram updates (buffer 1 is free: R holds buffer 0)
+      static_assert(sizeof(cplx) * kP * kPad + sizeof(float2) * kP * kPad <= sizeof(PairSmem::u),
+                    "R and the FP32 Gram must fit in the chunk buffers");
+      pair_evd_f32(SG, reinterpret_cast<float2*>(S.u.buf[1]), R, S.sc, t, tol_in, floor2,
+                   cross_only_evd(active[gi], round));
     } else {
       pair_evd_v1(SG, R, S.sc, t, tol_in, floor2, 1, cross_only_evd(active[gi], round));
     }

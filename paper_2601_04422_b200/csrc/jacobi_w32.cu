@@ -205,6 +205,7 @@ __device__ __forceinline__ void rotate_pair2(const Pair2& c, const Loader2& ld, 
   const int fr = lane >> 2, fk = lane & 3;
   const int rbase = 2 * (warp & 1), cj = warp >> 1;
   const int jb = 8 * cj + fr;
+  double* const xo[2] = {c.vec(8 * cj + 2 * fk), c.vec(8 * cj + 2 * fk + 1)};
   const cplx* Rs = S.v.Rs;
   for (int k = 0; k < nchunks; ++k) {
     wait_groups<0>();
@@ -236,8 +237,7 @@ __device__ __forceinline__ void rotate_pair2(const Pair2& c, const Loader2& ld, 
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
         const int e = 8 * (rbase + a) + fr;
-        const int j = 8 * cj + 2 * fk + v;
-        double* xj = c.vec(j);
+        double* xj = xo[v];
         xj[e0 + e] = t1[a][v] - t2[a][v];
         xj[c.mp + e0 + e] = t3[a][v] - t1[a][v] - t2[a][v];
       }
