@@ -31,6 +31,9 @@ int launch_theta(const GateDesc*, const GateDesc*, int, int, const cplx*, long l
                  CUtensorMap*, cudaStream_t);
 int theta_tiles(int dl, int dr);
 void jacobi_split_init();
+#ifdef MPSIM_AB_KNOBS
+void jacobi_phase_clocks(unsigned long long*, bool);
+#endif
 void launch_jacobi_sweep(const GateDesc*, int, int, cplx*, const int*, int*, double, double, const double*, double,
                          const int*, long long, double*, int*, cplx*, cplx*, double*, cplx*, int*, int, int,
                          cudaStream_t);
@@ -693,6 +696,18 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     // with off <= kQuadFinish: cyclic Jacobi converges quadratically there, so
     // the rotations of this sweep leave off ~ kQuadFinish^2 << tol and the
     // otherwise Gram-only confirmation sweep is skipped.
+#ifdef MPSIM_AB_KNOBS
+    if (sweep_debug()) {
+      unsigned long long c[8];
+      jacobi_phase_clocks(c, true);
+      if (c[6] > 0)
+        std::fprintf(stderr,
+                     "[mpsim]   per visit (SM clocks, thread 0): total %.0f = wait %.0f + gram %.0f + test %.0f + "
+                     "evd %.0f (%.0f per EVD, %llu EVDs) + rotation %.0f\n",
+                     (double)c[0] / c[6], (double)c[1] / c[6], (double)c[2] / c[6], (double)c[3] / c[6],
+                     (double)c[4] / c[6], c[7] ? (double)c[4] / c[7] : 0.0, c[7], (double)c[5] / c[6]);
+    }
+#endif
     if (sweep_debug()) {
       double mx = 0.0, mn = 1e300;
       long long act = 0, pairs = 0;

@@ -211,26 +211,74 @@ __device__ __forceinline__ void pair_evd_t(cplx* G, cplx* R, EvdScratchT<kPP>& S
     if (!any) break;
   }
 }
-// The same inner sweep with the Gram updates in FP32 (pre-asymptotic outer
-// sweeps, where rotation angles need a few digits only): G is copied to the
-// FP32 scratch G32 (kP x kPad float2), every 2 x 2 update of the Gram runs in
-// FP32, while the parameters the rotation is built from (cs, sn = cs t, the
-// phase ph = conj(g) / |g| normalised in FP64) and the accumulation R <- R J
-// stay FP64 — R is exactly as unitary as with pair_evd_v1; only the angles see
-// FP32 Gram values. Cuts the inner sweep's FP64 work (which shares the FP64
-// units with DMMA) by about two thirds. On exit G holds the rotated Gram (FP32
-// accurate). 256 threads.
-__device__ __forceinline__ void pair_evd_f32(cplx* G, float2* G32, cplx* R, EvdScratch& S, int t, double tol_in,
-                                             double floor2, bool cross) {
+// Pre-asymptotic inner sweep, FP32 throughout, then an exactly unitary R.
+//
+// Measured (A/B build, SM clocks per visit at chi=512): the FP64 inner sweep
+// takes ~38 % of a visit (135-180k cycles) although it is ~2 % of the visit's
+// FP64 work: DMMA executes on the FP64 units (37.1 vs 33.9 TF/s peaks), so
+// while the other CTAs of the SM rotate, every dependent FP64 instruction of
+// the EVD queues behind their DMMAs. Here the sweep's dependent chain is FP32
+// only (its own, idle pipe): G32 and R32 in FP32, the angles in FP32. R32 is
+// unitary to ~1e-7; R is its polar factor, two Newton-Schulz steps in FP64
+// on DMMA (R <- R (3 I - R^H R) / 2: 1e-7 -> 1e-14 -> 1e-28), i.e. unitary
+// to FP64 rounding like the FP64 sweep's R. The rotation R applies differs
+// from the exact inner-sweep rotation by ~1e-7 — irrelevant while the pair's
+// relative off-diagonals are >> 1e-7 (the host runs this only in sweeps whose
+// predecessor measured a largest relative off-diagonal above 1e-2).
+// Exact zeros survive: a zero vector's Gram row is zero, it is never rotated,
+// so its rows and columns of R32, R^H R and R stay those of the identity.
+//
+// Buffers (256 threads): G (FP64, kP x kPad, holds the pair Gram on entry; used
+// as scratch for R^H R afterwards), W (FP64, kP x kPad: G32 and R32 as float2
+// on entry to the polar step, then one NS iterate), R (FP64 output, kP x kPad).
+// store_inblock(G32) runs while G32 is alive (FP32-accurate in-block Grams).
+
+// C = op(A) B for 32 x 32 complex matrices in shared memory (pitch kPad),
+// op = conjugate transpose if ah; on DMMA, warp w computes output tiles
+// (w >> 1, 2 (w & 1) + {0, 1}); C must not alias A or B.
+__device__ __forceinline__ void gemm32c(const cplx* A, const cplx* B, cplx* C, bool ah, int t) {
+  const int lane = t & 31, warp = t >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int tr = warp >> 1, tc0 = 2 * (warp & 1);
+  double re[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, im[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int kk = 0; kk < kP / 4; ++kk) {
+    const int k = 4 * kk + fk, i = 8 * tr + fr;
+    cplx a = ah ? A[k * kPad + i] : A[i * kPad + k];
+    if (ah) a.y = -a.y;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const cplx b = B[k * kPad + 8 * (tc0 + c) + fr];
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(re[c][0]), "+d"(re[c][1]) : "d"(a.x), "d"(b.x));
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(re[c][0]), "+d"(re[c][1]) : "d"(-a.y), "d"(b.y));
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(im[c][0]), "+d"(im[c][1]) : "d"(a.x), "d"(b.y));
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(im[c][0]), "+d"(im[c][1]) : "d"(a.y), "d"(b.x));
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < 2; ++c)
+#pragma unroll
+    for (int v = 0; v < 2; ++v) C[(8 * tr + fr) * kPad + 8 * (tc0 + c) + 2 * fk + v] = make_double2(re[c][v], im[c][v]);
+}
+
+template <typename StoreInblock>
+__device__ __forceinline__ void pair_evd_f32(cplx* G, cplx* W, cplx* R, EvdScratch& S, int t, double floor2,
+                                             bool cross, StoreInblock store_inblock) {
+  float2* const G32 = reinterpret_cast<float2*>(W);
+  float2* const R32 = G32 + kP * kPad;
+  static_assert(2 * sizeof(float2) <= sizeof(cplx), "G32 and R32 share W");
   for (int idx = t; idx < kP * kP; idx += 256) {
     const int i = idx / kP, j = idx % kP;
-    R[i * kPad + j] = make_double2(i == j ? 1.0 : 0.0, 0.0);
     const cplx g = G[i * kPad + j];
     G32[i * kPad + j] = make_float2((float)g.x, i == j ? 0.0f : (float)g.y);
+    R32[i * kPad + j] = make_float2(i == j ? 1.0f : 0.0f, 0.0f);
   }
-  const float tol2 = (float)(tol_in * tol_in), floor2f = (float)floor2;
+  const float floor2f = (float)floor2;
   const int ba = t / (kP / 2), bb = t % (kP / 2);
-  if (t == 0) S.any = 0;
   __syncthreads();
   const int nsteps = cross ? kP / 2 : kP - 1;
   for (int step = 0; step < nsteps; ++step) {
@@ -244,53 +292,53 @@ __device__ __forceinline__ void pair_evd_f32(cplx* G, float2* G32, cplx* R, EvdS
       }
       const float a = G32[p * kPad + p].x, b = G32[q * kPad + q].x;
       const float2 g = G32[p * kPad + q];
-      const double c2 = (double)g.x * g.x + (double)g.y * g.y;  // exact: float products
-      double cs = 1.0, sn = 0.0;
-      cplx ph = make_double2(1.0, 0.0);
-      if (c2 > 0.0 && c2 > (double)tol2 * fabs((double)a * b) && fminf(a, b) > floor2f) {
-        const double inv_c = rsqrt(c2);
-        ph = make_double2(g.x * inv_c, -g.y * inv_c);
-        const float zf = (b - a) * 0.5f * (float)inv_c;
-        const float az = fabsf(zf);
-        const float tf = copysignf(1.0f, zf) / (az > 1e18f ? 2.0f * az : az + sqrtf(1.0f + zf * zf));
-        const double tt = (double)tf;
-        cs = rsqrt(1.0 + tt * tt);
+      const float c2 = g.x * g.x + g.y * g.y;
+      float cs = 1.0f, sn = 0.0f;
+      float2 ph = make_float2(1.0f, 0.0f);
+      if (c2 > 1e-14f * fabsf(a * b) && c2 > 0.0f && fminf(a, b) > floor2f) {
+        const float inv_c = rsqrtf(c2);
+        ph = make_float2(g.x * inv_c, -g.y * inv_c);
+        const float z = (b - a) * 0.5f * inv_c, az = fabsf(z);
+        const float tt = copysignf(1.0f, z) / (az > 1e18f ? 2.0f * az : az + sqrtf(1.0f + z * z));
+        cs = rsqrtf(1.0f + tt * tt);
         sn = cs * tt;
-        S.any = 1;
       }
-      S.cs[t] = cs;
-      S.sn[t] = sn;
-      S.ph[t] = ph;
-      S.csf[t] = (float)cs;
-      S.snf[t] = (float)sn;
-      S.phf[t] = make_float2((float)ph.x, (float)ph.y);
-      S.pp[t] = p;
-      S.pq[t] = q;
+      S.csf[t] = cs;
+      S.snf[t] = sn;
+      S.phf[t] = ph;
     }
     __syncthreads();
-    const double csb = S.cs[bb], snb = S.sn[bb];
-    const float csaf = S.csf[ba], snaf = S.snf[ba], csbf = S.csf[bb], snbf = S.snf[bb];
-    if (snaf != 0.0f || snbf != 0.0f || snb != 0.0) {
-      const int pa = S.pp[ba], qa = S.pq[ba], pb = S.pp[bb], qb = S.pq[bb];
+    const float csa = S.csf[ba], sna = S.snf[ba], csb = S.csf[bb], snb = S.snf[bb];
+    if (sna != 0.0f || snb != 0.0f) {
+      int pa, qa, pb, qb;
+      if (cross) {
+        pa = ba;
+        qa = kP / 2 + (ba + step) % (kP / 2);
+        pb = bb;
+        qb = kP / 2 + (bb + step) % (kP / 2);
+      } else {
+        rr_pair(step, ba, kP - 1, pa, qa);
+        rr_pair(step, bb, kP - 1, pb, qb);
+      }
       const float2 pha = S.phf[ba], phb = S.phf[bb];
-      const float2 jb_qp = make_float2(-phb.x * snbf, -phb.y * snbf), jb_qq = make_float2(phb.x * csbf, phb.y * csbf);
-      const float2 ca_qp = make_float2(-pha.x * snaf, pha.y * snaf), ca_qq = make_float2(pha.x * csaf, -pha.y * csaf);
-      const float2 b00 = G32[pa * kPad + pb], b01 = G32[pa * kPad + qb], b10 = G32[qa * kPad + pb],
-                   b11 = G32[qa * kPad + qb];
+      const float2 jb_qp = make_float2(-phb.x * snb, -phb.y * snb), jb_qq = make_float2(phb.x * csb, phb.y * csb);
+      const float2 ca_qp = make_float2(-pha.x * sna, pha.y * sna), ca_qq = make_float2(pha.x * csa, -pha.y * csa);
       auto fma2 = [](float2& acc, float2 x, float2 y) {  // acc += x y
         acc.x = fmaf(x.x, y.x, acc.x);
         acc.x = fmaf(-x.y, y.y, acc.x);
         acc.y = fmaf(x.x, y.y, acc.y);
         acc.y = fmaf(x.y, y.x, acc.y);
       };
-      float2 m00 = make_float2(csaf * b00.x, csaf * b00.y), m01 = make_float2(csaf * b01.x, csaf * b01.y);
-      float2 m10 = make_float2(snaf * b00.x, snaf * b00.y), m11 = make_float2(snaf * b01.x, snaf * b01.y);
+      const float2 b00 = G32[pa * kPad + pb], b01 = G32[pa * kPad + qb], b10 = G32[qa * kPad + pb],
+                   b11 = G32[qa * kPad + qb];
+      float2 m00 = make_float2(csa * b00.x, csa * b00.y), m01 = make_float2(csa * b01.x, csa * b01.y);
+      float2 m10 = make_float2(sna * b00.x, sna * b00.y), m11 = make_float2(sna * b01.x, sna * b01.y);
       fma2(m00, ca_qp, b10);
       fma2(m01, ca_qp, b11);
       fma2(m10, ca_qq, b10);
       fma2(m11, ca_qq, b11);
-      float2 n00 = make_float2(csbf * m00.x, csbf * m00.y), n01 = make_float2(snbf * m00.x, snbf * m00.y);
-      float2 n10 = make_float2(csbf * m10.x, csbf * m10.y), n11 = make_float2(snbf * m10.x, snbf * m10.y);
+      float2 n00 = make_float2(csb * m00.x, csb * m00.y), n01 = make_float2(snb * m00.x, snb * m00.y);
+      float2 n10 = make_float2(csb * m10.x, csb * m10.y), n11 = make_float2(snb * m10.x, snb * m10.y);
       fma2(n00, m01, jb_qp);
       fma2(n01, m01, jb_qq);
       fma2(n10, m11, jb_qp);
@@ -305,29 +353,43 @@ __device__ __forceinline__ void pair_evd_f32(cplx* G, float2* G32, cplx* R, EvdS
       G32[pa * kPad + qb] = n01;
       G32[qa * kPad + pb] = n10;
       G32[qa * kPad + qb] = n11;
-      if (snb != 0.0) {  // R <- R J_b in FP64
-        const cplx phd = S.ph[bb];
-        const cplx jqp = make_double2(-phd.x * snb, -phd.y * snb), jqq = make_double2(phd.x * csb, phd.y * csb);
+      if (snb != 0.0f) {  // R32 <- R32 J_b on rows (pa, qa), columns (pb, qb)
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           const int row = r == 0 ? pa : qa;
-          const cplx x0 = R[row * kPad + pb], x1 = R[row * kPad + qb];
-          cplx y0 = make_double2(csb * x0.x, csb * x0.y), y1 = make_double2(snb * x0.x, snb * x0.y);
-          cfma(y0, x1, jqp);
-          cfma(y1, x1, jqq);
-          R[row * kPad + pb] = y0;
-          R[row * kPad + qb] = y1;
+          const float2 x0 = R32[row * kPad + pb], x1 = R32[row * kPad + qb];
+          float2 y0 = make_float2(csb * x0.x, csb * x0.y), y1 = make_float2(snb * x0.x, snb * x0.y);
+          fma2(y0, x1, jb_qp);
+          fma2(y1, x1, jb_qq);
+          R32[row * kPad + pb] = y0;
+          R32[row * kPad + qb] = y1;
         }
       }
     }
     __syncthreads();
   }
+  store_inblock(G32);  // (FP32-accurate in-block Grams for the stored-Gram policy)
   for (int idx = t; idx < kP * kP; idx += 256) {
     const int i = idx / kP, j = idx % kP;
-    const float2 g = G32[i * kPad + j];
-    G[i * kPad + j] = make_double2(g.x, g.y);
+    const float2 r = R32[i * kPad + j];
+    R[i * kPad + j] = make_double2(r.x, r.y);
   }
   __syncthreads();
+  // polar factor: R <- R (3 I - R^H R) / 2, twice (R -> W -> R)
+  for (int it = 0; it < 2; ++it) {
+    cplx* const src = it == 0 ? R : W;
+    cplx* const dst = it == 0 ? W : R;
+    gemm32c(src, src, G, true, t);  // G <- R^H R
+    __syncthreads();
+    for (int idx = t; idx < kP * kP; idx += 256) {
+      const int i = idx / kP, j = idx % kP;
+      const cplx s = G[i * kPad + j];
+      G[i * kPad + j] = make_double2((i == j ? 1.5 : 0.0) - 0.5 * s.x, -0.5 * s.y);
+    }
+    __syncthreads();
+    gemm32c(src, G, dst, false, t);
+    __syncthreads();
+  }
 }
 
 __device__ __forceinline__ void pair_evd_v1(cplx* G, cplx* R, EvdScratch& S, int t, double tol_in, double floor2,

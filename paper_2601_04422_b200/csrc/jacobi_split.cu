@@ -337,6 +337,19 @@ __device__ __forceinline__ void gram_pass(PairSmem& S, const ChunkLoader& ld, in
   }
 }
 
+#ifdef MPSIM_AB_KNOBS
+// A/B builds: per-phase SM clock totals of the persistent sweep (thread 0 of
+// every CTA): 0 visits, 1 wait for blocks, 2 Gram pass, 3 assembly + test,
+// 4 EVD, 5 rotation, 6 visit count, 7 EVD count.
+__device__ unsigned long long g_phase_clk[8];
+#define PHASE_MARK(var) long long var = clock64()
+#define PHASE_ADD(i, v) \
+  if (threadIdx.x == 0) atomicAdd(&g_phase_clk[i], (unsigned long long)(v))
+#else
+#define PHASE_MARK(var)
+#define PHASE_ADD(i, v)
+#endif
+
 // Cross-block-only pair EVD: every round of a pre-asymptotic sweep (active
 // bit 2), else the rounds off a period of 2 (bit 16) or 3 (bits 16 | 32):
 // the remaining rounds still rotate the in-block pairs, which keeps the
@@ -418,7 +431,10 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
   cplx* const gblk_a = gblk + ((long long)gi * 2 * max_pairs + c.ba) * (kW * kW);
   cplx* const gblk_b = gblk + ((long long)gi * 2 * max_pairs + c.bb) * (kW * kW);
   const int nchunks = g.m_pad / kC;
+  PHASE_MARK(c_g0);
   gram_pass(S, ld, 0, nchunks, cross_only, t);
+  PHASE_MARK(c_g1);
+  PHASE_ADD(2, c_g1 - c_g0);
   if (cross_only) {
     const double* Gx = S.u.Gx;
     const int i = t >> 4, j = kW + (t & 15);
@@ -454,6 +470,8 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
     if (lane == 0 && r > 0.0) atomicAdd(offsum + gi, r);
   }
   const bool nd = pair_needs_rotation(SG, t, tolg, floor2, maxoff + gi);
+  PHASE_MARK(c_a1);
+  PHASE_ADD(3, c_a1 - c_g1);
   const long long slot = (long long)gi * max_pairs + k;
   if (t == 0) need[slot] = nd ? 1 : 0;
   auto store_inblock = [&]() {  // the in-block Grams for this sweep's later visits
@@ -472,6 +490,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
   if (probe == 1) return;  // profiling (MPSIM_PHASE_PROBE): Gram only
   if constexpr (kFuseEvd) {
     cplx* R = reinterpret_cast<cplx*>(S.u.buf);
+    bool evd32 = false;
     static_assert(sizeof(cplx) * kP * kPad <= sizeof(double) * 2 * kChunkPlane, "R must fit in buffer 0");
     const unsigned long long rpol = l2_policy(A.l2hint >= 1 ? 1 : 0);
     ld.pol = rpol;
@@ -479,18 +498,27 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
       for (int idx = t; idx < kP * kP; idx += 256)
         R[(idx / kP) * kPad + idx % kP] = make_double2(idx / kP == idx % kP ? 1.0 : 0.0, 0.0);
       __syncthreads();
-    } else if ((active[gi] & 64) && floor2 > 1e-36 && floor2 < 1e36) {
-      // pre-asymptotic sweep: FP32 Gram updates (buffer 1 is free: R holds buffer 0)
-      static_assert(sizeof(cplx) * kP * kPad + sizeof(float2) * kP * kPad <= sizeof(PairSmem::u),
-                    "R and the FP32 Gram must fit in the chunk buffers");
-      pair_evd_f32(SG, reinterpret_cast<float2*>(S.u.buf[1]), R, S.sc, t, tol_in, floor2,
-                   cross_only_evd(active[gi], round));
+    } else if (active[gi] & 64) {
+      // pre-asymptotic sweep: FP32 inner sweep + FP64 polar factor (evd.cuh);
+      // W = buffer 1 (R holds buffer 0), G is scratch after the sweep
+      static_assert(sizeof(cplx) * kP * kPad <= sizeof(double) * 2 * kChunkPlane, "W must fit in buffer 1");
+      pair_evd_f32(SG, reinterpret_cast<cplx*>(S.u.buf[1]), R, S.sc, t, floor2, cross_only_evd(active[gi], round),
+                   [&](const float2* G32) {
+                     const int r = t >> 4, q = t & 15;
+                     const float2 ga = G32[r * kPad + q], gb = G32[(kW + r) * kPad + kW + q];
+                     gblk_a[t] = make_double2(ga.x, ga.y);
+                     gblk_b[t] = make_double2(gb.x, gb.y);
+                   });
+      evd32 = true;
     } else {
       pair_evd_v1(SG, R, S.sc, t, tol_in, floor2, 1, cross_only_evd(active[gi], round));
     }
     if (probe == 2) return;  // Gram + EVD
     __syncthreads();
-    store_inblock();
+    PHASE_MARK(c_e1);
+    PHASE_ADD(4, c_e1 - c_a1);
+    PHASE_ADD(7, 1);
+    if (!evd32) store_inblock();
     if constexpr (kMode == 1) {
       cplx* rout = rbuf + slot * (kP * kP);
       for (int idx = t; idx < kP * kP; idx += 256) rout[idx] = R[(idx / kP) * kPad + idx % kP];
@@ -500,6 +528,8 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
       __syncthreads();  // R (aliased by the chunk buffers) has been read
       ld.issue(S.u.buf[0], (nchunks - 1) * kC);
       rotate_pair(c, ld, S.u.buf, S.v.Rs, 0, nchunks, t, 0, rpol, A.l2hint >= 1);
+      PHASE_MARK(c_r1);
+      PHASE_ADD(5, c_r1 - c_e1);
       if (t == 0) atomicAdd(rotated + gi, 1);
     }
   } else {
@@ -547,6 +577,7 @@ __global__ void __launch_bounds__(256, 4) jacobi_sweep_kernel(RoundArgs A, int n
     rr_pair(round, k, nb - 1, ba, bb);
     int* ra = ready + gi * 2 * A.max_pairs + ba;
     int* rb = ready + gi * 2 * A.max_pairs + bb;
+    PHASE_MARK(c_w0);
     if (t == 0) {
       int v;
       for (;;) {
@@ -561,8 +592,13 @@ __global__ void __launch_bounds__(256, 4) jacobi_sweep_kernel(RoundArgs A, int n
       }
     }
     __syncthreads();
+    PHASE_MARK(c_w1);
+    PHASE_ADD(1, c_w1 - c_w0);
     pair_visit<2>(A, gi, round, k, S);
     __syncthreads();  // every thread's writes of this visit are issued
+    PHASE_MARK(c_v1);
+    PHASE_ADD(0, c_v1 - c_w0);
+    PHASE_ADD(6, 1);
     if (t == 0) {
       __threadfence();
       asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ra), "r"(round + 1) : "memory");
@@ -827,6 +863,16 @@ __global__ void __launch_bounds__(256, 3) jacobi_rot_kernel(const GateDesc* __re
   rotate_pair(c, ld, S.buf, S.Rs, 0, nchunks, t);
   if (t == 0) atomicAdd(rotated + gi, 1);
 }
+
+#ifdef MPSIM_AB_KNOBS
+void jacobi_phase_clocks(unsigned long long* out, bool reset) {
+  cudaMemcpyFromSymbol(out, g_phase_clk, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_phase_clk, z, sizeof(z));
+  }
+}
+#endif
 
 void jacobi_split_init() {
   cudaFuncSetAttribute(jacobi_gram_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PairSmem));
