@@ -95,6 +95,7 @@ static bool w32_policy() {
 // Pair EVDs with FP32 Gram updates (bit 64) in the first sweep and in sweeps
 // whose predecessor's largest relative off-diagonal exceeded this; 0 = off
 // (A/B: MPSIM_EVD32_MAXOFF).
+constexpr int kEvd32MinN = 512;  // (operands with fewer vectors keep the FP64 inner sweep)
 static double evd32_maxoff() {
   static const double v = [] {
     const char* e = ab_knob("MPSIM_EVD32_MAXOFF");
@@ -596,7 +597,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   // rotation — whose Grams were then all computed exactly — ends it.
   const int first = ((jacobi_mode() >= 3 && inblock_policy() && first_sweep_inblock()) ? (1 | 4) : 1) |
                     alt_cross_bits() | (evd32_maxoff() > 0.0 ? 64 : 0);
-  for (int i = 0; i < ng; ++i) h_rot[i] = first;
+  for (int i = 0; i < ng; ++i) h_rot[i] = descs[i].n >= kEvd32MinN ? first : first & ~64;
   int n_list = 0;
   // flags h_rot[0, ng) -> device, with the list of active gates after them
   // (the cluster sweep claims its visits gate group by gate group over it)
@@ -750,7 +751,8 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // kept by the persistent sweep kernel; bit-for-bit the recomputed values)
       else if (h_rot[i] && exact_cache_policy()) h_rot[i] |= 8;
       // pre-asymptotic sweeps: pair EVDs with FP32 Gram updates (evd.cuh pair_evd_f32)
-      if (h_rot[i] && evd32_maxoff() > 0.0 && h_maxoff[i] > evd32_maxoff()) h_rot[i] |= 64;
+      if (h_rot[i] && evd32_maxoff() > 0.0 && h_maxoff[i] > evd32_maxoff() && descs[i].n >= kEvd32MinN)
+        h_rot[i] |= 64;
     }
     if (!any) {
       converged = true;

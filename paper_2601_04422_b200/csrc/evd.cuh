@@ -234,40 +234,46 @@ __device__ __forceinline__ void pair_evd_t(cplx* G, cplx* R, EvdScratchT<kPP>& S
 // store_inblock(G32) runs while G32 is alive (FP32-accurate in-block Grams).
 
 // C = op(A) B for 32 x 32 complex matrices in shared memory (pitch kPad),
-// op = conjugate transpose if ah; on DMMA, warp w computes output tiles
-// (w >> 1, 2 (w & 1) + {0, 1}); C must not alias A or B.
-__device__ __forceinline__ void gemm32c(const cplx* A, const cplx* B, cplx* C, bool ah, int t) {
+// op = conjugate transpose if ah; on DMMA with the three-real-product complex
+// multiply (T1 = Ar Br, T2 = Ai Bi, T3 = (Ar + Ai)(Br + Bi)); warp w computes
+// output tiles (w >> 1, 2 (w & 1) + {0, 1}); herm: only tiles on or above the
+// diagonal (C Hermitian; the caller mirrors). C must not alias A or B.
+__device__ __forceinline__ void gemm32c(const cplx* A, const cplx* B, cplx* C, bool ah, bool herm, int t) {
   const int lane = t & 31, warp = t >> 5;
   const int fr = lane >> 2, fk = lane & 3;
   const int tr = warp >> 1, tc0 = 2 * (warp & 1);
-  double re[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, im[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  if (herm && tr > tc0 + 1) return;
+  double t1[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, t2[2][2] = {{0.0, 0.0}, {0.0, 0.0}},
+         t3[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
   for (int kk = 0; kk < kP / 4; ++kk) {
     const int k = 4 * kk + fk, i = 8 * tr + fr;
     cplx a = ah ? A[k * kPad + i] : A[i * kPad + k];
     if (ah) a.y = -a.y;
+    const double as = a.x + a.y;
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
       const cplx b = B[k * kPad + 8 * (tc0 + c) + fr];
+      const double bs = b.x + b.y;
       asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                   : "+d"(re[c][0]), "+d"(re[c][1]) : "d"(a.x), "d"(b.x));
+                   : "+d"(t1[c][0]), "+d"(t1[c][1]) : "d"(a.x), "d"(b.x));
       asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                   : "+d"(re[c][0]), "+d"(re[c][1]) : "d"(-a.y), "d"(b.y));
+                   : "+d"(t2[c][0]), "+d"(t2[c][1]) : "d"(a.y), "d"(b.y));
       asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                   : "+d"(im[c][0]), "+d"(im[c][1]) : "d"(a.x), "d"(b.y));
-      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                   : "+d"(im[c][0]), "+d"(im[c][1]) : "d"(a.y), "d"(b.x));
+                   : "+d"(t3[c][0]), "+d"(t3[c][1]) : "d"(as), "d"(bs));
     }
   }
 #pragma unroll
   for (int c = 0; c < 2; ++c)
 #pragma unroll
-    for (int v = 0; v < 2; ++v) C[(8 * tr + fr) * kPad + 8 * (tc0 + c) + 2 * fk + v] = make_double2(re[c][v], im[c][v]);
+    for (int v = 0; v < 2; ++v)
+      C[(8 * tr + fr) * kPad + 8 * (tc0 + c) + 2 * fk + v] =
+          make_double2(t1[c][v] - t2[c][v], t3[c][v] - t1[c][v] - t2[c][v]);
 }
 
 template <typename StoreInblock>
 __device__ __forceinline__ void pair_evd_f32(cplx* G, cplx* W, cplx* R, EvdScratch& S, int t, double floor2,
-                                             bool cross, StoreInblock store_inblock) {
+                                             bool cross, StoreInblock store_inblock, int ns_iters = 2) {
   float2* const G32 = reinterpret_cast<float2*>(W);
   float2* const R32 = G32 + kP * kPad;
   static_assert(2 * sizeof(float2) <= sizeof(cplx), "G32 and R32 share W");
@@ -375,19 +381,59 @@ __device__ __forceinline__ void pair_evd_f32(cplx* G, cplx* W, cplx* R, EvdScrat
     R[i * kPad + j] = make_double2(r.x, r.y);
   }
   __syncthreads();
-  // polar factor: R <- R (3 I - R^H R) / 2, twice (R -> W -> R)
-  for (int it = 0; it < 2; ++it) {
-    cplx* const src = it == 0 ? R : W;
-    cplx* const dst = it == 0 ? W : R;
-    gemm32c(src, src, G, true, t);  // G <- R^H R
+  // polar factor, two Newton-Schulz steps R <- R - R E / 2, E = R^H R - I:
+  // step 1 in FP64 on DMMA (E ~ 1e-7: R E must be exact to 1e-16), step 2
+  // with E ~ 1e-14 (from an FP64 R^H R) and R E in FP32 (its error, ~1e-21,
+  // is below FP64 rounding of R). R -> W -> R.
+  if (ns_iters > 0) {
+    gemm32c(R, R, G, true, true, t);  // G <- R^H R (upper tiles)
     __syncthreads();
-    for (int idx = t; idx < kP * kP; idx += 256) {
+    for (int idx = t; idx < kP * kP; idx += 256) {  // G <- 3/2 I - G / 2 (mirrored)
       const int i = idx / kP, j = idx % kP;
+      if (i > j) continue;
       const cplx s = G[i * kPad + j];
-      G[i * kPad + j] = make_double2((i == j ? 1.5 : 0.0) - 0.5 * s.x, -0.5 * s.y);
+      const cplx v = make_double2((i == j ? 1.5 : 0.0) - 0.5 * s.x, i == j ? 0.0 : -0.5 * s.y);
+      G[i * kPad + j] = v;
+      G[j * kPad + i] = make_double2(v.x, -v.y);
     }
     __syncthreads();
-    gemm32c(src, G, dst, false, t);
+    gemm32c(R, G, W, false, false, t);  // W <- R (3 I - R^H R) / 2
+    __syncthreads();
+    gemm32c(W, W, G, true, true, t);  // G <- W^H W (upper tiles)
+    __syncthreads();
+    float2* const E32 = reinterpret_cast<float2*>(R);  // R (step-1 input) is dead
+    float2* const W32 = E32 + kP * kPad;
+    for (int idx = t; idx < kP * kP; idx += 256) {
+      const int i = idx / kP, j = idx % kP;
+      const cplx w = W[i * kPad + j];
+      W32[i * kPad + j] = make_float2((float)w.x, (float)w.y);
+      if (i > j) continue;
+      const cplx s = G[i * kPad + j];
+      const float2 e = make_float2((float)(s.x - (i == j ? 1.0 : 0.0)), i == j ? 0.0f : (float)s.y);
+      E32[i * kPad + j] = e;
+      E32[j * kPad + i] = make_float2(e.x, -e.y);
+    }
+    __syncthreads();
+    float2 pe[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {  // (W E)[i][j], FP32
+      const int idx = t + 256 * h, i = idx / kP, j = idx % kP;
+      float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll 8
+      for (int k = 0; k < kP; ++k) {
+        const float2 w = W32[i * kPad + k], e = E32[k * kPad + j];
+        acc.x = fmaf(w.x, e.x, fmaf(-w.y, e.y, acc.x));
+        acc.y = fmaf(w.x, e.y, fmaf(w.y, e.x, acc.y));
+      }
+      pe[h] = acc;
+    }
+    __syncthreads();  // E32 / W32 (aliasing R) are read
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int idx = t + 256 * h, i = idx / kP, j = idx % kP;
+      const cplx w = W[i * kPad + j];
+      R[i * kPad + j] = make_double2(w.x - 0.5 * (double)pe[h].x, w.y - 0.5 * (double)pe[h].y);
+    }
     __syncthreads();
   }
 }

@@ -508,7 +508,8 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
                      const float2 ga = G32[r * kPad + q], gb = G32[(kW + r) * kPad + kW + q];
                      gblk_a[t] = make_double2(ga.x, ga.y);
                      gblk_b[t] = make_double2(gb.x, gb.y);
-                   });
+                   },
+                   probe == 5 ? 0 : 2);
       evd32 = true;
     } else {
       pair_evd_v1(SG, R, S.sc, t, tol_in, floor2, 1, cross_only_evd(active[gi], round));
