@@ -33,6 +33,7 @@ int theta_tiles(int dl, int dr);
 void jacobi_split_init();
 #ifdef MPSIM_AB_KNOBS
 void jacobi_phase_clocks(unsigned long long*, bool);
+void jacobi_w32_phase_clocks(unsigned long long*, bool);
 #endif
 void launch_jacobi_sweep(const GateDesc*, int, int, cplx*, const int*, int*, double, double, const double*, double,
                          const int*, long long, double*, int*, cplx*, cplx*, double*, cplx*, int*, int, int,
@@ -699,8 +700,10 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     // otherwise Gram-only confirmation sweep is skipped.
 #ifdef MPSIM_AB_KNOBS
     if (sweep_debug()) {
-      unsigned long long c[8];
+      unsigned long long c[8], c2[8];
       jacobi_phase_clocks(c, true);
+      jacobi_w32_phase_clocks(c2, true);
+      if (c2[6] > 0) std::memcpy(c, c2, sizeof(c));
       if (c[6] > 0)
         std::fprintf(stderr,
                      "[mpsim]   per visit (SM clocks, thread 0): total %.0f = wait %.0f + gram %.0f + test %.0f + "

@@ -246,6 +246,23 @@ __device__ __forceinline__ void rotate_pair2(const Pair2& c, const Loader2& ld, 
 
 }  // namespace
 
+#ifdef MPSIM_AB_KNOBS
+__device__ unsigned long long g_phase_clk2[8];  // as jacobi_split.cu g_phase_clk
+#define PHASE_MARK2(var) long long var = clock64()
+#define PHASE_ADD2(i, v) \
+  if (threadIdx.x == 0) atomicAdd(&g_phase_clk2[i], (unsigned long long)(v))
+void jacobi_w32_phase_clocks(unsigned long long* out, bool reset) {
+  cudaMemcpyFromSymbol(out, g_phase_clk2, sizeof(unsigned long long) * 8);
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_phase_clk2, z, sizeof(z));
+  }
+}
+#else
+#define PHASE_MARK2(var)
+#define PHASE_ADD2(i, v)
+#endif
+
 struct SweepArgs2 {
   const GateDesc* gates;
   cplx* ws;
@@ -292,7 +309,10 @@ __device__ __forceinline__ void pair_visit2(const SweepArgs2& A, int gi, int rou
   cplx* const gblk_a = A.gblk + ((long long)gi * 2 * A.max_pairs + c.ba) * (kW2 * kW2);
   cplx* const gblk_b = A.gblk + ((long long)gi * 2 * A.max_pairs + c.bb) * (kW2 * kW2);
   const int nchunks = g.m_pad / kC2;
+  PHASE_MARK2(c_g0);
   gram_pass2(S, ld, nchunks, cross_only, t);
+  PHASE_MARK2(c_g1);
+  PHASE_ADD2(2, c_g1 - c_g0);
   cplx* const SG = S.v.G;
   const double* Gx = S.u.Gx;
   if (cross_only) {
@@ -332,6 +352,8 @@ __device__ __forceinline__ void pair_visit2(const SweepArgs2& A, int gi, int rou
     if ((t & 31) == 0 && r > 0.0) atomicAdd(A.offsum + gi, r);
   }
   const bool nd = pair_needs_rotation_t<kP2, kLdG, kT2>(SG, t, tolg, floor2, A.maxoff + gi);
+  PHASE_MARK2(c_a1);
+  PHASE_ADD2(3, c_a1 - c_g1);
   auto store_inblock = [&]() {
     for (int idx = t; idx < kW2 * kW2; idx += kT2) {
       const int r = idx / kW2, q = idx % kW2;
@@ -351,6 +373,9 @@ __device__ __forceinline__ void pair_visit2(const SweepArgs2& A, int gi, int rou
   ld.issue(S.u.stage[2], (nchunks - 1) * kC2);
   pair_evd_t<kP2, kLdG, kT2>(SG, S.u.R, S.sc, t, A.tol_in, floor2, 1, cross_only_evd2(act, round));
   __syncthreads();
+  PHASE_MARK2(c_e1);
+  PHASE_ADD2(4, c_e1 - c_a1);
+  PHASE_ADD2(7, 1);
   store_inblock();
   __syncthreads();  // G (aliased by Rs) has been stored
   for (int idx = t; idx < kP2 * kP2; idx += kT2) {
@@ -359,6 +384,8 @@ __device__ __forceinline__ void pair_visit2(const SweepArgs2& A, int gi, int rou
   }
   __syncthreads();  // R (aliased by stage 0) has been read
   rotate_pair2(c, ld, S, nchunks, t);
+  PHASE_MARK2(c_r1);
+  PHASE_ADD2(5, c_r1 - c_e1);
   if (t == 0) atomicAdd(A.rotated + gi, 1);
 }
 
@@ -389,6 +416,7 @@ __global__ void __launch_bounds__(kT2, 1) jacobi_sweep_w32_kernel(SweepArgs2 A, 
     rr_pair(round, k, nb - 1, ba, bb);
     int* ra = ready + gi * 2 * A.max_pairs + ba;
     int* rb = ready + gi * 2 * A.max_pairs + bb;
+    PHASE_MARK2(c_w0);
     if (t == 0) {
       int v;
       for (;;) {
@@ -403,8 +431,13 @@ __global__ void __launch_bounds__(kT2, 1) jacobi_sweep_w32_kernel(SweepArgs2 A, 
       }
     }
     __syncthreads();
+    PHASE_MARK2(c_w1);
+    PHASE_ADD2(1, c_w1 - c_w0);
     pair_visit2(A, gi, round, k, S);
     __syncthreads();  // every thread's writes of this visit are issued
+    PHASE_MARK2(c_v1);
+    PHASE_ADD2(0, c_v1 - c_w0);
+    PHASE_ADD2(6, 1);
     if (t == 0) {
       __threadfence();
       asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(ra), "r"(round + 1) : "memory");
