@@ -104,6 +104,15 @@ static double evd32_maxoff() {
   }();
   return v;
 }
+// Relative orthogonality a pair must reach (times max(sqrt(m), 32)): 4 eps;
+// A/B: MPSIM_JTOL (in units of eps).
+static double jacobi_tol() {
+  static const double v = [] {
+    const char* e = ab_knob("MPSIM_JTOL");
+    return (e ? std::atof(e) : 4.0) * 2.220446049250313e-16;
+  }();
+  return v;
+}
 void qrp_init();
 void split_init();
 void theta_init();
@@ -641,6 +650,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     // fraction of the cost. Final orthogonality is at the tol level.
     // (phase probes 1-2 run per round; probe 4, the visit without its EVD, runs persistent)
     const bool persistent = jacobi_mode() == 4 && sweep_policy();
+    const double jtol = jacobi_tol();
     if (persistent && use_w32 && !phase_probe()) {
       s.d_sweepctl.ensure(sizeof(int) * (1 + 2 * (size_t)ng * max_nb));
       launch_jacobi_sweep_w32(dg, ng, max_nb / 4, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, 4.0 * kEps,
@@ -652,14 +662,14 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     } else if (persistent && cluster_policy() && !phase_probe()) {
       s.d_sweepctl.ensure(sizeof(int) * (1 + 2 * (size_t)ng * max_nb));
       launch_jacobi_sweep_cl(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (const int*)s.d_active.p + ng, n_list,
-                             group_policy(), (int*)s.d_rot.p, 4.0 * kEps, 2.0 * kEps, (const double*)s.d_frob.p,
+                             group_policy(), (int*)s.d_rot.p, jtol, 2.0 * kEps, (const double*)s.d_frob.p,
                              kFloorRel2, (const int*)s.d_perm.p, perm_stride, (double*)s.d_maxoff.p,
                              (int*)s.d_need.p, (double*)s.d_offsum.p, (cplx*)s.d_gblk.p, (int*)s.d_sweepctl.p, st);
       s.launches += 1;
       ++s.jacobi_launches;
     } else if (persistent) {
       s.d_sweepctl.ensure(sizeof(int) * (1 + 2 * (size_t)ng * max_nb));
-      launch_jacobi_sweep(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, 4.0 * kEps, 2.0 * kEps,
+      launch_jacobi_sweep(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, jtol, 2.0 * kEps,
                           (const double*)s.d_frob.p, kFloorRel2, (const int*)s.d_perm.p, perm_stride,
                           (double*)s.d_maxoff.p, (int*)s.d_need.p, (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p,
                           (double*)s.d_offsum.p, (cplx*)s.d_gblk.p, (int*)s.d_sweepctl.p, phase_probe(), l2hint_policy(), st);
@@ -670,7 +680,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       // (per-round launches: A/B and phase probes)
       {
         launch_jacobi_round_split(dg, ng, max_nb / 2, ws, (const int*)s.d_active.p, (int*)s.d_rot.p, round,
-                                  4.0 * kEps, 2.0 * kEps, (const double*)s.d_frob.p, kFloorRel2,
+                                  jtol, 2.0 * kEps, (const double*)s.d_frob.p, kFloorRel2,
                                   (const int*)s.d_perm.p, perm_stride, (double*)s.d_maxoff.p, (int*)s.d_need.p,
                                   (cplx*)s.d_gbuf.p, (cplx*)s.d_rbuf.p, (double*)s.d_offsum.p, jacobi_mode() - 2,
                                   (cplx*)s.d_gblk.p, phase_probe(), st);

@@ -123,12 +123,9 @@ __device__ __forceinline__ void pair_evd_t(cplx* G, cplx* R, EvdScratchT<kPP>& S
         double cs = 1.0, sn = 0.0;
         cplx ph = make_double2(1.0, 0.0);
         if (c2 > 0.0 && c2 > tol2 * fabs(a * b) && fmin(a, b) > floor2) {
-          // the angle in FP32 (its own rsqrt, off the FP64 rsqrt's latency);
-          // ph and cs, which make J unitary, in FP64
           const double inv_c = rsqrt(c2);
-          const bool f32 = c2 > 1e-30 && c2 < 1e30;  // (float range; else from inv_c)
-          const float zf = f32 ? (float)(b - a) * 0.5f * rsqrtf((float)c2) : (float)((b - a) * 0.5 * inv_c);
           ph = make_double2(g.x * inv_c, -g.y * inv_c);  // e^{-i phi}, |ph| = 1 to rounding
+          const float zf = (float)((b - a) * 0.5 * inv_c);
           const float az = fabsf(zf);
           const float tf = copysignf(1.0f, zf) / (az > 1e18f ? 2.0f * az : az + sqrtf(1.0f + zf * zf));
           const double tt = (double)tf;
