@@ -113,6 +113,17 @@ static double jacobi_tol() {
   }();
   return v;
 }
+void launch_orthonormalize(const GateDesc*, int, int, int, cplx*, const double*, const int*, long long,
+                           const GateOut*, const double*, double, float2*, float2*, long long, cudaStream_t);
+// First-order orthonormalisation of the kept vectors before the split
+// (split.cu); A/B: MPSIM_ORTHO=0 skips it.
+static bool ortho_policy() {
+  static const bool on = [] {
+    const char* v = ab_knob("MPSIM_ORTHO");
+    return !(v != nullptr && std::string(v) == "0");
+  }();
+  return on;
+}
 void qrp_init();
 void split_init();
 void theta_init();
@@ -514,7 +525,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
                              std::to_string(kMaxSvdN) + " this build supports (bond dimension <= 8192)");
   long long ws_elems = 0;
   int max_tiles = 1, max_nb = 2, max_m = 1, max_n = 1;
-  int max_n0 = 1, qr_n_pad = 0, qr_m_pad = 0, qr_jm_pad = 0, max_out_m = 1;
+  int max_n0 = 1, qr_n_pad = 0, qr_m_pad = 0, qr_jm_pad = 0, max_out_m = 1, max_out_m_pad = 1;
   bool any_pre2 = false;
   for (const GateDesc& d : descs) {
     long long end = d.x0_off + (long long)d.n_pad * d.x0_ld;
@@ -533,6 +544,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     max_m = std::max(max_m, d.m);
     max_n = std::max(max_n, d.n);
     max_out_m = std::max(max_out_m, phase_desc(d, 4).m);
+    max_out_m_pad = std::max(max_out_m_pad, phase_desc(d, 4).m_pad);
   }
   const long long sig_stride = ((max_n + 31) / 32) * 32;
   long long perm_stride = 32;
@@ -786,6 +798,19 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     s.launches += 1 + npan;
   }
   const GateDesc* dout = dph + 4 * ng;
+  if (ortho_policy()) {
+    // kept vectors orthonormalised to O(E^2) before the split (split.cu)
+    long long kcap = 1;
+    for (const GateDesc& d : descs) kcap = std::max<long long>(kcap, std::min<long long>(d.n, d.max_bond));
+    const long long tstride = (long long)max_out_m_pad * kcap;
+    s.d_fcorr.ensure(sizeof(float2) * (size_t)ng * kcap * kcap);
+    s.d_tcorr.ensure(sizeof(float2) * (size_t)ng * tstride);
+    launch_orthonormalize(dout, ng, max_out_m, (int)kcap, ws, (const double*)s.d_sigma.p, (const int*)s.d_order.p,
+                          sig_stride, (const GateOut*)s.d_out.p, (const double*)s.d_frob.p, kFloorRel2,
+                          (float2*)s.d_fcorr.p, (float2*)s.d_tcorr.p, tstride, st);
+    check_launch("orthonormalize");
+    s.launches += 3;
+  }
   launch_write_factors(dout, ng, max_out_m, max_n, max_n0, ws, (const double*)s.d_sigma.p, (const int*)s.d_order.p, sig_stride,
                        (const GateOut*)s.d_out.p, (const double*)s.d_frob.p, kFloorRel2, st);
   check_launch("write_factors");

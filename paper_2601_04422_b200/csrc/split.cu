@@ -244,8 +244,137 @@ __global__ void __launch_bounds__(256, 2) cross_gram_kernel(const GateDesc* __re
   }
 }
 
+// ---- orthonormalisation of the kept vectors (first order, in place).
+// The converged Jacobi vectors are orthogonal only to the sweep tolerance
+// (relative off-diagonals <= 4 eps max(sqrt(m), 32)), so the split
+// U (U^H theta) [f = 0] or (theta V Sigma^-2)(Sigma V^H) [f = 1] reproduces
+// theta only to that tolerance per gate, and the excess compounds over a
+// circuit (measured on the C4 window: ~1e-11 by the first truncating gate).
+// With Y the kept normalised vectors and E = Y^H Y - I (FP64, ~1e-14),
+// Y <- Y (I - E / 2) makes them orthonormal to O(E^2); both split formulas
+// then apply the exact projector onto span(Y). In terms of the sigma-scaled
+// operand: X_j <- X_j - sum_i X_i F[i][j], F[i][j] = E[i][j] sigma_j /
+// (2 sigma_i); the product is a first-order term, computed in FP32.
+__global__ void __launch_bounds__(256, 2) ortho_gram_kernel(const GateDesc* __restrict__ gates,
+                                                            const cplx* __restrict__ ws,
+                                                            const double* __restrict__ sigma,
+                                                            const int* __restrict__ order, long long sig_stride,
+                                                            const GateOut* __restrict__ out,
+                                                            const double* __restrict__ frob2, double floor_rel2,
+                                                            float2* __restrict__ fbuf, int kcap) {
+  const GateDesc& g = gates[blockIdx.z];
+  const int k = out[blockIdx.z].k;
+  const int a0 = blockIdx.y * 32, b0 = blockIdx.x * 32;
+  if (a0 >= k || b0 >= k) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CrossSmem& S = *reinterpret_cast<CrossSmem*>(smem_raw);
+  const double floor2 = floor_rel2 * frob2[blockIdx.z];
+  const double* sg = sigma + blockIdx.z * sig_stride;
+  const int* od = order + blockIdx.z * sig_stride;
+  const cplx* X = ws + g.ws_off;
+  const int t = threadIdx.x;
+  auto xvec = [&](int j) { return X + (long long)(g.pre == 2 ? j : od[j]) * g.m_pad; };
+  auto pa = [&](int v) { return xvec(min(a0 + v, k - 1)); };
+  auto qb = [&](int v) { return xvec(min(b0 + v, k - 1)); };
+  pg::Loader ld;
+  ld.init(pa, qb, g.m_pad, g.m_pad, t);
+  pg::cross_gram(ld, S.u.buf, S.u.Wx, S.W, 33, 0, g.m_pad, t);
+  float2* F = fbuf + (long long)blockIdx.z * kcap * kcap;
+  for (int idx = t; idx < 32 * 32; idx += 256) {
+    const int i = a0 + idx / 32, j = b0 + idx % 32;
+    if (i >= k || j >= k) continue;
+    const double si = sg[i], sj = sg[j];
+    float2 f = make_float2(0.0f, 0.0f);
+    if (si * si > floor2 && sj * sj > floor2) {
+      const cplx c = S.W[(idx / 32) * 33 + idx % 32];
+      const double e_re = c.x / (si * sj) - (i == j ? 1.0 : 0.0), e_im = i == j ? 0.0 : c.y / (si * sj);
+      const double r = 0.5 * sj / si;
+      f = make_float2((float)(r * e_re), (float)(r * e_im));
+    }
+    F[(long long)i * kcap + j] = f;
+  }
+}
+
+// T_j[e] = sum_i X_i[e] F[i][j] (FP32) for a 32 x 32 tile of (rows e, kept j).
+__global__ void __launch_bounds__(256) ortho_tmul_kernel(const GateDesc* __restrict__ gates,
+                                                         const cplx* __restrict__ ws,
+                                                         const int* __restrict__ order, long long sig_stride,
+                                                         const GateOut* __restrict__ out,
+                                                         const float2* __restrict__ fbuf, int kcap,
+                                                         float2* __restrict__ tbuf, long long tstride) {
+  const GateDesc& g = gates[blockIdx.z];
+  const int k = out[blockIdx.z].k;
+  const int e0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  if (j0 >= k || e0 >= g.m) return;
+  __shared__ float2 xs[32][33], fs[32][33];
+  const int* od = order + blockIdx.z * sig_stride;
+  const cplx* X = ws + g.ws_off;
+  const float2* F = fbuf + (long long)blockIdx.z * kcap * kcap;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+  for (int i0 = 0; i0 < k; i0 += 32) {
+    for (int ii = ty; ii < 32; ii += 8) {
+      const int i = i0 + ii, e = e0 + tx;
+      float2 xv = make_float2(0.f, 0.f);
+      if (i < k && e < g.m) {
+        const cplx x = xs_get(X + (long long)(g.pre == 2 ? i : od[i]) * g.m_pad, g.m_pad, e);
+        xv = make_float2((float)x.x, (float)x.y);
+      }
+      xs[ii][tx] = xv;  // [i][e]
+      fs[ii][tx] = (i < k && j0 + tx < k) ? F[(long long)i * kcap + j0 + tx] : make_float2(0.f, 0.f);  // [i][j]
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int ii = 0; ii < 32; ++ii) {
+      const float2 x = xs[ii][tx];
+#pragma unroll
+      for (int h = 0; h < 4; ++h) {
+        const float2 f = fs[ii][ty + 8 * h];
+        acc[h].x = fmaf(x.x, f.x, fmaf(-x.y, f.y, acc[h].x));
+        acc[h].y = fmaf(x.x, f.y, fmaf(x.y, f.x, acc[h].y));
+      }
+    }
+    __syncthreads();
+  }
+  float2* T = tbuf + blockIdx.z * tstride;
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    const int j = j0 + ty + 8 * h, e = e0 + tx;
+    if (j < k && e < g.m) T[(long long)j * g.m_pad + e] = acc[h];
+  }
+}
+
+// X_j[e] -= T_j[e] over the kept vectors.
+__global__ void __launch_bounds__(256) ortho_apply_kernel(const GateDesc* __restrict__ gates, cplx* __restrict__ ws,
+                                                          const int* __restrict__ order, long long sig_stride,
+                                                          const GateOut* __restrict__ out,
+                                                          const float2* __restrict__ tbuf, long long tstride) {
+  const GateDesc& g = gates[blockIdx.z];
+  const int k = out[blockIdx.z].k;
+  const int j = blockIdx.y, e = blockIdx.x * 256 + threadIdx.x;
+  if (j >= k || e >= g.m) return;
+  const int* od = order + blockIdx.z * sig_stride;
+  double* x = reinterpret_cast<double*>(ws + g.ws_off + (long long)(g.pre == 2 ? j : od[j]) * g.m_pad);
+  const float2 d = tbuf[blockIdx.z * tstride + (long long)j * g.m_pad + e];
+  x[e] -= (double)d.x;
+  x[g.m_pad + e] -= (double)d.y;
+}
+
+void launch_orthonormalize(const GateDesc* d_gates, int n_gates, int max_m, int kcap, cplx* ws, const double* sigma,
+                           const int* order, long long sig_stride, const GateOut* d_out, const double* frob2,
+                           double floor_rel2, float2* fbuf, float2* tbuf, long long tstride, cudaStream_t st) {
+  const int kb = (kcap + 31) / 32;
+  ortho_gram_kernel<<<dim3(kb, kb, n_gates), 256, sizeof(CrossSmem), st>>>(d_gates, ws, sigma, order, sig_stride,
+                                                                          d_out, frob2, floor_rel2, fbuf, kcap);
+  ortho_tmul_kernel<<<dim3((max_m + 31) / 32, kb, n_gates), 256, 0, st>>>(d_gates, ws, order, sig_stride, d_out,
+                                                                         fbuf, kcap, tbuf, tstride);
+  ortho_apply_kernel<<<dim3((max_m + 255) / 256, kcap, n_gates), 256, 0, st>>>(d_gates, ws, order, sig_stride,
+                                                                             d_out, tbuf, tstride);
+}
+
 void split_init() {
   cudaFuncSetAttribute(cross_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CrossSmem));
+  cudaFuncSetAttribute(ortho_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CrossSmem));
 }
 
 void launch_norms(const GateDesc* d_gates, int n_gates, int max_n, const cplx* ws, double* sigma,

@@ -90,8 +90,9 @@ def test_c3_full_size_against_fixture(gpu):
 @pytest.mark.slow
 def test_c4_window_reaching_chi1024_against_fixture(gpu):
     # Open item: on this window (six truncating gates at chi =
-    # 1024, discarded weights up to 0.27) the GPU's weights drift from the
-    # oracle's by up to 2.2e-10 relative and amplitudes by up to 2.9e-8
-    # (median 5.5e-10), growing gate by gate from 1e-11, while LAPACK's zgesdd
-    # and zgesvj agree to 5e-14 / 7e-12; kept ranks and <Z>, <X> (1e-11) match.
-    _run(gpu, "c4_window", known_deviation="C4 window: GPU weights / amplitudes beyond 1e-10 (DESIGN.md §2)")
+    # 1024, discarded weights up to 0.27) the GPU's weights agree with the
+    # oracle's to 9e-12 and <Z>, <X> to 1.3e-12, but amplitudes differ by up
+    # to 1.7e-9 (median 1.9e-10), while LAPACK's zgesdd and zgesvj agree to
+    # 7e-12 (before the kept-vector orthonormalisation of split.cu: 2.2e-10 /
+    # 2.9e-8).
+    _run(gpu, "c4_window", known_deviation="C4 window: GPU amplitudes beyond 1e-10 (DESIGN.md §2)")
