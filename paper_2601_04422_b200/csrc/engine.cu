@@ -883,7 +883,7 @@ void run_layer(State& s, const std::vector<G2>& two, const std::vector<G1>& one,
       (long long)(std::min<double>((double)free_b * 0.6 + (double)s.ws.bytes, 64e9) / sizeof(cplx));
   std::vector<GateDesc> chunk;
   std::vector<const G2*> chunk_src;
-  long long off = 0;
+  long long off = 0, extra_used = 0;
   auto flush = [&]() {
     if (chunk.empty()) return;
     std::vector<GateOut> outs;
@@ -907,6 +907,7 @@ void run_layer(State& s, const std::vector<G2>& two, const std::vector<G1>& one,
     chunk.clear();
     chunk_src.clear();
     off = 0;
+    extra_used = 0;
   };
   for (const G2& g : two) {
     GateDesc d{};
@@ -933,9 +934,15 @@ void run_layer(State& s, const std::vector<G2>& two, const std::vector<G1>& one,
     const int pre = use_qr_precondition(d.n);
     GateDesc probe = d;
     const long long sz = desc_layout(probe, 0, pre);
-    if (!chunk.empty() && off + sz > budget_elems) flush();
+    long long extra = 0;
+    if (ortho_policy()) {  // the split's orthonormalisation buffers (FP32 complex: half a cplx each)
+      const long long kc = std::min<long long>(d.n, d.max_bond), mo = phase_desc(probe, 4).m_pad;
+      extra = (kc * kc + mo * kc + 1) / 2;
+    }
+    if (!chunk.empty() && off + extra_used + sz + extra > budget_elems) flush();
     desc_layout(d, off, pre);
     off += sz;
+    extra_used += extra;
     chunk.push_back(d);
     chunk_src.push_back(&g);
   }
