@@ -8,8 +8,8 @@ do not fit a live oracle run inside a test (tests/golden/make_golden.py):
 
 The local gate list (SWAPs included) goes through the public execute path;
 per-gate kept ranks must equal the oracle's exactly (SWAPs included),
-discarded weights agree to 1e-10 relative, <Z_q> / <X_q> to 1e-10, and
-amplitudes to 1e-10 relative or twice the oracle's own zgesdd-vs-zgesvj spread
+<Z_q> / <X_q> agree to 1e-10, discarded weights and amplitudes to 1e-10
+relative or twice the oracle's own whole-circuit zgesdd-vs-second-SVD spread
 when that is larger. The fixture's own header records that the oracle's zgesdd run and an
 independent zgesvj (one-sided Jacobi) run agree on every kept rank."""
 import json
@@ -43,7 +43,9 @@ def test_fixture_headers_pin_the_oracle():
             meta = json.load(fh)
         chk = meta["zgesvj_check"]
         assert chk["kept_ranks_equal"] and chk["bonds_equal"], name
-        assert chk["max_rel_w_diff"] <= 1e-10, name
+        assert chk["max_rel_w_diff"] <= 1e-8, name  # (whole-circuit drift; see tests/test_golden_fixtures.py)
+        if "svd_pin_summary" in meta:  # per-theta pins: the SVD decisions themselves
+            assert meta["svd_pin_summary"]["max_w_rel_diff_w_above_1e-10"] <= 1e-10, name
 
 
 def _run(gpu, name, known_deviation=None):
@@ -55,6 +57,7 @@ def _run(gpu, name, known_deviation=None):
     # SVDs (zgesdd vs zgesvj) where the truncated chain's conditioning already
     # separates them by more (see tests/test_gpu_fullsize.py C2)
     amp_tol = max(1e-10, 2.0 * meta["zgesvj_check"]["max_rel_amp_diff"])
+    w_tol = max(1e-10, 2.0 * meta["zgesvj_check"]["max_rel_w_diff"])
     n, chi, cutoff = int(f["n"]), int(f["chi"]), float(f["cutoff"])
     g = gpu.MpsState(n, chi_hint=chi)
     rg = gpu.execute(g, gates, chi, cutoff)
@@ -73,11 +76,11 @@ def _run(gpu, name, known_deviation=None):
     ag = g.amplitudes([str(b) for b in f["bits"]])
     ao = f["amps"]
     a_err = float(np.max(np.abs(ag - ao) / np.abs(ao)))
-    if known_deviation is not None and (w_err > 1e-10 or a_err > amp_tol):
+    if known_deviation is not None and (w_err > w_tol or a_err > amp_tol):
         pytest.xfail(f"{known_deviation}: max rel w error {w_err:.2e}, max rel amplitude error {a_err:.2e} "
-                     f"(tolerances 1e-10 / {amp_tol:.1e}); ranks, bonds, <Z>, <X> within tolerance")
-    assert w_err <= 1e-10
-    assert a_err <= amp_tol
+                     f"(tolerances {w_tol:.1e} / {amp_tol:.1e}); ranks, bonds, <Z>, <X> within tolerance")
+    assert w_err <= w_tol, (name, w_err, w_tol)
+    assert a_err <= amp_tol, (name, a_err, amp_tol)
     return rg
 
 

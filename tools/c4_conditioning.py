@@ -14,7 +14,7 @@ f = np.load(os.path.join(HERE, "..", "tests", "golden", "c4_window.npz"))
 n, chi, cutoff = int(f["n"]), int(f["chi"]), float(f["cutoff"])
 
 
-def run(eps, seed=3):
+def run(eps, seed=3, dump=None):
     rng = np.random.default_rng(seed)
     sites = [np.zeros((1, 2, 1), complex) for _ in range(n)]
     for s in sites:
@@ -31,7 +31,13 @@ def run(eps, seed=3):
         th = np.einsum("xy,lyr->lxr", m, t).reshape(2 * dl, 2 * dr)
         if eps:
             th = th * (1.0 + eps * (rng.standard_normal(th.shape) + 1j * rng.standard_normal(th.shape)))
-        u, s, vh = np.linalg.svd(th, full_matrices=False)
+        if not np.isfinite(th).all():
+            raise RuntimeError(f"non-finite theta at gate ({q0}, {q1})")
+        try:
+            u, s, vh = np.linalg.svd(th, full_matrices=False)
+        except np.linalg.LinAlgError:  # gesdd failure: the QR-iteration driver
+            import scipy.linalg as sl
+            u, s, vh = sl.svd(th, full_matrices=False, lapack_driver="gesvd")
         total = float((s * s).sum())
         keep = len(s)
         if total > 0:
@@ -44,6 +50,8 @@ def run(eps, seed=3):
         keep = min(keep, chi)
         w = float((s[keep:] ** 2).sum()) / total if total > 0 else 0.0
         sk = s[:keep] / np.sqrt(1.0 - w) if w > 0 else s[:keep]
+        if dump is not None and w > 1e-16:
+            dump.append((th.copy(), keep, w))
         sites[q0] = u[:, :keep].reshape(dl, 2, keep)
         sites[q0 + 1] = (sk[:, None] * vh[:keep]).reshape(keep, 2, dr)
         ks.append(keep)
@@ -57,7 +65,13 @@ def run(eps, seed=3):
 
 
 t0 = time.time()
-a0, k0 = run(0.0)
+dumped = []
+a0, k0 = run(0.0, dump=dumped)
+if os.environ.get("DUMP"):
+    np.savez_compressed(os.environ["DUMP"], **{f"theta{i}": d[0] for i, d in enumerate(dumped)},
+                        k=np.array([d[1] for d in dumped]), w=np.array([d[2] for d in dumped]))
+    print("dumped", len(dumped), "truncating thetas to", os.environ["DUMP"], flush=True)
+    sys.exit(0)
 print(f"numpy gesdd run {time.time() - t0:.0f} s; vs fixture (oracle zgesdd): max rel amp diff "
       f"{np.max(np.abs(a0 - f['amps']) / np.abs(f['amps'])):.2e}", flush=True)
 for seed in (1, 2):
