@@ -7,10 +7,11 @@ do not fit a live oracle run inside a test (tests/golden/make_golden.py):
                  centre bond reaches chi = 1024, then two more
 
 The local gate list (SWAPs included) goes through the public execute path;
-per-gate kept ranks must equal the oracle's exactly (SWAPs included),
-<Z_q> / <X_q> agree to 1e-10, discarded weights and amplitudes to 1e-10
-relative or twice the oracle's own whole-circuit zgesdd-vs-second-SVD spread
-when that is larger. The fixture's own header records that the oracle's zgesdd run and an
+per-gate kept ranks must equal the oracle's exactly (SWAPs included);
+discarded weights, amplitudes and <Z_q> / <X_q> agree to 1e-10 (relative,
+relative, absolute) or to twice the oracle's own whole-circuit spread between
+zgesdd and a second SVD when the header records a larger one (C3: after 1302
+truncating gates two correct SVDs leave amplitudes 4.4x apart). The fixture's own header records that the oracle's zgesdd run and an
 independent zgesvj (one-sided Jacobi) run agree on every kept rank."""
 import json
 import os
@@ -68,10 +69,13 @@ def _run(gpu, name, known_deviation=None):
     nz = w > 1e-16  # below: rank-deficient rounding noise
     assert (rg["gate_w"][~nz] <= 1e-16).all()
     assert (g.bond_dims() == f["bonds"]).all()
+    chk = meta["zgesvj_check"]
+    zx_tol = {id(PZ): max(1e-10, 2.0 * chk.get("max_abs_z_diff", 0.0)),
+              id(PX): max(1e-10, 2.0 * chk.get("max_abs_x_diff", 0.0))}
     for q, z, x in zip(f["qs"], f["z"], f["x"]):
         for op, ref in ((PZ, z), (PX, x)):
             got = g.expect_1q(op, int(q))
-            assert abs(got - ref) <= 1e-10 * max(1.0, abs(ref)), (name, int(q), got, ref)
+            assert abs(got - ref) <= zx_tol[id(op)] * max(1.0, abs(ref)), (name, int(q), got, ref, zx_tol[id(op)])
     w_err = float(np.max(np.abs(rg["gate_w"][nz] - w[nz]) / w[nz])) if nz.any() else 0.0
     ag = g.amplitudes([str(b) for b in f["bits"]])
     ao = f["amps"]
@@ -92,10 +96,7 @@ def test_c3_full_size_against_fixture(gpu):
 
 @pytest.mark.slow
 def test_c4_window_reaching_chi1024_against_fixture(gpu):
-    # Open item: on this window (six truncating gates at chi =
-    # 1024, discarded weights up to 0.27) the GPU's weights agree with the
-    # oracle's to 9e-12 and <Z>, <X> to 1.3e-12, but amplitudes differ by up
-    # to 1.7e-9 (median 1.9e-10), while LAPACK's zgesdd and zgesvj agree to
-    # 7e-12 (before the kept-vector orthonormalisation of split.cu: 2.2e-10 /
-    # 2.9e-8).
-    _run(gpu, "c4_window", known_deviation="C4 window: GPU amplitudes beyond 1e-10 (DESIGN.md §2)")
+    # (weights 7e-14, <Z>/<X> 1.5e-14, amplitudes 7e-11 measured; before the
+    # quadratic-phase exit was tightened to 1e-12 and the kept-vector
+    # orthonormalisation was added: 2.2e-10 / 1.5e-11 / 2.9e-8)
+    _run(gpu, "c4_window")
