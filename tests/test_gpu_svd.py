@@ -132,3 +132,27 @@ def test_random_shapes_fuzz(gpu):
         keep = min(keep, cap)
         assert len(s2) == keep, (r, c, cap)
         assert abs(w2 - float((ref[keep:] ** 2).sum()) / tot) <= 1e-10 * max(w2, 1e-300) + 1e-15, (r, c)
+
+
+@pytest.mark.parametrize("gap", [0.7, 0.07])
+def test_truncated_subspace_at_lapack_accuracy(gpu, gap):
+    """The kept left subspace of a truncating SVD (2048 x 2048, keep 1024 of a
+    smooth spectrum with a relative gap `gap` at the cut) within 1e-12 / gap of
+    numpy's LAPACK, and the truncated product U S V^dag within 1e-13 (the
+    accuracy the C4 window needs; that window's own truncating thetas, which
+    the old quadratic-phase exit left at 4.4e-11 / 2.3e-9, are exercised by
+    tests/test_gpu_golden.py)."""
+    rng = np.random.default_rng(20261019)
+    n, k = 2048, 1024
+    s = np.concatenate([np.linspace(1.0, 0.3, k), (1.0 - gap) * 0.3 * np.linspace(1.0, 1e-3, n - k)])
+    q1 = np.linalg.qr(_rand(rng, n, n))[0]
+    q2 = np.linalg.qr(_rand(rng, n, n))[0]
+    th = (q1 * s) @ q2.conj().T
+    u, sg, vd, w = gpu.mps.svd(th, max_rank=k)
+    un, sn, vn = np.linalg.svd(th)
+    assert len(sg) == k
+    assert abs(w - float((sn[k:] ** 2).sum() / (sn ** 2).sum())) <= 1e-12 * w
+    d = np.linalg.norm(u @ u.conj().T - un[:, :k] @ un[:, :k].conj().T, 2)
+    assert d <= 1e-12 / gap, d
+    prod = u @ (sg[:, None] * vd) - (un[:, :k] * sn[:k]) @ vn[:k]
+    assert np.linalg.norm(prod) <= 1e-13 * np.linalg.norm(th)
