@@ -729,9 +729,9 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
     }
     // A gate is done when no pair rotated, or (DMMA kernel, which reports the
     // largest relative off-diagonal it saw) when every pair entered this sweep
-    // with off <= kQuadFinish: cyclic Jacobi converges quadratically there, so
-    // the rotations of this sweep leave off ~ kQuadFinish^2 << tol and the
-    // otherwise Gram-only confirmation sweep is skipped.
+    // with off <= kQuadFinish (1e-12, within ~50x of the test's tolerance):
+    // the rotations of this sweep then leave the pairs at the rounding level
+    // and the otherwise Gram-only confirmation sweep is skipped.
 #ifdef MPSIM_AB_KNOBS
     if (sweep_debug()) {
       unsigned long long c[8], c2[8];
