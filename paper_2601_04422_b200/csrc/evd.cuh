@@ -49,8 +49,13 @@ __device__ __forceinline__ void rr_pair(int step, int k, int M, int& a, int& b) 
 template <int kPP, int kLd, int kT>
 __device__ __forceinline__ bool pair_needs_rotation_t(const cplx* G, int t, double tolg, double floor2,
                                                       double* maxoff = nullptr) {
+  // |G_ij|^2 > tolg^2 G_ii G_jj in FP64 without square roots or divisions
+  // (the FP64 units are shared with the other CTAs' DMMA); the squared ratio
+  // for maxoff, which only steers sweep policy, in FP32 when in range
   bool need = false;
-  double mx = 0.0;
+  float mx2 = 0.0f;
+  double mx2d = 0.0;
+  const double tolg2 = tolg * tolg;
 #pragma unroll
   for (int h = 0; h < (kPP * kPP / 4) / kT; ++h) {
     const int blk = t + h * kT;
@@ -61,17 +66,26 @@ __device__ __forceinline__ bool pair_needs_rotation_t(const cplx* G, int t, doub
       for (int b = 0; b < 2; ++b) {
         const int i = 2 * ip + a, j = 2 * jp + b;
         if (i < j) {
-          const double gij = sqrt(cabs2(G[i * kLd + j]));
+          const double g2 = cabs2(G[i * kLd + j]);
           const double gii = G[i * kLd + i].x, gjj = G[j * kLd + j].x;
-          if (gij > 0.0 && fmin(gii, gjj) > floor2) {
-            const double rel = gij / sqrt(gii * gjj);
-            mx = fmax(mx, rel);
-            if (rel > tolg) need = true;
+          if (g2 > 0.0 && fmin(gii, gjj) > floor2) {
+            const double d = gii * gjj;
+            if (g2 > tolg2 * d) need = true;
+            if (maxoff != nullptr) {
+              // FP32 when d is in (1e-12, 1e30): g2 <= d, and a g2 below
+              // FP32's normal range then means a squared ratio < 1e-26, under
+              // every threshold the host applies (the smallest: 1e-24)
+              if (d < 1e30 && d > 1e-12)
+                mx2 = fmaxf(mx2, __fdividef((float)g2, (float)d));
+              else
+                mx2d = fmax(mx2d, g2 / d);
+            }
           }
         }
       }
   }
   if (maxoff != nullptr) {
+    double mx = sqrt(fmax((double)mx2, mx2d));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((t & 31) == 0 && mx > 0.0)

@@ -464,7 +464,11 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
     // turns it into the sweep's rms off-norm (cross-only EVD policy)
     const int i = t >> 4, j = kW + (t & 15);
     const double gii = SG[i * kPad + i].x, gjj = SG[j * kPad + j].x;
-    double r = (fmin(gii, gjj) > floor2) ? cabs2(SG[i * kPad + j]) / (gii * gjj) : 0.0;
+    // (policy input only: the squared ratio in FP32 when in range)
+    const double c2 = cabs2(SG[i * kPad + j]), d = gii * gjj;
+    double r = 0.0;
+    if (fmin(gii, gjj) > floor2)
+      r = (d < 1e30 && d > 1e-12) ? (double)__fdividef((float)c2, (float)d) : c2 / d;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
     if (lane == 0 && r > 0.0) atomicAdd(offsum + gi, r);
