@@ -410,6 +410,14 @@ __device__ __forceinline__ void pair_evd_f32(cplx* G, cplx* W, cplx* R, EvdScrat
     __syncthreads();
     gemm32c(R, G, W, false, false, t);  // W <- R (3 I - R^H R) / 2
     __syncthreads();
+    if (ns_iters == 1) {  // (A/B: one step only, R unitary to ~1e-14)
+      for (int idx = t; idx < kP * kP; idx += 256) {
+        const int i = idx / kP, j = idx % kP;
+        R[i * kPad + j] = W[i * kPad + j];
+      }
+      __syncthreads();
+      return;
+    }
     gemm32c(W, W, G, true, true, t);  // G <- W^H W (upper tiles)
     __syncthreads();
     float2* const E32 = reinterpret_cast<float2*>(R);  // R (step-1 input) is dead

@@ -383,6 +383,7 @@ struct RoundArgs {
   int probe;
   int* blkok;  // per block: gblk holds its exact in-block Gram (persistent sweeps; nullable)
   int l2hint;  // L2 priorities: 0 none; 1 rotation loads / stores evict_first; 2 and Gram loads evict_last
+  int ns_iters = 2;  // Newton-Schulz steps of the FP32 pair EVD's polar factor (A/B)
 };
 
 // One pair visit (block pair k of gate gi in tournament round `round`).
@@ -513,7 +514,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
                      gblk_a[t] = make_double2(ga.x, ga.y);
                      gblk_b[t] = make_double2(gb.x, gb.y);
                    },
-                   probe == 5 ? 0 : 2);
+                   probe == 5 ? 0 : A.ns_iters);
       evd32 = true;
     } else {
       pair_evd_v1(SG, R, S.sc, t, tol_in, floor2, 1, cross_only_evd(active[gi], round));
@@ -914,6 +915,10 @@ static RoundArgs make_args(const GateDesc* d_gates, cplx* ws, const int* d_activ
   a.probe = probe;
   a.blkok = blkok;
   a.l2hint = l2hint;
+  {
+    const char* e = ab_knob("MPSIM_NS_ITERS");
+    a.ns_iters = e ? std::atoi(e) : 2;
+  }
   return a;
 }
 
