@@ -127,6 +127,9 @@ def main():
         X = th @ Q
     elif variant == "qrcp":
         X = sl.qr(th, pivoting=True, mode='economic')[1].conj().T.copy()
+    elif variant == "qrcp2":  # Drmac-Veselic: QRCP, then an (unpivoted) QR of R^H
+        X = sl.qr(th, pivoting=True, mode='economic')[1].conj().T.copy()
+        X = np.linalg.qr(X)[1].conj().T.copy()
     else:
         X = np.linalg.qr(th)[1].conj().T.copy()
         for _ in range({"qr2": 1, "qr3": 2, "qr4": 3}.get(variant, 0)):
