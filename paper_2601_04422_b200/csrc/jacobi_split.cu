@@ -558,7 +558,10 @@ __global__ void __launch_bounds__(256, 3) jacobi_gram_kernel(RoundArgs A, int ro
 // CTA's pair EVD overlaps the DMMA phases of its neighbours. Deadlock-free:
 // a visit only waits on visits claimed before it, all of which are held by
 // running CTAs.
-__global__ void __launch_bounds__(256, 4) jacobi_sweep_kernel(RoundArgs A, int n_gates, int max_rounds,
+#ifndef MPSIM_SWEEP_MINB
+#define MPSIM_SWEEP_MINB 4
+#endif
+__global__ void __launch_bounds__(256, MPSIM_SWEEP_MINB) jacobi_sweep_kernel(RoundArgs A, int n_gates, int max_rounds,
                                                               int* __restrict__ ctl) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   PairSmem& S = *reinterpret_cast<PairSmem*>(smem_raw);
