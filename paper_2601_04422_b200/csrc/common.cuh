@@ -78,8 +78,13 @@ struct GateDesc {
   // Jacobi operand X is R^H (n vectors of length m = n) and f = trans ^ 1.
   // pre = 2: a second step R^H = Q2 R2 (in the y2 area), Jacobi on R2^H, then
   // Z = Q1 [X; 0] in the QR area holds sigma * (left vectors): f = trans.
+  // pre = 4 (A/B): two more steps, R2^H = Q3 R3 (y3 area), R3^H = Q4 R4 (y4
+  // area), Jacobi on R4^H; theta = Q1 Q3 R4^H (Q2 Q4)^H, so Z = Q1 [Q3 X; 0].
   int pre, qr_m;
   long long qr_off, qr_m_pad, y2_off;
+  long long y3_off, y4_off;
+  int zsrc_ordered;  // Z formation reads its source in kept order (no permutation)
+  int pad4;
 };
 
 // Workspace layout of one descriptor starting at `off` (complex elements);
@@ -93,6 +98,9 @@ inline long long desc_layout(GateDesc& d, long long off, int pre) {
   d.pre = pre;
   d.ws_off = off;
   d.y2_off = 0;
+  d.y3_off = 0;
+  d.y4_off = 0;
+  d.zsrc_ordered = 0;
   if (pre == 0) {
     d.f = d.trans;
     d.n0 = d.n;
@@ -120,6 +128,11 @@ inline long long desc_layout(GateDesc& d, long long off, int pre) {
   d.x0_ld = d.qr_m_pad;
   d.qr_off = d.x0_off + (long long)d.n_pad * d.x0_ld;
   d.y2_off = d.qr_off + (long long)d.n_pad * d.qr_m_pad;
+  if (pre == 4) {
+    d.y3_off = d.y2_off + (long long)d.n_pad * d.m_pad;
+    d.y4_off = d.y3_off + (long long)d.n_pad * d.m_pad;
+    return 4LL * d.n_pad * d.m_pad + 2LL * d.n_pad * d.qr_m_pad;
+  }
   return 2LL * d.n_pad * d.m_pad + 2LL * d.n_pad * d.qr_m_pad;
 }
 

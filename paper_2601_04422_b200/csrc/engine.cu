@@ -134,12 +134,17 @@ void launch_qr_apply(const GateDesc*, int, int, int, cplx*, const cplx*, long lo
 // kQrMinN vectors: MPSIM_QR=2 (default) two QR steps, 1 one, 0 none.
 constexpr int kQrMinN = 128;
 constexpr int kMaxSvdN = kMaxSortN;  // derijk_kernel / truncate_kernel: one CTA, keys in shared memory
+// Default: two steps. A/B: MPSIM_QR=0, 1, 2, 4 force that many steps; -1 =
+// four for operands with >= kQr4MinN vectors (measured at chi = 512: 10 sweep
+// launches per layer instead of 11, but the bench step 1.3 % slower — the two
+// extra QR steps cost more than the sweep they save).
+constexpr int kQr4MinN = 512;
 static int qr_policy() {
   static const int v = [] {
     const char* e = ab_knob("MPSIM_QR");
     if (e == nullptr) return 2;
     const int x = std::atoi(e);
-    return x < 0 ? 0 : (x > 2 ? 2 : x);
+    return x < 0 ? -1 : (x >= 4 ? 4 : (x > 2 ? 2 : x));
   }();
   return v;
 }
@@ -501,31 +506,56 @@ static double quad_finish() {
 // operand comes from the theta kernel (src == nullptr) or from a row-major
 // device matrix (plain SVDs, bond-propagation carriers); descriptors with
 // pre = 1 are QR-preconditioned (qr_pre.cu) before the sweeps.
-int mpsim_gpu::use_qr_precondition(int n) { return n >= kQrMinN ? qr_policy() : 0; }
+int mpsim_gpu::use_qr_precondition(int n) {
+  if (n < kQrMinN) return 0;
+  const int p = qr_policy();
+  return p >= 0 ? p : (n >= kQr4MinN ? 4 : 2);
+}
 
 // The descriptor as each phase of run_two_chunk sees it (desc_layout holds the
 // Jacobi-phase view): 0 theta / load + first QR (R^H -> y2 for pre = 2),
 // 1 second QR (pre = 2 only), 2 Jacobi sweeps, 3 Z = Q1 [X; 0] (pre = 2 only),
 // 4 split epilogue.
+// pre = 4 adds 5 third QR (y3 -> R3^H into y4), 6 fourth QR (y4 -> R4^H
+// into X), 7 Q3 applied to the kept X (into y3, before phase 3 maps y3 by Q1).
 static GateDesc phase_desc(const GateDesc& d, int phase) {
   GateDesc e = d;
-  if (d.pre == 2) {
+  auto qr_on = [&](long long off) {
+    e.qr_off = off;
+    e.qr_m = d.n;
+    e.qr_m_pad = d.m_pad;
+  };
+  if (d.pre >= 2) {
     if (phase == 0) {
       e.ws_off = d.y2_off;
     } else if (phase == 1) {
-      e.qr_off = d.y2_off;
-      e.qr_m = d.n;
-      e.qr_m_pad = d.m_pad;
+      qr_on(d.y2_off);
+      if (d.pre == 4) e.ws_off = d.y3_off;
+    } else if (phase == 3 && d.pre == 4) {
+      e.ws_off = d.y3_off;  // Q3 X_kept, already in kept order
+      e.zsrc_ordered = 1;
     } else if (phase == 4) {
       e.ws_off = d.qr_off;
       e.m = d.qr_m;
       e.m_pad = (int)d.qr_m_pad;
+    } else if (phase == 5 || phase == 6 || phase == 7) {
+      if (d.pre != 4) {
+        e.pre = 0;
+      } else if (phase == 5) {
+        qr_on(d.y3_off);
+        e.ws_off = d.y4_off;
+      } else if (phase == 6) {
+        qr_on(d.y4_off);
+      } else {
+        qr_on(d.y3_off);
+      }
     }
-  } else if (phase == 1 || phase == 3) {
+  } else if (phase == 1 || phase == 3 || phase >= 5) {
     e.pre = 0;
   }
   return e;
 }
+constexpr int kPhases = 8;
 
 void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std::vector<GateOut>& outs,
                               const cplx* src, long long src_ld) {
@@ -538,11 +568,12 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   long long ws_elems = 0;
   int max_tiles = 1, max_nb = 2, max_m = 1, max_n = 1;
   int max_n0 = 1, qr_n_pad = 0, qr_m_pad = 0, qr_jm_pad = 0, max_out_m = 1, max_out_m_pad = 1;
-  bool any_pre2 = false;
+  bool any_pre2 = false, any_pre4 = false;
   for (const GateDesc& d : descs) {
     long long end = d.x0_off + (long long)d.n_pad * d.x0_ld;
     if (d.pre == 1) end = d.qr_off + (long long)d.n_pad * d.qr_m_pad;
     if (d.pre == 2) end = d.y2_off + (long long)d.n_pad * d.m_pad;
+    if (d.pre == 4) end = d.y4_off + (long long)d.n_pad * d.m_pad;
     ws_elems = std::max(ws_elems, end);
     max_n0 = std::max(max_n0, d.n0);
     if (d.pre) {
@@ -550,7 +581,8 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       qr_m_pad = std::max(qr_m_pad, (int)d.qr_m_pad);
       qr_jm_pad = std::max(qr_jm_pad, d.m_pad);
     }
-    any_pre2 = any_pre2 || d.pre == 2;
+    any_pre2 = any_pre2 || d.pre >= 2;
+    any_pre4 = any_pre4 || d.pre == 4;
     max_tiles = std::max(max_tiles, theta_tiles(d.dl, d.dr));
     max_nb = std::max(max_nb, d.nb);
     max_m = std::max(max_m, d.m);
@@ -563,24 +595,24 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   for (const GateDesc& d : descs) perm_stride = std::max<long long>(perm_stride, d.n_pad);
   s.d_perm.ensure(sizeof(int) * perm_stride * ng);
   s.ws.ensure((size_t)ws_elems * sizeof(cplx));
-  s.d_gates.ensure(sizeof(GateDesc) * 5 * ng);
+  s.d_gates.ensure(sizeof(GateDesc) * kPhases * ng);
   s.d_out.ensure(sizeof(GateOut) * ng);
   s.d_sigma.ensure(sizeof(double) * sig_stride * ng);
   s.d_order.ensure(sizeof(int) * sig_stride * ng);
   s.d_active.ensure(sizeof(int) * 2 * ng);  // active flags, then the active-gate list
   s.d_rot.ensure(sizeof(int) * ng);
   s.d_frob.ensure(sizeof(double) * ng);
-  s.h_gates.ensure(sizeof(GateDesc) * 5 * ng);
+  s.h_gates.ensure(sizeof(GateDesc) * kPhases * ng);
   s.h_out.ensure(sizeof(GateOut) * ng);
   s.h_rot.ensure(sizeof(int) * 2 * ng);
   {
     GateDesc* h = (GateDesc*)s.h_gates.p;
-    for (int ph = 0; ph < 5; ++ph)
+    for (int ph = 0; ph < kPhases; ++ph)
       for (int i = 0; i < ng; ++i) h[ph * ng + i] = phase_desc(descs[i], ph);
   }
   cudaStream_t st = s.st;
-  CK(cudaMemcpyAsync(s.d_gates.p, s.h_gates.p, sizeof(GateDesc) * 5 * ng, cudaMemcpyHostToDevice, st));
-  s.h2d_bytes += (long long)sizeof(GateDesc) * 5 * ng + (long long)sizeof(int) * ng;
+  CK(cudaMemcpyAsync(s.d_gates.p, s.h_gates.p, sizeof(GateDesc) * kPhases * ng, cudaMemcpyHostToDevice, st));
+  s.h2d_bytes += (long long)sizeof(GateDesc) * kPhases * ng + (long long)sizeof(int) * ng;
   CK(cudaMemsetAsync(s.ws.p, 0, (size_t)ws_elems * sizeof(cplx), st));
   const GateDesc* dph = (const GateDesc*)s.d_gates.p;
   const GateDesc* dg = dph + 2 * ng;  // Jacobi phase
@@ -621,6 +653,17 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
                      1, st);
     check_launch("qr_factor (second step)");
     s.launches += 2 * npan;
+  }
+  if (any_pre4) {
+    // third step (reflectors kept for Z), fourth step (scratch reflectors)
+    s.d_qrv3.ensure(sizeof(cplx) * (size_t)ng * npan * 32 * qr_jm_pad);
+    s.d_qrt3.ensure(sizeof(cplx) * (size_t)ng * npan * 32 * 32);
+    launch_qr_factor(dph + 5 * ng, ng, qr_n_pad, qr_jm_pad, ws, (cplx*)s.d_qrv3.p, qr_jm_pad, (cplx*)s.d_qrt3.p,
+                     npan, 1, st);
+    launch_qr_factor(dph + 6 * ng, ng, qr_n_pad, qr_jm_pad, ws, (cplx*)s.d_qrv2.p, qr_jm_pad, (cplx*)s.d_qrt2.p,
+                     npan, 1, st);
+    check_launch("qr_factor (third / fourth step)");
+    s.launches += 4 * npan;
   }
 
   int* h_rot = (int*)s.h_rot.p;
@@ -802,6 +845,13 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   launch_truncate(dg, ng, (double*)s.d_sigma.p, (int*)s.d_order.p, sig_stride, (GateOut*)s.d_out.p,
                   (const double*)s.d_frob.p, kFloorRel2, max_n, st);
   check_launch("truncate_kernel");
+  if (any_pre4) {  // Q3 X_kept into y3 (phase 3 then maps it by Q1)
+    launch_qr_apply(dph + 7 * ng, ng, qr_n_pad, qr_jm_pad, ws, (const cplx*)s.d_qrv3.p, qr_jm_pad,
+                    (const cplx*)s.d_qrt3.p, npan, (const int*)s.d_order.p, sig_stride, (const GateOut*)s.d_out.p,
+                    st);
+    check_launch("qr_apply (Q3)");
+    s.launches += 1 + npan;
+  }
   if (any_pre2) {
     launch_qr_apply(dph + 3 * ng, ng, qr_n_pad, qr_m_pad, ws, (const cplx*)s.d_qrv.p, qr_m_pad,
                     (const cplx*)s.d_qrt.p, npan, (const int*)s.d_order.p, sig_stride, (const GateOut*)s.d_out.p,

@@ -106,7 +106,7 @@ struct State {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   // workspaces
   DeviceBuf ws, d_gates, d_out, d_sigma, d_order, d_active, d_rot, d_frob, d_perm, d_maxoff, d_g1, q1, q2, q3, q4,
-      qbits, d_need, d_gbuf, d_rbuf, d_offsum, d_qrv, d_qrt, d_gblk, d_qrv2, d_qrt2, d_sweepctl, d_fcorr, d_tcorr;
+      qbits, d_need, d_gbuf, d_rbuf, d_offsum, d_qrv, d_qrt, d_gblk, d_qrv2, d_qrt2, d_sweepctl, d_fcorr, d_tcorr, d_qrv3, d_qrt3;
   PinnedBuf h_gates, h_out, h_rot, h_g1, h_small, h_maxoff, h_offsum, h_maps;
   DeviceBuf d_maps;  // per-gate TMA tensor maps of the theta kernel
   // instrumentation

@@ -562,7 +562,7 @@ __global__ void __launch_bounds__(256) qrp_zinit_kernel(const GateDesc* __restri
   const long long r = blockIdx.x * 256LL + threadIdx.x;
   const int j = blockIdx.y;
   if (r >= g.qr_m_pad || j >= out[blockIdx.z].k) return;
-  const cplx* X = ws + g.ws_off + (long long)order[blockIdx.z * sig_stride + j] * g.m_pad;
+  const cplx* X = ws + g.ws_off + (long long)(g.zsrc_ordered ? j : order[blockIdx.z * sig_stride + j]) * g.m_pad;
   cplx* Z = ws + g.qr_off + (long long)j * g.qr_m_pad;
   xs_set(Z, g.qr_m_pad, r, r < g.n ? xs_get(X, g.m_pad, r) : make_double2(0.0, 0.0));
 }

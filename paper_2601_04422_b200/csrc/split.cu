@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(256) copy_factor_kernel(const GateDesc* __rest
       if (j < k && e < g.m) {
         const double s = sg[j];
         if (s > 0.0) {
-          const cplx x = x_elem(g, X, g.pre == 2 ? j : od[j], e);
+          const cplx x = x_elem(g, X, g.pre >= 2 ? j : od[j], e);
           v = make_double2(x.x / s, x.y / s);
         } else {
           v = make_double2(e == j ? 1.0 : 0.0, 0.0);  // zero matrix: any unit column
@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(256) copy_factor_kernel(const GateDesc* __rest
     for (int jj = ty; jj < 32; jj += 8) {
       const int j = j0 + jj, e = e0 + tx;
       if (j < k && e < g.m) {
-        const cplx x = x_elem(g, X, g.pre == 2 ? j : od[j], e);
+        const cplx x = x_elem(g, X, g.pre >= 2 ? j : od[j], e);
         const long long off = (long long)j * g.ldv + (long long)(e / g.vsplit) * g.vsplit_ld + e % g.vsplit;
         g.v_out[off] = make_double2(o.scale * x.x, -o.scale * x.y);
       }
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(256, 2) cross_gram_kernel(const GateDesc* __re
   const cplx* X = ws + g.ws_off;
   const cplx* X0 = ws + g.x0_off;
   const int t = threadIdx.x;
-  auto xvec = [&](int j) { return X + (long long)(g.pre == 2 ? j : od[j]) * g.m_pad; };
+  auto xvec = [&](int j) { return X + (long long)(g.pre >= 2 ? j : od[j]) * g.m_pad; };
   auto x0vec = [&](int v) { return X0 + (long long)v * g.x0_ld; };
   // padding vectors (beyond n_a / n_b) load a valid vector, results discarded
   auto pa = [&](int v) { const int a = min(a0 + v, n_a - 1); return g.f == 0 ? xvec(a) : x0vec(a); };
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(256, 2) ortho_gram_kernel(const GateDesc* __re
   const int* od = order + blockIdx.z * sig_stride;
   const cplx* X = ws + g.ws_off;
   const int t = threadIdx.x;
-  auto xvec = [&](int j) { return X + (long long)(g.pre == 2 ? j : od[j]) * g.m_pad; };
+  auto xvec = [&](int j) { return X + (long long)(g.pre >= 2 ? j : od[j]) * g.m_pad; };
   auto pa = [&](int v) { return xvec(min(a0 + v, k - 1)); };
   auto qb = [&](int v) { return xvec(min(b0 + v, k - 1)); };
   pg::Loader ld;
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(256) ortho_tmul_kernel(const GateDesc* __restr
       const int i = i0 + ii, e = e0 + tx;
       float2 xv = make_float2(0.f, 0.f);
       if (i < k && e < g.m) {
-        const cplx x = xs_get(X + (long long)(g.pre == 2 ? i : od[i]) * g.m_pad, g.m_pad, e);
+        const cplx x = xs_get(X + (long long)(g.pre >= 2 ? i : od[i]) * g.m_pad, g.m_pad, e);
         xv = make_float2((float)x.x, (float)x.y);
       }
       xs[ii][tx] = xv;  // [i][e]
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(256) ortho_apply_kernel(const GateDesc* __rest
   const int j = blockIdx.y, e = blockIdx.x * 256 + threadIdx.x;
   if (j >= k || e >= g.m) return;
   const int* od = order + blockIdx.z * sig_stride;
-  double* x = reinterpret_cast<double*>(ws + g.ws_off + (long long)(g.pre == 2 ? j : od[j]) * g.m_pad);
+  double* x = reinterpret_cast<double*>(ws + g.ws_off + (long long)(g.pre >= 2 ? j : od[j]) * g.m_pad);
   const float2 d = tbuf[blockIdx.z * tstride + (long long)j * g.m_pad + e];
   x[e] -= (double)d.x;
   x[g.m_pad + e] -= (double)d.y;

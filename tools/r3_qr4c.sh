@@ -1,0 +1,7 @@
+#!/bin/bash
+L=paper_2601_04422_b200/libmpsim_gpu.so
+cp $L /tmp/product.so; cp tools/ab_libs/ab.so $L
+for rep in 1 2 3; do for v in MPSIM_QR=2 MPSIM_QR=-1; do
+  env $v timeout 600 python bench.py --steps 4 --warmup 3 --no-cpu-baseline --no-pipeline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', round(d['value'],2), d['clocks']['sm_mhz'], d['svd_sweeps'])"
+done; done
+cp /tmp/product.so $L
