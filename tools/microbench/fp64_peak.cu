@@ -1,5 +1,6 @@
 // FP64 peak microbenchmark: DFMA (CUDA cores) vs DMMA (mma.sync f64 tensor path).
 #include <cstdio>
+#include <cstdlib>
 #include <cuda_runtime.h>
 
 __global__ void dfma_kernel(double* out, int iters, double a, double b) {
@@ -43,7 +44,41 @@ __global__ void dmma_kernel(double* out, int iters) {
   if (s == 1234.5) out[0] = s;
 }
 
-int main() {
+// Sustained DMMA rate: back-to-back launches for ~seconds s (power-capped
+// clocks under a long load, the denominator for a kernel timed inside a
+// long step); prints the rate of each 0.5 s window and the SM clock.
+static int sustained(double seconds) {
+  double* d; cudaMalloc(&d, 8);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int threads = 256, blocks = sms * 8, iters = 20000;
+  const double flops_per_launch = 2.0 * 256 * 8 * iters * (double)blocks * (threads / 32);
+  dmma_kernel<0><<<blocks, threads>>>(d, 100);
+  cudaDeviceSynchronize();
+  double total_ms = 0, best = 0, last = 0;
+  while (total_ms < seconds * 1e3) {
+    cudaEventRecord(e0);
+    int n = 0;
+    float ms = 0;
+    while (ms < 500.f) {
+      dmma_kernel<0><<<blocks, threads>>>(d, iters);
+      ++n;
+      if (n % 8 == 0) { cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1); }
+    }
+    cudaEventRecord(e1); cudaEventSynchronize(e1); cudaEventElapsedTime(&ms, e0, e1);
+    last = flops_per_launch * n / ms / 1e9;
+    best = last > best ? last : best;
+    total_ms += ms;
+    int clk = 0;
+    cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, 0);
+    printf("sustained DMMA m8n8k4 t=%.1f s: %.2f TFLOP/s\n", total_ms / 1e3, last);
+  }
+  printf("sustained DMMA m8n8k4 over %.1f s: last window %.2f TFLOP/s, best %.2f\n", total_ms / 1e3, last, best);
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1) return sustained(atof(argv[1]));
   double* d; cudaMalloc(&d, 8);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
