@@ -82,7 +82,7 @@ void launch_jacobi_sweep_w32(const GateDesc*, int, int, cplx*, const int*, int*,
 // Persistent sweeps with 32-vector blocks (jacobi_w32.cu, A/B: MPSIM_W32=1)
 // when every operand's n_pad is a multiple of 64 and the largest is at least
 // kW32MinN. Measured slower than 16-vector blocks: not default.
-constexpr int kW32MinN = 256;
+constexpr int kW32MinN = 512;
 // Vector-count padding of gate and plain-SVD operands (a multiple of both
 // block pair widths, so either sweep kernel can run the batch).
 constexpr int kNAlign = 64;
