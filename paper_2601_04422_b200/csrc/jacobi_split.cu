@@ -362,6 +362,9 @@ __device__ __forceinline__ bool cross_only_evd(int active, int round) {
 
 // kMode 0: Gram only (G -> gbuf); 1: Gram + pair EVD (R -> rbuf); 2: the whole
 // pair visit, Gram + EVD + rotation, in one CTA.
+// Pre-asymptotic (in-block-cached) visits decide on rotation and report maxoff
+// from the cross entries alone.
+constexpr int kCrossTest = 1;
 struct RoundArgs {
   const GateDesc* gates;
   cplx* ws;
@@ -384,6 +387,7 @@ struct RoundArgs {
   int* blkok;  // per block: gblk holds its exact in-block Gram (persistent sweeps; nullable)
   int l2hint;  // L2 priorities: 0 none; 1 rotation loads / stores evict_first; 2 and Gram loads evict_last
   int ns_iters = 2;  // Newton-Schulz steps of the FP32 pair EVD's polar factor (A/B)
+  int xtest = kCrossTest;  // pre-asymptotic visits: rotation test on the cross entries only (A/B: MPSIM_XTEST)
 };
 
 // One pair visit (block pair k of gate gi in tournament round `round`).
@@ -460,6 +464,7 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
   __syncthreads();
   const double tolg = tol * fmax(sqrt((double)g.m), (double)kP);
   const double floor2 = floor_rel2 * frob2[gi];
+  double rx;  // this thread's squared relative cross off-diagonal
   {
     // sum of squared relative off-diagonals between the two blocks: the host
     // turns it into the sweep's rms off-norm (cross-only EVD policy)
@@ -470,11 +475,26 @@ __device__ __forceinline__ void pair_visit(const RoundArgs& A, int gi, int round
     double r = 0.0;
     if (fmin(gii, gjj) > floor2)
       r = (d < 1e30 && d > 1e-12) ? (double)__fdividef((float)c2, (float)d) : c2 / d;
+    rx = r;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
     if (lane == 0 && r > 0.0) atomicAdd(offsum + gi, r);
   }
-  const bool nd = pair_needs_rotation(SG, t, tolg, floor2, maxoff + gi);
+  bool nd;
+  if (approx && A.xtest) {
+    // pre-asymptotic visit: the in-block Grams are the cached EVD output, so
+    // the test and maxoff use the cross entries (the ratios above) only; the
+    // closing sweeps test every pair on exact Grams
+    double mx = rx;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0 && mx > 0.0)
+      atomicMax(reinterpret_cast<unsigned long long*>(maxoff + gi),
+                (unsigned long long)__double_as_longlong(sqrt(mx)));
+    nd = __syncthreads_or(rx > tolg * tolg);
+  } else {
+    nd = pair_needs_rotation(SG, t, tolg, floor2, maxoff + gi);
+  }
   PHASE_MARK(c_a1);
   PHASE_ADD(3, c_a1 - c_g1);
   const long long slot = (long long)gi * max_pairs + k;
@@ -921,6 +941,8 @@ static RoundArgs make_args(const GateDesc* d_gates, cplx* ws, const int* d_activ
   {
     const char* e = ab_knob("MPSIM_NS_ITERS");
     a.ns_iters = e ? std::atoi(e) : 2;
+    const char* x = ab_knob("MPSIM_XTEST");
+    a.xtest = x ? std::atoi(x) : kCrossTest;
   }
   return a;
 }
