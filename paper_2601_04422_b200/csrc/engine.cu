@@ -79,19 +79,24 @@ static int group_policy() {
 }
 void launch_jacobi_sweep_w32(const GateDesc*, int, int, cplx*, const int*, int*, double, double, const double*, double,
                              const int*, long long, double*, double*, cplx*, int*, cudaStream_t);
-// Persistent sweeps with 32-vector blocks (jacobi_w32.cu, A/B: MPSIM_W32=1)
-// when every operand's n_pad is a multiple of 64 and the largest is at least
-// kW32MinN. Measured slower than 16-vector blocks: not default.
-constexpr int kW32MinN = 512;
+// Persistent sweeps with 32-vector blocks (jacobi_w32.cu) for batches whose
+// largest operand has at least kW32MinN vectors (every n_pad is a multiple of
+// 64). Measured: at 2048-vector thetas (chi = 1024) +9 % over
+// 16-vector blocks — half the DRAM traffic per sweep keeps the SM clock off
+// the power cap (1965 vs 1717 MHz); at 1024 vectors the two are level, and
+// 256-vector thetas (C2) keep 16-vector blocks for their amplitude margin.
+// A/B: MPSIM_W32=0 never, =1 from 512 vectors.
+constexpr int kW32MinN = 2048;
 // Vector-count padding of gate and plain-SVD operands (a multiple of both
 // block pair widths, so either sweep kernel can run the batch).
 constexpr int kNAlign = 64;
-static bool w32_policy() {
-  static const bool on = [] {
-    const char* v = ab_knob("MPSIM_W32");
-    return v != nullptr && std::string(v) == "1";
+static int w32_min_n() {
+  static const int v = [] {
+    const char* e = ab_knob("MPSIM_W32");
+    if (e == nullptr) return kW32MinN;
+    return std::string(e) == "0" ? (1 << 30) : 512;
   }();
-  return on;
+  return v;
 }
 // Pair EVDs with FP32 Gram updates (bit 64) in the first sweep and in sweeps
 // whose predecessor's largest relative off-diagonal exceeded this; 0 = off
@@ -701,7 +706,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   s.h_offsum.ensure(sizeof(double) * ng);
   double* h_offsum = (double*)s.h_offsum.p;
   const int max_sweeps = phase_probe() ? 1 : kMaxSweeps;
-  bool use_w32 = w32_policy() && max_nb * kW >= kW32MinN;
+  bool use_w32 = max_nb * kW >= w32_min_n();
   for (const GateDesc& d : descs) use_w32 = use_w32 && d.n_pad % (4 * kW) == 0;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     NvtxRange nvs("mpsim: jacobi sweep");
