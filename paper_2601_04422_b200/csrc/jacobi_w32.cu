@@ -339,19 +339,41 @@ __device__ __forceinline__ void pair_visit2(const SweepArgs2& A, int gi, int rou
   __syncthreads();
   const double tolg = A.tol * fmax(sqrt((double)g.m), (double)kP);  // the W = 16 test's threshold
   const double floor2 = A.floor_rel2 * A.frob2[gi];
+  double rx = 0.0;   // this thread's largest squared relative cross off-diagonal
+  bool xneed = false;  // ... above the rotation threshold
   {
     // sum of squared relative off-diagonals between the two blocks (rms policy)
     double r = 0.0;
+    const double tolg2 = tolg * tolg;
     for (int idx = t; idx < kW2 * kW2; idx += kT2) {
       const int i = idx / kW2, j = kW2 + idx % kW2;
       const double gii = SG[i * kLdG + i].x, gjj = SG[j * kLdG + j].x;
-      if (fmin(gii, gjj) > floor2) r += cabs2(SG[i * kLdG + j]) / (gii * gjj);
+      if (fmin(gii, gjj) > floor2) {
+        const double c2 = cabs2(SG[i * kLdG + j]), d = gii * gjj;
+        const double q = (d < 1e30 && d > 1e-12) ? (double)__fdividef((float)c2, (float)d) : c2 / d;
+        r += q;
+        rx = fmax(rx, q);
+        xneed |= c2 > tolg2 * d;
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
     if ((t & 31) == 0 && r > 0.0) atomicAdd(A.offsum + gi, r);
   }
-  const bool nd = pair_needs_rotation_t<kP2, kLdG, kT2>(SG, t, tolg, floor2, A.maxoff + gi);
+  bool nd;
+  if (approx) {
+    // pre-asymptotic visit: the in-block Grams are the cached EVD output, so
+    // the test and maxoff use the cross entries only (as jacobi_split.cu)
+    double mx = rx;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((t & 31) == 0 && mx > 0.0)
+      atomicMax(reinterpret_cast<unsigned long long*>(A.maxoff + gi),
+                (unsigned long long)__double_as_longlong(sqrt(mx)));
+    nd = __syncthreads_or(xneed);
+  } else {
+    nd = pair_needs_rotation_t<kP2, kLdG, kT2>(SG, t, tolg, floor2, A.maxoff + gi);
+  }
   PHASE_MARK2(c_a1);
   PHASE_ADD2(3, c_a1 - c_g1);
   auto store_inblock = [&]() {
