@@ -17,6 +17,12 @@
 
 #include "common.cuh"
 
+// Pair-EVD G update of the 256-thread (16-vector block) sweeps: 0 = every
+// (row pair, column pair) block, 2 = Hermitian-folded (pair_evd_t kSym)
+#ifndef MPSIM_EVD_FOLD
+#define MPSIM_EVD_FOLD 0
+#endif
+
 namespace mpsim_gpu {
 
 template <int kPP>
@@ -109,7 +115,7 @@ __device__ __forceinline__ bool pair_needs_rotation(const cplx* G, int t, double
 // and mirrored (fewer FP64 instructions; measured +0.8 % for the 512-thread
 // 64 x 64 EVD of jacobi_w32.cu, where the update is FP64-throughput-bound; the
 // 256-thread 32 x 32 EVD keeps the full update: the split loops spill there).
-template <int kPP, int kLd, int kT, bool kSym = false>
+template <int kPP, int kLd, int kT, int kSym = 0>
 __device__ __forceinline__ void pair_evd_t(cplx* G, cplx* R, EvdScratchT<kPP>& S, int t, double tol_in,
                                            double floor2, int max_in, bool cross = false) {
   constexpr int kH = kPP / 2;
@@ -158,7 +164,91 @@ __device__ __forceinline__ void pair_evd_t(cplx* G, cplx* R, EvdScratchT<kPP>& S
         S.pq[t] = q;
       }
       __syncthreads();
-      if constexpr (kSym) {
+      if constexpr (kSym == 2) {
+        // one (row pair, column pair) block per thread, G kept exactly
+        // Hermitian: threads [0, kNU) take the blocks ba <= bb (folded as in
+        // kSym == 1) and update G (+ its mirror) and R; the others take the
+        // blocks ba > bb and update R only, so whole warps skip the G update
+        static_assert(kBlk == 1 && kH % 2 == 0, "one block per thread");
+        constexpr int kNU = kH * (kH + 1) / 2;
+        int ba, bb;
+        const bool doG = t < kNU;
+        if (doG) {
+          const int fi = t / (kH + 1), fj = t % (kH + 1);
+          ba = fj < kH - fi ? fi : kH - 1 - fi;
+          bb = fj < kH - fi ? fi + fj : kH - 1 - fi + (fj - (kH - fi));
+        } else {  // strictly upper (a < b) folded: rows a and kH - 2 - a share a row of kH
+          const int u = t - kNU, fi = u / kH, fj = u % kH;
+          int a, b;
+          if (fj < kH - 1 - fi) {
+            a = fi;
+            b = fi + 1 + fj;
+          } else {
+            a = kH - 2 - fi;
+            b = kH - 1 - fi + (fj - (kH - 1 - fi));
+          }
+          ba = b;
+          bb = a;
+        }
+        const double csa = S.cs[ba], sna = S.sn[ba], csb = S.cs[bb], snb = S.sn[bb];
+        int pa, qa, pb, qb;
+        if (cross) {
+          pa = ba;
+          qa = kH + (ba + step) % kH;
+          pb = bb;
+          qb = kH + (bb + step) % kH;
+        } else {
+          rr_pair(step, ba, kPP - 1, pa, qa);
+          rr_pair(step, bb, kPP - 1, pb, qb);
+        }
+        const cplx phb = S.ph[bb];
+        const cplx jb_qp = make_double2(-phb.x * snb, -phb.y * snb), jb_qq = make_double2(phb.x * csb, phb.y * csb);
+        if (doG && (sna != 0.0 || snb != 0.0)) {
+          const cplx pha = S.ph[ba];
+          const cplx ca_qp = make_double2(-pha.x * sna, pha.y * sna), ca_qq = make_double2(pha.x * csa, -pha.y * csa);
+          const cplx b00 = G[pa * kLd + pb], b01 = G[pa * kLd + qb], b10 = G[qa * kLd + pb], b11 = G[qa * kLd + qb];
+          cplx m00 = make_double2(csa * b00.x, csa * b00.y), m01 = make_double2(csa * b01.x, csa * b01.y);
+          cplx m10 = make_double2(sna * b00.x, sna * b00.y), m11 = make_double2(sna * b01.x, sna * b01.y);
+          cfma(m00, ca_qp, b10);
+          cfma(m01, ca_qp, b11);
+          cfma(m10, ca_qq, b10);
+          cfma(m11, ca_qq, b11);
+          cplx n00 = make_double2(csb * m00.x, csb * m00.y), n01 = make_double2(snb * m00.x, snb * m00.y);
+          cplx n10 = make_double2(csb * m10.x, csb * m10.y), n11 = make_double2(snb * m10.x, snb * m10.y);
+          cfma(n00, m01, jb_qp);
+          cfma(n01, m01, jb_qq);
+          cfma(n10, m11, jb_qp);
+          cfma(n11, m11, jb_qq);
+          if (ba == bb) {
+            n00.y = 0.0;
+            n11.y = 0.0;
+            n01 = make_double2(0.0, 0.0);
+            n10 = make_double2(0.0, 0.0);
+          }
+          G[pa * kLd + pb] = n00;
+          G[pa * kLd + qb] = n01;
+          G[qa * kLd + pb] = n10;
+          G[qa * kLd + qb] = n11;
+          if (ba != bb) {
+            G[pb * kLd + pa] = make_double2(n00.x, -n00.y);
+            G[qb * kLd + pa] = make_double2(n01.x, -n01.y);
+            G[pb * kLd + qa] = make_double2(n10.x, -n10.y);
+            G[qb * kLd + qa] = make_double2(n11.x, -n11.y);
+          }
+        }
+        if (snb != 0.0) {
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int row = r == 0 ? pa : qa;
+            const cplx x0 = R[row * kLd + pb], x1 = R[row * kLd + qb];
+            cplx y0 = make_double2(csb * x0.x, csb * x0.y), y1 = make_double2(snb * x0.x, snb * x0.y);
+            cfma(y0, x1, jb_qp);
+            cfma(y1, x1, jb_qq);
+            R[row * kLd + pb] = y0;
+            R[row * kLd + qb] = y1;
+          }
+        }
+      } else if constexpr (kSym == 1) {
       // G stays exactly Hermitian: only the (row pair, column pair) blocks with
       // ba <= bb are formed — kH (kH + 1) / 2 of them, folded into kH / 2 rows
       // of kH + 1 so whole warps drop out — and each off-diagonal block is
@@ -555,7 +645,7 @@ __device__ __forceinline__ void pair_evd_f32(cplx* G, cplx* W, cplx* R, EvdScrat
 
 __device__ __forceinline__ void pair_evd_v1(cplx* G, cplx* R, EvdScratch& S, int t, double tol_in, double floor2,
                                             int max_in, bool cross = false) {
-  pair_evd_t<kP, kPad, 256>(G, R, S, t, tol_in, floor2, max_in, cross);
+  pair_evd_t<kP, kPad, 256, MPSIM_EVD_FOLD>(G, R, S, t, tol_in, floor2, max_in, cross);
 }
 
 }  // namespace mpsim_gpu

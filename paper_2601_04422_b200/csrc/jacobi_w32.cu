@@ -393,7 +393,7 @@ __device__ __forceinline__ void pair_visit2(const SweepArgs2& A, int gi, int rou
   if (t == 0) *ok_a = *ok_b = 0;
   // the rotation's first chunk (the pass's last) loads into stage 2 during the EVD
   ld.issue(S.u.stage[2], (nchunks - 1) * kC2);
-  pair_evd_t<kP2, kLdG, kT2, true>(SG, S.u.R, S.sc, t, A.tol_in, floor2, 1, cross_only_evd2(act, round));
+  pair_evd_t<kP2, kLdG, kT2, 1>(SG, S.u.R, S.sc, t, A.tol_in, floor2, 1, cross_only_evd2(act, round));
   __syncthreads();
   PHASE_MARK2(c_e1);
   PHASE_ADD2(4, c_e1 - c_a1);
