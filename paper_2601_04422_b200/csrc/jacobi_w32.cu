@@ -97,6 +97,13 @@ struct Smem2 {
 static_assert(sizeof(cplx) * kP2 * kLdG <= sizeof(double) * 2 * kStage2, "R must leave stage 2 free");
 
 // column offset (plane + vector) of real-extended column `col` in a chunk stage
+// Cross-only Gram passes in three real products: at chi = 1024 +1.5 % (the
+// pass is DMMA-bound here, one CTA per SM at the full clock), all parity
+// green (profiles/sweep_ab_r02.txt). -DMPSIM_W32_GAUSS=0 restores four.
+#ifndef MPSIM_W32_GAUSS
+#define MPSIM_W32_GAUSS 1
+#endif
+constexpr bool kGauss2 = MPSIM_W32_GAUSS;
 __device__ __forceinline__ int coff2(int col) { return (col < kP2 ? 0 : kPlane2) + (col & (kP2 - 1)) * kPitch2; }
 
 // Gram pass over all chunks into S.u.Gx: the 64 cross tiles (cross_only) or
@@ -112,7 +119,37 @@ __device__ __forceinline__ void gram_pass2(Smem2& S, const Loader2& ld, int nchu
   };
   ld.issue(S.u.stage[0], 0);
   if (nchunks > 1) ld.issue(S.u.stage[1], kC2);
-  if (cross_only) {
+  if (cross_only && kGauss2) {
+    // the complex cross block X_a^H X_b in three real products (Gauss):
+    // T1 = Ar^T Br, T2 = Ai^T Bi, T3 = (Ar + Ai)^T (Br - Bi); Re = T1 + T2,
+    // Im = T1 - T2 - T3: 48 tiles instead of 64. Warp w owns tile position
+    // (w >> 2, w & 3) of the 32 x 32 block: four loads and two adds feed three
+    // DMMAs per k-step. Re lands in Gx's (Re_a, Re_b) tiles, Im in (Re_a, Im_b).
+    const int tr = warp >> 2, tc = warp & 3;
+    const int oar = coff2(8 * tr + fr), oai = coff2(kP2 + 8 * tr + fr);
+    const int obr = coff2(kW2 + 8 * tc + fr), obi = coff2(kP2 + kW2 + 8 * tc + fr);
+    double t1[2] = {0.0, 0.0}, t2[2] = {0.0, 0.0}, t3[2] = {0.0, 0.0};
+    for (int k = 0; k < nchunks; ++k) {
+      next_chunk(k);
+      const double* B = S.u.stage[k % 3];
+#pragma unroll
+      for (int ks = 0; ks < kC2 / 4; ++ks) {
+        const int row = 4 * ks + fk;
+        const double ar = B[row + oar], ai = B[row + oai], br = B[row + obr], bi = B[row + obi];
+        dmma(t1[0], t1[1], ar, br);
+        dmma(t2[0], t2[1], ai, bi);
+        dmma(t3[0], t3[1], ar + ai, br - bi);
+      }
+    }
+    __syncthreads();  // the last stage is read; Gx aliases the stages
+    double* const row = S.u.Gx + (8 * tr + fr) * kLdGx;
+#pragma unroll
+    for (int v = 0; v < 2; ++v) {
+      row[kW2 + 8 * tc + 2 * fk + v] = t1[v] + t2[v];
+      row[kP2 + kW2 + 8 * tc + 2 * fk + v] = t1[v] - t2[v] - t3[v];
+    }
+    __syncthreads();
+  } else if (cross_only) {
     // block q of the cross Gram: rows Re_a (tiles 0-3) / Im_a (8-11), columns
     // Re_b (4-7) / Im_b (12-15); warp >> 2 picks the tile row: one A and four
     // B loads feed four DMMAs per k-step
@@ -318,8 +355,8 @@ __device__ __forceinline__ void pair_visit2(const SweepArgs2& A, int gi, int rou
   if (cross_only) {
     for (int idx = t; idx < kW2 * kW2; idx += kT2) {
       const int i = idx / kW2, j = kW2 + idx % kW2;
-      const double re = Gx[i * kLdGx + j] + Gx[(kP2 + i) * kLdGx + kP2 + j];
-      const double im = Gx[i * kLdGx + kP2 + j] - Gx[(kP2 + i) * kLdGx + j];
+      const double re = kGauss2 ? Gx[i * kLdGx + j] : Gx[i * kLdGx + j] + Gx[(kP2 + i) * kLdGx + kP2 + j];
+      const double im = kGauss2 ? Gx[i * kLdGx + kP2 + j] : Gx[i * kLdGx + kP2 + j] - Gx[(kP2 + i) * kLdGx + j];
       SG[i * kLdG + j] = make_double2(re, im);
       SG[j * kLdG + i] = make_double2(re, -im);
       const int r = idx / kW2, q = idx % kW2;
