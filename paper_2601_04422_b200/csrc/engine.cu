@@ -252,10 +252,25 @@ static int phase_probe() {
   return v;
 }
 
+#ifndef MPSIM_W32_ALT
+#define MPSIM_W32_ALT 3
+#endif
+constexpr int kW32AltCross = MPSIM_W32_ALT;
 // Cross-block-only pair EVDs outside a period of rounds in the asymptotic
 // sweeps: MPSIM_ALT_CROSS=2 (odd rounds, default), 3 (two rounds in three)
 // or 0 (full EVDs every round, A/B). Returns the active bits to add.
-static int alt_cross_bits() {
+// The 32-vector-block sweep defaults to two rounds in three: its 64 x 64 full
+// EVD is relatively dearer (chi = 1024: +0.55 % for one more sweep launch per
+// three layers, parity green; profiles/sweep_ab_r02.txt). MPSIM_W32_ALT_CROSS (A/B).
+static int alt_cross_bits(bool w32 = false) {
+  if (w32) {
+    static const int bits32 = [] {
+      const char* v = ab_knob("MPSIM_W32_ALT_CROSS");
+      const int p = v ? std::atoi(v) : kW32AltCross;
+      return p == 2 ? 16 : p == 3 ? (16 | 32) : 0;
+    }();
+    return bits32;
+  }
   static const int bits = [] {
     const char* v = ab_knob("MPSIM_ALT_CROSS");
     const int p = v ? std::atoi(v) : 2;
@@ -672,13 +687,16 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   }
 
   int* h_rot = (int*)s.h_rot.p;
+  bool use_w32 = max_nb * kW >= w32_min_n();
+  for (const GateDesc& d : descs) use_w32 = use_w32 && d.n_pad % (4 * kW) == 0;
+  const bool w32_sweeps = use_w32 && jacobi_mode() == 4 && sweep_policy() && !phase_probe();
   // The first sweep of a fresh theta is pre-asymptotic: it reuses the pair
   // EVDs' in-block Grams from round 1 on (bit 4) like the sweeps the maxoff
   // policy below flags. It cannot end the iteration through kQuadFinish (its
   // maxoff saw in-block values that may be stale); only a sweep without any
   // rotation — whose Grams were then all computed exactly — ends it.
   const int first = ((jacobi_mode() >= 3 && inblock_policy() && first_sweep_inblock()) ? (1 | 4) : 1) |
-                    alt_cross_bits() | (evd32_maxoff() > 0.0 ? 64 : 0);
+                    alt_cross_bits(w32_sweeps) | (evd32_maxoff() > 0.0 ? 64 : 0);
   for (int i = 0; i < ng; ++i) h_rot[i] = descs[i].n >= kEvd32MinN ? first : first & ~64;
   int n_list = 0;
   // flags h_rot[0, ng) -> device, with the list of active gates after them
@@ -706,8 +724,6 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
   s.h_offsum.ensure(sizeof(double) * ng);
   double* h_offsum = (double*)s.h_offsum.p;
   const int max_sweeps = phase_probe() ? 1 : kMaxSweeps;
-  bool use_w32 = max_nb * kW >= w32_min_n();
-  for (const GateDesc& d : descs) use_w32 = use_w32 && d.n_pad % (4 * kW) == 0;
   for (int sweep = 0; sweep < max_sweeps; ++sweep) {
     NvtxRange nvs("mpsim: jacobi sweep");
     CK(cudaMemsetAsync(s.d_rot.p, 0, sizeof(int) * ng, st));
@@ -828,7 +844,7 @@ void mpsim_gpu::run_two_chunk(State& s, const std::vector<GateDesc>& descs, std:
       if (h_rot[i] && cross_policy() && rms > cross_rms() && h_maxoff[i] > 1e-3 && sweep < cross_sweeps() &&
           descs[i].nb >= 8)
         h_rot[i] |= 2;
-      if (h_rot[i]) h_rot[i] |= alt_cross_bits();
+      if (h_rot[i]) h_rot[i] |= alt_cross_bits(w32_sweeps);
       // pre-asymptotic and early asymptotic sweeps reuse the in-block Grams the
       // pair EVDs leave behind (jacobi_split.cu); the closing sweeps recompute all
       if (h_rot[i] && jacobi_mode() >= 3 && inblock_policy() && h_maxoff[i] > kInblockMaxoff) h_rot[i] |= 4;
