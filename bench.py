@@ -143,13 +143,19 @@ def fp64_peak():
     return float(d["dmma_tflops"]), "profiles/fp64_peak.json (measured DMMA m8n8k4 microbenchmark, this pool)"
 
 
-def ncu_traffic():
+def ncu_traffic(chi=512):
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
-    return d.get("jacobi_sweep_kernel", {}).get("dram_bytes_per_launch")
+    return d.get(sweep_kernel(chi), {}).get("dram_bytes_per_launch") if chi == 512 else None
+
+
+def sweep_kernel(chi=512):
+    """The library's sweep kernel for a saturated chi-layer: 32-vector blocks
+    from 1024-vector thetas (engine.cu kW32MinN), else 16-vector blocks."""
+    return "jacobi_sweep_w32_kernel" if 2 * chi >= 1024 else "jacobi_sweep_kernel"
 
 
 # ---------------------------------------------------------------- CPU reference path
@@ -323,9 +329,9 @@ def main():
         "circuit_wall_s": wall_total,
         "roofline": {
             "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved / peak, "traffic": ncu_traffic(),
-            "kernel": "jacobi_sweep_kernel (one persistent launch per Jacobi sweep: every pair visit = DMMA "
-                      "Gram + pair EVD + DMMA rotation)",
+            "frac": achieved / peak, "traffic": ncu_traffic(args.chi),
+            "kernel": sweep_kernel(args.chi) + " (one persistent launch per Jacobi sweep: every pair visit = "
+                      "DMMA Gram + pair EVD + DMMA rotation)",
             "definition": "algorithmic SVD flops 32*M*N^2 per decomposed theta (SURVEY 8(d)) / CUDA-event "
                           "time of all Jacobi sweep launches on the library stream (QR preconditioning, "
                           "theta and the split epilogue excluded; see jacobi_share_of_step); traffic = DRAM "

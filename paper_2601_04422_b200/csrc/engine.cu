@@ -81,12 +81,15 @@ void launch_jacobi_sweep_w32(const GateDesc*, int, int, cplx*, const int*, int*,
                              const int*, long long, double*, double*, cplx*, int*, cudaStream_t);
 // Persistent sweeps with 32-vector blocks (jacobi_w32.cu) for batches whose
 // largest operand has at least kW32MinN vectors (every n_pad is a multiple of
-// 64). Measured: at 2048-vector thetas (chi = 1024) +9 % over
-// 16-vector blocks — half the DRAM traffic per sweep keeps the SM clock off
-// the power cap (1965 vs 1717 MHz); at 1024 vectors the two are level, and
-// 256-vector thetas (C2) keep 16-vector blocks for their amplitude margin.
+// 64). Measured (profiles/sweep_ab_r02.txt): half the DRAM
+// traffic per sweep keeps the SM clock off the power cap (1965 MHz vs
+// 1717-1845 for 16-vector blocks): with the symmetric EVD update, the cross
+// test, three-product cross Grams and two-in-three cross-only EVD rounds,
+// 1024-vector thetas (chi = 512) run 119-120 gates/s vs 115 on the same box,
+// 2048-vector thetas (chi = 1024) 16.5 vs 14.7. 256-vector thetas (C2) keep
+// 16-vector blocks for their amplitude margin.
 // A/B: MPSIM_W32=0 never, =1 from 512 vectors.
-constexpr int kW32MinN = 2048;
+constexpr int kW32MinN = 1024;
 // Vector-count padding of gate and plain-SVD operands (a multiple of both
 // block pair widths, so either sweep kernel can run the batch).
 constexpr int kNAlign = 64;
